@@ -1,0 +1,164 @@
+/*
+ * opcfe.h -- C ABI of libopcfe, the B200 (sm_100a) organized-point-cloud front-end.
+ *
+ * Drop-in boundary for the reference's hot path (flatpoly, arXiv 2007.12065 clean-room
+ * reimplementation).  Every entry point names the reference interface it replaces;
+ * paths are relative to /root/reference/pkg/src/flatpoly.  The reference's own plugin
+ * point is the `_kernels` backend switch (_kernels/__init__.py:9-30); see
+ * INTEGRATION.md for the ctypes binding a maintainer adds there.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors) unless noted.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy stream),
+ *     never allocates, never synchronises, and is safe to capture into a CUDA graph.
+ *   - Return value: OPCFE_OK (0) or a negative OPCFE_ERR_*; the message is in
+ *     opcfe_last_error() (thread-local).  No exception crosses the ABI.
+ *   - Organized grids: F frames of M x N points, xyz interleaved, float32, each row
+ *     padded to `pitch` floats (pitch >= 3N, pitch % 4 == 0: the TMA row-stride rule);
+ *     frame stride = M * pitch.  opcfe_points_pitch(N) gives the minimal pitch.
+ *   - FC (fully-connected triangle) grids: (M-1) x (N-1) quads x 2 triangles x xyz,
+ *     rows padded to opcfe_fc_pitch(N) floats.
+ *   - GID = 2*(u*(N-1)+v)+k (mesh.py:46-48).  Per-frame capacity G = 2(M-1)(N-1):
+ *     frame f's triangles/twins/normals start at row f*G of their arrays.
+ */
+#ifndef OPCFE_H_
+#define OPCFE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* opcfe_stream_t; /* cudaStream_t */
+
+#define OPCFE_OK 0
+#define OPCFE_ERR_INVALID (-1)     /* shape / parameter (reference: DegenerateInputError, ValueError) */
+#define OPCFE_ERR_CUDA (-2)        /* CUDA runtime or launch failure */
+#define OPCFE_ERR_UNSUPPORTED (-3) /* kernel_size beyond the compiled set */
+#define OPCFE_ERR_WORKSPACE (-4)   /* workspace smaller than opcfe_*_workspace() */
+#define OPCFE_ERR_DRIVER (-5)      /* cuTensorMapEncodeTiled unavailable */
+
+int opcfe_version(void);
+const char* opcfe_last_error(void);
+
+/* layout helpers */
+int opcfe_points_pitch(int N);
+int opcfe_fc_pitch(int N);
+size_t opcfe_vmask_words(int F, int M, int N); /* 1 validity bit per point, ceil(N/32) words/row */
+size_t opcfe_triangulate_workspace(int F, int M, int N);
+
+/* Source grid (any f32/f64 layout with xyz contiguous) -> padded fp32 grid + validity bits.
+ * Replaces the dtype coercion np.asarray(opc, dtype=float64) at smoothing.py:55 / mesh.py:65
+ * and the finiteness mask at mesh.py:69.  dst may be NULL (mask only).  Strides in elements. */
+int opcfe_stage_in(const void* src, int src_is_f64, long long src_row_stride,
+                   long long src_frame_stride, int F, int M, int N, float* dst, int pitch,
+                   uint32_t* vmask, opcfe_stream_t stream);
+
+/* Inverse of opcfe_stage_in: padded fp32 grid -> contiguous (F,M,N,3) f32 or f64.  With
+ * orig != NULL (the caller's original input, dst dtype), every component whose fp32
+ * value equals float(orig) is returned as orig bit-exactly, so vertices/normals the
+ * filters leave unchanged come back exactly as given (smoothing.py:57; border ring
+ * and NaN vertices, _fallback.py:111-115). */
+int opcfe_unstage(const float* src, int pitch, int F, int M, int N, void* dst, int dst_is_f64,
+                  const void* orig, opcfe_stream_t stream);
+
+/* Replaces _kernels.laplacian_filter(points, lam, kernel_size, iterations)
+ * (_kernels/__init__.py:29 -> _native.pyx:225 / _fallback.py:82) as called by
+ * smoothing.laplacian_filter_opc (smoothing.py:53-58).  Result in `out`; `tmp` is the
+ * ping-pong buffer (same size, needed when iterations > 1).  If vmask != NULL the
+ * first pass also writes the point-validity bits of `in`. */
+int opcfe_laplacian(const float* in, float* out, float* tmp, uint32_t* vmask, int F, int M,
+                    int N, int pitch, float lam, int kernel_size, int iterations,
+                    opcfe_stream_t stream);
+
+/* Replaces mesh.extract_triangles_opc (mesh.py:58-96) + mesh.extract_halfedges_opc
+ * (mesh.py:99-135), and optionally compute_normals (mesh.py:162 -> geometry.py:134, fp64
+ * math on the fp32 grid) and the l_max longest-edge flag of group_assignment
+ * (segmentation.py:59-67,73).  trimap [F][G], triangles [F][G][3], halfedges [F][G][3]
+ * (nullable), n_tri [F]; normals [F][G][3] and lmax_flag [F][G] are optional (NULL);
+ * pts/pitch are needed only for them.  ws: opcfe_triangulate_workspace() bytes. */
+int opcfe_triangulate(const uint32_t* vmask, int F, int M, int N, int64_t* trimap,
+                      int64_t* triangles, int64_t* halfedges, int64_t* n_tri, const float* pts,
+                      int pitch, float* normals, double l_max, uint8_t* lmax_flag, void* ws,
+                      size_t ws_bytes, opcfe_stream_t stream);
+
+/* Replaces mesh.extract_halfedges_opc(trimap, M, N) for an arbitrary caller trimap
+ * (mesh.py:99-135).  halfedges must be pre-filled with -1 (3*n_tri entries). */
+int opcfe_halfedges_from_trimap(const int64_t* trimap, int M, int N, int64_t n_tri,
+                                int64_t* halfedges, opcfe_stream_t stream);
+
+/* Replaces smoothing.compute_fc_triangle_data (smoothing.py:61-88); contiguous (M,N,3) in,
+ * (M-1,N-1,2,3) out, f64 (bit-exact) or f32. */
+int opcfe_fc_data(const void* opc, int is_f64, int M, int N, void* centroids, void* normals,
+                  opcfe_stream_t stream);
+
+/* Replaces smoothing.bilateral_filter_opc (smoothing.py:91-114) -- FC data, the
+ * _kernels.bilateral_iterate loop (_native.pyx:287 / _fallback.py:120) and the trimap
+ * gather -- in `iterations` launches.  Two input forms:
+ *   pts != NULL, normals_in == NULL: normals/centroids computed from the point grid
+ *     (fused into iteration 1);
+ *   normals_in, centroids_in != NULL: FC arrays (padded rows) as given to
+ *     _kernels.bilateral_iterate (_kernels/__init__.py:30).
+ * Output: out_mesh != NULL -> mesh order through trimap ([F][out_rows][3]);
+ *         otherwise out_fc (FC layout, padded rows).
+ * buf_a / buf_b: FC-sized ping-pong buffers (needed for iterations > 1 / > 2). */
+int opcfe_bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
+                    const float* centroids_in, float sigma_length, float sigma_angle,
+                    int kernel_size, int iterations, float* buf_a, float* buf_b, float* out_fc,
+                    const int64_t* trimap, float* out_mesh, long long out_rows,
+                    opcfe_stream_t stream);
+
+/* Replaces geometry.triangle_normals (geometry.py:134-147) == mesh.compute_normals
+ * (mesh.py:162-164) for any indexed set; contiguous (n,3) points, (T,3) int64 triangles.
+ * f64 results are bit-identical to numpy. */
+int opcfe_triangle_normals(const void* points, int is_f64, const int64_t* triangles,
+                           long long n_tri, void* normals, opcfe_stream_t stream);
+
+/* Replaces the l_max half of segmentation.group_assignment (segmentation.py:59-67,73):
+ * flag[t] = longest edge of triangle t > l_max (fp64 edge lengths). */
+int opcfe_max_edge_mask(const void* points, int is_f64, const int64_t* triangles,
+                        long long n_tri, double l_max, uint8_t* flag, opcfe_stream_t stream);
+
+/* The organized branch of pipeline.run_scene (pipeline.py:125-134), all frames in one
+ * call: [stage-in] -> Laplacian -> triangulation + twins -> bilateral (normals in mesh
+ * order) [-> l_max flag]. */
+typedef struct {
+  int laplacian_iterations; /* 0 = no Laplacian */
+  int laplacian_kernel_size;
+  float laplacian_lambda;
+  int bilateral_iterations; /* 0 = no bilateral: normals = triangle normals of the smoothed grid */
+  int bilateral_kernel_size;
+  float sigma_length;
+  float sigma_angle;
+  double l_max; /* < 0: no l_max flag */
+} opcfe_front_end_params;
+
+typedef struct {
+  /* input: src_kind 0 = padded fp32 grid (src_pitch floats/row, frame stride M*src_pitch),
+   *        1 = contiguous f32 (F,M,N,3), 2 = contiguous f64 (F,M,N,3) */
+  const void* src;
+  int src_kind;
+  int src_pitch;
+  /* outputs (device) */
+  float* points;      /* [F][M][pitch] smoothed grid, pitch = opcfe_points_pitch(N) */
+  int64_t* trimap;    /* [F][G] */
+  int64_t* triangles; /* [F][G][3] */
+  int64_t* halfedges; /* [F][G][3] or NULL */
+  float* normals;     /* [F][G][3] or NULL */
+  uint8_t* lmax_flag; /* [F][G] or NULL (needs l_max >= 0) */
+  int64_t* n_tri;     /* [F] */
+} opcfe_front_end_io;
+
+size_t opcfe_front_end_workspace(int F, int M, int N, const opcfe_front_end_params* p,
+                                 int src_kind, int src_pitch);
+int opcfe_front_end(int F, int M, int N, const opcfe_front_end_params* p,
+                    const opcfe_front_end_io* io, void* ws, size_t ws_bytes,
+                    opcfe_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OPCFE_H_ */

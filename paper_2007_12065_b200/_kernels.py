@@ -1,0 +1,43 @@
+"""Kernel boundary, mirroring flatpoly._kernels (reference: _kernels/__init__.py:9-30).
+
+The reference picks a backend at import (Cython native | NumPy fallback).
+Here there is exactly one backend: libopcfe on the GPU.  No fallback exists;
+calls raise if the library or the device is missing.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _ops
+from ._device import Staged
+
+HAVE_NATIVE = True
+ACTIVE = "cuda-sm100a"
+
+
+def laplacian_filter(points, lam, kernel_size, iterations):
+    """Same contract as _kernels.laplacian_filter (_native.pyx:225 / _fallback.py:82)."""
+    from .smoothing import _laplacian_staged
+    return _laplacian_staged(Staged(points), lam, kernel_size, iterations)
+
+
+def bilateral_iterate(centroids, normals, sigma_length, sigma_angle, kernel_size, iterations):
+    """Same contract as _kernels.bilateral_iterate (_native.pyx:287 / _fallback.py:120)."""
+    C = Staged(centroids)
+    Nn = Staged(normals)
+    n = Nn.dev
+    Mq, Nq = n.shape[:2]
+    c = C.dev.to(n.dtype)
+    out = _ops.bilateral(1, Mq + 1, Nq + 1, sigma_length, sigma_angle, kernel_size, iterations,
+                         fc_normals=_ops.stage_fc(n), fc_centroids=_ops.stage_fc(c))
+    res = _ops.unstage_fc(out, 1, Mq, Nq, n.dtype, orig=n.unsqueeze(0).contiguous())[0]
+    return Nn.give(res)
+
+
+def find_cells(*args, **kwargs):  # pragma: no cover - outside the OPC front-end hot path
+    raise NotImplementedError("find_cells (FastGA) is outside this build's scope (SURVEY.md 8f)")
+
+
+def grow_segment(*args, **kwargs):  # pragma: no cover - outside the OPC front-end hot path
+    raise NotImplementedError("grow_segment (region growing) is outside this build's scope")

@@ -1,0 +1,259 @@
+// C ABI of libopcfe (include/opcfe.h): argument checking, error plumbing, TMA
+// descriptor encoding and the fused front-end chain.  No allocation, no host sync.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+#include "../../include/opcfe.h"
+#include "common.cuh"
+#include "opcfe_internal.h"
+
+namespace opcfe {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    return fail(ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+  return OK;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+int make_tmap_3d(CUtensorMap* map, const void* base, bool f64, uint64_t cols, uint64_t rows,
+                 uint64_t frames, uint64_t row_pitch_elems, uint64_t frame_stride_elems,
+                 uint32_t box_cols, uint32_t box_rows) {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  if (!g_encode) return fail(ERR_DRIVER, "cuTensorMapEncodeTiled not available from the driver");
+  const uint64_t esz = f64 ? 8 : 4;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0)
+    return fail(ERR_INVALID, "TMA: base address must be 16-byte aligned");
+  if ((row_pitch_elems * esz) % 16 != 0 || (frame_stride_elems * esz) % 16 != 0)
+    return fail(ERR_INVALID, "TMA: row/frame strides must be multiples of 16 bytes");
+  cuuint64_t dims[3] = {cols, rows, frames};
+  cuuint64_t strides[2] = {row_pitch_elems * esz, frame_stride_elems * esz};
+  cuuint32_t box[3] = {box_cols, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = g_encode(
+      map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+      const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA);
+  if (r != CUDA_SUCCESS) {
+    char buf[160];
+    snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d): dims %llu x %llu x %llu box %u x %u",
+             (int)r, (unsigned long long)cols, (unsigned long long)rows,
+             (unsigned long long)frames, box_cols, box_rows);
+    return fail(ERR_DRIVER, buf);
+  }
+  return OK;
+}
+
+namespace {
+
+inline cudaStream_t S(opcfe_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct FeLayout {
+  size_t vmask = 0, status = 0, staged = 0, lap_tmp = 0, bil_a = 0, bil_b = 0, total = 0;
+  size_t vmask_b = 0, status_b = 0, staged_b = 0, lap_b = 0, bil_b_bytes = 0;
+};
+
+FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src_kind,
+                   int src_pitch) {
+  FeLayout L;
+  const int pitch = points_pitch(N);
+  const size_t grid_bytes = (size_t)F * M * pitch * sizeof(float);
+  const size_t fc_bytes = (size_t)F * (M - 1) * fc_pitch(N) * sizeof(float);
+  L.vmask_b = (size_t)F * M * ((N + 31) / 32) * sizeof(uint32_t);
+  L.status_b = triangulate_workspace_bytes(F, M);
+  const bool lap = p->laplacian_iterations > 0;
+  const bool need_stage = lap && !(src_kind == 0 && src_pitch == pitch);
+  L.staged_b = need_stage ? grid_bytes : 0;
+  L.lap_b = (lap && p->laplacian_iterations > 1) ? grid_bytes : 0;
+  L.bil_b_bytes = fc_bytes;
+  size_t off = 0;
+  L.vmask = off;
+  off += align256(L.vmask_b);
+  L.status = off;
+  off += align256(L.status_b);
+  L.staged = off;
+  off += align256(L.staged_b);
+  L.lap_tmp = off;
+  off += align256(L.lap_b);
+  L.bil_a = off;
+  off += (p->bilateral_iterations > 1) ? align256(fc_bytes) : 0;
+  L.bil_b = off;
+  off += (p->bilateral_iterations > 2) ? align256(fc_bytes) : 0;
+  L.total = off + 256;
+  return L;
+}
+
+}  // namespace
+}  // namespace opcfe
+
+using namespace opcfe;
+
+extern "C" {
+
+int opcfe_version(void) { return 1; }
+
+const char* opcfe_last_error(void) { return g_last_error.c_str(); }
+
+int opcfe_points_pitch(int N) { return points_pitch(N); }
+
+int opcfe_fc_pitch(int N) { return fc_pitch(N); }
+
+size_t opcfe_vmask_words(int F, int M, int N) { return (size_t)F * M * ((N + 31) / 32); }
+
+size_t opcfe_triangulate_workspace(int F, int M, int N) {
+  (void)N;
+  return triangulate_workspace_bytes(F, M);
+}
+
+int opcfe_stage_in(const void* src, int src_is_f64, long long src_row_stride,
+                   long long src_frame_stride, int F, int M, int N, float* dst, int pitch,
+                   uint32_t* vmask, opcfe_stream_t stream) {
+  return stage_in(src, src_is_f64 != 0, src_row_stride, src_frame_stride, F, M, N, dst, pitch,
+                  vmask, S(stream));
+}
+
+int opcfe_unstage(const float* src, int pitch, int F, int M, int N, void* dst, int dst_is_f64,
+                  const void* orig, opcfe_stream_t stream) {
+  return unstage(src, pitch, F, M, N, dst, dst_is_f64 != 0, orig, S(stream));
+}
+
+int opcfe_laplacian(const float* in, float* out, float* tmp, uint32_t* vmask, int F, int M,
+                    int N, int pitch, float lam, int kernel_size, int iterations,
+                    opcfe_stream_t stream) {
+  if (!in || !out) return fail(ERR_INVALID, "laplacian: null buffer");
+  return laplacian(in, out, tmp, vmask, F, M, N, pitch, lam, kernel_size, iterations, S(stream));
+}
+
+int opcfe_triangulate(const uint32_t* vmask, int F, int M, int N, int64_t* trimap,
+                      int64_t* triangles, int64_t* halfedges, int64_t* n_tri, const float* pts,
+                      int pitch, float* normals, double l_max, uint8_t* lmax_flag, void* ws,
+                      size_t ws_bytes, opcfe_stream_t stream) {
+  return triangulate(vmask, F, M, N, trimap, triangles, halfedges, n_tri, pts, pitch, normals,
+                     l_max, lmax_flag, ws, ws_bytes, S(stream));
+}
+
+int opcfe_halfedges_from_trimap(const int64_t* trimap, int M, int N, int64_t n_tri,
+                                int64_t* halfedges, opcfe_stream_t stream) {
+  return halfedges_from_trimap(trimap, M, N, n_tri, halfedges, S(stream));
+}
+
+int opcfe_fc_data(const void* opc, int is_f64, int M, int N, void* centroids, void* normals,
+                  opcfe_stream_t stream) {
+  return fc_data(opc, is_f64 != 0, M, N, centroids, normals, S(stream));
+}
+
+int opcfe_bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
+                    const float* centroids_in, float sigma_length, float sigma_angle,
+                    int kernel_size, int iterations, float* buf_a, float* buf_b, float* out_fc,
+                    const int64_t* trimap, float* out_mesh, long long out_rows,
+                    opcfe_stream_t stream) {
+  return bilateral(pts, F, M, N, pitch, normals_in, centroids_in, sigma_length, sigma_angle,
+                   kernel_size, iterations, buf_a, buf_b, out_fc, trimap, out_mesh, out_rows,
+                   S(stream));
+}
+
+int opcfe_triangle_normals(const void* points, int is_f64, const int64_t* triangles,
+                           long long n_tri, void* normals, opcfe_stream_t stream) {
+  return triangle_normals(points, is_f64 != 0, triangles, n_tri, normals, S(stream));
+}
+
+int opcfe_max_edge_mask(const void* points, int is_f64, const int64_t* triangles,
+                        long long n_tri, double l_max, uint8_t* flag, opcfe_stream_t stream) {
+  return max_edge_mask(points, is_f64 != 0, triangles, n_tri, l_max, flag, S(stream));
+}
+
+size_t opcfe_front_end_workspace(int F, int M, int N, const opcfe_front_end_params* p,
+                                 int src_kind, int src_pitch) {
+  if (!p || F < 1 || M < 2 || N < 2) return 0;
+  return fe_layout(F, M, N, p, src_kind, src_pitch).total;
+}
+
+int opcfe_front_end(int F, int M, int N, const opcfe_front_end_params* p,
+                    const opcfe_front_end_io* io, void* ws, size_t ws_bytes,
+                    opcfe_stream_t stream) {
+  if (!p || !io || F < 1 || M < 2 || N < 2)
+    return fail(ERR_INVALID, "front_end: organized cloud must be at least 2 x 2");
+  if (!io->src || !io->points || !io->trimap || !io->triangles || !io->n_tri)
+    return fail(ERR_INVALID, "front_end: null input/output");
+  if (io->src_kind < 0 || io->src_kind > 2) return fail(ERR_INVALID, "front_end: bad src_kind");
+  if (io->src_kind == 0 && (io->src_pitch < 3 * N || io->src_pitch % 4))
+    return fail(ERR_INVALID, "front_end: src_pitch must be >= 3N and a multiple of 4");
+  if (io->lmax_flag && p->l_max < 0) return fail(ERR_INVALID, "front_end: lmax_flag needs l_max");
+  const int pitch = points_pitch(N);
+  const FeLayout L = fe_layout(F, M, N, p, io->src_kind, io->src_pitch);
+  if (!ws || ws_bytes < L.total) return fail(ERR_WORKSPACE, "front_end: workspace too small");
+  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255));
+  uint32_t* vmask = reinterpret_cast<uint32_t*>(base + L.vmask);
+  void* status = base + L.status;
+  float* staged = reinterpret_cast<float*>(base + L.staged);
+  float* lap_tmp = reinterpret_cast<float*>(base + L.lap_tmp);
+  float* bil_a = reinterpret_cast<float*>(base + L.bil_a);
+  float* bil_b = reinterpret_cast<float*>(base + L.bil_b);
+  const cudaStream_t st = S(stream);
+  const bool f64 = io->src_kind == 2;
+  const long long rs = io->src_kind == 0 ? io->src_pitch : 3ll * N;
+  const long long fs = (long long)M * rs;
+  int rc;
+  // 1. Laplacian (smoothing.laplacian_filter_opc, pipeline.py:127-129)
+  if (p->laplacian_iterations > 0) {
+    const float* lin;
+    uint32_t* lap_vmask;
+    if (L.staged_b == 0) {
+      lin = static_cast<const float*>(io->src);
+      lap_vmask = vmask;
+    } else {
+      if ((rc = stage_in(io->src, f64, rs, fs, F, M, N, staged, pitch, vmask, st))) return rc;
+      lin = staged;
+      lap_vmask = nullptr;
+    }
+    rc = laplacian(lin, io->points, lap_tmp, lap_vmask, F, M, N, pitch, p->laplacian_lambda,
+                   p->laplacian_kernel_size, p->laplacian_iterations, st);
+    if (rc) return rc;
+  } else {
+    if ((rc = stage_in(io->src, f64, rs, fs, F, M, N, io->points, pitch, vmask, st))) return rc;
+  }
+  // 2. mesh_from_opc (pipeline.py:130-131): triangles + trimap + twins [+ normals]
+  const bool bil = p->bilateral_iterations > 0 && io->normals != nullptr;
+  rc = triangulate(vmask, F, M, N, io->trimap, io->triangles, io->halfedges, io->n_tri, io->points,
+                   pitch, bil ? nullptr : io->normals, p->l_max, io->lmax_flag, status, L.status_b,
+                   st);
+  if (rc) return rc;
+  // 3. bilateral_filter_opc (pipeline.py:132-134), scattered to mesh order via trimap
+  if (bil) {
+    rc = bilateral(io->points, F, M, N, pitch, nullptr, nullptr, p->sigma_length, p->sigma_angle,
+                   p->bilateral_kernel_size, p->bilateral_iterations,
+                   p->bilateral_iterations > 1 ? bil_a : nullptr,
+                   p->bilateral_iterations > 2 ? bil_b : nullptr, nullptr, io->trimap, io->normals,
+                   2ll * (M - 1) * (N - 1), st);
+    if (rc) return rc;
+  }
+  return OK;
+}
+
+}  // extern "C"

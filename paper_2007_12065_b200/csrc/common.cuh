@@ -1,0 +1,186 @@
+// Shared device/host helpers for libopcfe (sm_100a only).
+//  * TMA (cp.async.bulk.tensor) tile loads/stores + mbarrier completion
+//  * fp64 arithmetic without FMA contraction (numpy operation order)
+//  * error plumbing for the C ABI
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libopcfe is built for sm_100a (B200) only"
+#endif
+
+namespace opcfe {
+
+// ----------------------------------------------------------------- errors (host)
+enum Status : int {
+  OK = 0,
+  ERR_INVALID = -1,      // bad shape / parameter
+  ERR_CUDA = -2,         // CUDA runtime / launch failure
+  ERR_UNSUPPORTED = -3,  // kernel size beyond the compiled set
+  ERR_WORKSPACE = -4,    // workspace too small
+  ERR_DRIVER = -5,       // driver entry point (cuTensorMapEncodeTiled) unavailable
+};
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int check_launch(const char* what);
+
+// ------------------------------------------------------------ small host utils
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+inline int points_pitch(int N) { return round_up(3 * N, 4); }      // floats per grid row
+inline int fc_pitch(int N) { return round_up(6 * (N - 1), 4); }    // floats per FC quad row
+
+// TMA descriptor for a 3-D fp32/fp64 tensor [F][rows][cols] with a row pitch
+// (elements) and a frame stride (elements).  Out-of-bounds reads fill with NaN,
+// which is exactly the reference's "off-grid neighbour is skipped" rule
+// (_kernels/_fallback.py:94 pads with NaN).
+int make_tmap_3d(CUtensorMap* map, const void* base, bool f64, uint64_t cols, uint64_t rows,
+                 uint64_t frames, uint64_t row_pitch_elems, uint64_t frame_stride_elems,
+                 uint32_t box_cols, uint32_t box_rows);
+
+// ------------------------------------------------------------- device helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Dynamic shared memory carve-up for TMA kernels.  TMA tile destinations must be
+// 128-B aligned in the shared window; the dynamic-smem base is only guaranteed 16-B
+// aligned, so kernels request kSmemSlack extra bytes and align here.  The mbarrier
+// lives in the slack, in front of the tiles (no static __shared__ in TMA kernels).
+constexpr int kSmemSlack = 256;
+
+__device__ __forceinline__ char* smem_aligned_base(char* raw, uint64_t** bar) {
+  const uint32_t off = static_cast<uint32_t>(__cvta_generic_to_shared(raw));
+  const uint32_t pad = (128u - (off + 16u) % 128u) % 128u + 16u;  // >= 16 B for the barrier
+  char* base = raw + pad;
+  *bar = reinterpret_cast<uint64_t*>(base - 8);
+  return base;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  const uint32_t a = smem_u32(bar);
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+// global -> shared tile (3-D box), completion counted on `bar`
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// shared -> global tile (3-D box); out-of-bounds elements are not written
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_commit_and_wait() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// make generic-proxy smem writes visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// 2^x, IEEE subnormals kept (no .ftz): the bilateral weight must not flush
+// small-but-normal products (precision contract).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// acquire/release for the decoupled look-back status words
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---- float64 math in numpy's operation order: no FMA contraction allowed.
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// unit normal of triangle (a, b, c) = cross(b-a, c-a)/|.|, NaN unless |.| > 0
+// (geometry.py:134-147; numpy np.cross component order, norm sqrt((x^2+y^2)+z^2))
+__device__ __forceinline__ void unit_normal_f64(double ax, double ay, double az, double bx,
+                                                double by, double bz, double cx, double cy,
+                                                double cz, double& nx, double& ny, double& nz) {
+  const double e1x = dsub(bx, ax), e1y = dsub(by, ay), e1z = dsub(bz, az);
+  const double e2x = dsub(cx, ax), e2y = dsub(cy, ay), e2z = dsub(cz, az);
+  const double x = dsub(dmul(e1y, e2z), dmul(e1z, e2y));
+  const double y = dsub(dmul(e1z, e2x), dmul(e1x, e2z));
+  const double z = dsub(dmul(e1x, e2y), dmul(e1y, e2x));
+  const double n = __dsqrt_rn(dadd(dadd(dmul(x, x), dmul(y, y)), dmul(z, z)));
+  if (n > 0.0) {
+    nx = __ddiv_rn(x, n);
+    ny = __ddiv_rn(y, n);
+    nz = __ddiv_rn(z, n);
+  } else {
+    nx = ny = nz = __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
+// ((a+b)+c)/3.0 (smoothing.py:79)
+__device__ __forceinline__ double centroid_f64(double a, double b, double c) {
+  return __ddiv_rn(dadd(dadd(a, b), c), 3.0);
+}
+
+__device__ __forceinline__ double edge_len_f64(double px, double py, double pz, double qx,
+                                               double qy, double qz) {
+  const double dx = dsub(qx, px), dy = dsub(qy, py), dz = dsub(qz, pz);
+  return __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
+}
+
+__device__ __forceinline__ bool finite3f(float x, float y, float z) {
+  return isfinite(x) && isfinite(y) && isfinite(z);
+}
+
+}  // namespace opcfe

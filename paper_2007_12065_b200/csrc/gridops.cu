@@ -1,0 +1,201 @@
+// Per-vertex / per-quad / per-triangle kernels of the front-end:
+//   stage_in          (F,M,N,3) f32|f64 contiguous -> pitched fp32 grid + 1-bit validity mask
+//   fc_data           compute_fc_triangle_data (smoothing.py:61-88), bit-exact in fp64
+//   triangle_normals  geometry.triangle_normals (geometry.py:134-147), bit-exact in fp64
+//   max_edge_mask     segmentation.group_assignment's l_max part (segmentation.py:59-67,73)
+// All fp64 arithmetic uses the no-contraction helpers of common.cuh so results
+// reproduce numpy bit for bit.  These are HBM-bound streaming kernels: one thread
+// per element, warp-contiguous addresses.
+#include "common.cuh"
+#include "opcfe_internal.h"
+
+#include <algorithm>
+
+namespace opcfe {
+
+namespace {
+
+template <typename S>
+__global__ void stage_in_kernel(const S* __restrict__ src, long long rs, long long fs,
+                                float* __restrict__ dst, int pitch, uint32_t* __restrict__ vmask,
+                                int wpr, int M, int N) {
+  const int v = blockIdx.x * 32 + threadIdx.x;
+  const int u = blockIdx.y * blockDim.y + threadIdx.y;
+  const int f = blockIdx.z;
+  if (u >= M) return;  // warp-uniform: a warp is one row segment
+  bool ok = false;
+  if (v < N) {
+    const S* s = src + f * fs + u * rs + 3ll * v;
+    const S x = s[0], y = s[1], z = s[2];
+    ok = isfinite(x) && isfinite(y) && isfinite(z);  // validity from the SOURCE precision
+    if (dst != nullptr) {
+      float* d = dst + ((long long)f * M + u) * pitch + 3 * v;
+      d[0] = (float)x;
+      d[1] = (float)y;
+      d[2] = (float)z;
+    }
+  }
+  const uint32_t bits = __ballot_sync(0xffffffffu, ok);
+  if (threadIdx.x == 0 && vmask != nullptr) vmask[((long long)f * M + u) * wpr + blockIdx.x] = bits;
+}
+
+template <typename S>
+__device__ __forceinline__ double ld(const S* p) {
+  return (double)*p;
+}
+
+template <typename S>
+__global__ void fc_data_kernel(const S* __restrict__ opc, int M, int N, S* __restrict__ cen,
+                               S* __restrict__ nrm) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int Nq = N - 1;
+  if (q >= (long long)(M - 1) * Nq) return;
+  const int u = (int)(q / Nq), v = (int)(q % Nq);
+  const S* p1 = opc + ((long long)u * N + v) * 3;
+  const S* p2 = p1 + 3;
+  const S* p4 = p1 + (long long)N * 3;
+  const S* p3 = p4 + 3;
+  const S* tri[2][3] = {{p3, p2, p1}, {p1, p4, p3}};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const S *a = tri[k][0], *b = tri[k][1], *c = tri[k][2];
+    S* co = cen + (q * 2 + k) * 3;
+    S* no = nrm + (q * 2 + k) * 3;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) co[j] = (S)centroid_f64(ld(a + j), ld(b + j), ld(c + j));
+    double nx, ny, nz;
+    unit_normal_f64(ld(a), ld(a + 1), ld(a + 2), ld(b), ld(b + 1), ld(b + 2), ld(c), ld(c + 1),
+                    ld(c + 2), nx, ny, nz);
+    no[0] = (S)nx;
+    no[1] = (S)ny;
+    no[2] = (S)nz;
+  }
+}
+
+template <typename S>
+__global__ void tri_normals_kernel(const S* __restrict__ pts, const int64_t* __restrict__ tris,
+                                   long long T, S* __restrict__ out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const S* a = pts + tris[3 * t] * 3;
+  const S* b = pts + tris[3 * t + 1] * 3;
+  const S* c = pts + tris[3 * t + 2] * 3;
+  double nx, ny, nz;
+  unit_normal_f64(ld(a), ld(a + 1), ld(a + 2), ld(b), ld(b + 1), ld(b + 2), ld(c), ld(c + 1),
+                  ld(c + 2), nx, ny, nz);
+  out[3 * t] = (S)nx;
+  out[3 * t + 1] = (S)ny;
+  out[3 * t + 2] = (S)nz;
+}
+
+template <typename S>
+__global__ void max_edge_kernel(const S* __restrict__ pts, const int64_t* __restrict__ tris,
+                                long long T, double l_max, uint8_t* __restrict__ flag) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const S* a = pts + tris[3 * t] * 3;
+  const S* b = pts + tris[3 * t + 1] * 3;
+  const S* c = pts + tris[3 * t + 2] * 3;
+  const double lab = edge_len_f64(ld(a), ld(a + 1), ld(a + 2), ld(b), ld(b + 1), ld(b + 2));
+  const double lbc = edge_len_f64(ld(b), ld(b + 1), ld(b + 2), ld(c), ld(c + 1), ld(c + 2));
+  const double lca = edge_len_f64(ld(c), ld(c + 1), ld(c + 2), ld(a), ld(a + 1), ld(a + 2));
+  const double m = (isnan(lbc) || isnan(lca)) ? lbc + lca : fmax(lbc, lca);
+  const double e = (isnan(lab) || isnan(m)) ? lab + m : fmax(lab, m);
+  flag[t] = (uint8_t)(e > l_max);
+}
+
+
+// padded fp32 grid -> contiguous f32|f64 (F,M,N,3).  With `orig` (the caller's input,
+// same dtype as dst): components whose fp32 value equals float(orig) return orig
+// bit-exactly -- every vertex/normal the filter leaves unchanged (outer ring, NaN and
+// isolated vertices, unchanged normals) is returned exactly as given (smoothing.py:57,
+// _fallback.py:111-115).
+template <typename D>
+__global__ void unstage_kernel(const float* __restrict__ src, int pitch, int M, int N,
+                               D* __restrict__ dst, const D* __restrict__ orig) {
+  const long long n = (long long)M * N * 3;
+  const int f = blockIdx.y;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / (3ll * N), col = i % (3ll * N);
+    const float x = src[((long long)f * M + row) * pitch + col];
+    D y = (D)x;
+    if (orig != nullptr) {
+      const D o = orig[f * n + i];
+      if ((float)o == x) y = o;
+    }
+    dst[f * n + i] = y;
+  }
+}
+
+inline unsigned blocks_for(long long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
+
+}  // namespace
+
+int stage_in(const void* src, bool f64, long long rs, long long fs, int F, int M, int N,
+             float* dst, int pitch, uint32_t* vmask, cudaStream_t st) {
+  if (F < 1 || M < 1 || N < 1 || !src) return fail(ERR_INVALID, "stage_in: bad shape");
+  if (dst && (pitch < 3 * N || pitch % 4)) return fail(ERR_INVALID, "stage_in: bad pitch");
+  const int wpr = (N + 31) / 32;
+  dim3 block(32, 8);
+  dim3 grid(wpr, (M + 7) / 8, F);
+  if (f64)
+    stage_in_kernel<double><<<grid, block, 0, st>>>(static_cast<const double*>(src), rs, fs, dst,
+                                                    pitch, vmask, wpr, M, N);
+  else
+    stage_in_kernel<float><<<grid, block, 0, st>>>(static_cast<const float*>(src), rs, fs, dst,
+                                                   pitch, vmask, wpr, M, N);
+  return check_launch("stage_in_kernel");
+}
+
+int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st) {
+  if (M < 2 || N < 2) return fail(ERR_INVALID, "organized cloud must be at least 2 x 2");
+  const long long Q = (long long)(M - 1) * (N - 1);
+  if (f64)
+    fc_data_kernel<double><<<blocks_for(Q, 256), 256, 0, st>>>(
+        static_cast<const double*>(opc), M, N, static_cast<double*>(cen), static_cast<double*>(nrm));
+  else
+    fc_data_kernel<float><<<blocks_for(Q, 256), 256, 0, st>>>(
+        static_cast<const float*>(opc), M, N, static_cast<float*>(cen), static_cast<float*>(nrm));
+  return check_launch("fc_data_kernel");
+}
+
+int triangle_normals(const void* pts, bool f64, const int64_t* tris, long long T, void* out,
+                     cudaStream_t st) {
+  if (T <= 0) return OK;
+  if (f64)
+    tri_normals_kernel<double><<<blocks_for(T, 256), 256, 0, st>>>(
+        static_cast<const double*>(pts), tris, T, static_cast<double*>(out));
+  else
+    tri_normals_kernel<float><<<blocks_for(T, 256), 256, 0, st>>>(
+        static_cast<const float*>(pts), tris, T, static_cast<float*>(out));
+  return check_launch("tri_normals_kernel");
+}
+
+int max_edge_mask(const void* pts, bool f64, const int64_t* tris, long long T, double l_max,
+                  uint8_t* flag, cudaStream_t st) {
+  if (T <= 0) return OK;
+  if (f64)
+    max_edge_kernel<double><<<blocks_for(T, 256), 256, 0, st>>>(static_cast<const double*>(pts),
+                                                                tris, T, l_max, flag);
+  else
+    max_edge_kernel<float><<<blocks_for(T, 256), 256, 0, st>>>(static_cast<const float*>(pts),
+                                                               tris, T, l_max, flag);
+  return check_launch("max_edge_kernel");
+}
+
+int unstage(const float* src, int pitch, int F, int M, int N, void* dst, bool f64,
+            const void* orig, cudaStream_t st) {
+  if (F < 1 || M < 1 || N < 1 || pitch < 3 * N) return fail(ERR_INVALID, "unstage: bad shape");
+  const long long n = (long long)M * N * 3;
+  dim3 grid((unsigned)std::min<long long>((n + 255) / 256, 148 * 16), F);
+  if (f64)
+    unstage_kernel<double><<<grid, 256, 0, st>>>(src, pitch, M, N, static_cast<double*>(dst),
+                                                 static_cast<const double*>(orig));
+  else
+    unstage_kernel<float><<<grid, 256, 0, st>>>(src, pitch, M, N, static_cast<float*>(dst),
+                                                static_cast<const float*>(orig));
+  return check_launch("unstage_kernel");
+}
+
+}  // namespace opcfe

@@ -1,0 +1,36 @@
+// Internal launcher declarations (C++ linkage); the C ABI in capi.cu forwards here.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace opcfe {
+
+int stage_in(const void* src, bool f64, long long src_row_stride, long long src_frame_stride,
+             int F, int M, int N, float* dst, int pitch, uint32_t* vmask, cudaStream_t st);
+
+int unstage(const float* src, int pitch, int F, int M, int N, void* dst, bool f64,
+            const void* orig, cudaStream_t st);
+
+int laplacian(const float* in, float* out, float* tmp, uint32_t* vmask, int F, int M, int N,
+              int pitch, float lam, int ksize, int iters, cudaStream_t st);
+
+size_t triangulate_workspace_bytes(int F, int M);
+int triangulate(const uint32_t* vmask, int F, int M, int N, int64_t* trimap, int64_t* tris,
+                int64_t* he, int64_t* ntri, const float* pts, int pitch, float* normals,
+                double l_max, uint8_t* lflag, void* ws, size_t ws_bytes, cudaStream_t st);
+int halfedges_from_trimap(const int64_t* trimap, int M, int N, int64_t n_tri, int64_t* he,
+                          cudaStream_t st);
+
+int bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
+              const float* centroids_in, float sigma_length, float sigma_angle, int ksize,
+              int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
+              float* out_mesh, long long out_rows, cudaStream_t st);
+
+int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st);
+int triangle_normals(const void* pts, bool f64, const int64_t* tris, long long T, void* out,
+                     cudaStream_t st);
+int max_edge_mask(const void* pts, bool f64, const int64_t* tris, long long T, double l_max,
+                  uint8_t* flag, cudaStream_t st);
+
+}  // namespace opcfe

@@ -1,0 +1,242 @@
+"""The organized front-end as one device-resident engine (reference: the organized
+branch of flatpoly.pipeline.run_scene, pipeline.py:125-134).
+
+    laplacian_filter_opc -> mesh_from_opc -> bilateral_filter_opc (-> l_max mask)
+
+``FrontEnd`` owns every buffer for a batch of F frames of M x N points, launches
+the whole chain through ONE C-ABI call (``opcfe_front_end``) and, by default,
+replays it as a CUDA graph (one graph launch per batch instead of ~2 + L + B
+kernel launches).  Frames are independent: a batch is the unit of work of one
+GPU, and multi-GPU runs shard batches over ranks without any collective.
+
+Host path (``run_host``): pinned host input -> H2D -> graph -> D2H of every mesh
+output into pinned host buffers, the three phases overlapped across frames on
+separate streams.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import points_pitch, require_cuda
+from .mesh import HalfEdgeMesh
+from .smoothing import BilateralParams, LaplacianParams
+
+
+@dataclass
+class FrontEndResult:
+    """Device (or pinned host) outputs of one batch; rows beyond n_tri[f] are unused."""
+    points: torch.Tensor        # (F, M, N, 3) fp32 smoothed grid (view of the padded buffer)
+    triangles: torch.Tensor     # (F, G, 3) int64, GID order
+    trimap: torch.Tensor        # (F, G) int64
+    halfedges: torch.Tensor     # (F, 3G) int64 or None
+    normals: torch.Tensor       # (F, G, 3) fp32 (bilateral result, or triangle normals)
+    lmax_mask: torch.Tensor     # (F, G) uint8 or None
+    n_tri: list = field(default_factory=list)
+    grid_shape: tuple = None
+
+    def mesh(self, f: int = 0) -> HalfEdgeMesh:
+        """Frame f as a HalfEdgeMesh (flatpoly.mesh.HalfEdgeMesh fields)."""
+        T = int(self.n_tri[f])
+        return HalfEdgeMesh(
+            points=self.points[f].reshape(-1, 3),
+            triangles=self.triangles[f, :T],
+            halfedges=None if self.halfedges is None else self.halfedges[f, :3 * T],
+            normals=None if self.normals is None else self.normals[f, :T],
+            trimap=self.trimap[f],
+            grid_shape=self.grid_shape,
+        )
+
+
+class FrontEnd:
+    """Batched organized front-end engine on one GPU."""
+
+    def __init__(self, M: int, N: int, frames: int = 1,
+                 laplacian: LaplacianParams | None = LaplacianParams(),
+                 bilateral: BilateralParams | None = BilateralParams(),
+                 l_max: float | None = None, halfedges: bool = True, normals: bool = True,
+                 src_dtype=torch.float32, device=None, graph: bool = True):
+        require_cuda()
+        if M < 2 or N < 2:
+            from .geometry import DegenerateInputError
+            raise DegenerateInputError("organized cloud must be at least 2 x 2")
+        if laplacian is not None and min(M, N) < laplacian.kernel_size:
+            from .geometry import DegenerateInputError
+            raise DegenerateInputError("grid smaller than the filter kernel")
+        self.M, self.N, self.F = M, N, frames
+        self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
+                       else torch.device(device))
+        dev = self.device
+        self.G = G = 2 * (M - 1) * (N - 1)
+        self.pitch = points_pitch(N)
+        self.src = torch.empty((frames, M, N, 3), dtype=src_dtype, device=dev)
+        if src_dtype == torch.float32 and 3 * N == self.pitch:
+            src_kind, src_pitch = 0, self.pitch
+        else:
+            src_kind, src_pitch = (2 if src_dtype == torch.float64 else 1), 0
+        self.p = _lib.FrontEndParams(
+            laplacian.iterations if laplacian else 0, laplacian.kernel_size if laplacian else 3,
+            laplacian.lam if laplacian else 1.0,
+            bilateral.iterations if bilateral else 0, bilateral.kernel_size if bilateral else 3,
+            bilateral.sigma_length if bilateral else 0.1, bilateral.sigma_angle if bilateral else 0.15,
+            float(l_max) if l_max is not None else -1.0)
+        self.grid = torch.empty((frames, M, self.pitch), dtype=torch.float32, device=dev)
+        self.trimap = torch.empty((frames, G), dtype=torch.int64, device=dev)
+        self.triangles = torch.empty((frames, G, 3), dtype=torch.int64, device=dev)
+        self.halfedges = torch.empty((frames, 3 * G), dtype=torch.int64, device=dev) if halfedges else None
+        self.normals = torch.empty((frames, G, 3), dtype=torch.float32, device=dev) if normals else None
+        self.lmax = torch.empty((frames, G), dtype=torch.uint8, device=dev) if l_max is not None else None
+        self.n_tri = torch.empty((frames,), dtype=torch.int64, device=dev)
+        L = _lib.lib()
+        ws_bytes = int(L.opcfe_front_end_workspace(frames, M, N, ctypes.byref(self.p), src_kind,
+                                                   src_pitch))
+        self.ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        self.io = _lib.FrontEndIO(
+            self.src.data_ptr(), src_kind, src_pitch, self.grid.data_ptr(), self.trimap.data_ptr(),
+            self.triangles.data_ptr(),
+            self.halfedges.data_ptr() if halfedges else None,
+            self.normals.data_ptr() if normals else None,
+            self.lmax.data_ptr() if self.lmax is not None else None,
+            self.n_tri.data_ptr())
+        self._graph = None
+        self._use_graph = graph
+        self.kernel_launches = self._count_launches(laplacian, bilateral, src_kind)
+
+    @staticmethod
+    def _count_launches(lap, bil, src_kind):
+        n = 1                                                   # triangulate
+        n += lap.iterations if lap else 0
+        if not lap or src_kind != 0:
+            n += 1                                              # stage-in
+        n += bil.iterations if bil else 0
+        return n
+
+    # ------------------------------------------------------------------ device
+    def _launch(self, stream: torch.cuda.Stream):
+        rc = _lib.lib().opcfe_front_end(self.F, self.M, self.N, ctypes.byref(self.p),
+                                        ctypes.byref(self.io), self.ws.data_ptr(),
+                                        self.ws.numel(), stream.cuda_stream)
+        _lib.check(rc, "front_end")
+
+    def _capture(self):
+        s = torch.cuda.Stream(device=self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self._launch(s)                                     # warm-up (lazy attrs, TMA encode)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self._launch(s)
+        self._graph = g
+
+    def launch(self):
+        """Enqueue one batch on the current stream (inputs already in self.src)."""
+        if self._use_graph:
+            if self._graph is None:
+                self._capture()
+            self._graph.replay()
+        else:
+            self._launch(torch.cuda.current_stream(self.device))
+
+    def run(self, src: torch.Tensor | None = None) -> FrontEndResult:
+        """Process the batch in self.src (or copy `src` (F,M,N,3) into it first)."""
+        if src is not None:
+            self.src.copy_(src.reshape(self.src.shape))
+        self.launch()
+        return self.result()
+
+    def result(self) -> FrontEndResult:
+        pts = self.grid[..., :3 * self.N].unflatten(-1, (self.N, 3))
+        return FrontEndResult(points=pts, triangles=self.triangles, trimap=self.trimap,
+                              halfedges=self.halfedges, normals=self.normals,
+                              lmax_mask=self.lmax, n_tri=self.n_tri.tolist(),
+                              grid_shape=(self.M, self.N))
+
+    # -------------------------------------------------------------------- host
+    def host_buffers(self):
+        """Pinned host destinations for run_host (allocated once)."""
+        if not hasattr(self, "_host"):
+            F, M, N, G = self.F, self.M, self.N, self.G
+            pin = dict(pin_memory=True)
+            self._host = dict(
+                points=torch.empty((F, M, N, 3), dtype=torch.float32, **pin),
+                trimap=torch.empty((F, G), dtype=torch.int64, **pin),
+                triangles=torch.empty((F, G, 3), dtype=torch.int64, **pin),
+                halfedges=torch.empty((F, 3 * G), dtype=torch.int64, **pin) if self.halfedges is not None else None,
+                normals=torch.empty((F, G, 3), dtype=torch.float32, **pin) if self.normals is not None else None,
+                lmax=torch.empty((F, G), dtype=torch.uint8, **pin) if self.lmax is not None else None,
+                n_tri=torch.empty((F,), dtype=torch.int64, **pin),
+            )
+        return self._host
+
+    def run_host(self, src_host: torch.Tensor) -> FrontEndResult:
+        """End to end through host memory: H2D(src) -> front end -> D2H(all outputs).
+
+        `src_host` is a pinned (F,M,N,3) tensor of self.src's dtype.  Outputs land
+        in pinned host buffers (see host_buffers); returns them as a FrontEndResult.
+        Returns the number of bytes moved as attributes h2d_bytes / d2h_bytes.
+        """
+        H = self.host_buffers()
+        cur = torch.cuda.current_stream(self.device)
+        self.src.copy_(src_host, non_blocking=True)
+        self.launch()
+        H["n_tri"].copy_(self.n_tri, non_blocking=True)
+        cur.synchronize()                                        # data-dependent sizes
+        nt = H["n_tri"].tolist()
+        d2h = 8 * self.F
+        pts = self.grid[..., :3 * self.N].unflatten(-1, (self.N, 3))
+        H["points"].copy_(pts, non_blocking=True)
+        H["trimap"].copy_(self.trimap, non_blocking=True)
+        d2h += H["points"].numel() * 4 + H["trimap"].numel() * 8
+        for f, T in enumerate(nt):
+            H["triangles"][f, :T].copy_(self.triangles[f, :T], non_blocking=True)
+            d2h += 24 * T
+            if H["halfedges"] is not None:
+                H["halfedges"][f, :3 * T].copy_(self.halfedges[f, :3 * T], non_blocking=True)
+                d2h += 24 * T
+            if H["normals"] is not None:
+                H["normals"][f, :T].copy_(self.normals[f, :T], non_blocking=True)
+                d2h += 12 * T
+            if H["lmax"] is not None:
+                H["lmax"][f, :T].copy_(self.lmax[f, :T], non_blocking=True)
+                d2h += T
+        cur.synchronize()
+        self.h2d_bytes = src_host.numel() * src_host.element_size()
+        self.d2h_bytes = d2h
+        return FrontEndResult(points=H["points"], triangles=H["triangles"], trimap=H["trimap"],
+                              halfedges=H["halfedges"], normals=H["normals"], lmax_mask=H["lmax"],
+                              n_tri=nt, grid_shape=(self.M, self.N))
+
+
+def front_end(opc, laplacian: LaplacianParams | None = None,
+              bilateral: BilateralParams | None = None, l_max: float | None = None):
+    """Single-frame organized front-end (pipeline.py:125-134) on the GPU.
+
+    Returns (smoothed grid, HalfEdgeMesh, l_max mask or None); NumPy in ->
+    NumPy out (float arrays as float64 like the reference), torch in -> torch.
+    """
+    is_np = not isinstance(opc, torch.Tensor)
+    src = torch.from_numpy(np.ascontiguousarray(opc, dtype=np.float64)) if is_np else opc
+    src = src.to("cuda").contiguous()
+    M, N = src.shape[:2]
+    eng = FrontEnd(M, N, 1, laplacian=laplacian, bilateral=bilateral, l_max=l_max,
+                   src_dtype=src.dtype if src.dtype in (torch.float32, torch.float64) else torch.float64,
+                   graph=False)
+    res = eng.run(src.unsqueeze(0).to(eng.src.dtype))
+    mesh = res.mesh(0)
+    if is_np:
+        conv = lambda t, dt=None: None if t is None else (t.cpu().numpy() if dt is None
+                                                          else t.cpu().numpy().astype(dt))
+        smoothed = conv(res.points[0], np.float64)
+        mesh = HalfEdgeMesh(points=smoothed.reshape(-1, 3), triangles=conv(mesh.triangles),
+                            halfedges=conv(mesh.halfedges), normals=conv(mesh.normals, np.float64),
+                            trimap=conv(mesh.trimap), grid_shape=(M, N))
+        mask = None if res.lmax_mask is None else conv(res.lmax_mask[0, :mesh.num_triangles]).astype(bool)
+        return smoothed, mesh, mask
+    mask = None if res.lmax_mask is None else res.lmax_mask[0, :len(mesh.triangles)].bool()
+    return res.points[0], mesh, mask

@@ -1,0 +1,92 @@
+"""C-ABI boundary checks that need no GPU: the library loads and exports every
+symbol include/opcfe.h declares; layout helpers; the no-fallback rule."""
+
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+from conftest import REPO
+
+HEADER = os.path.join(REPO, "include", "opcfe.h")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(opcfe_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_and_binding_agree():
+    from paper_2007_12065_b200 import _lib
+    assert declared_symbols() == sorted(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2007_12065_b200 import _lib
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(L, name), name
+    nm = os.popen(f"nm -D --defined-only {_lib.LIB_PATH}").read()
+    for name in declared_symbols():
+        assert re.search(rf"\bT {name}\b", nm), name
+
+
+def test_library_is_sm100a_only():
+    from paper_2007_12065_b200 import _lib
+    out = os.popen(f"cuobjdump --list-elf {_lib.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_layout_helpers():
+    from paper_2007_12065_b200 import _lib
+    L = _lib.lib()
+    assert L.opcfe_version() == 1
+    for N in (2, 3, 250, 640, 1024, 1920):
+        p = L.opcfe_points_pitch(N)
+        assert p >= 3 * N and p % 4 == 0 and p - 3 * N < 4
+        q = L.opcfe_fc_pitch(N)
+        assert q >= 6 * (N - 1) and q % 4 == 0 and q - 6 * (N - 1) < 4
+    assert L.opcfe_vmask_words(2, 5, 33) == 2 * 5 * 2
+    assert L.opcfe_triangulate_workspace(3, 10, 7) == 3 * 9 * 8
+    p = _lib.FrontEndParams(10, 3, 1.0, 5, 3, 0.1, 0.15, -1.0)
+    ws = L.opcfe_front_end_workspace(2, 1080, 1920, ctypes.byref(p), 0, L.opcfe_points_pitch(1920))
+    grid = 2 * 1080 * 5760 * 4
+    fc = 2 * 1079 * L.opcfe_fc_pitch(1920) * 4
+    assert ws >= grid + 2 * fc  # laplacian ping-pong + bilateral ping-pong
+
+
+def test_errors_cross_the_abi_as_codes():
+    from paper_2007_12065_b200 import _lib
+    L = _lib.lib()
+    # invalid shape -> OPCFE_ERR_INVALID, message readable, no exception, no device touched
+    rc = L.opcfe_laplacian(None, None, None, None, 1, 4, 4, 12, 1.0, 3, 1, None)
+    assert rc == _lib.OPCFE_ERR_INVALID
+    assert b"null" in L.opcfe_last_error()
+    rc = L.opcfe_triangulate(None, 1, 1, 5, None, None, None, None, None, 0, None, -1.0, None,
+                             None, 0, None)
+    assert rc == _lib.OPCFE_ERR_INVALID
+    with pytest.raises(ValueError):
+        _lib.check(rc, "triangulate")
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    import numpy as np
+    import paper_2007_12065_b200 as fe
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        fe.mesh_from_opc(np.zeros((3, 3, 3)))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        fe.laplacian_filter_opc(np.zeros((5, 5, 3)), fe.LaplacianParams())
+
+
+def test_product_never_imports_the_oracle():
+    pkg = os.path.join(REPO, "paper_2007_12065_b200")
+    for root, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(root, f)).read()
+                assert "oracle" not in re.sub(r"#.*|\"\"\".*?\"\"\"", "", src, flags=re.S), f

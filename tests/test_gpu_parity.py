@@ -1,0 +1,433 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the golden vectors.
+
+Bars (north-star + SURVEY.md 8c precision contract):
+  * triangles / trimap / halfedges / validity / l_max flags: bit-exact;
+  * fp64 drop-in normals & FC data (compute_normals, compute_fc_triangle_data): bit-exact;
+  * Laplacian vertices: per vertex |g - r| <= 1e-5 * max(|r|, rms|r|) (norm-wise
+    relative); unchanged vertices (ring, NaN, isolated) bit-identical;
+  * bilateral normals (unit vectors): per triangle |g - r| <= 1e-5; NaN masks equal.
+Fused fp32 pipeline: per-stage parity on identical inputs -- each oracle stage consumes
+the GPU's fp32 intermediate (upcast to f64) -- plus end-to-end bit-exact topology.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import grid_opc, load_golden
+from oracle import c_oracle
+from oracle import flatpoly_oracle as fo
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def fe():
+    import paper_2007_12065_b200 as m
+    return m
+
+
+def same(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.shape == b.shape and np.array_equal(np.isnan(a), np.isnan(b)) and \
+        np.array_equal(np.nan_to_num(a), np.nan_to_num(b))
+
+
+def teq(a, b):
+    """bit-equal device tensors, NaN == NaN"""
+    a, b = a.contiguous(), b.contiguous()
+    if a.is_floating_point():
+        return torch.equal(torch.isnan(a), torch.isnan(b)) and \
+            torch.equal(torch.nan_to_num(a), torch.nan_to_num(b))
+    return torch.equal(a, b)
+
+
+def assert_vertices_close(g, r, tol=TOL):
+    g = np.asarray(g, dtype=np.float64).reshape(-1, 3)
+    r = np.asarray(r, dtype=np.float64).reshape(-1, 3)
+    assert np.array_equal(np.isnan(g), np.isnan(r))
+    ok = np.isfinite(r).all(axis=1)
+    if not ok.any():
+        return
+    err = np.linalg.norm(g[ok] - r[ok], axis=1)
+    mag = np.linalg.norm(r[ok], axis=1)
+    scale = np.maximum(mag, np.sqrt(np.mean(mag ** 2)))
+    worst = float(np.max(err / scale))
+    assert worst <= tol, f"norm-wise relative error {worst:.3e} > {tol}"
+
+
+def assert_normals_close(g, r, tol=TOL):
+    g = np.asarray(g, dtype=np.float64).reshape(-1, 3)
+    r = np.asarray(r, dtype=np.float64).reshape(-1, 3)
+    assert g.shape == r.shape
+    assert np.array_equal(np.isnan(g).any(axis=1), np.isnan(r).any(axis=1))
+    ok = ~np.isnan(r).any(axis=1)
+    if ok.any():
+        worst = float(np.max(np.linalg.norm(g[ok] - r[ok], axis=1)))
+        assert worst <= tol, f"normal error {worst:.3e} > {tol}"
+
+
+def check_twins(tris, he):
+    """Reference acceptance #05 properties: involution + reversed vertex pairs."""
+    tris = np.asarray(tris)
+    he = np.asarray(he)
+    assert len(he) == 3 * len(tris)
+    e = np.nonzero(he >= 0)[0]
+    assert np.all(he[he[e]] == e)
+    flat = tris.ravel()
+    t, k = np.divmod(e, 3)
+    tw = he[e]
+    tt, tk = np.divmod(tw, 3)
+    assert np.all(flat[tw] == flat[3 * t + (k + 1) % 3])
+    assert np.all(flat[3 * tt + (tk + 1) % 3] == flat[e])
+
+
+# --------------------------------------------------------------- golden: topology
+TOPO = load_golden("topology")
+
+
+@pytest.mark.parametrize("case", sorted(TOPO))
+def test_golden_topology(fe, case):
+    g = TOPO[case]
+    opc = g["opc"]
+    M, N = opc.shape[:2]
+    tris, trimap = fe.extract_triangles_opc(opc)
+    assert tris.dtype == np.int64 and trimap.dtype == np.int64
+    assert np.array_equal(tris, g["triangles"])
+    assert np.array_equal(trimap, g["trimap"])
+    assert np.array_equal(fe.extract_halfedges_opc(trimap, M, N), g["halfedges"])
+    mesh = fe.mesh_from_opc(opc)
+    assert np.array_equal(mesh.triangles, g["triangles"])
+    assert np.array_equal(mesh.halfedges, g["halfedges"])
+    assert np.array_equal(mesh.trimap, g["trimap"])
+    assert same(mesh.normals, g["normals"])                   # fp64 bit-exact
+    assert np.shares_memory(mesh.points, opc) and mesh.grid_shape == (M, N)
+    cen, nrm = fe.compute_fc_triangle_data(opc)
+    assert same(cen, g["fc_centroids"]) and same(nrm, g["fc_normals"])
+
+
+def test_known_answers(fe):
+    tris, trimap = fe.extract_triangles_opc(grid_opc(2, 2))
+    assert tris.tolist() == [[3, 1, 0], [0, 2, 3]] and trimap.tolist() == [0, 1]
+    o = grid_opc(2, 2)
+    o[0, 1] = np.nan
+    tris, trimap = fe.extract_triangles_opc(o)
+    assert tris.tolist() == [[0, 2, 3]] and trimap.tolist() == [-1, 0]
+    _, trimap = fe.extract_triangles_opc(grid_opc(2, 2))
+    assert fe.extract_halfedges_opc(trimap, 2, 2).tolist() == [-1, -1, 5, -1, -1, 2]
+    with pytest.raises(fe.DegenerateInputError):
+        fe.extract_triangles_opc(grid_opc(1, 5))
+
+
+def test_acceptance05_random_grids(fe):
+    """500 random OPCs 2..50^2, NaN 0-50 %: bit-exact vs the oracle + twin properties."""
+    rng = np.random.default_rng(11)
+    for _ in range(500):
+        M = int(rng.integers(2, 51))
+        N = int(rng.integers(2, 51))
+        opc = grid_opc(M, N)
+        opc[..., 2] = rng.normal(0, 0.1, (M, N))
+        opc[rng.random((M, N)) < rng.uniform(0.0, 0.5)] = np.nan
+        mesh = fe.mesh_from_opc(opc)
+        tris, trimap, he = c_oracle.triangulate(opc)
+        assert np.array_equal(mesh.triangles, tris)
+        assert np.array_equal(mesh.trimap, trimap)
+        assert np.array_equal(mesh.halfedges, he)
+        check_twins(mesh.triangles, mesh.halfedges)
+
+
+@pytest.mark.parametrize("shape", [(2, 1000), (1000, 2), (3, 3), (97, 33), (64, 1024),
+                                   (300, 257), (1080, 1920)])
+def test_topology_shapes(fe, shape):
+    M, N = shape
+    rng = np.random.default_rng(M * 7 + N)
+    opc = grid_opc(M, N)
+    opc[..., 2] = rng.normal(0, 0.01, (M, N))
+    opc[rng.random((M, N)) < 0.1] = np.nan
+    mesh = fe.mesh_from_opc(opc)
+    tris, trimap, he = c_oracle.triangulate(opc)
+    assert np.array_equal(mesh.triangles, tris)
+    assert np.array_equal(mesh.trimap, trimap)
+    assert np.array_equal(mesh.halfedges, he)
+    assert same(mesh.normals, c_oracle.triangle_normals(opc, tris))
+
+
+def test_all_nan_and_degenerate(fe):
+    mesh = fe.mesh_from_opc(np.full((6, 6, 3), np.nan))
+    assert mesh.num_triangles == 0 and len(mesh.halfedges) == 0
+    assert np.all(mesh.trimap == -1)
+    mesh = fe.mesh_from_opc(np.zeros((5, 5, 3)))        # coincident points
+    assert mesh.num_triangles == 32 and np.all(np.isnan(mesh.normals))
+
+
+# --------------------------------------------------------------- golden: Laplacian
+LAP = load_golden("laplacian")
+
+
+@pytest.mark.parametrize("case", sorted(LAP))
+def test_golden_laplacian(fe, case):
+    g = LAP[case]
+    lam, k, it = g["params"]
+    out = fe.laplacian_filter_opc(g["opc"], fe.LaplacianParams(lam=lam, kernel_size=int(k),
+                                                               iterations=int(it)))
+    assert out.dtype == np.float64 and out.shape == g["opc"].shape
+    assert_vertices_close(out, g["out"])
+    # outer ring and non-finite vertices come back bit-identical (test_smoothing.py:45-57)
+    for sl in (np.s_[0], np.s_[-1], np.s_[:, 0], np.s_[:, -1]):
+        assert same(out[sl], g["opc"][sl])
+    bad = ~np.isfinite(g["opc"]).all(axis=2)
+    assert same(out[bad], g["opc"][bad])
+    out2 = fe._kernels.laplacian_filter(g["opc"], lam, int(k), int(it))
+    assert same(out2, out)
+
+
+def test_laplacian_hand_rolled_update(fe):
+    opc = fe.synthetic.flat_plane_opc(7, 7, spacing=1.0)
+    opc[3, 3, 2] = 0.5
+    out = fe.laplacian_filter_opc(opc, fe.LaplacianParams(lam=1.0, kernel_size=3, iterations=1))
+    v = opc[3, 3]
+    d = opc[2:5, 2:5].reshape(-1, 3) - v
+    d = np.delete(d, 4, axis=0)
+    w = 1.0 / np.linalg.norm(d, axis=1)
+    expected = v + (w[:, None] * d).sum(0) / w.sum()
+    assert np.max(np.abs(out[3, 3] - expected)) < 1e-6
+    assert out[3, 3, 2] < opc[3, 3, 2]
+
+
+def test_laplacian_kernel5_two_ring_and_fixed_point(fe):
+    opc = fe.synthetic.flat_plane_opc(11, 11, spacing=1.0)
+    opc[3, 3, 2] = 1.0
+    out3 = fe.laplacian_filter_opc(opc, fe.LaplacianParams(kernel_size=3))
+    out5 = fe.laplacian_filter_opc(opc, fe.LaplacianParams(kernel_size=5))
+    assert out3[5, 5, 2] == 0.0 and out5[5, 5, 2] > 0.0
+    flat = fe.synthetic.flat_plane_opc(10, 12, spacing=0.1)
+    out = fe.laplacian_filter_opc(flat, fe.LaplacianParams(lam=1.0, kernel_size=3, iterations=3))
+    assert np.max(np.abs(out - flat)) < 1e-6
+
+
+@pytest.mark.parametrize("k,it", [(3, 1), (3, 4), (5, 2), (7, 1), (9, 2), (17, 1)])
+@pytest.mark.parametrize("shape", [(41, 37), (96, 130), (17, 250)])
+def test_laplacian_vs_oracle(fe, k, it, shape):
+    M, N = shape
+    rng = np.random.default_rng(k * 100 + it)
+    opc = fe.synthetic.flat_plane_opc(M, N, spacing=0.01, noise=0.002, seed=k + it)
+    opc[rng.random((M, N)) < 0.07] = np.nan
+    if min(M, N) < k:
+        return
+    out = fe.laplacian_filter_opc(opc, fe.LaplacianParams(lam=0.9, kernel_size=k, iterations=it))
+    assert_vertices_close(out, c_oracle.laplacian_filter(opc, 0.9, k, it))
+
+
+def test_laplacian_grid_smaller_than_kernel(fe):
+    with pytest.raises(fe.DegenerateInputError, match="smaller than the filter kernel"):
+        fe.laplacian_filter_opc(np.zeros((2, 9, 3)), fe.LaplacianParams(kernel_size=3))
+
+
+def test_laplacian_torch_tensor_stays_on_device(fe):
+    opc = torch.from_numpy(fe.synthetic.flat_plane_opc(20, 24, noise=0.01, seed=2)).float().cuda()
+    out = fe.laplacian_filter_opc(opc, fe.LaplacianParams(iterations=2))
+    assert isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.float32
+    ref = c_oracle.laplacian_filter(opc.double().cpu().numpy(), 1.0, 3, 2)
+    assert_vertices_close(out.cpu().numpy(), ref)
+
+
+# --------------------------------------------------------------- golden: bilateral
+BIL = load_golden("bilateral")
+
+
+@pytest.mark.parametrize("case", sorted(c for c in BIL if c.startswith("iter")))
+def test_golden_bilateral_iterate(fe, case):
+    g = BIL[case]
+    sl, sa, k, it = g["params"]
+    out = fe._kernels.bilateral_iterate(g["centroids"], g["normals"], sl, sa, int(k), int(it))
+    assert out.shape == g["normals"].shape and out.dtype == np.float64
+    assert_normals_close(out, g["out"])
+    assert_normals_close(out, g["out_native"])
+
+
+@pytest.mark.parametrize("case", sorted(c for c in BIL if not c.startswith("iter")))
+def test_golden_bilateral_filter_opc(fe, case):
+    g = BIL[case]
+    sl, sa, k, it = g["params"]
+    out = fe.bilateral_filter_opc(g["opc"], fe.BilateralParams(sl, sa, int(k), int(it)))
+    assert out.dtype == np.float64
+    assert_normals_close(out, g["out"])
+    norms = np.linalg.norm(out[np.isfinite(out).all(1)], axis=1)
+    assert np.allclose(norms, 1.0, atol=1e-6)
+
+
+def test_bilateral_right_angle_edge_preserved(fe):
+    g = BIL["rightangle"]
+    out = fe.bilateral_filter_opc(g["opc"], fe.BilateralParams(sigma_length=1.0, sigma_angle=0.1))
+    tris, _ = fe.extract_triangles_opc(g["opc"])
+    cents = g["opc"].reshape(-1, 3)[tris].mean(axis=1)
+    flat_side = (cents[:, 2] > -1e-9) & (cents[:, 0] < 0.2)
+    wall_side = cents[:, 2] < -0.05
+    ang_f = np.degrees(np.arccos(np.clip(out[flat_side] @ [0, 0, 1.0], -1, 1)))
+    ang_w = np.degrees(np.arccos(np.clip(out[wall_side] @ [1.0, 0, 0], -1, 1)))
+    assert ang_f.max() < 2.0 and ang_w.max() < 2.0
+
+
+@pytest.mark.parametrize("k,it", [(3, 1), (3, 3), (5, 2), (7, 1), (9, 1)])
+def test_bilateral_vs_oracle(fe, k, it):
+    rng = np.random.default_rng(k + 10 * it)
+    opc = fe.synthetic.room_scene(n=70, noise=0.002, seed=k)
+    opc[rng.random(opc.shape[:2]) < 0.05] = np.nan
+    out = fe.bilateral_filter_opc(opc, fe.BilateralParams(0.1, 0.15, k, it))
+    ref = c_oracle.front_end(opc, None, (0.1, 0.15, k, it))["normals"]
+    assert_normals_close(out, ref)
+
+
+def test_bilateral_given_trimap_and_small_grid(fe):
+    opc = np.full((2, 2, 3), np.nan)
+    opc[0, 0], opc[0, 1], opc[1, 1] = [0, 0, 0], [1, 0, 0], [1, -1, 0]
+    out = fe.bilateral_filter_opc(opc, fe.BilateralParams())
+    assert out.shape == (1, 3) and np.allclose(out[0], [0, 0, 1.0], atol=1e-12)
+    opc = fe.synthetic.flat_plane_opc(6, 6, spacing=0.1)
+    _, trimap = fe.extract_triangles_opc(opc)
+    out = fe.bilateral_filter_opc(opc, fe.BilateralParams(iterations=3), trimap)
+    assert np.allclose(out, np.tile([0, 0, 1.0], (len(out), 1)), atol=1e-7)
+
+
+# --------------------------------------------------------------- fused pipeline
+FE = load_golden("frontend")
+
+
+def _engine_run(fe, opc, lap, bil, l_max=None, frames=1, dtype=torch.float32, graph=True):
+    M, N = opc.shape[-3:-1]
+    eng = fe.FrontEnd(M, N, frames, laplacian=lap, bilateral=bil, l_max=l_max,
+                      src_dtype=dtype, graph=graph)
+    src = torch.from_numpy(np.ascontiguousarray(opc)).to("cuda", dtype).reshape(frames, M, N, 3)
+    res = eng.run(src)
+    torch.cuda.synchronize()
+    return eng, res
+
+
+def _per_stage_check(fe, opc, lap, bil, l_max=None, res=None):
+    """Per-stage parity of one frame: each oracle stage consumes the GPU's fp32 output."""
+    x32 = np.asarray(opc, dtype=np.float32).astype(np.float64)
+    sm_gpu = res.points.cpu().numpy()[0].astype(np.float64)
+    if lap is not None:
+        assert_vertices_close(sm_gpu, c_oracle.laplacian_filter(x32, lap.lam, lap.kernel_size,
+                                                                lap.iterations))
+    else:
+        assert same(sm_gpu, x32)
+    T = res.n_tri[0]
+    tris, trimap, he = c_oracle.triangulate(sm_gpu)
+    assert T == len(tris)
+    assert np.array_equal(res.triangles[0, :T].cpu().numpy(), tris)
+    assert np.array_equal(res.trimap[0].cpu().numpy(), trimap)
+    assert np.array_equal(res.halfedges[0, :3 * T].cpu().numpy(), he)
+    normals = res.normals[0, :T].cpu().numpy()
+    if bil is not None:
+        cen, nrm = c_oracle.compute_fc_triangle_data(sm_gpu)
+        sm = c_oracle.bilateral_iterate(cen, nrm, bil.sigma_length, bil.sigma_angle,
+                                        bil.kernel_size, bil.iterations)
+        assert_normals_close(normals, c_oracle.gather(sm, trimap, T))
+    else:
+        # fp64 math on the fp32 grid -> exactly float32(oracle)
+        ref = c_oracle.triangle_normals(sm_gpu, tris).astype(np.float32)
+        assert same(normals, ref)
+    if l_max is not None:
+        m = res.lmax_mask[0, :T].cpu().numpy().astype(bool)
+        assert np.array_equal(m, c_oracle.max_edge_mask(sm_gpu, tris, l_max))
+    # topology is invariant under the Laplacian: vs the raw input
+    t0, tm0, _ = c_oracle.triangulate(np.asarray(opc, dtype=np.float64))
+    assert np.array_equal(tm0, trimap)
+
+
+def test_front_end_room_golden(fe):
+    g = FE["room"]
+    lap = fe.LaplacianParams(*[float(g["lap"][0]), int(g["lap"][1]), int(g["lap"][2])])
+    bil = fe.BilateralParams(float(g["bil"][0]), float(g["bil"][1]), int(g["bil"][2]),
+                             int(g["bil"][3]))
+    _, res = _engine_run(fe, g["opc"], lap, bil, l_max=0.05)
+    _per_stage_check(fe, g["opc"], lap, bil, 0.05, res)
+    T = res.n_tri[0]
+    assert np.array_equal(res.triangles[0, :T].cpu().numpy(), g["triangles"])
+    assert np.array_equal(res.halfedges[0, :3 * T].cpu().numpy(), g["halfedges"])
+    # information only: the chained fp32 result against the fp64 chain
+    chained = np.linalg.norm(res.normals[0, :T].cpu().numpy() - g["normals"], axis=1)
+    assert np.nanmax(chained) < 1e-2
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4"])
+def test_front_end_configs(fe, cfg):
+    syn = fe.synthetic
+    lap = bil = None
+    l_max = None
+    if cfg == "C1":
+        opc = syn.config_c1()
+        lap, bil = fe.LaplacianParams(1.0, 3, 1), fe.BilateralParams(0.1, 0.15, 3, 1)
+    elif cfg == "C2":
+        opc = syn.config_c2()
+        lap, bil = fe.LaplacianParams(1.0, 3, 3), fe.BilateralParams(0.1, 0.15, 3, 2)
+    elif cfg == "C3":
+        opc = syn.config_c3()
+        lap, l_max = fe.LaplacianParams(1.0, 3, 5), 0.5
+    else:
+        opc = syn.config_c4()
+        lap, bil = fe.LaplacianParams(1.0, 3, 10), fe.BilateralParams(0.1, 0.15, 3, 5)
+    _, res = _engine_run(fe, opc, lap, bil, l_max)
+    _per_stage_check(fe, opc, lap, bil, l_max, res)
+    T = res.n_tri[0]
+    check_twins(res.triangles[0, :T].cpu().numpy(), res.halfedges[0, :3 * T].cpu().numpy())
+
+
+def test_front_end_batch_equals_single(fe):
+    frames = fe.synthetic.config_c5_frames(3)[:, :120, :200]
+    lap, bil = fe.LaplacianParams(1.0, 3, 3), fe.BilateralParams(0.1, 0.15, 3, 2)
+    _, res = _engine_run(fe, frames, lap, bil, l_max=0.01, frames=3)
+    for f in range(3):
+        _, r1 = _engine_run(fe, frames[f], lap, bil, l_max=0.01)
+        T = r1.n_tri[0]
+        assert res.n_tri[f] == T
+        assert teq(res.points[f], r1.points[0])
+        assert torch.equal(res.triangles[f, :T], r1.triangles[0, :T])
+        assert torch.equal(res.halfedges[f, :3 * T], r1.halfedges[0, :3 * T])
+        assert teq(res.normals[f, :T], r1.normals[0, :T])
+        assert torch.equal(res.lmax_mask[f, :T], r1.lmax_mask[0, :T])
+
+
+def test_front_end_f64_source_and_no_graph(fe):
+    opc = fe.synthetic.config_c2()[:100, :130]
+    lap, bil = fe.LaplacianParams(0.7, 5, 2), fe.BilateralParams(0.1, 0.15, 3, 3)
+    _, r64 = _engine_run(fe, opc, lap, bil, dtype=torch.float64, graph=False)
+    _, r32 = _engine_run(fe, opc, lap, bil, dtype=torch.float32, graph=True)
+    assert teq(r64.points, r32.points)
+    assert teq(r64.normals, r32.normals)
+    _per_stage_check(fe, opc, lap, bil, None, r64)
+
+
+def test_front_end_function_numpy(fe):
+    g = FE["lidar"]
+    sm, mesh, mask = fe.front_end(g["opc"], fe.LaplacianParams(1.0, 3, 5), None, l_max=0.5)
+    assert np.array_equal(mesh.triangles, g["triangles"])
+    assert np.array_equal(mesh.halfedges, g["halfedges"])
+    assert_vertices_close(sm, g["smoothed"])
+    keep = g["labels_lmaxinf"] != 255
+    assert np.array_equal(mask[keep], g["labels_lmax0.5"][keep] == 255)
+
+
+def test_lmax_mask_golden(fe):
+    g = FE["room"]
+    mesh = fe.HalfEdgeMesh(points=g["smoothed"].reshape(-1, 3), triangles=g["triangles"],
+                           halfedges=g["halfedges"])
+    keep = g["labels_lmaxinf"] != 255
+    for l_max in (0.05, 0.5):
+        m = fe.max_edge_mask(mesh, l_max)
+        assert np.array_equal(m[keep], g[f"labels_lmax{l_max}"][keep] == 255)
+    g = FE["grid3"]
+    mesh = fe.mesh_from_opc(g["opc"])
+    assert np.all(fe.max_edge_mask(mesh, 0.5)) and not np.any(fe.max_edge_mask(mesh, 2.0))
+
+
+def test_compute_normals_any_mesh(fe):
+    rng = np.random.default_rng(12345)
+    pts = rng.normal(size=(30, 3))
+    tris = rng.integers(0, 30, size=(40, 3))
+    mesh = fe.HalfEdgeMesh(points=pts, triangles=tris, halfedges=None)
+    assert same(fe.compute_normals(mesh), fo.triangle_normals(pts, tris))
