@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark: frames/s of the organized front-end (Laplacian + mesh + bilateral) on 1080p.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+Workload (BASELINE.json configs[3], the config the metric is quoted on): 1080x1920
+organized clouds, 10 Laplacian (lam 1, k 3) + 5 bilateral (sl 0.1, sa 0.15, k 3)
+iterations, full mesh + half-edge twins.  A step = one batch of F frames per GPU
+(F * 25 MB fp32 input > L2, so every step streams from HBM).  Frames are
+independent: ranks shard batches, no collective on the data path (weak scaling).
+
+One JSON line on rank 0:
+  value      device-resident whole-job frames/s (inputs in HBM, CUDA events, max over ranks)
+  e2e        same metric through the host API: pinned f64 host frames -> H2D -> front end
+             -> D2H of every mesh output (points, triangles, twins, trimap, normals)
+  roofline   dominant kernel: algorithmic bytes / CUDA-event time vs the
+             measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline  the reference's own CPU path (oracle/_ref = its compiled Cython kernels)
+             on this host's cores, on a bounded sample
+--impl reference times only that CPU path (rank 0) and prints the same line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "frames/sec (HBM GB/s vs roofline) for smooth+mesh of 1080p organized PC, 1/2/4/8 GPU"
+LAP = (1.0, 3, 10)
+BIL = (0.1, 0.15, 3, 5)
+M, N = 1080, 1920
+
+
+def config_dict(frames):
+    return {"workload": "C4: 1080x1920 organized cloud (room scene), 10 Laplacian + 5 bilateral "
+                        "iterations, full mesh + half-edge twins",
+            "frames_per_gpu_per_step": frames, "grid": [M, N],
+            "laplacian": {"lam": LAP[0], "kernel_size": LAP[1], "iterations": LAP[2]},
+            "bilateral": {"sigma_length": BIL[0], "sigma_angle": BIL[1], "kernel_size": BIL[2],
+                          "iterations": BIL[3]},
+            "l2": f"inputs larger than L2: {frames} x 24.9 MB fp32 per step per GPU; "
+                  "outputs/workspace ~0.45 GB per frame",
+            "outputs": "smoothed grid fp32, triangles/trimap/halfedges int64, normals fp32"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        load = [r for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        if not load:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        mhz = [float(r[0]) for r in load]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in load:
+            for name, v in zip(names, r[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": float(load[0][1]),
+                "reasons": sorted(reasons), "samples": len(load),
+                "power_w_max": max(float(r[2]) for r in load if r[2].replace(".", "").isdigit())}
+
+
+# ------------------------------------------------------------------ reference arm
+def cpu_reference(steps, warmup, budget_s=None):
+    """Time the reference's own CPU implementation on this host (bounded sample)."""
+    import numpy as np
+    from oracle import ref_frontend
+    from paper_2007_12065_b200 import synthetic
+    frame = synthetic.config_c4()
+    cores = len(os.sched_getaffinity(0))
+    rows = 136                                  # ~1/8 frame per task
+    pool = ref_frontend.ReferencePool(frame, cores, rows, LAP, BIL)
+    try:
+        for _ in range(warmup):
+            pool.step()
+        times, credit = [], 0.0
+        for _ in range(steps):
+            dt, fr = pool.step()
+            times.append(dt)
+            credit += fr
+            if budget_s is not None and sum(times) > budget_s:
+                break
+    finally:
+        pool.close()
+    total = sum(times)
+    return {"value": credit / total, "unit": "frames/s", "cores": cores,
+            "kind": ref_frontend.kind(),
+            "sample": f"{len(times)} steps x {cores} processes, each a {rows}x{N} row strip of "
+                      f"the C4 frame ({rows / M:.3f} frame) through laplacian_filter (reference "
+                      "Cython) -> triangles/twins/normals (NumPy, as the reference) -> FC data "
+                      "-> bilateral_iterate (reference Cython) -> gather; single-threaded "
+                      "math per process",
+            "ms_per_step": 1e3 * total / len(times), "steps_timed": len(times),
+            "np_version": np.__version__}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    cb = cpu_reference(args.steps, args.warmup)
+    line = {"metric": METRIC, "value": cb["value"], "unit": "frames/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": cb["steps_timed"], "warmup": args.warmup,
+            "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args.frames),
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def algorithmic_bytes(frames, T):
+    """SURVEY.md 8d per-frame algorithmic bytes (fp32 AoS, int64 indices, per pass)."""
+    P = M * N
+    Q = (M - 1) * (N - 1)
+    G = 2 * Q
+    return {
+        "laplacian_per_launch": frames * 24 * P,
+        "triangulate_per_launch": frames * (12 * P + 16 * G + 48 * T),
+        # bilateral stage: FC normals+centroids (12P + 48Q) + 72Q per iteration +
+        # mesh-order gather (12G + 12T); per launch = stage / iterations
+        "bilateral_stage": frames * ((12 * P + 48 * Q) + BIL[3] * 72 * Q + 12 * G + 12 * T),
+        "frame_total": (24 * P * LAP[2] + 12 * P + 16 * G + 48 * T
+                        + (12 * P + 48 * Q) + BIL[3] * 72 * Q + 12 * G + 12 * T),
+    }
+
+
+def load_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2007_12065_b200 as fe
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    F = args.frames
+    base = torch.from_numpy(fe.synthetic.config_c4()).to(dev, torch.float32)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    frames = base.unsqueeze(0) + 0.002 * torch.randn((F, M, N, 3), generator=g, device=dev)
+    eng = fe.FrontEnd(M, N, F, laplacian=fe.LaplacianParams(*LAP),
+                      bilateral=fe.BilateralParams(*BIL), src_dtype=torch.float32, graph=False)
+    eng.src.copy_(frames)
+    del frames
+    stream = torch.cuda.current_stream(dev)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for row in ev:                                  # materialise the cudaEvent_t handles
+        for e in row:
+            e.record(stream)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        eng.launch_profiled(ev[0])
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        t_start.record(stream)
+        for k in range(args.steps):
+            eng.launch_profiled(ev[k])
+        t_end.record(stream)
+        barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    stage = {"stage_in": [], "laplacian": [], "triangulate": [], "bilateral": []}
+    for row in ev:
+        stage["stage_in"].append(row[0].elapsed_time(row[1]))
+        stage["laplacian"].append(row[1].elapsed_time(row[2]))
+        stage["triangulate"].append(row[2].elapsed_time(row[3]))
+        stage["bilateral"].append(row[3].elapsed_time(row[4]))
+    stage_ms = {k: sum(v) / len(v) for k, v in stage.items()}
+    T = int(eng.n_tri[0].item())
+    # max over ranks (device time)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = world * F * args.steps / (max_ms / 1e3)
+
+    # ---------------- e2e through the host API (pinned f64 host frames -> outputs on host)
+    e2e = None
+    if not args.no_e2e:
+        eng64 = fe.FrontEnd(M, N, F, laplacian=fe.LaplacianParams(*LAP),
+                            bilateral=fe.BilateralParams(*BIL), src_dtype=torch.float64,
+                            graph=True)
+        host = torch.empty((F, M, N, 3), dtype=torch.float64, pin_memory=True)
+        host.copy_(eng.src.double().cpu())
+        eng64.run_host(host)                        # warm-up (graph capture, pinned outputs)
+        e2e_steps = max(3, min(args.steps, 10))
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            eng64.run_host(host)
+        e1.record(stream)
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * F * e2e_steps / (float(te.item()) / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(eng64.h2d_bytes), "d2h_bytes_per_step": int(eng64.d2h_bytes),
+               "steps": e2e_steps,
+               "path": "FrontEnd.run_host: pinned f64 host frames -> H2D -> opcfe_front_end "
+                       "(CUDA graph) -> D2H of smoothed grid, triangles, trimap, halfedges, "
+                       "normals into pinned host buffers"}
+        del eng64
+
+    if rank != 0:
+        return 0
+    # ---------------- roofline of the dominant kernel
+    peak, peak_src = load_peaks()
+    ab = algorithmic_bytes(F, T)
+    per_kernel = {
+        "laplacian_kernel": (ab["laplacian_per_launch"], stage_ms["laplacian"] / LAP[2], LAP[2]),
+        "triangulate_kernel": (ab["triangulate_per_launch"], stage_ms["triangulate"], 1),
+        "bilateral_kernel": (ab["bilateral_stage"] / BIL[3], stage_ms["bilateral"] / BIL[3], BIL[3]),
+    }
+    share = {k: v[1] * v[2] for k, v in per_kernel.items()}
+    dom = max(share, key=share.get)
+    bytes_pl, ms_pl, _ = per_kernel[dom]
+    achieved = bytes_pl / (ms_pl / 1e3) / 1e9
+    traffic = load_traffic().get(dom)
+    kernels = {k: {"bytes_per_launch": b, "ms_per_launch": round(ms, 4),
+                   "GBps": round(b / (ms / 1e3) / 1e9, 1),
+                   "frac": round(b / (ms / 1e3) / 1e9 / peak, 3), "launches_per_step": n}
+               for k, (b, ms, n) in per_kernel.items()}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cb = cpu_reference(steps=3, warmup=0, budget_s=25.0)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    launches = eng.kernel_launches * args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config_dict(F),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
+                     "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": traffic, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_pl,
+                     "note": "algorithmic bytes per SURVEY.md 8d (unfused); fusion can make "
+                             "achieved exceed DRAM traffic"},
+        "kernels": kernels,
+        "stage_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
+        "frame_hbm_frac": round(ab["frame_total"] * F / (max_ms / args.steps / 1e3) / 1e9 / peak, 4),
+        "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+        "clocks": clk.summary(), "n_tri_per_frame": T,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--frames", type=int, default=8, help="frames per GPU per step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

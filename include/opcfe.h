@@ -96,9 +96,12 @@ int opcfe_fc_data(const void* opc, int is_f64, int M, int N, void* centroids, vo
 
 /* Replaces smoothing.bilateral_filter_opc (smoothing.py:91-114) -- FC data, the
  * _kernels.bilateral_iterate loop (_native.pyx:287 / _fallback.py:120) and the trimap
- * gather -- in `iterations` launches.  Two input forms:
+ * gather -- in `iterations` launches.  Three input forms:
  *   pts != NULL, normals_in == NULL: normals/centroids computed from the point grid
  *     (fused into iteration 1);
+ *   pts != NULL, normals_in != NULL, centroids_in == NULL: continue filtering from the
+ *     given FC normals (centroids from the grid): bilateral_iterate(.., k) followed by
+ *     bilateral_iterate(.., m) equals bilateral_iterate(.., k + m) (_native.pyx:305);
  *   normals_in, centroids_in != NULL: FC arrays (padded rows) as given to
  *     _kernels.bilateral_iterate (_kernels/__init__.py:30).
  * Output: out_mesh != NULL -> mesh order through trimap ([F][out_rows][3]);
@@ -156,6 +159,14 @@ size_t opcfe_front_end_workspace(int F, int M, int N, const opcfe_front_end_para
 int opcfe_front_end(int F, int M, int N, const opcfe_front_end_params* p,
                     const opcfe_front_end_io* io, void* ws, size_t ws_bytes,
                     opcfe_stream_t stream);
+
+/* opcfe_front_end with 5 optional cudaEvent_t (NULL entries skipped) recorded on `stream`
+ * at the stage boundaries: [0] start, [1] after stage-in, [2] after the Laplacian,
+ * [3] after triangulation, [4] after the bilateral filter (end) -- the analogue of the
+ * reference's per-stage _Timer (pipeline.py:55-68, stages laplacian/front_end/bilateral). */
+int opcfe_front_end_profiled(int F, int M, int N, const opcfe_front_end_params* p,
+                             const opcfe_front_end_io* io, void* ws, size_t ws_bytes,
+                             opcfe_stream_t stream, void* const* stage_events);
 
 #ifdef __cplusplus
 }

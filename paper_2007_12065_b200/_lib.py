@@ -28,7 +28,7 @@ EXPORTS = (
     "opcfe_laplacian",
     "opcfe_triangulate", "opcfe_halfedges_from_trimap", "opcfe_fc_data", "opcfe_bilateral",
     "opcfe_triangle_normals", "opcfe_max_edge_mask", "opcfe_front_end_workspace",
-    "opcfe_front_end",
+    "opcfe_front_end", "opcfe_front_end_profiled",
 )
 
 
@@ -98,6 +98,9 @@ def _declare(L):
         "opcfe_front_end_workspace": (sz, [i, i, i, ctypes.POINTER(FrontEndParams), i, i]),
         "opcfe_front_end": (i, [i, i, i, ctypes.POINTER(FrontEndParams),
                                 ctypes.POINTER(FrontEndIO), vp, sz, vp]),
+        "opcfe_front_end_profiled": (i, [i, i, i, ctypes.POINTER(FrontEndParams),
+                                         ctypes.POINTER(FrontEndIO), vp, sz, vp,
+                                         ctypes.POINTER(ctypes.c_void_p)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -13,26 +13,36 @@
 //     wsum > 0 and |acc| > 1e-30 else n;
 //   * gather to mesh order through trimap (smoothing.py:108-114).
 //
-// B200 mapping: one CTA = 32x8 quads (both triangles of a quad per thread, so each
-// neighbour quad is read once from shared memory for two outputs).  Tile+halo
-// inputs arrive by TMA 3-D box loads with NaN out-of-bounds fill (== the
-// reference's "off-grid neighbours are skipped"): the point tile (centroids are
-// recomputed from points every iteration: 12 B/point instead of 24 B/quad of
-// stored centroids) and, after iteration 1, the previous normal tile.  Iteration 1
-// computes the FC normals with fp64 edges + cross product (no cancellation on
-// slivers) and an fp32 normalisation.  Weights use ex2 with
-// pre-scaled exponents; the |acc| > 1e-30 test is evaluated underflow-safely as
-// |acc/wsum| * wsum > 1e-30.
+// B200 mapping (issue-bound kernel: ~14 FP32 ops + 1 MUFU per directed pair, 34 pairs
+// per quad at k=3, against 60 B of HBM traffic per quad):
+//   * one CTA = 32 x 16 quads, 256 threads, each thread 2 vertically adjacent quads
+//     (both triangles of each), so a neighbour record loaded from shared memory feeds
+//     up to 4 output triangles;
+//   * tile + halo arrive by TMA 3-D box loads with NaN out-of-bounds fill (== the
+//     reference's "off-grid neighbours are skipped"): the point tile (centroids are
+//     recomputed from points every iteration: 12 B/point instead of 24 B/quad of
+//     stored centroids) and, after iteration 1, the previous normal tile;
+//   * a pack step turns each halo quad into 4 float4 planes (conflict-free LDS.128):
+//     per triangle n' = n*sqrt(B), c' = c*sqrt(A) with B, A the exponent scales
+//     pre-multiplied by log2(e), so  w = ex2(-(|c'_i - c'_j|^2 + |n'_i - n'_j|^2)).
+//     Missing / NaN-normal triangles carry n' = 0, c' = 1e18, so their weight to any
+//     valid triangle underflows to exactly 0: no per-pair NaN test;
+//   * iteration 1 computes FC normals with fp64 edges + cross product (no cancellation
+//     on slivers) and an fp32 normalisation;
+//   * the |acc| > 1e-30 test is evaluated underflow-safely as |acc/wsum| * wsum
+//     (SURVEY.md 8c); accumulation order per triangle is the reference's (du, dv, kk).
 #include "common.cuh"
 #include "opcfe_internal.h"
+
+#include <cmath>
 
 namespace opcfe {
 
 namespace {
 
 constexpr int kBilTQW = 32;  // interior quads per tile row (= one warp)
-constexpr int kBilTQH = 8;   // interior quad rows per tile
-constexpr int kBilNT = kBilTQW * kBilTQH;
+constexpr int kBilTQH = 16;  // interior quad rows per tile (2 per thread)
+constexpr int kBilNT = 256;
 
 enum BilMode : int {
   kFromPoints = 0,     // iteration 1: normals + centroids from the point grid
@@ -42,36 +52,40 @@ enum BilMode : int {
 
 template <int H>
 struct BilTile {
-  // TMA rule: box starts along the innermost dimension must be 16-B aligned.  FC rows
-  // are 24 B per quad -> start LQ = round_up(H, 2) quads left of the tile; point rows
-  // are 12 B per point -> start LP = round_up(H, 4) points left.
+  // TMA rule (measured on B200): a box start along the innermost dimension must be
+  // 16-B aligned.  FC rows are 24 B per quad -> the box starts LQ = round_up(H, 2)
+  // quads left of the tile; point rows are 12 B per point -> LP = round_up(H, 4).
   static constexpr int LQ = (H + 1) / 2 * 2;
   static constexpr int LP = (H + 3) / 4 * 4;
-  static constexpr int QW = ((LQ + kBilTQW + H + 1) / 2) * 2;  // FC box width (quads)
+  static constexpr int QW = ((LQ + kBilTQW + H + 1) / 2) * 2;      // FC box width (quads)
   static constexpr int QH = kBilTQH + 2 * H;
   static constexpr int PW = ((LP + kBilTQW + H + 1 + 3) / 4) * 4;  // point box width
   static constexpr int PH = QH + 1;
   static constexpr int PSHIFT = LP - LQ;  // point column of pack column 0
+  static constexpr int NQ = QW * QH;      // quads in the pack
   static constexpr int PTS_F = ((PW * 3 * PH) + 31) / 32 * 32;
   static constexpr int FC_F = ((QW * 6 * QH) + 31) / 32 * 32;
-  static constexpr int PACK_F = QW * QH * 12;
+  static constexpr int PACK_F = 16 * NQ;  // 4 float4 planes
   static constexpr int OUT_F = kBilTQW * 6 * kBilTQH;
-  static_assert(QW * 6 <= 256 && PW * 3 <= 256, "TMA box inner extent must be <= 256");
+  static_assert(QW * 6 <= 256 && PW * 3 <= 256 && PH <= 256, "TMA box extent must be <= 256");
   static_assert((QW * 6) % 4 == 0, "FC box rows must be 16-B multiples");
+  static_assert(FC_F >= OUT_F, "out tile aliases the FC normal tile");
 };
 
+// out tile: its own region in mode 0; aliases the (dead after packing) FC tile otherwise
 template <int H, int MODE>
 constexpr int bil_smem_bytes() {
   using T = BilTile<H>;
   return (((MODE != kNormalsCentBuf) ? T::PTS_F : 0) + ((MODE != kFromPoints) ? T::FC_F : 0) +
-          ((MODE == kNormalsCentBuf) ? T::FC_F : 0) + T::PACK_F + T::OUT_F) *
+          ((MODE == kNormalsCentBuf) ? T::FC_F : 0) + T::PACK_F +
+          ((MODE == kFromPoints) ? T::OUT_F : 0)) *
              4 +
          kSmemSlack;
 }
 
 struct BilArgs {
   int M, N;          // point grid (Mq = M-1, Nq = N-1 quads)
-  float A, B;        // log2(e)/(2 sl^2), log2(e)/(2 sa^2)
+  float sA, sB;      // sqrt(log2(e)/(2 sl^2)), sqrt(log2(e)/(2 sa^2))
   const int64_t* trimap;  // scatter mode: per frame [G]
   long long tm_fs;
   float* out_mesh;   // scatter destination: per frame [cap][3]
@@ -81,8 +95,9 @@ struct BilArgs {
 
 // FC normal for the bilateral input: edges and cross product in fp64 (exact edge
 // differences of fp32 vertices; no cancellation on slivers), normalisation in fp32.
-// |n - float32(reference)| ~ 1e-7, far inside the 1e-5 contract, at ~1/8 the cost of
-// the correctly rounded fp64 divide/sqrt used where bit-exact normals are returned.
+// |n - float32(reference)| ~ 1e-7, far inside the 1e-5 contract, at a fraction of the
+// cost of the correctly rounded fp64 divide/sqrt used where bit-exact normals are
+// returned (gridops.cu).
 __device__ __forceinline__ void unit_normal_fast(const float* pa, const float* pb, const float* pc,
                                                  float* n) {
   const double e1x = (double)pb[0] - pa[0], e1y = (double)pb[1] - pa[1], e1z = (double)pb[2] - pa[2];
@@ -95,8 +110,9 @@ __device__ __forceinline__ void unit_normal_fast(const float* pa, const float* p
     const float fx = (float)x, fy = (float)y, fz = (float)z;
     // rescale into fp32 range before squaring (tiny triangles: |x| ~ 1e-20)
     const float sc = fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz)));
-    const float gx = fx / sc, gy = fy / sc, gz = fz / sc;
-    const float r = rsqrtf(gx * gx + gy * gy + gz * gz);
+    const float is = 1.0f / sc;
+    const float gx = fx * is, gy = fy * is, gz = fz * is;
+    const float r = 1.0f / sqrtf(gx * gx + gy * gy + gz * gz);
     n[0] = gx * r;
     n[1] = gy * r;
     n[2] = gz * r;
@@ -105,8 +121,30 @@ __device__ __forceinline__ void unit_normal_fast(const float* pa, const float* p
   }
 }
 
+struct Tri {
+  float nx, ny, nz, S, cx, cy, cz;
+};
+
+__device__ __forceinline__ Tri tri_from(const float4& n, const float4& c) {
+  return Tri{n.x, n.y, n.z, n.w, c.x, c.y, c.z};
+}
+
+// log2 of the weight between two packed triangles: -(|dc'|^2 + |dn'|^2).  Both terms
+// from differences: the dot form |n_i|^2 + |n_j|^2 - 2 n_i.n_j cancels catastrophically
+// for near-parallel normals (measured 4.6e-5 after 5 iterations at 1080p, > 1e-5).
+__device__ __forceinline__ float neg_log2w(const Tri& i, const Tri& j) {
+  const float dx = j.cx - i.cx, dy = j.cy - i.cy, dz = j.cz - i.cz;
+  const float ex = j.nx - i.nx, ey = j.ny - i.ny, ez = j.nz - i.nz;
+  float e = -(dx * dx);
+  e = fmaf(-dy, dy, e);
+  e = fmaf(-dz, dz, e);
+  e = fmaf(-ex, ex, e);
+  e = fmaf(-ey, ey, e);
+  return fmaf(-ez, ez, e);
+}
+
 template <int H, int MODE, bool SCATTER>
-__global__ void __launch_bounds__(kBilNT)
+__global__ void __launch_bounds__(kBilNT, 3)
     bilateral_kernel(const __grid_constant__ CUtensorMap tpts, const __grid_constant__ CUtensorMap tnrm,
                      const __grid_constant__ CUtensorMap tcen, const __grid_constant__ CUtensorMap tout,
                      BilArgs a) {
@@ -120,9 +158,9 @@ __global__ void __launch_bounds__(kBilNT)
   if (MODE != kNormalsCentBuf) { pts_s = p; p += T::PTS_F; }
   if (MODE != kFromPoints) { nrm_s = p; p += T::FC_F; }
   if (MODE == kNormalsCentBuf) { cen_s = p; p += T::FC_F; }
-  float4* pack = reinterpret_cast<float4*>(p);
+  float4* pk = reinterpret_cast<float4*>(p);  // planes: [0] n0',S0 [1] c0' [2] n1',S1 [3] c1'
   p += T::PACK_F;
-  float* out_s = p;
+  float* out_s = (MODE == kFromPoints) ? p : nrm_s;
   uint64_t& bar = *barp;
 
   const int Mq = a.M - 1, Nq = a.N - 1;
@@ -147,15 +185,16 @@ __global__ void __launch_bounds__(kBilNT)
   }
   mbar_wait(&bar, 0);
 
-  // ---- build the packed per-quad record {n0, n1, c0, c1} for interior + halo
-  for (int q = threadIdx.x; q < T::QW * T::QH; q += kBilNT) {
+  const float sA = a.sA, sB = a.sB;
+  // ---- pack every halo quad into the 4 planes (scaled + sentinel-encoded)
+  for (int q = threadIdx.x; q < T::NQ; q += kBilNT) {
     const int r = q / T::QW, c = q % T::QW;
     float n[6], cc[6];
     if (MODE == kNormalsCentBuf) {
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
-        n[j] = nrm_s[(r * T::QW + c) * 6 + j];
-        cc[j] = cen_s[(r * T::QW + c) * 6 + j];
+        n[j] = nrm_s[q * 6 + j];
+        cc[j] = cen_s[q * 6 + j];
       }
     } else {
       const float* P1 = pts_s + (r * T::PW + c + T::PSHIFT) * 3;
@@ -172,117 +211,142 @@ __global__ void __launch_bounds__(kBilNT)
       }
       if (MODE == kNormalsBuf) {
 #pragma unroll
-        for (int j = 0; j < 6; ++j) n[j] = nrm_s[(r * T::QW + c) * 6 + j];
+        for (int j = 0; j < 6; ++j) n[j] = nrm_s[q * 6 + j];
+      }
+      if (MODE == kFromPoints) {  // raw normals of interior quads: the "unchanged" output
+        const int ir = r - H, ic = c - T::LQ;
+        if (ir >= 0 && ir < kBilTQH && ic >= 0 && ic < kBilTQW) {
+#pragma unroll
+          for (int j = 0; j < 6; ++j) out_s[(ir * kBilTQW + ic) * 6 + j] = n[j];
+        }
       }
     }
-    float4* rec = pack + (r * T::QW + c) * 3;
-    rec[0] = make_float4(n[0], n[1], n[2], n[3]);
-    rec[1] = make_float4(n[4], n[5], cc[0], cc[1]);
-    rec[2] = make_float4(cc[2], cc[3], cc[4], cc[5]);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const bool ok = !(isnan(n[3 * k]) || isnan(n[3 * k + 1]) || isnan(n[3 * k + 2]) ||
+                        isnan(cc[3 * k]) || isnan(cc[3 * k + 1]) || isnan(cc[3 * k + 2]));
+      const float nx = ok ? n[3 * k] * sB : 0.f, ny = ok ? n[3 * k + 1] * sB : 0.f,
+                  nz = ok ? n[3 * k + 2] * sB : 0.f;
+      const float S = nx * nx + ny * ny + nz * nz;
+      pk[(2 * k) * T::NQ + q] = make_float4(nx, ny, nz, S);
+      pk[(2 * k + 1) * T::NQ + q] = ok ? make_float4(cc[3 * k] * sA, cc[3 * k + 1] * sA,
+                                                     cc[3 * k + 2] * sA, 0.f)
+                                       : make_float4(1e18f, 1e18f, 1e18f, 0.f);
+    }
   }
   __syncthreads();
 
-  // ---- one thread per interior quad: both triangles
-  const int tx = threadIdx.x % kBilTQW, ty = threadIdx.x / kBilTQW;
-  const int u = u0 + ty, v = q0 + tx;
-  const float4* own = pack + ((ty + H) * T::QW + (tx + T::LQ)) * 3;
-  const float4 o0 = own[0], o1 = own[1], o2 = own[2];
-  const float n0x = o0.x, n0y = o0.y, n0z = o0.z, n1x = o0.w, n1y = o1.x, n1z = o1.y;
-  const float c0x = o1.z, c0y = o1.w, c0z = o2.x, c1x = o2.y, c1y = o2.z, c1z = o2.w;
-  const bool val0 = !(isnan(n0x) || isnan(n0y) || isnan(n0z));
-  const bool val1 = !(isnan(n1x) || isnan(n1y) || isnan(n1z));
-  float a0x = 0.f, a0y = 0.f, a0z = 0.f, w0s = 0.f;
-  float a1x = 0.f, a1y = 0.f, a1z = 0.f, w1s = 0.f;
-  const float A = a.A, B = a.B;
-  if (val0 || val1) {
+  // ---- two vertically adjacent interior quads per thread
+  const int tx = threadIdx.x % kBilTQW, ty = threadIdx.x / kBilTQW;  // ty in [0, 8)
+  const int R0 = 2 * ty + H, C = tx + T::LQ;                         // pack pos of quad 0
+  float raw[2][6];  // unchanged-output fallback (the caller's normals)
 #pragma unroll
-    for (int du = -H; du <= H; ++du) {
+  for (int o = 0; o < 2; ++o) {
+    const float* src = (MODE == kFromPoints) ? out_s + ((2 * ty + o) * kBilTQW + tx) * 6
+                                             : nrm_s + ((R0 + o) * T::QW + C) * 6;
 #pragma unroll
-      for (int dv = -H; dv <= H; ++dv) {
-        const float4* nb = own + (du * T::QW + dv) * 3;
-        const float4 r0 = nb[0], r1 = nb[1], r2 = nb[2];
-        const float m[2][3] = {{r0.x, r0.y, r0.z}, {r0.w, r1.x, r1.y}};
-        const float d[2][3] = {{r1.z, r1.w, r2.x}, {r2.y, r2.z, r2.w}};
+    for (int j = 0; j < 6; ++j) raw[o][j] = src[j];
+  }
+  Tri own[2][2];
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+    const int q = (R0 + o) * T::QW + C;
+    own[o][0] = tri_from(pk[q], pk[T::NQ + q]);
+    own[o][1] = tri_from(pk[2 * T::NQ + q], pk[3 * T::NQ + q]);
+  }
+  float acc[2][2][4];  // [own quad][triangle][x, y, z, wsum]
+#pragma unroll
+  for (int o = 0; o < 2; ++o)
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[o][k][j] = 0.f;
+
+#pragma unroll
+  for (int dr = -H; dr <= H + 1; ++dr) {
+#pragma unroll
+    for (int dc = -H; dc <= H; ++dc) {
+      const int q = (R0 + dr) * T::QW + C + dc;
+      const Tri nb[2] = {tri_from(pk[q], pk[T::NQ + q]),
+                         tri_from(pk[2 * T::NQ + q], pk[3 * T::NQ + q])};
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        const int du = dr - o;
+        if (du < -H || du > H) continue;
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
-          // neighbour triangle kk vs own triangle 0
-          if (!(du == 0 && dv == 0 && kk == 0)) {
-            const float ex = d[kk][0] - c0x, ey = d[kk][1] - c0y, ez = d[kk][2] - c0z;
-            const float fx = m[kk][0] - n0x, fy = m[kk][1] - n0y, fz = m[kk][2] - n0z;
-            const float dc2 = ex * ex + ey * ey + ez * ez;
-            const float dn2 = fx * fx + fy * fy + fz * fz;
-            const float w = ex2_approx(-(dc2 * A + dn2 * B));
-            if (w == w) {  // NaN neighbour normal / centroid -> skipped
-              a0x += m[kk][0] * w;
-              a0y += m[kk][1] * w;
-              a0z += m[kk][2] * w;
-              w0s += w;
-            }
-          }
-          if (!(du == 0 && dv == 0 && kk == 1)) {
-            const float ex = d[kk][0] - c1x, ey = d[kk][1] - c1y, ez = d[kk][2] - c1z;
-            const float fx = m[kk][0] - n1x, fy = m[kk][1] - n1y, fz = m[kk][2] - n1z;
-            const float dc2 = ex * ex + ey * ey + ez * ez;
-            const float dn2 = fx * fx + fy * fy + fz * fz;
-            const float w = ex2_approx(-(dc2 * A + dn2 * B));
-            if (w == w) {
-              a1x += m[kk][0] * w;
-              a1y += m[kk][1] * w;
-              a1z += m[kk][2] * w;
-              w1s += w;
-            }
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            if (du == 0 && dc == 0 && kk == k) continue;
+            const float w = ex2_approx(neg_log2w(own[o][k], nb[kk]));
+            acc[o][k][0] = fmaf(nb[kk].nx, w, acc[o][k][0]);
+            acc[o][k][1] = fmaf(nb[kk].ny, w, acc[o][k][1]);
+            acc[o][k][2] = fmaf(nb[kk].nz, w, acc[o][k][2]);
+            acc[o][k][3] += w;
           }
         }
       }
     }
   }
-  // underflow-safe normalisation: n = m/|m|, m = acc/wsum; |acc| > 1e-30 <=> |m|*wsum > 1e-30
-  float r0x = n0x, r0y = n0y, r0z = n0z, r1x = n1x, r1y = n1y, r1z = n1z;
-  if (val0 && w0s > 0.f) {
-    const float iw = 1.f / w0s;
-    const float mx = a0x * iw, my = a0y * iw, mz = a0z * iw;
-    const float len = sqrtf(mx * mx + my * my + mz * mz);
-    if (len * w0s > 1e-30f) {
-      r0x = mx / len;
-      r0y = my / len;
-      r0z = mz / len;
-    }
-  }
-  if (val1 && w1s > 0.f) {
-    const float iw = 1.f / w1s;
-    const float mx = a1x * iw, my = a1y * iw, mz = a1z * iw;
-    const float len = sqrtf(mx * mx + my * my + mz * mz);
-    if (len * w1s > 1e-30f) {
-      r1x = mx / len;
-      r1y = my / len;
-      r1z = mz / len;
+
+  // underflow-safe normalisation: n = m/|m|, m = acc'/wsum; |acc| > 1e-30 <=> |m| wsum > 1e-30 sB
+  const float thr = 1e-30f * sB;
+  float res[2][6];
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      float* r = &res[o][3 * k];
+      const float* n = &raw[o][3 * k];
+      r[0] = n[0];
+      r[1] = n[1];
+      r[2] = n[2];
+      const bool valid = !(isnan(n[0]) || isnan(n[1]) || isnan(n[2]));
+      const float ws = acc[o][k][3];
+      if (valid && ws > 0.f) {
+        const float iw = rcp_approx(ws);
+        const float mx = acc[o][k][0] * iw, my = acc[o][k][1] * iw, mz = acc[o][k][2] * iw;
+        // IEEE sqrt + reciprocal (~1.5 ulp): the stored normals feed the next iteration's
+        // weights, so rounding here compounds over the iterations
+        const float len = sqrtf(mx * mx + my * my + mz * mz);
+        if (len * ws > thr) {
+          const float il = 1.0f / len;
+          r[0] = mx * il;
+          r[1] = my * il;
+          r[2] = mz * il;
+        }
+      }
     }
   }
 
   if (SCATTER) {
-    if (u < Mq && v < Nq) {
-      const long long g = 2ll * ((long long)u * Nq + v);
-      const longlong2 tm = *reinterpret_cast<const longlong2*>(a.trimap + f * a.tm_fs + g);
-      float* o = a.out_mesh + f * a.out_fs;
-      if (tm.x >= 0 && tm.x < a.n_out) {
-        o[3 * tm.x] = r0x;
-        o[3 * tm.x + 1] = r0y;
-        o[3 * tm.x + 2] = r0z;
-      }
-      if (tm.y >= 0 && tm.y < a.n_out) {
-        o[3 * tm.y] = r1x;
-        o[3 * tm.y + 1] = r1y;
-        o[3 * tm.y + 2] = r1z;
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      const int u = u0 + 2 * ty + o, v = q0 + tx;
+      if (u < Mq && v < Nq) {
+        const long long g = 2ll * ((long long)u * Nq + v);
+        const longlong2 tm = *reinterpret_cast<const longlong2*>(a.trimap + f * a.tm_fs + g);
+        float* dst = a.out_mesh + f * a.out_fs;
+        if (tm.x >= 0 && tm.x < a.n_out) {
+          dst[3 * tm.x] = res[o][0];
+          dst[3 * tm.x + 1] = res[o][1];
+          dst[3 * tm.x + 2] = res[o][2];
+        }
+        if (tm.y >= 0 && tm.y < a.n_out) {
+          dst[3 * tm.y] = res[o][3];
+          dst[3 * tm.y + 1] = res[o][4];
+          dst[3 * tm.y + 2] = res[o][5];
+        }
       }
     }
   } else {
-    float* o = out_s + (ty * kBilTQW + tx) * 6;
-    o[0] = r0x;
-    o[1] = r0y;
-    o[2] = r0z;
-    o[3] = r1x;
-    o[4] = r1y;
-    o[5] = r1z;
+    if (MODE != kFromPoints) __syncthreads();  // out tile aliases the FC tile read above
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      float* dst = out_s + ((2 * ty + o) * kBilTQW + tx) * 6;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) dst[j] = res[o][j];
+    }
     fence_proxy_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -308,21 +372,20 @@ int launch_bil(const CUtensorMap& tp, const CUtensorMap& tn, const CUtensorMap& 
   return check_launch("bilateral_kernel");
 }
 
-template <int H, int MODE>
-int launch_mode(bool scatter, const CUtensorMap& tp, const CUtensorMap& tn, const CUtensorMap& tc,
-                const CUtensorMap& to, const BilArgs& a, int F, cudaStream_t st) {
-  return scatter ? launch_bil<H, MODE, true>(tp, tn, tc, to, a, F, st)
-                 : launch_bil<H, MODE, false>(tp, tn, tc, to, a, F, st);
-}
-
 template <int H>
 int launch_any(int mode, bool scatter, const CUtensorMap& tp, const CUtensorMap& tn,
                const CUtensorMap& tc, const CUtensorMap& to, const BilArgs& a, int F,
                cudaStream_t st) {
   switch (mode) {
-    case kFromPoints: return launch_mode<H, kFromPoints>(scatter, tp, tn, tc, to, a, F, st);
-    case kNormalsBuf: return launch_mode<H, kNormalsBuf>(scatter, tp, tn, tc, to, a, F, st);
-    default: return launch_mode<H, kNormalsCentBuf>(scatter, tp, tn, tc, to, a, F, st);
+    case kFromPoints:
+      return scatter ? launch_bil<H, kFromPoints, true>(tp, tn, tc, to, a, F, st)
+                     : launch_bil<H, kFromPoints, false>(tp, tn, tc, to, a, F, st);
+    case kNormalsBuf:
+      return scatter ? launch_bil<H, kNormalsBuf, true>(tp, tn, tc, to, a, F, st)
+                     : launch_bil<H, kNormalsBuf, false>(tp, tn, tc, to, a, F, st);
+    default:
+      return scatter ? launch_bil<H, kNormalsCentBuf, true>(tp, tn, tc, to, a, F, st)
+                     : launch_bil<H, kNormalsCentBuf, false>(tp, tn, tc, to, a, F, st);
   }
 }
 
@@ -337,10 +400,6 @@ int launch_h(int h, int mode, bool scatter, const CUtensorMap& tp, const CUtenso
     default: return fail(ERR_UNSUPPORTED, "bilateral: kernel_size > 9 is not compiled in");
   }
 }
-
-struct Maps {
-  CUtensorMap pts, nin, cin, ld_a, st_a, ld_b, st_b;
-};
 
 int box_q(int h) { return ((((h + 1) / 2 * 2) + kBilTQW + h + 1) / 2) * 2; }
 int box_p(int h) { return ((((h + 3) / 4 * 4) + kBilTQW + h + 1 + 3) / 4) * 4; }
@@ -357,30 +416,25 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
     return fail(ERR_INVALID, "bilateral: sigma scales must be positive");
   const int h = ksize / 2;
   if (h > 4) return fail(ERR_UNSUPPORTED, "bilateral: kernel_size > 9 is not compiled in");
-  const bool from_arrays = normals_in != nullptr;
-  if (from_arrays && centroids_in == nullptr)
-    return fail(ERR_INVALID, "bilateral: FC normals given without FC centroids");
+  // input forms: FC arrays (normals + centroids) | point grid | point grid + FC normals
+  // to continue from (centroids from the grid: the fused pipeline's iterations 2..B)
+  const bool from_arrays = normals_in != nullptr && centroids_in != nullptr;
+  const bool resume = normals_in != nullptr && centroids_in == nullptr;
   if (!from_arrays && (pts == nullptr || pitch < 3 * N || pitch % 4))
     return fail(ERR_INVALID, "bilateral: point grid (pitch multiple of 4 floats) required");
   const bool scatter = out_mesh != nullptr;
   if (scatter && trimap == nullptr) return fail(ERR_INVALID, "bilateral: scatter needs trimap");
   if (!scatter && out_fc == nullptr) return fail(ERR_INVALID, "bilateral: no output given");
-  const int nbuf_needed = (iters > 1 ? 1 : 0) + (iters > 2 ? 1 : 0);
-  if ((nbuf_needed >= 1 && !buf_a) || (nbuf_needed >= 2 && !buf_b))
+  if ((iters > 1 && !buf_a) || (iters > 2 && !buf_b))
     return fail(ERR_INVALID, "bilateral: ping-pong buffers required");
 
   const int Mq = M - 1, Nq = N - 1;
   const int fcp = fc_pitch(N);
   const uint64_t fc_fs = (uint64_t)Mq * fcp;
-  const uint64_t pt_fs = (uint64_t)M * pitch;
   const int QW = box_q(h), QH = kBilTQH + 2 * h, PW = box_p(h), PH = QH + 1;
-  Maps mp;
+  // kernel parameters need a valid encoding even where a mode ignores the map
+  CUtensorMap m_pts, m_nin, m_cin, ld_a, st_a, ld_b, st_b, st_fin;
   int rc;
-  const float* any = from_arrays ? normals_in : pts;
-  // unused maps still need a valid encoding (kernel params); point them at `any`
-  if (!from_arrays) {
-    if ((rc = make_tmap_3d(&mp.pts, pts, false, 3ull * N, M, F, pitch, pt_fs, PW * 3, PH))) return rc;
-  }
   auto fc_load = [&](CUtensorMap* m, const float* b) {
     return make_tmap_3d(m, b, false, 6ull * Nq, Mq, F, fcp, fc_fs, QW * 6, QH);
   };
@@ -388,52 +442,45 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
     return make_tmap_3d(m, b, false, 6ull * Nq, Mq, F, fcp, fc_fs, kBilTQW * 6, kBilTQH);
   };
   if (from_arrays) {
-    if ((rc = fc_load(&mp.nin, normals_in))) return rc;
-    if ((rc = fc_load(&mp.cin, centroids_in))) return rc;
-    mp.pts = mp.nin;
+    if ((rc = fc_load(&m_nin, normals_in)) || (rc = fc_load(&m_cin, centroids_in))) return rc;
+    m_pts = m_nin;
   } else {
-    mp.nin = mp.pts;
-    mp.cin = mp.pts;
+    if ((rc = make_tmap_3d(&m_pts, pts, false, 3ull * N, M, F, pitch, (uint64_t)M * pitch,
+                           PW * 3, PH)))
+      return rc;
+    m_nin = m_cin = m_pts;
+    if (resume && (rc = fc_load(&m_nin, normals_in))) return rc;
   }
-  float* fin_dst = scatter ? nullptr : out_fc;
-  CUtensorMap st_fin;
-  if (fin_dst) {
-    if ((rc = fc_store(&st_fin, fin_dst))) return rc;
+  if (!scatter) {
+    if ((rc = fc_store(&st_fin, out_fc))) return rc;
   } else {
-    st_fin = mp.pts;
+    st_fin = m_pts;
   }
-  if (buf_a) {
-    if ((rc = fc_load(&mp.ld_a, buf_a)) || (rc = fc_store(&mp.st_a, buf_a))) return rc;
-  }
-  if (buf_b) {
-    if ((rc = fc_load(&mp.ld_b, buf_b)) || (rc = fc_store(&mp.st_b, buf_b))) return rc;
-  }
-  (void)any;
+  if (buf_a && ((rc = fc_load(&ld_a, buf_a)) || (rc = fc_store(&st_a, buf_a)))) return rc;
+  if (buf_b && ((rc = fc_load(&ld_b, buf_b)) || (rc = fc_store(&st_b, buf_b)))) return rc;
 
   BilArgs a;
   a.M = M;
   a.N = N;
-  const float log2e = 1.4426950408889634f;
-  a.A = (float)(1.4426950408889634 / (2.0 * (double)sigma_length * (double)sigma_length));
-  a.B = (float)(1.4426950408889634 / (2.0 * (double)sigma_angle * (double)sigma_angle));
-  (void)log2e;
+  a.sA = (float)std::sqrt(1.4426950408889634 / (2.0 * (double)sigma_length * sigma_length));
+  a.sB = (float)std::sqrt(1.4426950408889634 / (2.0 * (double)sigma_angle * sigma_angle));
   a.trimap = trimap;
   a.tm_fs = 2ll * Mq * Nq;
   a.out_mesh = out_mesh;
   a.out_fs = 3ll * out_rows;
   a.n_out = out_rows;
 
-  // iteration schedule: it0 reads (points | arrays), writes A; itk reads A/B, writes B/A;
-  // last iteration scatters (mesh order) or stores to out_fc.
-  const CUtensorMap* src_n = &mp.nin;
+  // it0 reads (points | arrays) and writes A; it_k reads A/B and writes B/A; the last
+  // iteration scatters to mesh order (trimap) or stores to out_fc.
+  const CUtensorMap* src_n = &m_nin;
   for (int it = 0; it < iters; ++it) {
     const bool last = it == iters - 1;
-    const int mode = it == 0 ? (from_arrays ? kNormalsCentBuf : kFromPoints)
-                             : (from_arrays ? kNormalsCentBuf : kNormalsBuf);
-    const CUtensorMap* dst = last ? &st_fin : ((it % 2 == 0) ? &mp.st_a : &mp.st_b);
-    rc = launch_h(h, mode, last && scatter, mp.pts, *src_n, mp.cin, *dst, a, F, st);
+    const int mode = from_arrays ? kNormalsCentBuf
+                                 : ((it == 0 && !resume) ? kFromPoints : kNormalsBuf);
+    const CUtensorMap* dst = last ? &st_fin : ((it % 2 == 0) ? &st_a : &st_b);
+    rc = launch_h(h, mode, last && scatter, m_pts, *src_n, m_cin, *dst, a, F, st);
     if (rc) return rc;
-    src_n = (it % 2 == 0) ? &mp.ld_a : &mp.ld_b;
+    src_n = (it % 2 == 0) ? &ld_a : &ld_b;
   }
   return OK;
 }

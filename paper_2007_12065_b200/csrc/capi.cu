@@ -194,9 +194,19 @@ size_t opcfe_front_end_workspace(int F, int M, int N, const opcfe_front_end_para
   return fe_layout(F, M, N, p, src_kind, src_pitch).total;
 }
 
-int opcfe_front_end(int F, int M, int N, const opcfe_front_end_params* p,
-                    const opcfe_front_end_io* io, void* ws, size_t ws_bytes,
-                    opcfe_stream_t stream) {
+}  // extern "C"
+
+namespace {
+
+inline void mark(void* const* ev, int i, cudaStream_t st) {
+  if (ev && ev[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), st);
+}
+
+// ev (optional): 5 cudaEvent_t recorded at stage boundaries
+//   [0] start  [1] after stage-in  [2] after Laplacian  [3] after triangulation  [4] end
+int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
+                   const opcfe_front_end_io* io, void* ws, size_t ws_bytes,
+                   opcfe_stream_t stream, void* const* ev) {
   if (!p || !io || F < 1 || M < 2 || N < 2)
     return fail(ERR_INVALID, "front_end: organized cloud must be at least 2 x 2");
   if (!io->src || !io->points || !io->trimap || !io->triangles || !io->n_tri)
@@ -220,6 +230,7 @@ int opcfe_front_end(int F, int M, int N, const opcfe_front_end_params* p,
   const long long rs = io->src_kind == 0 ? io->src_pitch : 3ll * N;
   const long long fs = (long long)M * rs;
   int rc;
+  mark(ev, 0, st);
   // 1. Laplacian (smoothing.laplacian_filter_opc, pipeline.py:127-129)
   if (p->laplacian_iterations > 0) {
     const float* lin;
@@ -232,18 +243,22 @@ int opcfe_front_end(int F, int M, int N, const opcfe_front_end_params* p,
       lin = staged;
       lap_vmask = nullptr;
     }
+    mark(ev, 1, st);
     rc = laplacian(lin, io->points, lap_tmp, lap_vmask, F, M, N, pitch, p->laplacian_lambda,
                    p->laplacian_kernel_size, p->laplacian_iterations, st);
     if (rc) return rc;
   } else {
     if ((rc = stage_in(io->src, f64, rs, fs, F, M, N, io->points, pitch, vmask, st))) return rc;
+    mark(ev, 1, st);
   }
+  mark(ev, 2, st);
   // 2. mesh_from_opc (pipeline.py:130-131): triangles + trimap + twins [+ normals]
   const bool bil = p->bilateral_iterations > 0 && io->normals != nullptr;
   rc = triangulate(vmask, F, M, N, io->trimap, io->triangles, io->halfedges, io->n_tri, io->points,
                    pitch, bil ? nullptr : io->normals, p->l_max, io->lmax_flag, status, L.status_b,
                    st);
   if (rc) return rc;
+  mark(ev, 3, st);
   // 3. bilateral_filter_opc (pipeline.py:132-134), scattered to mesh order via trimap
   if (bil) {
     rc = bilateral(io->points, F, M, N, pitch, nullptr, nullptr, p->sigma_length, p->sigma_angle,
@@ -253,7 +268,24 @@ int opcfe_front_end(int F, int M, int N, const opcfe_front_end_params* p,
                    2ll * (M - 1) * (N - 1), st);
     if (rc) return rc;
   }
+  mark(ev, 4, st);
   return OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int opcfe_front_end(int F, int M, int N, const opcfe_front_end_params* p,
+                    const opcfe_front_end_io* io, void* ws, size_t ws_bytes,
+                    opcfe_stream_t stream) {
+  return front_end_impl(F, M, N, p, io, ws, ws_bytes, stream, nullptr);
+}
+
+int opcfe_front_end_profiled(int F, int M, int N, const opcfe_front_end_params* p,
+                             const opcfe_front_end_io* io, void* ws, size_t ws_bytes,
+                             opcfe_stream_t stream, void* const* stage_events) {
+  return front_end_impl(F, M, N, p, io, ws, ws_bytes, stream, stage_events);
 }
 
 }  // extern "C"

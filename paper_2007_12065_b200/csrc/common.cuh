@@ -125,11 +125,26 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-// 2^x, IEEE subnormals kept (no .ftz): the bilateral weight must not flush
-// small-but-normal products (precision contract).
+// 2^x as ONE MUFU.EX2 (.ftz: the non-ftz form adds range fix-ups around the MUFU).
+// Flushing results below 2^-126 is harmless for the bilateral weights: a triangle
+// whose weights are all that small has |acc| < 17 * 2^-126 < 1e-30 and is left
+// unchanged by the reference too (_native.pyx:352-360).
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
-  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 1/sqrt(x) and 1/x as single MUFU ops (~1 ulp); inputs below 2^-126 are out of range
+// for the callers (squared distances of distinct vertices / weight sums >= 2^-126).
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 

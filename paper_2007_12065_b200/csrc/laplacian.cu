@@ -99,8 +99,10 @@ __global__ void __launch_bounds__(kLapNT)
           const float* q = pc + (du * T::BW + dv) * 3;
           const float dx = q[0] - px, dy = q[1] - py, dz = q[2] - pz;
           const float d2 = dx * dx + dy * dy + dz * dz;
-          if (d2 > 0.f) {  // false for NaN (missing / off-grid) and coincident points
-            const float w = rsqrtf(d2);
+          // false for NaN (missing / off-grid) and coincident points; >= FLT_MIN keeps the
+          // ftz MUFU.RSQ in range (distinct fp32 vertices closer than 1e-19 m do not occur)
+          if (d2 >= 1.17549435e-38f) {
+            const float w = rsqrt_approx(d2);
             ax += dx * w;
             ay += dy * w;
             az += dz * w;
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(kLapNT)
         }
       }
       if (ws > 0.f) {
-        const float s = lam / ws;
+        const float s = lam * rcp_approx(ws);
         ox = px + s * ax;
         oy = py + s * ay;
         oz = pz + s * az;

@@ -143,6 +143,18 @@ class FrontEnd:
         else:
             self._launch(torch.cuda.current_stream(self.device))
 
+    def launch_profiled(self, events):
+        """Enqueue one batch without the graph, recording 5 stage-boundary CUDA events
+        ([0] start, [1] after stage-in, [2] after Laplacian, [3] after triangulation,
+        [4] end) on the current stream -- the reference's per-stage _Timer
+        (pipeline.py:55-68) measured on the device."""
+        arr = (ctypes.c_void_p * 5)(*[None if e is None else e.cuda_event for e in events])
+        s = torch.cuda.current_stream(self.device)
+        rc = _lib.lib().opcfe_front_end_profiled(self.F, self.M, self.N, ctypes.byref(self.p),
+                                                 ctypes.byref(self.io), self.ws.data_ptr(),
+                                                 self.ws.numel(), s.cuda_stream, arr)
+        _lib.check(rc, "front_end_profiled")
+
     def run(self, src: torch.Tensor | None = None) -> FrontEndResult:
         """Process the batch in self.src (or copy `src` (F,M,N,3) into it first)."""
         if src is not None:
