@@ -12,13 +12,19 @@
 //   * optional fused extras: mesh-order normals (geometry.py:134-147, fp64 math)
 //     and the l_max longest-edge flag (segmentation.py:59-67,73, fp64 math).
 //
-// B200 mapping: one CTA per quad row (grid = rows x frames).  The CTA
-//   1. counts the valid GIDs of rows u-1 and u from the 1-bit point-validity mask,
-//   2. gets the exclusive prefix of row u by a single-pass DECOUPLED LOOK-BACK over
-//      per-row status words (one warp reads 32 predecessors per step),
-//   3. re-scans rows u-1, u, u+1 chunk by chunk with a packed 3-field warp-shuffle
-//      block scan, which yields trimap[] of every neighbour needed for the twins --
-//      so twins are emitted in the same pass, without reading trimap back.
+// B200 mapping: one CTA per quad row (grid = rows x frames), 8 warps, a warp = 32
+// consecutive quads.
+//   * Validity is pure bit algebra on the 1-bit point mask: from 3 mask words per
+//     point row a warp gets the 32-quad first/second masks of rows u-1, u, u+1 and of
+//     the left/right neighbour quads with a few shifts/ANDs (lane-uniform), so ranks
+//     inside the warp are popc(mask & lanemask_lt) -- no shuffles, no per-quad loads.
+//   * The row's base offset comes from a single-pass DECOUPLED LOOK-BACK over per-row
+//     status words (one warp inspects 32 predecessors per step); rows u-1 / u+1 bases
+//     follow from the counts, so every twin index (which needs trimap of the rows above
+//     and below) is computed in the same pass -- trimap is never read back.
+//   * Triangles and twins (int64, 24 B each) are staged in shared memory per 256-quad
+//     chunk and written out as contiguous, fully coalesced 8-B streams; trimap pairs
+//     are written as 16-B stores.
 // Integer outputs are bit-exact by construction (deterministic GID-order ranks).
 #include "common.cuh"
 #include "opcfe_internal.h"
@@ -28,6 +34,8 @@ namespace opcfe {
 namespace {
 
 constexpr int kTriNT = 256;
+constexpr int kTriWarps = kTriNT / 32;
+constexpr int kChunk = kTriNT;  // quads per chunk (one per thread)
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagInc = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
@@ -51,48 +59,34 @@ struct TriArgs {
   double l_max;
 };
 
-struct RowBits {
-  const uint32_t* vm;
-  int wpr, Mq, Nq;
-  __device__ __forceinline__ uint32_t bit(int u, int v) const {
-    return (__ldg(vm + (long long)u * wpr + (v >> 5)) >> (v & 31)) & 1u;
-  }
-  // bit0 = first triangle valid, bit1 = second; 0 off-grid
-  __device__ __forceinline__ uint32_t quad(int u, int v) const {
-    if (u < 0 || u >= Mq || v < 0 || v >= Nq) return 0u;
-    const uint32_t p1 = bit(u, v), p2 = bit(u, v + 1), p3 = bit(u + 1, v + 1), p4 = bit(u + 1, v);
-    return (p1 & p2 & p3) | ((p1 & p3 & p4) << 1);
-  }
+// validity bits of point row r around the 32-point group starting at v0 = 32*word
+struct PtBits {
+  uint32_t a, a1, a2, am;  // bit i = point v0+i, v0+i+1, v0+i+2, v0+i-1
 };
 
-// exclusive block scan of a packed 3 x 10-bit counter word; returns the exclusive
-// prefix, writes the block total to *total (all threads)
-__device__ __forceinline__ uint32_t block_exscan_packed(uint32_t x, uint32_t* warp_tot,
-                                                        uint32_t* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t inc = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  if (lane == 31) warp_tot[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t t = lane < kTriNT / 32 ? warp_tot[lane] : 0u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    if (lane < kTriNT / 32) warp_tot[lane] = t;  // inclusive over warps
-  }
-  __syncthreads();
-  const uint32_t warp_base = warp > 0 ? warp_tot[warp - 1] : 0u;
-  *total = warp_tot[kTriNT / 32 - 1];
-  const uint32_t ex = warp_base + inc - x;
-  __syncthreads();  // warp_tot reused by the next chunk
-  return ex;
+__device__ __forceinline__ PtBits pt_bits(const uint32_t* row, int word, int wpr) {
+  const uint32_t w0 = __ldg(row + word);
+  const uint32_t w1 = (word + 1 < wpr) ? __ldg(row + word + 1) : 0u;
+  const uint32_t wm = (word > 0) ? __ldg(row + word - 1) : 0u;
+  return PtBits{w0, (w0 >> 1) | (w1 << 31), (w0 >> 2) | (w1 << 30), (w0 << 1) | (wm >> 31)};
+}
+
+// first / second masks of a quad row from its two point rows (top t, bottom b)
+struct QuadBits {
+  uint32_t f, s;     // quads v0+i
+  uint32_t fr, sr;   // quads v0+i+1 (right neighbour)
+  uint32_t fl, sl;   // quads v0+i-1 (left neighbour)
+};
+
+__device__ __forceinline__ QuadBits quad_bits(const PtBits& t, const PtBits& b) {
+  QuadBits q;
+  q.f = t.a & t.a1 & b.a1;    // p1 & p2 & p3
+  q.s = t.a & b.a1 & b.a;     // p1 & p3 & p4
+  q.fr = t.a1 & t.a2 & b.a2;
+  q.sr = t.a1 & b.a2 & b.a1;
+  q.fl = t.am & t.a & b.a;
+  q.sl = t.am & b.a & b.am;
+  return q;
 }
 
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
@@ -130,29 +124,39 @@ __device__ __forceinline__ void emit_extras(const TriArgs& a, int f, long long t
   }
 }
 
-__global__ void __launch_bounds__(kTriNT) triangulate_kernel(TriArgs a) {
-  __shared__ uint32_t warp_tot[kTriNT / 32];
-  __shared__ unsigned long long red[kTriNT / 32];
+__global__ void __launch_bounds__(kTriNT, 4) triangulate_kernel(TriArgs a) {
+  __shared__ unsigned long long red[kTriWarps];
+  __shared__ uint32_t wtot[kTriWarps];
   __shared__ long long s_base;
   __shared__ unsigned long long s_tot;
+  __shared__ int64_t tris_s[2 * kChunk * 3];
+  __shared__ int64_t he_s[2 * kChunk * 3];
 
   const int u = blockIdx.x;
   const int f = blockIdx.y;
   const int Mq = a.M - 1, Nq = a.N - 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  RowBits rb{a.vmask + f * a.vm_fs, a.wpr, Mq, Nq};
+  const uint32_t* vm = a.vmask + f * a.vm_fs;
+  const int groups = (Nq + 31) / 32;
 
   // ---- 1. valid-GID counts of rows u (low 32 bits) and u-1 (high 32 bits)
   unsigned long long cnt = 0;
-  for (int v = threadIdx.x; v < Nq; v += kTriNT) {
-    cnt += __popc(rb.quad(u, v));
-    cnt += (unsigned long long)__popc(rb.quad(u - 1, v)) << 32;
+  for (int g = threadIdx.x; g < groups; g += kTriNT) {
+    const PtBits pu = pt_bits(vm + (long long)u * a.wpr, g, a.wpr);
+    const PtBits pd = pt_bits(vm + (long long)(u + 1) * a.wpr, g, a.wpr);
+    const QuadBits qu = quad_bits(pu, pd);
+    cnt += __popc(qu.f) + __popc(qu.s);
+    if (u > 0) {
+      const PtBits pp = pt_bits(vm + (long long)(u - 1) * a.wpr, g, a.wpr);
+      const QuadBits qp = quad_bits(pp, pu);
+      cnt += (unsigned long long)(__popc(qp.f) + __popc(qp.s)) << 32;
+    }
   }
   cnt = warp_sum_u64(cnt);
   if (lane == 0) red[warp] = cnt;
   __syncthreads();
   if (warp == 0) {
-    unsigned long long t = lane < kTriNT / 32 ? red[lane] : 0ull;
+    unsigned long long t = lane < kTriWarps ? red[lane] : 0ull;
     t = warp_sum_u64(t);
     // ---- 2. decoupled look-back over the rows of this frame
     unsigned long long* st = a.status + (long long)f * Mq;
@@ -191,63 +195,90 @@ __global__ void __launch_bounds__(kTriNT) triangulate_kernel(TriArgs a) {
   const long long base_prev = base_cur - (long long)(s_tot >> 32);
   const long long base_next = base_cur + tot_cur;
 
-  // ---- 3. chunked re-scan of rows u-1 / u / u+1 and emission
+  // ---- 3. chunks of 256 quads: bit algebra per warp, block scan over warps, emission
   const long long fG = (long long)f * a.G;
   int64_t* trimap = a.trimap + fG;
   int64_t* tris = a.tris + fG * 3;
   int64_t* he = a.he ? a.he + fG * 3 : nullptr;
   const int N = a.N;
+  const uint32_t lt = (1u << lane) - 1u;
   long long carry_p = 0, carry_c = 0, carry_n = 0;
-  for (int c0 = 0; c0 < Nq; c0 += kTriNT) {
-    const int v = c0 + threadIdx.x;
-    const uint32_t qc = rb.quad(u, v);
-    const uint32_t qp = rb.quad(u - 1, v);
-    const uint32_t qn = rb.quad(u + 1, v);
-    const uint32_t packed = __popc(qp) | (__popc(qc) << 10) | (__popc(qn) << 20);
-    uint32_t total;
-    const uint32_t ex = block_exscan_packed(packed, warp_tot, &total);
-    const long long pre_p = carry_p + (ex & 1023u);
-    const long long pre_c = carry_c + ((ex >> 10) & 1023u);
-    const long long pre_n = carry_n + ((ex >> 20) & 1023u);
+  for (int c0 = 0; c0 < Nq; c0 += kChunk) {
+    const int g = (c0 >> 5) + warp;  // this warp's 32-quad group
+    const int v = 32 * g + lane;
+    QuadBits qc{}, qp{}, qn{};
+    if (g < groups) {
+      const PtBits pu = pt_bits(vm + (long long)u * a.wpr, g, a.wpr);
+      const PtBits pd = pt_bits(vm + (long long)(u + 1) * a.wpr, g, a.wpr);
+      qc = quad_bits(pu, pd);
+      if (u > 0) qp = quad_bits(pt_bits(vm + (long long)(u - 1) * a.wpr, g, a.wpr), pu);
+      if (u + 1 < Mq) qn = quad_bits(pd, pt_bits(vm + (long long)(u + 2) * a.wpr, g, a.wpr));
+    }
+    // per-warp totals of rows u-1 / u / u+1, packed 3 x 10 bits (<= 64 each)
+    if (lane == 0) {
+      wtot[warp] = (__popc(qp.f) + __popc(qp.s)) | ((__popc(qc.f) + __popc(qc.s)) << 10) |
+                   ((__popc(qn.f) + __popc(qn.s)) << 20);
+    }
+    __syncthreads();
+    uint32_t woff = 0, ctot = 0;
+#pragma unroll
+    for (int w = 0; w < kTriWarps; ++w) {
+      const uint32_t x = wtot[w];
+      woff += (w < warp) ? x : 0u;
+      ctot += x;
+    }
+    const uint32_t bf = (qc.f >> lane) & 1u, bs = (qc.s >> lane) & 1u;
+    const long long loc_c = ((woff >> 10) & 1023u) + __popc(qc.f & lt) + __popc(qc.s & lt);
+    const long long pre_c = carry_c + loc_c;
+    const long long pre_p = carry_p + (woff & 1023u) + __popc(qp.f & lt) + __popc(qp.s & lt);
+    const long long pre_n = carry_n + ((woff >> 20) & 1023u) + __popc(qn.f & lt) + __popc(qn.s & lt);
     if (v < Nq) {
-      const long long g = 2ll * ((long long)u * Nq + v);
+      const long long gid = 2ll * ((long long)u * Nq + v);
       const long long t0 = base_cur + pre_c;
-      const long long t1 = t0 + (qc & 1u);
-      const longlong2 tm = make_longlong2((qc & 1u) ? t0 : -1ll, (qc & 2u) ? t1 : -1ll);
-      *reinterpret_cast<longlong2*>(trimap + g) = tm;
+      const long long t1 = t0 + bf;
+      *reinterpret_cast<longlong2*>(trimap + gid) = make_longlong2(bf ? t0 : -1ll, bs ? t1 : -1ll);
       const int64_t i1 = (int64_t)u * N + v, i2 = i1 + 1, i4 = i1 + N, i3 = i4 + 1;
-      if (qc & 1u) {
-        int64_t* o = tris + 3 * t0;
-        o[0] = i3;
-        o[1] = i2;
-        o[2] = i1;
+      const int l0 = (int)loc_c, l1 = l0 + (int)bf;
+      if (bf) {
+        tris_s[3 * l0] = i3;
+        tris_s[3 * l0 + 1] = i2;
+        tris_s[3 * l0 + 2] = i1;
         if (he) {
-          const uint32_t qr = rb.quad(u, v + 1);
-          int64_t* e = he + 3 * t0;
-          e[0] = (qr & 2u) ? 3 * (base_cur + pre_c + __popc(qc) + (qr & 1u)) + 0 : -1;
-          e[1] = (qp & 2u) ? 3 * (base_prev + pre_p + (qp & 1u)) + 1 : -1;
-          e[2] = (qc & 2u) ? 3 * t1 + 2 : -1;
+          he_s[3 * l0] = ((qc.sr >> lane) & 1u)
+                             ? 3 * (t0 + bf + bs + ((qc.fr >> lane) & 1u)) + 0 : -1;
+          he_s[3 * l0 + 1] = ((qp.s >> lane) & 1u)
+                                 ? 3 * (base_prev + pre_p + ((qp.f >> lane) & 1u)) + 1 : -1;
+          he_s[3 * l0 + 2] = bs ? 3 * t1 + 2 : -1;
         }
         if (a.normals || a.lflag) emit_extras(a, f, t0, i3, i2, i1);
       }
-      if (qc & 2u) {
-        int64_t* o = tris + 3 * t1;
-        o[0] = i1;
-        o[1] = i4;
-        o[2] = i3;
+      if (bs) {
+        tris_s[3 * l1] = i1;
+        tris_s[3 * l1 + 1] = i4;
+        tris_s[3 * l1 + 2] = i3;
         if (he) {
-          const uint32_t ql = rb.quad(u, v - 1);
-          int64_t* e = he + 3 * t1;
-          e[0] = (ql & 1u) ? 3 * (base_cur + pre_c - __popc(ql)) + 0 : -1;
-          e[1] = (qn & 1u) ? 3 * (base_next + pre_n) + 1 : -1;
-          e[2] = (qc & 1u) ? 3 * t0 + 2 : -1;
+          const uint32_t lf = (qc.fl >> lane) & 1u, ls = (qc.sl >> lane) & 1u;
+          he_s[3 * l1] = lf ? 3 * (t0 - lf - ls) + 0 : -1;
+          he_s[3 * l1 + 1] = ((qn.f >> lane) & 1u) ? 3 * (base_next + pre_n) + 1 : -1;
+          he_s[3 * l1 + 2] = bf ? 3 * t0 + 2 : -1;
         }
         if (a.normals || a.lflag) emit_extras(a, f, t1, i1, i4, i3);
       }
     }
-    carry_p += total & 1023u;
-    carry_c += (total >> 10) & 1023u;
-    carry_n += (total >> 20) & 1023u;
+    __syncthreads();
+    // coalesced copy-out of this chunk's triangles [base_cur + carry_c, + n)
+    const int n = (int)((ctot >> 10) & 1023u);
+    const long long t_first = base_cur + carry_c;
+    int64_t* tdst = tris + 3 * t_first;
+    for (int i = threadIdx.x; i < 3 * n; i += kTriNT) tdst[i] = tris_s[i];
+    if (he) {
+      int64_t* hdst = he + 3 * t_first;
+      for (int i = threadIdx.x; i < 3 * n; i += kTriNT) hdst[i] = he_s[i];
+    }
+    carry_p += ctot & 1023u;
+    carry_c += n;
+    carry_n += (ctot >> 20) & 1023u;
+    __syncthreads();  // wtot / staging reused by the next chunk
   }
   if (u == Mq - 1 && threadIdx.x == 0) a.ntri[f] = base_cur + tot_cur;
 }
