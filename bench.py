@@ -191,6 +191,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_2007_12065_b200 as fe
+    from paper_2007_12065_b200 import distributed as D
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -237,10 +238,7 @@ def run_ours(args, rank, world, local_rank):
     stage_ms = {k: sum(v) / len(v) for k, v in stage.items()}
     T = int(eng.n_tri[0].item())
     # max over ranks (device time)
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = D.max_over_ranks(elapsed_ms, dev)
     value = world * F * args.steps / (max_ms / 1e3)
 
     # ---------------- e2e through the host API (pinned f64 host frames -> outputs on host)
@@ -260,10 +258,8 @@ def run_ours(args, rank, world, local_rank):
             eng64.run_host(host)
         e1.record(stream)
         barrier()
-        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * F * e2e_steps / (float(te.item()) / 1e3), "unit": "frames/s",
+        te = D.max_over_ranks(e0.elapsed_time(e1), dev)
+        e2e = {"value": world * F * e2e_steps / (te / 1e3), "unit": "frames/s",
                "h2d_bytes_per_step": int(eng64.h2d_bytes), "d2h_bytes_per_step": int(eng64.d2h_bytes),
                "steps": e2e_steps,
                "path": "FrontEnd.run_host: pinned f64 host frames -> H2D -> opcfe_front_end "
