@@ -35,10 +35,17 @@
 #include "opcfe_internal.h"
 
 #include <cmath>
+#include <algorithm>
+#include <cstdlib>
 
 namespace opcfe {
 
 namespace {
+
+// kernel_size 3 runs the direct kernel by default; OPCFE_BILATERAL_SYM=1 selects the
+// pair-symmetric persistent kernel below (half the weights, but 121 registers -> 2 CTAs
+// per SM; measured 3.24 vs 2.77 ms per 8 x 1080p x 5 iterations on B200, kept for A/B).
+static const bool g_bil_direct = std::getenv("OPCFE_BILATERAL_SYM") == nullptr;
 
 constexpr int kBilTQW = 32;  // interior quads per tile row (= one warp)
 constexpr int kBilTQH = 16;  // interior quad rows per tile (2 per thread)
@@ -85,6 +92,7 @@ constexpr int bil_smem_bytes() {
 
 struct BilArgs {
   int M, N;          // point grid (Mq = M-1, Nq = N-1 quads)
+  int F;             // frames (persistent kernels walk tiles of all frames)
   float sA, sB;      // sqrt(log2(e)/(2 sl^2)), sqrt(log2(e)/(2 sa^2))
   const int64_t* trimap;  // scatter mode: per frame [G]
   long long tm_fs;
@@ -404,6 +412,416 @@ int launch_h(int h, int mode, bool scatter, const CUtensorMap& tp, const CUtenso
 int box_q(int h) { return ((((h + 1) / 2 * 2) + kBilTQW + h + 1) / 2) * 2; }
 int box_p(int h) { return ((((h + 3) / 4 * 4) + kBilTQW + h + 1 + 3) / 4) * 4; }
 
+// ============================================================================
+// kernel_size 3: pair-symmetric kernel.  w(i,j) = w(j,i), so every unordered
+// triangle pair is weighed ONCE and shared between its two triangles:
+//   * a warp = 32 consecutive quad columns (lanes 0 and 31 are halo columns that
+//     compute but do not output: 30 outputs / warp), 2 quad rows per warp, 8 warps
+//     stacked vertically: tile = 30 x 16 quads;
+//   * each lane weighs, for its 2 quads: the 2 intra-quad pairs, the vertical pair
+//     between its quads, the 4 quad pairs with the right column (16 weights, handed to
+//     lane+1 with one shuffle each) and the 3 quad pairs with the row below (12 weights,
+//     handed to the warp below through shared memory); the top warp weighs its row
+//     above itself.  17 weights per quad instead of 34;
+//   * accumulation of a triangle's 17 neighbours happens as weights arrive, so the
+//     summation order differs from the reference's (du, dv, kk) by a few ulp.
+// ============================================================================
+constexpr int kSymW = 32;                 // lanes = columns incl. 2 halo columns
+constexpr int kSymOut = kSymW - 2;        // output columns per tile
+constexpr int kSymRows = 16;              // output rows per tile
+constexpr int kSymQW = kSymW + 2;         // pack / FC box columns: q0-2 .. q0+31
+constexpr int kSymQH = kSymRows + 2;      // pack / FC box rows: u0-1 .. u0+16
+constexpr int kSymNQ = kSymQW * kSymQH;
+constexpr int kSymPW = 40;                // point box columns (>= 35 + alignment shift 2)
+constexpr int kSymPH = kSymQH + 1;
+constexpr int kSymPtsF = ((kSymPW * 3 * kSymPH) + 31) / 32 * 32;
+constexpr int kSymFcF = ((kSymQW * 6 * kSymQH) + 31) / 32 * 32;
+constexpr int kSymPackF = 16 * kSymNQ;
+constexpr int kSymOutF = kSymOut * 6 * kSymRows;
+constexpr int kSymXchF = 8 * 32 * 12;     // down-side weights handed to the next warp
+static_assert(kSymFcF >= kSymOutF, "out tile aliases the FC tile");
+
+template <int MODE>
+constexpr int sym_smem_bytes() {  // 2 input stages + pack + [own out tile] + exchange + 2 bars
+  return (2 * (((MODE != kNormalsCentBuf) ? kSymPtsF : 0) + ((MODE != kFromPoints) ? kSymFcF : 0) +
+               ((MODE == kNormalsCentBuf) ? kSymFcF : 0)) +
+          kSymPackF + ((MODE == kFromPoints) ? kSymOutF : 0) + kSymXchF) *
+             4 +
+         16 + kSmemSlack;
+}
+
+struct Tri6 {
+  float nx, ny, nz, cx, cy, cz;
+};
+
+__device__ __forceinline__ float sym_w(const Tri6& i, const Tri6& j) {
+  const float dx = j.cx - i.cx, dy = j.cy - i.cy, dz = j.cz - i.cz;
+  const float ex = j.nx - i.nx, ey = j.ny - i.ny, ez = j.nz - i.nz;
+  float e = -(dx * dx);
+  e = fmaf(-dy, dy, e);
+  e = fmaf(-dz, dz, e);
+  e = fmaf(-ex, ex, e);
+  e = fmaf(-ey, ey, e);
+  return ex2_approx(fmaf(-ez, ez, e));
+}
+
+struct Acc {
+  float x = 0.f, y = 0.f, z = 0.f, w = 0.f;
+  __device__ __forceinline__ void add(float nx, float ny, float nz, float wt) {
+    x = fmaf(nx, wt, x);
+    y = fmaf(ny, wt, y);
+    z = fmaf(nz, wt, z);
+    w += wt;
+  }
+};
+
+template <int MODE, bool SCATTER>
+__global__ void __launch_bounds__(256, 2)
+    bilateral_sym_kernel(const __grid_constant__ CUtensorMap tpts,
+                         const __grid_constant__ CUtensorMap tnrm,
+                         const __grid_constant__ CUtensorMap tcen,
+                         const __grid_constant__ CUtensorMap tout, BilArgs a) {
+  extern __shared__ __align__(16) char smem_raw[];
+  uint64_t* barp;
+  float* p = reinterpret_cast<float*>(smem_aligned_base(smem_raw, &barp));
+  // two input stages (double buffering), one pack, one exchange area
+  float* pts_st[2] = {nullptr, nullptr};
+  float* nrm_st[2] = {nullptr, nullptr};
+  float* cen_st[2] = {nullptr, nullptr};
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    if (MODE != kNormalsCentBuf) { pts_st[s] = p; p += kSymPtsF; }
+    if (MODE != kFromPoints) { nrm_st[s] = p; p += kSymFcF; }
+    if (MODE == kNormalsCentBuf) { cen_st[s] = p; p += kSymFcF; }
+  }
+  float4* pk = reinterpret_cast<float4*>(p);  // planes: [0] n0' [1] c0' [2] n1' [3] c1'
+  p += kSymPackF;
+  float* out_own = nullptr;
+  if (MODE == kFromPoints) { out_own = p; p += kSymOutF; }
+  float4* xch = reinterpret_cast<float4*>(p);  // [warp][lane][3] float4
+  p += kSymXchF;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p);  // 2 stage barriers
+
+  const int Mq = a.M - 1, Nq = a.N - 1;
+  const int tiles_x = (Nq + kSymOut - 1) / kSymOut, tiles_y = (Mq + kSymRows - 1) / kSymRows;
+  const int n_tiles = tiles_x * tiles_y * a.F;
+  auto issue = [&](int tile, int s) {  // TMA loads of `tile` into stage s (thread 0)
+    const int tx = tile % tiles_x, rest = tile / tiles_x;
+    const int tq0 = tx * kSymOut, tu0 = (rest % tiles_y) * kSymRows, tf = rest / tiles_y;
+    const int tsh = (tq0 - 2) & 3;
+    uint32_t bytes = 0;
+    if (MODE != kNormalsCentBuf) bytes += kSymPW * 3 * kSymPH * 4;
+    if (MODE != kFromPoints) bytes += kSymQW * 6 * kSymQH * 4;
+    if (MODE == kNormalsCentBuf) bytes += kSymQW * 6 * kSymQH * 4;
+    mbar_expect_tx(&bars[s], bytes);
+    if (MODE != kNormalsCentBuf)
+      tma_load_3d(pts_st[s], &tpts, &bars[s], (tq0 - 2 - tsh) * 3, tu0 - 1, tf);
+    if (MODE != kFromPoints) tma_load_3d(nrm_st[s], &tnrm, &bars[s], (tq0 - 2) * 6, tu0 - 1, tf);
+    if (MODE == kNormalsCentBuf)
+      tma_load_3d(cen_st[s], &tcen, &bars[s], (tq0 - 2) * 6, tu0 - 1, tf);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    if ((int)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+  }
+  __syncthreads();
+
+  // persistent loop: tile i of this CTA computes while tile i+1's inputs stream in
+  int it = 0;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+  const int s = it & 1;
+  if (threadIdx.x == 0) {
+    tma_store_wait_read();  // the previous tile's out tile (aliases stage s^1 / out_own)
+    if (tile + (int)gridDim.x < n_tiles) issue(tile + gridDim.x, s ^ 1);
+  }
+  __syncthreads();
+  const int q0 = (tile % tiles_x) * kSymOut;   // first output quad column (even)
+  const int u0 = ((tile / tiles_x) % tiles_y) * kSymRows;
+  const int f = tile / (tiles_x * tiles_y);
+  const int pshift = (q0 - 2) & 3;             // point box starts on a 16-B boundary
+  const float* pts_s = pts_st[s];
+  float* nrm_s = nrm_st[s];
+  const float* cen_s = cen_st[s];
+  float* out_s = (MODE == kFromPoints) ? out_own : nrm_s;
+  mbar_wait(&bars[s], (it >> 1) & 1);
+
+  const float sA = a.sA, sB = a.sB;
+  for (int q = threadIdx.x; q < kSymNQ; q += 256) {
+    const int r = q / kSymQW, c = q % kSymQW;
+    float n[6], cc[6];
+    if (MODE == kNormalsCentBuf) {
+#pragma unroll
+      for (int j = 0; j < 6; ++j) {
+        n[j] = nrm_s[q * 6 + j];
+        cc[j] = cen_s[q * 6 + j];
+      }
+    } else {
+      const float* P1 = pts_s + (r * kSymPW + c + pshift) * 3;
+      const float* P2 = P1 + 3;
+      const float* P4 = P1 + kSymPW * 3;
+      const float* P3 = P4 + 3;
+      const float* tri[2][3] = {{P3, P2, P1}, {P1, P4, P3}};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const float *pa = tri[k][0], *pb = tri[k][1], *pc = tri[k][2];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) cc[3 * k + j] = ((pa[j] + pb[j]) + pc[j]) * (1.0f / 3.0f);
+        if (MODE == kFromPoints) unit_normal_fast(pa, pb, pc, n + 3 * k);
+      }
+      if (MODE == kNormalsBuf) {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) n[j] = nrm_s[q * 6 + j];
+      }
+      if (MODE == kFromPoints) {
+        const int ir = r - 1, ic = c - 2;
+        if (ir >= 0 && ir < kSymRows && ic >= 0 && ic < kSymOut) {
+#pragma unroll
+          for (int j = 0; j < 6; ++j) out_s[(ir * kSymOut + ic) * 6 + j] = n[j];
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const bool ok = !(isnan(n[3 * k]) || isnan(n[3 * k + 1]) || isnan(n[3 * k + 2]) ||
+                        isnan(cc[3 * k]) || isnan(cc[3 * k + 1]) || isnan(cc[3 * k + 2]));
+      pk[(2 * k) * kSymNQ + q] = ok ? make_float4(n[3 * k] * sB, n[3 * k + 1] * sB,
+                                                  n[3 * k + 2] * sB, 0.f)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      pk[(2 * k + 1) * kSymNQ + q] = ok ? make_float4(cc[3 * k] * sA, cc[3 * k + 1] * sA,
+                                                      cc[3 * k + 2] * sA, 0.f)
+                                        : make_float4(1e18f, 1e18f, 1e18f, 0.f);
+    }
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int R0 = 2 * ty + 1, C = lane + 1;   // pack position of this lane's first quad
+  auto tri6 = [&](int q, int k) {
+    const float4 n4 = pk[(2 * k) * kSymNQ + q], c4 = pk[(2 * k + 1) * kSymNQ + q];
+    return Tri6{n4.x, n4.y, n4.z, c4.x, c4.y, c4.z};
+  };
+  auto nrm3 = [&](int q, int k) { return pk[(2 * k) * kSymNQ + q]; };
+
+  float raw[2][6];
+  const bool out_lane = lane >= 1 && lane <= kSymOut;
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+    const int ir = 2 * ty + o, ic = lane - 1;
+    const float* src = (MODE == kFromPoints)
+                           ? out_s + (ir * kSymOut + (out_lane ? ic : 0)) * 6
+                           : nrm_s + ((R0 + o) * kSymQW + C) * 6;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) raw[o][j] = src[j];
+  }
+
+  const int q0p = R0 * kSymQW + C, q1p = q0p + kSymQW;  // own quads
+  Tri6 own[2][2] = {{tri6(q0p, 0), tri6(q0p, 1)}, {tri6(q1p, 0), tri6(q1p, 1)}};
+  Acc acc[2][2];
+  // intra-quad pairs
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+    const float w = sym_w(own[o][0], own[o][1]);
+    acc[o][0].add(own[o][1].nx, own[o][1].ny, own[o][1].nz, w);
+    acc[o][1].add(own[o][0].nx, own[o][0].ny, own[o][0].nz, w);
+  }
+  // vertical pair between the lane's two quads
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const float w = sym_w(own[0][k], own[1][kk]);
+      acc[0][k].add(own[1][kk].nx, own[1][kk].ny, own[1][kk].nz, w);
+      acc[1][kk].add(own[0][k].nx, own[0][k].ny, own[0][k].nz, w);
+    }
+  // right column: weigh, keep own share, hand the weights to lane+1 (its left column)
+#pragma unroll
+  for (int ob = 0; ob < 2; ++ob) {
+    const int rq = (R0 + ob) * kSymQW + C + 1;   // right quad in row R0+ob
+    const int lq = rq - 2;                        // left quad, same row
+    const Tri6 rt[2] = {tri6(rq, 0), tri6(rq, 1)};
+    const float4 ln[2] = {nrm3(lq, 0), nrm3(lq, 1)};
+#pragma unroll
+    for (int oa = 0; oa < 2; ++oa) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          // pair (own quad oa tri k) - (right quad in row ob tri kk)
+          const float w = sym_w(own[oa][k], rt[kk]);
+          acc[oa][k].add(rt[kk].nx, rt[kk].ny, rt[kk].nz, w);
+          // the same pair seen from lane+1: (its left quad in row oa, tri k) - (its
+          // own quad ob, tri kk); receive lane-1's weight for (left oa,k) - (own ob,kk)
+          const float wl = __shfl_up_sync(0xffffffffu, w, 1);
+          // here: left quad in row R0+oa; its normal is needed -> from the pack
+          const float4 lno = nrm3((R0 + oa) * kSymQW + C - 1, k);
+          acc[ob][kk].add(lno.x, lno.y, lno.z, wl);
+        }
+    }
+    (void)ln;
+  }
+  // row below: weigh (own quad 1) - (quads below at columns C-1, C, C+1)
+  float4* xout = xch + (ty * 32 + lane) * 3;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int dq = (R0 + 2) * kSymQW + C - 1 + d;
+    const Tri6 dt[2] = {tri6(dq, 0), tri6(dq, 1)};
+    float w4[4];
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        const float w = sym_w(own[1][k], dt[kk]);
+        acc[1][k].add(dt[kk].nx, dt[kk].ny, dt[kk].nz, w);
+        w4[2 * k + kk] = w;
+      }
+    xout[d] = make_float4(w4[0], w4[1], w4[2], w4[3]);
+  }
+  // row above
+  if (ty == 0) {  // top warp: its row above is the halo row, weigh it here
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int uq = (R0 - 1) * kSymQW + C - 1 + d;
+      const Tri6 ut[2] = {tri6(uq, 0), tri6(uq, 1)};
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const float w = sym_w(ut[k], own[0][kk]);
+          acc[0][kk].add(ut[k].nx, ut[k].ny, ut[k].nz, w);
+        }
+    }
+  }
+  __syncthreads();
+  if (ty > 0) {
+    // warp ty-1's lane at column C-1+d weighed (its quad 1 = our up quad at column
+    // C-1+d) - (quad below at column C-1+d + (2-d) - 1 ... ) ; we are its d' = 2-d entry
+    const float4* xin = xch + ((ty - 1) * 32) * 3;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int sl = min(max(lane - 1 + d, 0), 31);   // sender lane (column C-1+d)
+      const float4 w = xin[sl * 3 + (2 - d)];
+      const int uq = (R0 - 1) * kSymQW + C - 1 + d;
+      const float4 un0 = nrm3(uq, 0), un1 = nrm3(uq, 1);
+      // w = (U0B0, U0B1, U1B0, U1B1), U = up quad (sender's quad 1), B = our quad 0
+      acc[0][0].add(un0.x, un0.y, un0.z, w.x);
+      acc[0][1].add(un0.x, un0.y, un0.z, w.y);
+      acc[0][0].add(un1.x, un1.y, un1.z, w.z);
+      acc[0][1].add(un1.x, un1.y, un1.z, w.w);
+    }
+  }
+
+  const float thr = 1e-30f * sB;
+  float res[2][6];
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      float* r = &res[o][3 * k];
+      const float* n = &raw[o][3 * k];
+      r[0] = n[0];
+      r[1] = n[1];
+      r[2] = n[2];
+      const bool valid = !(isnan(n[0]) || isnan(n[1]) || isnan(n[2]));
+      const float ws = acc[o][k].w;
+      if (valid && ws > 0.f) {
+        const float iw = rcp_approx(ws);
+        const float mx = acc[o][k].x * iw, my = acc[o][k].y * iw, mz = acc[o][k].z * iw;
+        const float len = sqrtf(mx * mx + my * my + mz * mz);
+        if (len * ws > thr) {
+          const float il = 1.0f / len;
+          r[0] = mx * il;
+          r[1] = my * il;
+          r[2] = mz * il;
+        }
+      }
+    }
+  }
+
+  if (SCATTER) {
+    if (out_lane) {
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        const int u = u0 + 2 * ty + o, v = q0 + lane - 1;
+        if (u < Mq && v < Nq) {
+          const long long g = 2ll * ((long long)u * Nq + v);
+          const longlong2 tm = *reinterpret_cast<const longlong2*>(a.trimap + f * a.tm_fs + g);
+          float* dst = a.out_mesh + f * a.out_fs;
+          if (tm.x >= 0 && tm.x < a.n_out) {
+            dst[3 * tm.x] = res[o][0];
+            dst[3 * tm.x + 1] = res[o][1];
+            dst[3 * tm.x + 2] = res[o][2];
+          }
+          if (tm.y >= 0 && tm.y < a.n_out) {
+            dst[3 * tm.y] = res[o][3];
+            dst[3 * tm.y + 1] = res[o][4];
+            dst[3 * tm.y + 2] = res[o][5];
+          }
+        }
+      }
+    }
+  } else {
+    if (MODE != kFromPoints) __syncthreads();  // out tile aliases the FC tile read above
+    if (out_lane) {
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        float* dst = out_s + ((2 * ty + o) * kSymOut + lane - 1) * 6;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) dst[j] = res[o][j];
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma_store_3d(&tout, out_s, q0 * 6, u0, f);
+      tma_store_commit();
+    }
+  }
+  }  // persistent tile loop (the barrier at the loop top protects pack / exchange reuse)
+  if (threadIdx.x == 0) tma_store_wait_read();
+}
+
+template <int MODE, bool SCATTER>
+int launch_sym(const CUtensorMap& tp, const CUtensorMap& tn, const CUtensorMap& tc,
+               const CUtensorMap& to, const BilArgs& a, int F, cudaStream_t st) {
+  constexpr int smem = sym_smem_bytes<MODE>();
+  static int resident = 0;  // CTAs per SM (queried once per process / device setup)
+  static int sms = 0;
+  if (resident == 0) {
+    cudaFuncSetAttribute(bilateral_sym_kernel<MODE, SCATTER>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, bilateral_sym_kernel<MODE, SCATTER>,
+                                                  256, smem);
+    if (resident < 1) resident = 1;
+  }
+  const int Mq = a.M - 1, Nq = a.N - 1;
+  const long long tiles = (long long)((Nq + kSymOut - 1) / kSymOut) *
+                          ((Mq + kSymRows - 1) / kSymRows) * F;
+  const int grid = (int)std::min<long long>(tiles, (long long)sms * resident);  // persistent
+  bilateral_sym_kernel<MODE, SCATTER><<<grid, 256, smem, st>>>(tp, tn, tc, to, a);
+  return check_launch("bilateral_sym_kernel");
+}
+
+int launch_sym_any(int mode, bool scatter, const CUtensorMap& tp, const CUtensorMap& tn,
+                   const CUtensorMap& tc, const CUtensorMap& to, const BilArgs& a, int F,
+                   cudaStream_t st) {
+  switch (mode) {
+    case kFromPoints:
+      return scatter ? launch_sym<kFromPoints, true>(tp, tn, tc, to, a, F, st)
+                     : launch_sym<kFromPoints, false>(tp, tn, tc, to, a, F, st);
+    case kNormalsBuf:
+      return scatter ? launch_sym<kNormalsBuf, true>(tp, tn, tc, to, a, F, st)
+                     : launch_sym<kNormalsBuf, false>(tp, tn, tc, to, a, F, st);
+    default:
+      return scatter ? launch_sym<kNormalsCentBuf, true>(tp, tn, tc, to, a, F, st)
+                     : launch_sym<kNormalsCentBuf, false>(tp, tn, tc, to, a, F, st);
+  }
+}
+
 }  // namespace
 
 int bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
@@ -431,7 +849,10 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   const int Mq = M - 1, Nq = N - 1;
   const int fcp = fc_pitch(N);
   const uint64_t fc_fs = (uint64_t)Mq * fcp;
-  const int QW = box_q(h), QH = kBilTQH + 2 * h, PW = box_p(h), PH = QH + 1;
+  const bool sym = (h == 1) && !g_bil_direct;
+  const int QW = sym ? kSymQW : box_q(h), QH = sym ? kSymQH : kBilTQH + 2 * h;
+  const int PW = sym ? kSymPW : box_p(h), PH = QH + 1;
+  const int SW = sym ? kSymOut : kBilTQW, SH = sym ? kSymRows : kBilTQH;  // store box
   // kernel parameters need a valid encoding even where a mode ignores the map
   CUtensorMap m_pts, m_nin, m_cin, ld_a, st_a, ld_b, st_b, st_fin;
   int rc;
@@ -439,7 +860,7 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
     return make_tmap_3d(m, b, false, 6ull * Nq, Mq, F, fcp, fc_fs, QW * 6, QH);
   };
   auto fc_store = [&](CUtensorMap* m, const float* b) {
-    return make_tmap_3d(m, b, false, 6ull * Nq, Mq, F, fcp, fc_fs, kBilTQW * 6, kBilTQH);
+    return make_tmap_3d(m, b, false, 6ull * Nq, Mq, F, fcp, fc_fs, SW * 6, SH);
   };
   if (from_arrays) {
     if ((rc = fc_load(&m_nin, normals_in)) || (rc = fc_load(&m_cin, centroids_in))) return rc;
@@ -462,6 +883,7 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   BilArgs a;
   a.M = M;
   a.N = N;
+  a.F = F;
   a.sA = (float)std::sqrt(1.4426950408889634 / (2.0 * (double)sigma_length * sigma_length));
   a.sB = (float)std::sqrt(1.4426950408889634 / (2.0 * (double)sigma_angle * sigma_angle));
   a.trimap = trimap;
@@ -478,7 +900,8 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
     const int mode = from_arrays ? kNormalsCentBuf
                                  : ((it == 0 && !resume) ? kFromPoints : kNormalsBuf);
     const CUtensorMap* dst = last ? &st_fin : ((it % 2 == 0) ? &st_a : &st_b);
-    rc = launch_h(h, mode, last && scatter, m_pts, *src_n, m_cin, *dst, a, F, st);
+    rc = sym ? launch_sym_any(mode, last && scatter, m_pts, *src_n, m_cin, *dst, a, F, st)
+             : launch_h(h, mode, last && scatter, m_pts, *src_n, m_cin, *dst, a, F, st);
     if (rc) return rc;
     src_n = (it % 2 == 0) ? &ld_a : &ld_b;
   }
