@@ -281,7 +281,8 @@ def run_ours(args, rank, world, local_rank):
     dom = max(share, key=share.get)
     bytes_pl, ms_pl, _ = per_kernel[dom]
     achieved = bytes_pl / (ms_pl / 1e3) / 1e9
-    traffic = load_traffic().get(dom)
+    tr = load_traffic().get(dom)  # ncu --set full DRAM bytes (profiles/traffic.json)
+    traffic = None if tr is None else round(tr["dram_bytes_per_launch_per_frame"] * F)
     kernels = {k: {"bytes_per_launch": b, "ms_per_launch": round(ms, 4),
                    "GBps": round(b / (ms / 1e3) / 1e9, 1),
                    "frac": round(b / (ms / 1e3) / 1e9 / peak, 3), "launches_per_step": n}

@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --frames 2"
 timeout 300 $CMD > gpurun_out/plain5.log 2>&1 || exit 1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:bilateral_sym -s 6 -c 1 -o gpurun_out/prof_sym $CMD > gpurun_out/ncu_bilsym.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:bilateral_kernel -s 6 -c 1 -o gpurun_out/prof_bil3 $CMD > gpurun_out/ncu_bilsym.log 2>&1
 ls -la gpurun_out/*.ncu-rep

@@ -1,0 +1,116 @@
+"""Summarise an ncu capture set (profiles/collect.sh) into tracked files under profiles/.
+
+    python profiles/summarize.py r01        # reads gpurun_out/r01_*, writes profiles/r01_*
+
+Writes:
+  profiles/<tag>_launches.csv      the raw launch list (gpu__time_duration per launch)
+  profiles/<tag>_summary.md        per-kernel share of the step + key --set full metrics
+  profiles/traffic.json            DRAM bytes per launch per frame for bench.py's roofline
+"""
+
+from __future__ import annotations
+
+import collections
+import csv
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+OUT = os.path.join(os.path.dirname(HERE), "gpurun_out")
+FRAMES = 2  # collect.sh profiles bench.py --frames 2
+
+METRICS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.per_cycle_active", "launch__registers_per_thread",
+    "launch__occupancy_limit_shared_mem", "smsp__inst_executed.sum",
+    "lts__t_bytes.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+]
+
+
+def raw_metrics(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    if len(rows) < 3:
+        return {}
+    h, u, v = rows[0], rows[1], rows[2]
+    d = {"kernel": v[h.index("Kernel Name")] if "Kernel Name" in h else "?"}
+    for m in METRICS:
+        if m in h:
+            i = h.index(m)
+            d[m] = (v[i], u[i])
+    stalls = {}
+    for i, name in enumerate(h):
+        if name.startswith("smsp__average_warps_issue_stalled_") and \
+                name.endswith("_per_issue_active.ratio"):
+            try:
+                stalls[name[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]] = float(v[i])
+            except ValueError:
+                pass
+    d["stalls"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:6])
+    return d
+
+
+def launch_shares(path):
+    rows = list(csv.reader(open(path)))
+    hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hdr]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = collections.defaultdict(list)
+    for r in rows[hdr + 1:]:
+        if len(r) > vi:
+            name = r[ki].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
+            agg[name].append(float(r[vi].replace(",", "")))
+    tot = sum(sum(v) for v in agg.values())
+    return {k: (len(v), sum(v) / len(v), sum(v) / tot) for k, v in agg.items()}
+
+
+def main(tag):
+    lines = [f"# ncu summary {tag}", "",
+             "Command: `python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline "
+             f"--frames {FRAMES}` (1080x1920, lap 10 + bil 5).  Launch-list times are "
+             "cold-cache and serialised: compare SHARES with bench.py's stage times.", ""]
+    lp = os.path.join(OUT, f"{tag}_launches.csv")
+    if os.path.exists(lp):
+        shutil.copy(lp, os.path.join(HERE, f"{tag}_launches.csv"))
+        lines += ["## Launch list (all launches of the command)", "",
+                  "| kernel | launches | mean us | share |", "|---|---|---|---|"]
+        for k, (n, mean, share) in sorted(launch_shares(lp).items(), key=lambda kv: -kv[1][2]):
+            lines.append(f"| {k} | {n} | {mean / 1e3:.1f} | {share:.3f} |")
+        lines.append("")
+    traffic = {}
+    for short, kname in (("lap", "laplacian_kernel"), ("tri", "triangulate_kernel"),
+                         ("bil", "bilateral_kernel")):
+        rep = os.path.join(OUT, f"{tag}_{short}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        d = raw_metrics(rep)
+        lines += [f"## {kname} (`--set full`, one launch, {FRAMES} frames)", "",
+                  f"`{d.get('kernel', '?')[:140]}`", "", "| metric | value |", "|---|---|"]
+        for m in METRICS:
+            if m in d:
+                lines.append(f"| {m} | {d[m][0]} {d[m][1]} |")
+        lines.append(f"| top stalls (cycles per issue) | "
+                     f"{', '.join(f'{k} {v:.2f}' for k, v in d['stalls'].items())} |")
+        lines.append("")
+        rb = float(d["dram__bytes_read.sum"][0]) * (1e6 if d["dram__bytes_read.sum"][1] == "Mbyte" else 1)
+        wb = float(d["dram__bytes_write.sum"][0]) * (1e6 if d["dram__bytes_write.sum"][1] == "Mbyte" else 1)
+        traffic[kname] = {"dram_bytes_per_launch_per_frame": (rb + wb) / FRAMES,
+                          "dram_read_bytes": rb, "dram_write_bytes": wb, "frames": FRAMES,
+                          "capture": f"profiles/{tag}_summary.md"}
+    with open(os.path.join(HERE, f"{tag}_summary.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    with open(os.path.join(HERE, "traffic.json"), "w") as f:
+        json.dump(traffic, f, indent=1)
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01")

@@ -470,3 +470,32 @@ def test_compute_normals_any_mesh(fe):
     mesh = fe.HalfEdgeMesh(points=pts, triangles=tris, halfedges=None)
     assert same(fe.compute_normals(mesh), fo.triangle_normals(pts, tris))
 
+
+def test_bilateral_symmetric_kernel_path():
+    """kernel_size 3 runs the direct kernel; OPCFE_BILATERAL_SYM=1 selects the
+    pair-symmetric persistent one.  Both must meet the contract (fresh process: the
+    switch is read at library load)."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+import paper_2007_12065_b200 as fe
+from oracle import c_oracle
+for seed, it in ((5, 1), (6, 3)):
+    opc = fe.synthetic.room_scene(n=97, noise=0.002, seed=seed)
+    opc[np.random.default_rng(seed).random(opc.shape[:2]) < 0.05] = np.nan
+    out = fe.bilateral_filter_opc(opc, fe.BilateralParams(0.1, 0.15, 3, it))
+    ref = c_oracle.front_end(opc, None, (0.1, 0.15, 3, it))["normals"]
+    ok = np.isfinite(ref).all(1)
+    assert np.array_equal(ok, np.isfinite(out).all(1))
+    print(float(np.max(np.linalg.norm(out[ok] - ref[ok], axis=1))))
+'''
+    from conftest import REPO
+    for env in ({}, {"OPCFE_BILATERAL_SYM": "1"}):
+        r = subprocess.run([sys.executable, "-c", code], cwd=REPO, capture_output=True, text=True,
+                           env={**os.environ, **env}, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert max(float(x) for x in r.stdout.split()) <= TOL
+
