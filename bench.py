@@ -244,28 +244,29 @@ def run_ours(args, rank, world, local_rank):
     # ---------------- e2e through the host API (pinned f64 host frames -> outputs on host)
     e2e = None
     if not args.no_e2e:
-        eng64 = fe.FrontEnd(M, N, F, laplacian=fe.LaplacianParams(*LAP),
-                            bilateral=fe.BilateralParams(*BIL), src_dtype=torch.float64,
-                            graph=True)
+        pipe = fe.HostPipeline(M, N, laplacian=fe.LaplacianParams(*LAP),
+                               bilateral=fe.BilateralParams(*BIL), src_dtype=torch.float64,
+                               device=dev)
         host = torch.empty((F, M, N, 3), dtype=torch.float64, pin_memory=True)
         host.copy_(eng.src.double().cpu())
-        eng64.run_host(host)                        # warm-up (graph capture, pinned outputs)
+        pipe.run(host)                              # warm-up (pinned outputs allocated)
         e2e_steps = max(3, min(args.steps, 10))
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e2e_steps):
-            eng64.run_host(host)
+            pipe.run(host)
         e1.record(stream)
         barrier()
         te = D.max_over_ranks(e0.elapsed_time(e1), dev)
         e2e = {"value": world * F * e2e_steps / (te / 1e3), "unit": "frames/s",
-               "h2d_bytes_per_step": int(eng64.h2d_bytes), "d2h_bytes_per_step": int(eng64.d2h_bytes),
+               "h2d_bytes_per_step": int(pipe.h2d_bytes), "d2h_bytes_per_step": int(pipe.d2h_bytes),
                "steps": e2e_steps,
-               "path": "FrontEnd.run_host: pinned f64 host frames -> H2D -> opcfe_front_end "
-                       "(CUDA graph) -> D2H of smoothed grid, triangles, trimap, halfedges, "
-                       "normals into pinned host buffers"}
-        del eng64
+               "path": "HostPipeline.run: pinned f64 host frames -> H2D -> opcfe_front_end "
+                       "(CUDA graph per frame) -> D2H of smoothed grid, trimap, triangles, "
+                       "halfedges, normals into pinned host buffers; frame i+1's H2D + compute "
+                       "overlap frame i's D2H on separate streams"}
+        del pipe
 
     if rank != 0:
         return 0
@@ -316,7 +317,7 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--frames", type=int, default=8, help="frames per GPU per step")

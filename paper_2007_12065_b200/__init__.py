@@ -9,7 +9,7 @@ There is no CPU fallback.
 
 from . import _kernels, synthetic
 from ._kernels import ACTIVE as kernel_backend
-from .frontend import FrontEnd, FrontEndResult, front_end
+from .frontend import FrontEnd, FrontEndResult, HostPipeline, front_end
 from .geometry import DegenerateInputError, triangle_normals
 from .mesh import (HalfEdgeMesh, compute_normals, extract_halfedges_opc, extract_triangles_opc,
                    extract_tri_mesh_from_organized_point_cloud, gid_of, gid_to_uvk, mesh_from_opc)

@@ -225,6 +225,101 @@ class FrontEnd:
                               n_tri=nt, grid_shape=(self.M, self.N))
 
 
+class HostPipeline:
+    """End-to-end frames through host memory with copies overlapped across frames.
+
+    Two single-frame FrontEnd slots (each a CUDA graph) and three streams: frame i+1's
+    H2D and front end run while frame i's outputs stream back (D2H).  A frame's D2H is
+    sized by its own triangle count (one event wait per frame on the host), so exactly
+    the drop-in outputs travel: smoothed grid (fp32), trimap, triangles, halfedges
+    (int64) and normals (fp32), as mesh_from_opc + bilateral_filter_opc return them.
+    """
+
+    def __init__(self, M, N, laplacian=LaplacianParams(), bilateral=BilateralParams(),
+                 l_max=None, src_dtype=torch.float64, device=None):
+        self.slots = [FrontEnd(M, N, 1, laplacian=laplacian, bilateral=bilateral, l_max=l_max,
+                               src_dtype=src_dtype, device=device, graph=True) for _ in range(2)]
+        dev = self.slots[0].device
+        self.M, self.N, self.G = M, N, self.slots[0].G
+        self.s_h2d = torch.cuda.Stream(device=dev)
+        self.s_cmp = torch.cuda.Stream(device=dev)
+        self.s_d2h = torch.cuda.Stream(device=dev)
+        self.ev_h2d = [torch.cuda.Event() for _ in range(2)]
+        self.ev_cmp = [torch.cuda.Event() for _ in range(2)]
+        self.ev_d2h = [torch.cuda.Event() for _ in range(2)]
+        self.ntri_host = torch.empty((2,), dtype=torch.int64, pin_memory=True)
+        self._host = None
+        self.kernel_launches = self.slots[0].kernel_launches
+        for s in self.slots:   # capture both graphs up front
+            s.launch()
+        torch.cuda.synchronize(dev)
+
+    def host_outputs(self, F):
+        if self._host is None or self._host["points"].shape[0] < F:
+            M, N, G = self.M, self.N, self.G
+            pin = dict(pin_memory=True)
+            self._host = dict(
+                points=torch.empty((F, M, N, 3), dtype=torch.float32, **pin),
+                trimap=torch.empty((F, G), dtype=torch.int64, **pin),
+                triangles=torch.empty((F, G, 3), dtype=torch.int64, **pin),
+                halfedges=torch.empty((F, 3 * G), dtype=torch.int64, **pin),
+                normals=torch.empty((F, G, 3), dtype=torch.float32, **pin),
+            )
+        return self._host
+
+    def _enqueue(self, src_host, i):
+        k = i % 2
+        eng = self.slots[k]
+        with torch.cuda.stream(self.s_h2d):
+            self.s_h2d.wait_event(self.ev_cmp[k])      # slot input consumed by frame i-2
+            eng.src.copy_(src_host[i:i + 1], non_blocking=True)
+            self.ev_h2d[k].record(self.s_h2d)
+        with torch.cuda.stream(self.s_cmp):
+            self.s_cmp.wait_event(self.ev_h2d[k])
+            self.s_cmp.wait_event(self.ev_d2h[k])      # slot outputs drained (frame i-2)
+            eng._graph.replay()
+            self.ntri_host[k].copy_(eng.n_tri[0], non_blocking=True)
+            self.ev_cmp[k].record(self.s_cmp)
+
+    def _drain(self, H, i):
+        k = i % 2
+        eng = self.slots[k]
+        self.ev_cmp[k].synchronize()                    # n_tri of frame i is on the host
+        T = int(self.ntri_host[k])
+        with torch.cuda.stream(self.s_d2h):
+            self.s_d2h.wait_event(self.ev_cmp[k])
+            H["points"][i].copy_(eng.grid[0, :, :3 * self.N].unflatten(-1, (self.N, 3)),
+                                 non_blocking=True)
+            H["trimap"][i].copy_(eng.trimap[0], non_blocking=True)
+            H["triangles"][i, :T].copy_(eng.triangles[0, :T], non_blocking=True)
+            H["halfedges"][i, :3 * T].copy_(eng.halfedges[0, :3 * T], non_blocking=True)
+            H["normals"][i, :T].copy_(eng.normals[0, :T], non_blocking=True)
+            self.ev_d2h[k].record(self.s_d2h)
+        return T, (self.M * self.N * 12 + self.G * 8 + T * (24 + 24 + 12))
+
+    def run(self, src_host: torch.Tensor) -> FrontEndResult:
+        """src_host: pinned (F, M, N, 3).  Returns pinned host outputs (valid until the next run)."""
+        F = src_host.shape[0]
+        H = self.host_outputs(F)
+        for s in (self.s_h2d, self.s_cmp, self.s_d2h):
+            s.wait_stream(torch.cuda.current_stream(self.slots[0].device))
+        nt, d2h = [], 0
+        self._enqueue(src_host, 0)
+        for i in range(F):
+            if i + 1 < F:
+                self._enqueue(src_host, i + 1)
+            T, b = self._drain(H, i)
+            nt.append(T)
+            d2h += b + 8
+        torch.cuda.current_stream(self.slots[0].device).wait_stream(self.s_d2h)
+        self.h2d_bytes = src_host.numel() * src_host.element_size()
+        self.d2h_bytes = d2h
+        return FrontEndResult(points=H["points"][:F], triangles=H["triangles"][:F],
+                              trimap=H["trimap"][:F], halfedges=H["halfedges"][:F],
+                              normals=H["normals"][:F], lmax_mask=None, n_tri=nt,
+                              grid_shape=(self.M, self.N))
+
+
 def front_end(opc, laplacian: LaplacianParams | None = None,
               bilateral: BilateralParams | None = None, l_max: float | None = None):
     """Single-frame organized front-end (pipeline.py:125-134) on the GPU.

@@ -499,3 +499,24 @@ for seed, it in ((5, 1), (6, 3)):
         assert r.returncode == 0, r.stderr[-2000:]
         assert max(float(x) for x in r.stdout.split()) <= TOL
 
+
+def test_host_pipeline_matches_device_engine(fe):
+    """HostPipeline (overlapped H2D / graph / D2H per frame) returns exactly what the
+    device engine computes, with D2H sized by each frame's triangle count."""
+    frames = fe.synthetic.config_c5_frames(3)[:, :90, :130]
+    lap, bil = fe.LaplacianParams(1.0, 3, 2), fe.BilateralParams(0.1, 0.15, 3, 2)
+    pipe = fe.HostPipeline(90, 130, laplacian=lap, bilateral=bil)
+    host = torch.from_numpy(frames).pin_memory()
+    res = pipe.run(host)
+    torch.cuda.synchronize()
+    _, ref = _engine_run(fe, frames, lap, bil, frames=3, dtype=torch.float64)
+    for f in range(3):
+        T = ref.n_tri[f]
+        assert res.n_tri[f] == T
+        assert teq(res.points[f], ref.points[f].cpu())
+        assert teq(res.trimap[f], ref.trimap[f].cpu())
+        assert teq(res.triangles[f, :T], ref.triangles[f, :T].cpu())
+        assert teq(res.halfedges[f, :3 * T], ref.halfedges[f, :3 * T].cpu())
+        assert teq(res.normals[f, :T], ref.normals[f, :T].cpu())
+    assert pipe.h2d_bytes == host.numel() * 8 and pipe.d2h_bytes > 0
+
