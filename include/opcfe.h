@@ -121,6 +121,15 @@ int opcfe_triangle_normals(const void* points, int is_f64, const int64_t* triang
 
 /* Replaces the l_max half of segmentation.group_assignment (segmentation.py:59-67,73):
  * flag[t] = longest edge of triangle t > l_max (fp64 edge lengths). */
+/* Replaces segmentation.group_assignment (segmentation.py:52-74) on a mesh's normals:
+ * labels[t] = argmax_g n_t . d_g (first max; fp64 FMA chain as numpy's BLAS matmul),
+ * 255 unless the best score >= ang_min, 255 where lmax_flag[t] (nullable) is set.
+ * F frames of T rows each; n_tri (device [F], nullable) bounds the live rows. */
+int opcfe_group_assignment(const void* normals, int is_f64, long long T, int F,
+                           const int64_t* n_tri, const double* dominant, int n_dominant,
+                           double ang_min, const uint8_t* lmax_flag, uint8_t* labels,
+                           opcfe_stream_t stream);
+
 int opcfe_max_edge_mask(const void* points, int is_f64, const int64_t* triangles,
                         long long n_tri, double l_max, uint8_t* flag, opcfe_stream_t stream);
 
@@ -136,6 +145,11 @@ typedef struct {
   float sigma_length;
   float sigma_angle;
   double l_max; /* < 0: no l_max flag */
+  /* group_assignment (segmentation.py:52-74) fused after the normals: device f64
+   * [n_dominant][3] dominant normals, or NULL for no labels */
+  const double* dominant_normals;
+  int n_dominant;
+  double ang_min;
 } opcfe_front_end_params;
 
 typedef struct {
@@ -152,6 +166,7 @@ typedef struct {
   float* normals;     /* [F][G][3] or NULL */
   uint8_t* lmax_flag; /* [F][G] or NULL (needs l_max >= 0) */
   int64_t* n_tri;     /* [F] */
+  uint8_t* labels;    /* [F][G] group labels (255 = unassigned) or NULL */
 } opcfe_front_end_io;
 
 size_t opcfe_front_end_workspace(int F, int M, int N, const opcfe_front_end_params* p,

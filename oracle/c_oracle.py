@@ -41,6 +41,7 @@ def lib():
         L.oracle_triangulate.restype = ctypes.c_int64
         L.oracle_tri_normals.argtypes = [_dp, _lp, ctypes.c_int64, _dp]
         L.oracle_max_edge.argtypes = [_dp, _lp, ctypes.c_int64, d, _bp]
+        L.oracle_group_assign.argtypes = [_dp, ctypes.c_int64, _dp, i, d, _bp, _bp]
         L.oracle_gather.argtypes = [_dp, _lp, ctypes.c_int64, _dp]
         _lib = L
     return _lib
@@ -103,6 +104,19 @@ def triangle_normals(points, triangles):
     t = np.ascontiguousarray(triangles, dtype=np.int64)
     out = np.empty((len(t), 3))
     lib().oracle_tri_normals(_ptr(p, _dp), _ptr(t, _lp), len(t), _ptr(out, _dp))
+    return out
+
+
+def group_assignment(points, triangles, normals, dominant_normals, l_max, ang_min):
+    """segmentation.py:52-74 (C restatement; BLAS FMA order for the scores)."""
+    dn = np.ascontiguousarray(np.atleast_2d(dominant_normals), dtype=np.float64)
+    if not 1 <= len(dn) <= 254:
+        raise ValueError(f"need 1..254 dominant normals, got {len(dn)}")
+    nrm = _f64(normals).reshape(-1, 3)
+    flag = max_edge_mask(points, triangles, l_max).astype(np.uint8)
+    out = np.empty(len(nrm), dtype=np.uint8)
+    lib().oracle_group_assign(_ptr(nrm, _dp), len(nrm), _ptr(dn, _dp), len(dn), float(ang_min),
+                              _ptr(flag, _bp), _ptr(out, _bp))
     return out
 
 

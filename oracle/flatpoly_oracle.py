@@ -308,6 +308,23 @@ def max_edge_mask(points, triangles, l_max):
     return longest > l_max
 
 
+def group_assignment(points, triangles, normals, dominant_normals, l_max, ang_min):
+    """Per-triangle group labels (uint8): segmentation.py:52-74.
+
+    argmax over n . d (numpy matmul, first maximum; NaN maximal), 255 unless the best
+    score >= ang_min, 255 where the longest edge > l_max.
+    """
+    dn = np.atleast_2d(np.asarray(dominant_normals, dtype=np.float64))
+    if not 1 <= len(dn) <= 254:
+        raise ValueError(f"need 1..254 dominant normals, got {len(dn)}")
+    sims = np.asarray(normals, dtype=np.float64) @ dn.T
+    labels = np.argmax(sims, axis=1).astype(np.uint8)
+    best = sims[np.arange(len(sims)), labels]
+    labels[~(best >= ang_min)] = 255
+    labels[max_edge_mask(points, triangles, l_max)] = 255
+    return labels
+
+
 def front_end(opc, laplacian=None, bilateral=None, l_max=None):
     """Organized branch of pipeline.run_scene: pipeline.py:125-134.
 

@@ -229,6 +229,27 @@ static double edge_len(const double *p, const double *q) {
   return sqrt((dx * dx + dy * dy) + dz * dz);
 }
 
+/* group labels: segmentation.py:52-74.  Scores in the FMA order of numpy's BLAS matmul
+ * (normals @ dn.T -> dgemm k-loop: fma(n2,d2, fma(n1,d1, n0*d0))); first maximum wins,
+ * NaN maximal; 255 unless best >= ang_min; flag (nullable) forces 255. */
+void oracle_group_assign(const double *nrm, int64_t T, const double *dn, int G, double ang_min,
+                         const uint8_t *flag, uint8_t *labels) {
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < T; ++t) {
+    const double *n = nrm + 3 * t;
+    double best = fma(n[2], dn[2], fma(n[1], dn[1], n[0] * dn[0]));
+    int arg = 0;
+    for (int g = 1; g < G && !isnan(best); ++g) {
+      double s = fma(n[2], dn[3 * g + 2], fma(n[1], dn[3 * g + 1], n[0] * dn[3 * g]));
+      if (isnan(s) || s > best) { best = s; arg = g; }
+    }
+    uint8_t lab = (uint8_t)arg;
+    if (!(best >= ang_min)) lab = 255;
+    if (flag && flag[t]) lab = 255;
+    labels[t] = lab;
+  }
+}
+
 void oracle_max_edge(const double *pts, const int64_t *tris, int64_t T, double l_max,
                      uint8_t *flag) {
 #pragma omp parallel for schedule(static)

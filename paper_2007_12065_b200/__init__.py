@@ -13,7 +13,7 @@ from .frontend import FrontEnd, FrontEndResult, HostPipeline, front_end
 from .geometry import DegenerateInputError, triangle_normals
 from .mesh import (HalfEdgeMesh, compute_normals, extract_halfedges_opc, extract_triangles_opc,
                    extract_tri_mesh_from_organized_point_cloud, gid_of, gid_to_uvk, mesh_from_opc)
-from .segmentation import UNASSIGNED, max_edge_mask
+from .segmentation import MAX_GROUPS, UNASSIGNED, group_assignment, max_edge_mask
 from .smoothing import (BilateralParams, LaplacianParams, bilateral_filter_opc, bilateral_opc,
                         compute_fc_triangle_data, laplacian_filter_opc, laplacian_opc)
 
@@ -23,7 +23,8 @@ __all__ = [
     "kernel_backend", "FrontEnd", "FrontEndResult", "front_end", "DegenerateInputError",
     "triangle_normals", "HalfEdgeMesh", "compute_normals", "extract_halfedges_opc",
     "extract_triangles_opc", "extract_tri_mesh_from_organized_point_cloud", "gid_of",
-    "gid_to_uvk", "mesh_from_opc", "UNASSIGNED", "max_edge_mask", "BilateralParams",
+    "gid_to_uvk", "mesh_from_opc", "UNASSIGNED", "MAX_GROUPS", "group_assignment",
+    "max_edge_mask", "BilateralParams",
     "LaplacianParams", "bilateral_filter_opc", "bilateral_opc", "compute_fc_triangle_data",
     "laplacian_filter_opc", "laplacian_opc",
 ]

@@ -27,7 +27,7 @@ EXPORTS = (
     "opcfe_vmask_words", "opcfe_triangulate_workspace", "opcfe_stage_in", "opcfe_unstage",
     "opcfe_laplacian",
     "opcfe_triangulate", "opcfe_halfedges_from_trimap", "opcfe_fc_data", "opcfe_bilateral",
-    "opcfe_triangle_normals", "opcfe_max_edge_mask", "opcfe_front_end_workspace",
+    "opcfe_triangle_normals", "opcfe_group_assignment", "opcfe_max_edge_mask", "opcfe_front_end_workspace",
     "opcfe_front_end", "opcfe_front_end_profiled",
 )
 
@@ -43,6 +43,9 @@ class FrontEndParams(ctypes.Structure):
         ("sigma_length", ctypes.c_float),
         ("sigma_angle", ctypes.c_float),
         ("l_max", ctypes.c_double),
+        ("dominant_normals", ctypes.c_void_p),
+        ("n_dominant", ctypes.c_int),
+        ("ang_min", ctypes.c_double),
     ]
 
 
@@ -59,6 +62,7 @@ class FrontEndIO(ctypes.Structure):
         ("normals", ctypes.c_void_p),
         ("lmax_flag", ctypes.c_void_p),
         ("n_tri", ctypes.c_void_p),
+        ("labels", ctypes.c_void_p),
     ]
 
 
@@ -95,6 +99,7 @@ def _declare(L):
         "opcfe_bilateral": (i, [vp, i, i, i, i, vp, vp, f, f, i, i, vp, vp, vp, vp, vp, ll, vp]),
         "opcfe_triangle_normals": (i, [vp, i, vp, ll, vp, vp]),
         "opcfe_max_edge_mask": (i, [vp, i, vp, ll, d, vp, vp]),
+        "opcfe_group_assignment": (i, [vp, i, ll, i, vp, vp, i, d, vp, vp, vp]),
         "opcfe_front_end_workspace": (sz, [i, i, i, ctypes.POINTER(FrontEndParams), i, i]),
         "opcfe_front_end": (i, [i, i, i, ctypes.POINTER(FrontEndParams),
                                 ctypes.POINTER(FrontEndIO), vp, sz, vp]),

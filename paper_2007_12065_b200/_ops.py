@@ -159,6 +159,23 @@ def triangle_normals(points: torch.Tensor, triangles: torch.Tensor):
     return out
 
 
+def group_assignment(normals: torch.Tensor, dominant: torch.Tensor, ang_min: float,
+                     lflag: torch.Tensor | None = None, n_tri: torch.Tensor | None = None):
+    """(F?, T, 3) normals (f32/f64) x (G, 3) f64 dominant normals -> uint8 labels (F?, T)."""
+    batched = normals.dim() == 3
+    F = normals.shape[0] if batched else 1
+    T = normals.shape[-2]
+    out = torch.empty(normals.shape[:-1], dtype=torch.uint8, device=normals.device)
+    dn = dominant.to(device=normals.device, dtype=torch.float64).contiguous()
+    _lib.check(_lib.lib().opcfe_group_assignment(normals.data_ptr(),
+                                                 int(normals.dtype == torch.float64), T, F,
+                                                 ptr(n_tri), dn.data_ptr(), dn.shape[0],
+                                                 float(ang_min), ptr(lflag), out.data_ptr(),
+                                                 stream()),
+               "group_assignment")
+    return out
+
+
 def max_edge_mask(points: torch.Tensor, triangles: torch.Tensor, l_max: float):
     T = triangles.shape[0]
     out = torch.empty((T,), dtype=torch.uint8, device=points.device)

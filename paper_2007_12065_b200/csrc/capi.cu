@@ -183,6 +183,15 @@ int opcfe_triangle_normals(const void* points, int is_f64, const int64_t* triang
   return triangle_normals(points, is_f64 != 0, triangles, n_tri, normals, S(stream));
 }
 
+int opcfe_group_assignment(const void* normals, int is_f64, long long T, int F,
+                           const int64_t* n_tri, const double* dominant, int n_dominant,
+                           double ang_min, const uint8_t* lmax_flag, uint8_t* labels,
+                           opcfe_stream_t stream) {
+  if (!normals || !dominant || !labels) return fail(ERR_INVALID, "group_assignment: null buffer");
+  return group_assignment(normals, is_f64 != 0, T, F, n_tri, dominant, n_dominant, ang_min,
+                          lmax_flag, labels, S(stream));
+}
+
 int opcfe_max_edge_mask(const void* points, int is_f64, const int64_t* triangles,
                         long long n_tri, double l_max, uint8_t* flag, opcfe_stream_t stream) {
   return max_edge_mask(points, is_f64 != 0, triangles, n_tri, l_max, flag, S(stream));
@@ -266,6 +275,14 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
                    p->bilateral_iterations > 1 ? bil_a : nullptr,
                    p->bilateral_iterations > 2 ? bil_b : nullptr, nullptr, io->trimap, io->normals,
                    2ll * (M - 1) * (N - 1), st);
+    if (rc) return rc;
+  }
+  // 4. group labels (segmentation.group_assignment) on the final normals
+  if (p->dominant_normals && io->labels) {
+    if (!io->normals) return fail(ERR_INVALID, "front_end: labels need normals");
+    rc = group_assignment(io->normals, false, 2ll * (M - 1) * (N - 1), F, io->n_tri,
+                          p->dominant_normals, p->n_dominant, p->ang_min,
+                          p->l_max >= 0 ? io->lmax_flag : nullptr, io->labels, st);
     if (rc) return rc;
   }
   mark(ev, 4, st);

@@ -128,6 +128,44 @@ __global__ void unstage_kernel(const float* __restrict__ src, int pitch, int M, 
   }
 }
 
+// group_assignment (segmentation.py:52-74): per triangle, argmax over the dominant normals
+// of n . d (first maximum wins; NaN counts as maximal, numpy argmax), UNASSIGNED (255)
+// unless best >= ang_min, and 255 where the l_max flag is set.  The dot products use the
+// FMA chain fma(n2,d2, fma(n1,d1, n0*d0)) in fp64 -- the k-loop of the OpenBLAS dgemm
+// kernel numpy's `normals @ dn.T` dispatches to (checked bit-for-bit in this image), so
+// labels match the reference except at exact-rounding ties between two scores.
+// Frames: `T` rows per frame with the live count in n_tri[f] (nullable = all rows).
+template <typename S>
+__global__ void group_assign_kernel(const S* __restrict__ normals, long long T, int F,
+                                    const int64_t* __restrict__ n_tri,
+                                    const double* __restrict__ dn, int G, double ang_min,
+                                    const uint8_t* __restrict__ lflag, uint8_t* __restrict__ labels) {
+  __shared__ double sd[254 * 3];
+  for (int i = threadIdx.x; i < 3 * G; i += blockDim.x) sd[i] = dn[i];
+  __syncthreads();
+  const int f = blockIdx.y;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long live = n_tri ? n_tri[f] : T;
+  if (t >= live || t >= T) return;
+  const long long row = f * T + t;
+  const double n0 = (double)normals[3 * row], n1 = (double)normals[3 * row + 1],
+               n2 = (double)normals[3 * row + 2];
+  double best = fma(n2, sd[2], fma(n1, sd[1], n0 * sd[0]));
+  int arg = 0;
+  for (int g = 1; g < G; ++g) {
+    if (isnan(best)) break;  // the first NaN is the argmax
+    const double s = fma(n2, sd[3 * g + 2], fma(n1, sd[3 * g + 1], n0 * sd[3 * g]));
+    if (isnan(s) || s > best) {
+      best = s;
+      arg = g;
+    }
+  }
+  uint8_t lab = (uint8_t)arg;
+  if (!(best >= ang_min)) lab = 255;  // catches NaN normals too (segmentation.py:72)
+  if (lflag != nullptr && lflag[row]) lab = 255;
+  labels[row] = lab;
+}
+
 inline unsigned blocks_for(long long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
 }  // namespace
@@ -170,6 +208,21 @@ int triangle_normals(const void* pts, bool f64, const int64_t* tris, long long T
     tri_normals_kernel<float><<<blocks_for(T, 256), 256, 0, st>>>(
         static_cast<const float*>(pts), tris, T, static_cast<float*>(out));
   return check_launch("tri_normals_kernel");
+}
+
+int group_assignment(const void* normals, bool f64, long long T, int F, const int64_t* n_tri,
+                     const double* dominant, int G, double ang_min, const uint8_t* lflag,
+                     uint8_t* labels, cudaStream_t st) {
+  if (G < 1 || G > 254) return fail(ERR_INVALID, "need 1..254 dominant normals");
+  if (T <= 0 || F < 1) return OK;
+  dim3 grid(blocks_for(T, 256), F);
+  if (f64)
+    group_assign_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(normals), T, F,
+                                                       n_tri, dominant, G, ang_min, lflag, labels);
+  else
+    group_assign_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(normals), T, F,
+                                                      n_tri, dominant, G, ang_min, lflag, labels);
+  return check_launch("group_assign_kernel");
 }
 
 int max_edge_mask(const void* pts, bool f64, const int64_t* tris, long long T, double l_max,

@@ -30,6 +30,9 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
 int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st);
 int triangle_normals(const void* pts, bool f64, const int64_t* tris, long long T, void* out,
                      cudaStream_t st);
+int group_assignment(const void* normals, bool f64, long long T, int F, const int64_t* n_tri,
+                     const double* dominant, int G, double ang_min, const uint8_t* lflag,
+                     uint8_t* labels, cudaStream_t st);
 int max_edge_mask(const void* pts, bool f64, const int64_t* tris, long long T, double l_max,
                   uint8_t* flag, cudaStream_t st);
 

@@ -39,6 +39,7 @@ class FrontEndResult:
     lmax_mask: torch.Tensor     # (F, G) uint8 or None
     n_tri: list = field(default_factory=list)
     grid_shape: tuple = None
+    labels: torch.Tensor = None  # (F, G) uint8 group labels (255 = unassigned) or None
 
     def mesh(self, f: int = 0) -> HalfEdgeMesh:
         """Frame f as a HalfEdgeMesh (flatpoly.mesh.HalfEdgeMesh fields)."""
@@ -60,6 +61,7 @@ class FrontEnd:
                  laplacian: LaplacianParams | None = LaplacianParams(),
                  bilateral: BilateralParams | None = BilateralParams(),
                  l_max: float | None = None, halfedges: bool = True, normals: bool = True,
+                 dominant_normals=None, ang_min: float = 0.95,
                  src_dtype=torch.float32, device=None, graph: bool = True):
         require_cuda()
         if M < 2 or N < 2:
@@ -85,6 +87,15 @@ class FrontEnd:
             bilateral.iterations if bilateral else 0, bilateral.kernel_size if bilateral else 3,
             bilateral.sigma_length if bilateral else 0.1, bilateral.sigma_angle if bilateral else 0.15,
             float(l_max) if l_max is not None else -1.0)
+        self.dn = None
+        if dominant_normals is not None:   # fused group_assignment (segmentation.py:52-74)
+            dn = torch.as_tensor(np.atleast_2d(np.asarray(dominant_normals, dtype=np.float64)))
+            if not 1 <= dn.shape[0] <= 254:
+                raise ValueError(f"need 1..254 dominant normals, got {dn.shape[0]}")
+            self.dn = dn.to(dev).contiguous()
+            self.p.dominant_normals = self.dn.data_ptr()
+            self.p.n_dominant = self.dn.shape[0]
+            self.p.ang_min = float(ang_min)
         self.grid = torch.empty((frames, M, self.pitch), dtype=torch.float32, device=dev)
         self.trimap = torch.empty((frames, G), dtype=torch.int64, device=dev)
         self.triangles = torch.empty((frames, G, 3), dtype=torch.int64, device=dev)
@@ -92,6 +103,8 @@ class FrontEnd:
         self.normals = torch.empty((frames, G, 3), dtype=torch.float32, device=dev) if normals else None
         self.lmax = torch.empty((frames, G), dtype=torch.uint8, device=dev) if l_max is not None else None
         self.n_tri = torch.empty((frames,), dtype=torch.int64, device=dev)
+        self.labels = torch.empty((frames, G), dtype=torch.uint8, device=dev) \
+            if self.dn is not None else None
         L = _lib.lib()
         ws_bytes = int(L.opcfe_front_end_workspace(frames, M, N, ctypes.byref(self.p), src_kind,
                                                    src_pitch))
@@ -102,10 +115,12 @@ class FrontEnd:
             self.halfedges.data_ptr() if halfedges else None,
             self.normals.data_ptr() if normals else None,
             self.lmax.data_ptr() if self.lmax is not None else None,
-            self.n_tri.data_ptr())
+            self.n_tri.data_ptr(),
+            self.labels.data_ptr() if self.labels is not None else None)
         self._graph = None
         self._use_graph = graph
-        self.kernel_launches = self._count_launches(laplacian, bilateral, src_kind)
+        self.kernel_launches = self._count_launches(laplacian, bilateral, src_kind) + \
+            (1 if self.labels is not None else 0)
 
     @staticmethod
     def _count_launches(lap, bil, src_kind):
@@ -166,7 +181,7 @@ class FrontEnd:
         pts = self.grid[..., :3 * self.N].unflatten(-1, (self.N, 3))
         return FrontEndResult(points=pts, triangles=self.triangles, trimap=self.trimap,
                               halfedges=self.halfedges, normals=self.normals,
-                              lmax_mask=self.lmax, n_tri=self.n_tri.tolist(),
+                              lmax_mask=self.lmax, n_tri=self.n_tri.tolist(), labels=self.labels,
                               grid_shape=(self.M, self.N))
 
     # -------------------------------------------------------------------- host

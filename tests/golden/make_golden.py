@@ -232,7 +232,45 @@ def main():
     fe["grid3/labels_lmax0.5"] = group_assignment(mesh, up, 0.5, 0.5)
     fe["grid3/labels_lmax2.0"] = group_assignment(mesh, up, 2.0, 0.5)
     np.savez_compressed(os.path.join(HERE, "frontend.npz"), **fe)
-    for f in ("topology", "laplacian", "bilateral", "frontend"):
+
+    # ------------------------------------------------- group_assignment (segmentation.py:52)
+    grp = {}
+    from flatpoly.mesh import HalfEdgeMesh
+    planes = np.array([[0, 0, 1.0], [-1.0, 0, 0], [1.0, 0, 0], [0, -1.0, 0], [0, 1.0, 0]])
+    sm = laplacian_filter_opc(scene.opc, lp)
+    mesh = mesh_from_opc(sm)
+    mesh.normals = bilateral_filter_opc(sm, bp, mesh.trimap)
+    for name, (msh, dn, l_max, ang) in {
+            "room": (mesh, planes, 0.5, 0.96),
+            "room_loose": (mesh, planes[:3], 0.5, 0.5)}.items():
+        grp[f"{name}/points"] = msh.points
+        grp[f"{name}/triangles"] = msh.triangles
+        grp[f"{name}/normals"] = msh.normals
+        grp[f"{name}/dominant"] = dn
+        grp[f"{name}/params"] = np.array([l_max, ang])
+        grp[f"{name}/labels"] = group_assignment(msh, dn, l_max, ang)
+    rng = np.random.default_rng(99)
+    pts = rng.normal(size=(3000, 3))
+    tris = rng.integers(0, 3000, size=(6000, 3))
+    nrm = rng.normal(size=(6000, 3))
+    nrm /= np.linalg.norm(nrm, axis=1)[:, None]
+    nrm[rng.random(6000) < 0.05] = np.nan
+    dn = rng.normal(size=(40, 3))
+    dn /= np.linalg.norm(dn, axis=1)[:, None]
+    msh = HalfEdgeMesh(points=pts, triangles=tris, halfedges=None, normals=nrm)
+    grp["random/points"], grp["random/triangles"], grp["random/normals"] = pts, tris, nrm
+    grp["random/dominant"] = dn
+    grp["random/params"] = np.array([3.0, 0.6])
+    grp["random/labels"] = group_assignment(msh, dn, 3.0, 0.6)
+    # exact normal match at ang_min = 1.0 (tests/test_segmentation.py:28-31)
+    msh = mesh_from_opc(flat_plane_opc(3, 3, spacing=0.1))
+    grp["exact/points"], grp["exact/triangles"], grp["exact/normals"] = \
+        msh.points, msh.triangles, msh.normals
+    grp["exact/dominant"] = up
+    grp["exact/params"] = np.array([1.0, 1.0])
+    grp["exact/labels"] = group_assignment(msh, up, 1.0, 1.0)
+    np.savez_compressed(os.path.join(HERE, "groups.npz"), **grp)
+    for f in ("topology", "laplacian", "bilateral", "frontend", "groups"):
         p = os.path.join(HERE, f + ".npz")
         print(f"{p}: {os.path.getsize(p) / 1024:.1f} KiB")
 

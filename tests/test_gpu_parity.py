@@ -500,6 +500,44 @@ for seed, it in ((5, 1), (6, 3)):
         assert max(float(x) for x in r.stdout.split()) <= TOL
 
 
+GROUPS = load_golden("groups")
+
+
+@pytest.mark.parametrize("case", sorted(GROUPS))
+def test_golden_group_assignment(fe, case):
+    """segmentation.group_assignment drop-in: bit-exact labels (fp64 scores in the BLAS
+    FMA order, fp64 edge lengths)."""
+    g = GROUPS[case]
+    l_max, ang = g["params"]
+    mesh = fe.HalfEdgeMesh(points=g["points"], triangles=g["triangles"], halfedges=None,
+                           normals=g["normals"])
+    lab = fe.group_assignment(mesh, g["dominant"], l_max, ang)
+    assert lab.dtype == np.uint8 and np.array_equal(lab, g["labels"])
+    with pytest.raises(ValueError, match="dominant normals"):
+        fe.group_assignment(mesh, np.zeros((255, 3)), l_max, ang)
+
+
+def test_front_end_fused_labels(fe):
+    """Labels fused after the bilateral pass == oracle group_assignment on the GPU's own
+    fp32 normals / smoothed grid (per-stage parity)."""
+    opc = fe.synthetic.config_c2()
+    lap, bil = fe.LaplacianParams(1.0, 3, 3), fe.BilateralParams(0.1, 0.15, 3, 2)
+    dn = np.array([[0, 0, 1.0], [-1.0, 0, 0], [1.0, 0, 0], [0, -1.0, 0], [0, 1.0, 0]])
+    M, N = opc.shape[:2]
+    eng = fe.FrontEnd(M, N, 1, laplacian=lap, bilateral=bil, l_max=0.05, dominant_normals=dn,
+                      ang_min=0.96)
+    res = eng.run(torch.from_numpy(opc).float().cuda().unsqueeze(0))
+    torch.cuda.synchronize()
+    T = res.n_tri[0]
+    sm = res.points[0].cpu().numpy().astype(np.float64)
+    ref = c_oracle.group_assignment(sm.reshape(-1, 3), res.triangles[0, :T].cpu().numpy(),
+                                    res.normals[0, :T].cpu().numpy().astype(np.float64), dn,
+                                    0.05, 0.96)
+    lab = res.labels[0, :T].cpu().numpy()
+    assert np.array_equal(lab, ref)
+    assert 0 < (lab == 255).sum() < T and eng.kernel_launches == 3 + 1 + 2 + 1
+
+
 def test_host_pipeline_matches_device_engine(fe):
     """HostPipeline (overlapped H2D / graph / D2H per frame) returns exactly what the
     device engine computes, with D2H sized by each frame's triangle count."""

@@ -115,6 +115,22 @@ def test_lmax_mask_matches_group_assignment(impl):
     assert np.all(g["labels_lmax0.5"] == 255) and np.all(g["labels_lmax2.0"] == 0)
 
 
+GROUPS = load_golden("groups")
+
+
+@pytest.mark.parametrize("impl", [fo, c_oracle], ids=["numpy", "c"])
+@pytest.mark.parametrize("case", sorted(GROUPS))
+def test_group_assignment_oracles(impl, case):
+    g = GROUPS[case]
+    l_max, ang = g["params"]
+    lab = impl.group_assignment(g["points"], g["triangles"], g["normals"], g["dominant"],
+                                l_max, ang)
+    assert lab.dtype == np.uint8 and np.array_equal(lab, g["labels"])
+    with pytest.raises(ValueError):
+        impl.group_assignment(g["points"], g["triangles"], g["normals"], np.zeros((0, 3)),
+                              l_max, ang)
+
+
 def test_lidar_front_end():
     g = FE["lidar"]
     lam, k, it = g["lap"]
