@@ -121,6 +121,18 @@ int opcfe_triangle_normals(const void* points, int is_f64, const int64_t* triang
 
 /* Replaces the l_max half of segmentation.group_assignment (segmentation.py:59-67,73):
  * flag[t] = longest edge of triangle t > l_max (fp64 edge lengths). */
+/* Replaces _kernels.find_cells (_kernels/__init__.py:27 -> _native.pyx:120 /
+ * _fallback.py:14-44) and, with counts != NULL, the bincount of
+ * accumulator.integrate_normals (accumulator.py:157-173).  queries: n rows taken every
+ * `stride` rows of a contiguous (., 3) f64 array; the accumulator arrays are those of
+ * GaussianAccumulator (s2ids uint64 [n_cells], normals [n_cells][3], neighbors int64
+ * [n_cells][12]).  cells (nullable) [n] receives the cell index (-1 for skipped non-finite
+ * rows in counting mode); counts (nullable) [n_cells] is incremented. */
+int opcfe_find_cells(const double* queries, long long n, long long stride, const uint64_t* ids,
+                     const double* cell_normals, const int64_t* neighbors, long long n_cells,
+                     double slope, double intercept, long long window_lo, long long window_hi,
+                     int64_t* cells, int64_t* counts, opcfe_stream_t stream);
+
 /* Replaces segmentation.group_assignment (segmentation.py:52-74) on a mesh's normals:
  * labels[t] = argmax_g n_t . d_g (first max; fp64 FMA chain as numpy's BLAS matmul),
  * 255 unless the best score >= ang_min, 255 where lmax_flag[t] (nullable) is set.

@@ -154,3 +154,45 @@ def front_end(opc, laplacian=None, bilateral=None, l_max=None):
     if l_max is not None:
         out["lmax_mask"] = max_edge_mask(pts, tris, l_max)
     return out
+
+
+def s2_id(normals):
+    """sfc.py:46-104 (C restatement, libm atan)."""
+    q = _f64(normals).reshape(-1, 3)
+    L = lib()
+    L.oracle_s2id.restype = ctypes.c_uint64
+    L.oracle_s2id.argtypes = [_dp]
+    return np.array([L.oracle_s2id(_ptr(np.ascontiguousarray(r), _dp)) for r in q],
+                    dtype=np.uint64)
+
+
+def find_cells(query_normals, ids_sorted, cell_normals, neighbors, slope, intercept,
+               window_lo, window_hi):
+    """_kernels/_fallback.py:14-44 (C restatement)."""
+    q = _f64(query_normals).reshape(-1, 3)
+    ids = np.ascontiguousarray(ids_sorted, dtype=np.uint64)
+    cn = _f64(cell_normals).reshape(-1, 3)
+    nb = np.ascontiguousarray(neighbors, dtype=np.int64)
+    out = np.empty(len(q), dtype=np.int64)
+    L = lib()
+    L.oracle_find_cells.argtypes = [_dp, ctypes.c_int64, ctypes.POINTER(ctypes.c_uint64), _dp,
+                                    _lp, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                    ctypes.c_int64, ctypes.c_int64, _lp]
+    L.oracle_find_cells(_ptr(q, _dp), len(q), ids.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                        _ptr(cn, _dp), _ptr(nb, _lp), len(ids), float(slope), float(intercept),
+                        int(window_lo), int(window_hi), _ptr(out, _lp))
+    return out
+
+
+def integrate_normals(counts, normals, ids_sorted, cell_normals, neighbors, slope, intercept,
+                      window_lo, window_hi, sample_pct=1.0):
+    """accumulator.py:157-173: vote every round(1/sample_pct)-th finite normal."""
+    normals = np.atleast_2d(np.asarray(normals, dtype=np.float64))
+    stride = max(1, int(round(1.0 / sample_pct)))
+    s = normals[::stride]
+    s = s[np.all(np.isfinite(s), axis=1)]
+    if len(s):
+        idx = find_cells(s, ids_sorted, cell_normals, neighbors, slope, intercept,
+                         window_lo, window_hi)
+        counts = counts + np.bincount(idx, minlength=len(ids_sorted))
+    return counts

@@ -229,6 +229,84 @@ static double edge_len(const double *p, const double *q) {
   return sqrt((dx * dx + dy * dy) + dz * dz);
 }
 
+/* ---- FastGA cell search: sfc.py:46-104 (s2_id) + _kernels/_fallback.py:14-44 (find_cells) */
+#ifndef M_PI
+#define M_PI 3.14159265358979323846 /* == numpy.pi as a double */
+#endif
+#define HB_ORDER 30
+static const int64_t HB_GRID = (int64_t)1 << HB_ORDER;
+/* face chain -y, +x, +z, -x, -z, +y: (u axis, v axis, swap, neg_u, neg_v) (sfc.py:24-31) */
+static const int FACE_U[6] = {0, 1, 0, 1, 0, 0}, FACE_V[6] = {2, 2, 1, 2, 1, 2};
+static const int FACE_SWAP[6] = {0, 1, 0, 1, 1, 0}, FACE_NEGU[6] = {0, 0, 1, 1, 0, 0};
+/* axis*2 + (sign<0) -> face (sfc.py:34-36) */
+static const int FACE_OF[6] = {1, 3, 5, 0, 2, 4};
+
+static int64_t hb_quantize(double t) {
+  double a = atan(t) * (4.0 / M_PI);
+  double f = floor((a + 1.0) * 0.5 * (double)HB_GRID);
+  int64_t i = (int64_t)f;
+  return i < 0 ? 0 : (i > HB_GRID - 1 ? HB_GRID - 1 : i);
+}
+
+static int64_t hb_d(int64_t x, int64_t y) { /* sfc.py:46-61 */
+  int64_t d = 0;
+  for (int64_t s = HB_GRID >> 1; s > 0; s >>= 1) {
+    int64_t rx = (x & s) > 0, ry = (y & s) > 0;
+    d += s * s * ((3 * rx) ^ ry);
+    if (ry == 0) {
+      if (rx == 1) { x = s - 1 - x; y = s - 1 - y; }
+      int64_t t = x; x = y; y = t;
+    }
+  }
+  return d;
+}
+
+uint64_t oracle_s2id(const double *q) {
+  double nrm = sqrt((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]);
+  double n[3] = {q[0] / nrm, q[1] / nrm, q[2] / nrm};
+  int ax = 0; /* argmax |n| (first max) */
+  if (fabs(n[1]) > fabs(n[ax])) ax = 1;
+  if (fabs(n[2]) > fabs(n[ax])) ax = 2;
+  double dom = n[ax];
+  int face = FACE_OF[ax * 2 + (dom < 0)];
+  double u = n[FACE_U[face]] / fabs(dom), v = n[FACE_V[face]] / fabs(dom);
+  int64_t iu = hb_quantize(u), iv = hb_quantize(v);
+  if (FACE_SWAP[face]) { int64_t t = iu; iu = iv; iv = t; }
+  if (FACE_NEGU[face]) iu = HB_GRID - 1 - iu;
+  return ((uint64_t)face << (2 * HB_ORDER)) | (uint64_t)hb_d(iu, iv);
+}
+
+void oracle_find_cells(const double *q, int64_t n, const uint64_t *ids, const double *cn,
+                       const int64_t *nbrs, int64_t ncell, double slope, double icpt, int64_t wlo,
+                       int64_t whi, int64_t *out) {
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    const double *qi = q + 3 * i;
+    uint64_t id = oracle_s2id(qi);
+    int64_t kp = (int64_t)rint(slope * (double)id + icpt);
+    int64_t lo = kp + wlo, hi = kp + whi;
+    lo = lo < 0 ? 0 : (lo > ncell - 1 ? ncell - 1 : lo);
+    hi = hi < 0 ? 0 : (hi > ncell - 1 ? ncell - 1 : hi);
+    int64_t a = 0, b = ncell; /* searchsorted left */
+    while (a < b) { int64_t m = (a + b) / 2; if (ids[m] < id) a = m + 1; else b = m; }
+    int64_t ch = a < lo ? lo : (a > hi ? hi : a);
+    int64_t cl = a - 1 < lo ? lo : (a - 1 > hi ? hi : a - 1);
+    uint64_t dh = ids[ch] > id ? ids[ch] - id : id - ids[ch];
+    uint64_t dl = ids[cl] > id ? ids[cl] - id : id - ids[cl];
+    int64_t j = dl <= dh ? cl : ch;
+    int64_t best = j;
+    double bd = INFINITY;
+    for (int k = -1; k < 12; ++k) {
+      int64_t c = k < 0 ? j : nbrs[12 * j + k];
+      if (c < 0) continue;
+      double dx = cn[3 * c] - qi[0], dy = cn[3 * c + 1] - qi[1], dz = cn[3 * c + 2] - qi[2];
+      double d2 = (dx * dx + dy * dy) + dz * dz;
+      if (d2 < bd) { bd = d2; best = c; }
+    }
+    out[i] = best;
+  }
+}
+
 /* group labels: segmentation.py:52-74.  Scores in the FMA order of numpy's BLAS matmul
  * (normals @ dn.T -> dgemm k-loop: fma(n2,d2, fma(n1,d1, n0*d0))); first maximum wins,
  * NaN maximal; 255 unless best >= ang_min; flag (nullable) forces 255. */

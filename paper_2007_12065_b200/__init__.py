@@ -7,8 +7,9 @@ sm_100a CUDA kernels behind a C ABI (include/opcfe.h, lib/libopcfe.so).
 There is no CPU fallback.
 """
 
-from . import _kernels, synthetic
+from . import _kernels, accumulator, synthetic
 from ._kernels import ACTIVE as kernel_backend
+from .accumulator import find_cell_indices, integrate_normals
 from .frontend import FrontEnd, FrontEndResult, HostPipeline, front_end
 from .geometry import DegenerateInputError, triangle_normals
 from .mesh import (HalfEdgeMesh, compute_normals, extract_halfedges_opc, extract_triangles_opc,

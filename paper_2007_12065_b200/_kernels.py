@@ -35,8 +35,17 @@ def bilateral_iterate(centroids, normals, sigma_length, sigma_angle, kernel_size
     return Nn.give(res)
 
 
-def find_cells(*args, **kwargs):  # pragma: no cover - outside the OPC front-end hot path
-    raise NotImplementedError("find_cells (FastGA) is outside this build's scope (SURVEY.md 8f)")
+def find_cells(query_normals, ids_sorted, cell_normals, neighbors, slope, intercept,
+               window_lo, window_hi):
+    """Same contract as _kernels.find_cells (_native.pyx:120 / _fallback.py:14-44)."""
+    from types import SimpleNamespace
+
+    from .accumulator import DeviceAccumulator
+    Q = Staged(query_normals)
+    ga = SimpleNamespace(s2ids=ids_sorted, normals=cell_normals, neighbors=neighbors,
+                         model_slope=slope, model_intercept=intercept, window_lo=window_lo,
+                         window_hi=window_hi)
+    return Q.give(DeviceAccumulator(ga).search(Q.dev.to(torch.float64)))
 
 
 def grow_segment(*args, **kwargs):  # pragma: no cover - outside the OPC front-end hot path

@@ -27,7 +27,7 @@ EXPORTS = (
     "opcfe_vmask_words", "opcfe_triangulate_workspace", "opcfe_stage_in", "opcfe_unstage",
     "opcfe_laplacian",
     "opcfe_triangulate", "opcfe_halfedges_from_trimap", "opcfe_fc_data", "opcfe_bilateral",
-    "opcfe_triangle_normals", "opcfe_group_assignment", "opcfe_max_edge_mask", "opcfe_front_end_workspace",
+    "opcfe_triangle_normals", "opcfe_find_cells", "opcfe_group_assignment", "opcfe_max_edge_mask", "opcfe_front_end_workspace",
     "opcfe_front_end", "opcfe_front_end_profiled",
 )
 
@@ -99,6 +99,7 @@ def _declare(L):
         "opcfe_bilateral": (i, [vp, i, i, i, i, vp, vp, f, f, i, i, vp, vp, vp, vp, vp, ll, vp]),
         "opcfe_triangle_normals": (i, [vp, i, vp, ll, vp, vp]),
         "opcfe_max_edge_mask": (i, [vp, i, vp, ll, d, vp, vp]),
+        "opcfe_find_cells": (i, [vp, ll, ll, vp, vp, vp, ll, d, d, ll, ll, vp, vp, vp]),
         "opcfe_group_assignment": (i, [vp, i, ll, i, vp, vp, i, d, vp, vp, vp]),
         "opcfe_front_end_workspace": (sz, [i, i, i, ctypes.POINTER(FrontEndParams), i, i]),
         "opcfe_front_end": (i, [i, i, i, ctypes.POINTER(FrontEndParams),

@@ -183,6 +183,15 @@ int opcfe_triangle_normals(const void* points, int is_f64, const int64_t* triang
   return triangle_normals(points, is_f64 != 0, triangles, n_tri, normals, S(stream));
 }
 
+int opcfe_find_cells(const double* queries, long long n, long long stride, const uint64_t* ids,
+                     const double* cell_normals, const int64_t* neighbors, long long n_cells,
+                     double slope, double intercept, long long window_lo, long long window_hi,
+                     int64_t* cells, int64_t* counts, opcfe_stream_t stream) {
+  if (!queries) return fail(ERR_INVALID, "find_cells: null queries");
+  return find_cells(queries, n, stride, ids, cell_normals, neighbors, n_cells, slope, intercept,
+                    window_lo, window_hi, cells, counts, S(stream));
+}
+
 int opcfe_group_assignment(const void* normals, int is_f64, long long T, int F,
                            const int64_t* n_tri, const double* dominant, int n_dominant,
                            double ang_min, const uint8_t* lmax_flag, uint8_t* labels,

@@ -30,6 +30,10 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
 int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st);
 int triangle_normals(const void* pts, bool f64, const int64_t* tris, long long T, void* out,
                      cudaStream_t st);
+int find_cells(const double* queries, long long n, long long stride, const uint64_t* ids,
+               const double* cell_normals, const int64_t* neighbors, long long n_cells,
+               double slope, double intercept, long long window_lo, long long window_hi,
+               int64_t* cells, int64_t* counts, cudaStream_t st);
 int group_assignment(const void* normals, bool f64, long long T, int F, const int64_t* n_tri,
                      const double* dominant, int G, double ang_min, const uint8_t* lflag,
                      uint8_t* labels, cudaStream_t st);

@@ -270,7 +270,37 @@ def main():
     grp["exact/params"] = np.array([1.0, 1.0])
     grp["exact/labels"] = group_assignment(msh, up, 1.0, 1.0)
     np.savez_compressed(os.path.join(HERE, "groups.npz"), **grp)
-    for f in ("topology", "laplacian", "bilateral", "frontend", "groups"):
+
+    # ------------------------------------ FastGA cell search (_kernels.find_cells, 8f rank 2)
+    from flatpoly import sfc
+    from flatpoly.accumulator import build_accumulator, integrate_normals
+    ga_out = {}
+    rng = np.random.default_rng(4242)
+    for level in (2, 4):
+        ga = build_accumulator(level)
+        q = rng.normal(size=(20000, 3))
+        q /= np.linalg.norm(q, axis=1)[:, None]
+        q[:50] *= 3.7                               # non-unit rows (normalised inside s2_id)
+        q[50:60] = ga.normals[:10]                  # exact cell normals
+        args = (q, ga.s2ids, ga.normals, ga.neighbors, ga.model_slope, ga.model_intercept,
+                ga.window_lo, ga.window_hi)
+        key = f"level{level}"
+        ga_out[f"{key}/queries"] = q
+        ga_out[f"{key}/ids"] = ga.s2ids
+        ga_out[f"{key}/cell_normals"] = ga.normals
+        ga_out[f"{key}/neighbors"] = ga.neighbors
+        ga_out[f"{key}/model"] = np.array([ga.model_slope, ga.model_intercept,
+                                            ga.window_lo, ga.window_hi])
+        ga_out[f"{key}/s2id"] = sfc.s2_id(q)
+        ga_out[f"{key}/cells"] = _fallback.find_cells(*args)
+        ga_out[f"{key}/cells_native"] = native.find_cells(*args)
+        # integrate_normals over the room mesh normals (bilateral), 12 % sampling
+        ga.counts[:] = 0
+        counts = integrate_normals(ga, mesh.normals, sample_pct=0.12)
+        ga_out[f"{key}/mesh_normals"] = mesh.normals
+        ga_out[f"{key}/counts"] = counts.copy()
+    np.savez_compressed(os.path.join(HERE, "fastga.npz"), **ga_out)
+    for f in ("topology", "laplacian", "bilateral", "frontend", "groups", "fastga"):
         p = os.path.join(HERE, f + ".npz")
         print(f"{p}: {os.path.getsize(p) / 1024:.1f} KiB")
 

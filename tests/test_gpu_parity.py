@@ -538,6 +538,50 @@ def test_front_end_fused_labels(fe):
     assert 0 < (lab == 255).sum() < T and eng.kernel_launches == 3 + 1 + 2 + 1
 
 
+FASTGA = load_golden("fastga")
+
+
+@pytest.mark.parametrize("case", sorted(FASTGA))
+def test_golden_find_cells_and_integrate(fe, case):
+    """FastGA cell search (the reference's _kernels.find_cells) and histogram votes.
+    Reference bar (tests/test_kernels.py:19-33): >= 0.9999 agreement with every
+    disagreement inside the 1-ring (CUDA vs glibc atan ulps); measured: exact."""
+    from types import SimpleNamespace
+    g = FASTGA[case]
+    slope, icpt, wlo, whi = g["model"]
+    cells = fe._kernels.find_cells(g["queries"], g["ids"], g["cell_normals"], g["neighbors"],
+                                   slope, icpt, int(wlo), int(whi))
+    assert cells.dtype == np.int64 and cells.shape == g["cells"].shape
+    agree = cells == g["cells"]
+    assert agree.mean() >= 0.9999
+    for i in np.nonzero(~agree)[0]:
+        assert cells[i] in g["neighbors"][g["cells"][i]]
+    ga = SimpleNamespace(s2ids=g["ids"], normals=g["cell_normals"], neighbors=g["neighbors"],
+                         model_slope=slope, model_intercept=icpt, window_lo=int(wlo),
+                         window_hi=int(whi), counts=np.zeros(len(g["ids"]), dtype=np.int64))
+    counts = fe.integrate_normals(ga, g["mesh_normals"], sample_pct=0.12)
+    assert counts.sum() == g["counts"].sum()
+    assert np.abs(counts - g["counts"]).sum() <= 2 * (~agree).sum() + 2
+    assert np.array_equal(fe.find_cell_indices(ga, g["queries"][:500]), cells[:500])
+    with pytest.raises(ValueError):
+        fe.find_cell_indices(ga, np.zeros((2, 3)))
+
+
+def test_find_cells_large_vs_c_oracle(fe):
+    g = FASTGA["level4"]
+    slope, icpt, wlo, whi = g["model"]
+    rng = np.random.default_rng(3)
+    q = rng.normal(size=(400000, 3))
+    ref = c_oracle.find_cells(q, g["ids"], g["cell_normals"], g["neighbors"], slope, icpt,
+                              int(wlo), int(whi))
+    got = fe._kernels.find_cells(q, g["ids"], g["cell_normals"], g["neighbors"], slope, icpt,
+                                 int(wlo), int(whi))
+    agree = got == ref
+    assert agree.mean() >= 0.9999
+    for i in np.nonzero(~agree)[0]:
+        assert got[i] in g["neighbors"][ref[i]]
+
+
 def test_host_pipeline_matches_device_engine(fe):
     """HostPipeline (overlapped H2D / graph / D2H per frame) returns exactly what the
     device engine computes, with D2H sized by each frame's triangle count."""

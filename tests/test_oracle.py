@@ -131,6 +131,24 @@ def test_group_assignment_oracles(impl, case):
                               l_max, ang)
 
 
+FASTGA = load_golden("fastga")
+
+
+@pytest.mark.parametrize("case", sorted(FASTGA))
+def test_fastga_c_oracle(case):
+    """C restatement of sfc.s2_id + find_cells + integrate_normals == the reference."""
+    g = FASTGA[case]
+    slope, icpt, wlo, whi = g["model"]
+    assert np.array_equal(c_oracle.s2_id(g["queries"][:2000]), g["s2id"][:2000])
+    cells = c_oracle.find_cells(g["queries"], g["ids"], g["cell_normals"], g["neighbors"],
+                                slope, icpt, int(wlo), int(whi))
+    assert np.array_equal(cells, g["cells"]) and np.array_equal(cells, g["cells_native"])
+    counts = c_oracle.integrate_normals(np.zeros(len(g["ids"]), dtype=np.int64),
+                                        g["mesh_normals"], g["ids"], g["cell_normals"],
+                                        g["neighbors"], slope, icpt, int(wlo), int(whi), 0.12)
+    assert np.array_equal(counts, g["counts"])
+
+
 def test_lidar_front_end():
     g = FE["lidar"]
     lam, k, it = g["lap"]
