@@ -290,7 +290,6 @@ __global__ void __launch_bounds__(kBilNT, 3)
             acc[o][k][0] = fmaf(nb[kk].nx, w, acc[o][k][0]);
             acc[o][k][1] = fmaf(nb[kk].ny, w, acc[o][k][1]);
             acc[o][k][2] = fmaf(nb[kk].nz, w, acc[o][k][2]);
-            acc[o][k][3] += w;
           }
         }
       }
@@ -310,14 +309,18 @@ __global__ void __launch_bounds__(kBilNT, 3)
       r[1] = n[1];
       r[2] = n[2];
       const bool valid = !(isnan(n[0]) || isnan(n[1]) || isnan(n[2]));
-      const float ws = acc[o][k][3];
-      if (valid && ws > 0.f) {
-        const float iw = rcp_approx(ws);
-        const float mx = acc[o][k][0] * iw, my = acc[o][k][1] * iw, mz = acc[o][k][2] * iw;
+      // wsum is not accumulated: wsum == 0 implies acc == 0, so the reference's
+      // `wsum > 0 and |acc| > 1e-30` (_native.pyx:352-360) is just |acc| > 1e-30, here
+      // |acc'| > 1e-30 sqrt(B) evaluated underflow-safely as s * |acc'/s|, s = max |acc'_i|
+      const float ax = acc[o][k][0], ay = acc[o][k][1], az = acc[o][k][2];
+      const float s = fmaxf(fabsf(ax), fmaxf(fabsf(ay), fabsf(az)));
+      if (valid && s > 0.f) {
+        const float is = rcp_approx(s);  // a common scale: cancels in the normalisation
+        const float mx = ax * is, my = ay * is, mz = az * is;
         // IEEE sqrt + reciprocal (~1.5 ulp): the stored normals feed the next iteration's
         // weights, so rounding here compounds over the iterations
         const float len = sqrtf(mx * mx + my * my + mz * mz);
-        if (len * ws > thr) {
+        if (len * s > thr) {
           const float il = 1.0f / len;
           r[0] = mx * il;
           r[1] = my * il;
