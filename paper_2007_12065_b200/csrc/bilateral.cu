@@ -371,12 +371,8 @@ template <int H, int MODE, bool SCATTER>
 int launch_bil(const CUtensorMap& tp, const CUtensorMap& tn, const CUtensorMap& tc,
                const CUtensorMap& to, const BilArgs& a, int F, cudaStream_t st) {
   constexpr int smem = bil_smem_bytes<H, MODE>();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(bilateral_kernel<H, MODE, SCATTER>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static unsigned long long attr_mask = 0;
+  ensure_smem_attr(bilateral_kernel<H, MODE, SCATTER>, smem, attr_mask);
   const int Mq = a.M - 1, Nq = a.N - 1;
   dim3 grid((Nq + kBilTQW - 1) / kBilTQW, (Mq + kBilTQH - 1) / kBilTQH, F);
   bilateral_kernel<H, MODE, SCATTER><<<grid, kBilNT, smem, st>>>(tp, tn, tc, to, a);
@@ -789,11 +785,11 @@ template <int MODE, bool SCATTER>
 int launch_sym(const CUtensorMap& tp, const CUtensorMap& tn, const CUtensorMap& tc,
                const CUtensorMap& to, const BilArgs& a, int F, cudaStream_t st) {
   constexpr int smem = sym_smem_bytes<MODE>();
-  static int resident = 0;  // CTAs per SM (queried once per process / device setup)
+  static unsigned long long attr_mask = 0;
+  ensure_smem_attr(bilateral_sym_kernel<MODE, SCATTER>, smem, attr_mask);
+  static int resident = 0;  // CTAs per SM (same on every B200 of the box)
   static int sms = 0;
   if (resident == 0) {
-    cudaFuncSetAttribute(bilateral_sym_kernel<MODE, SCATTER>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

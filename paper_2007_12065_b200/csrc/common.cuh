@@ -43,6 +43,18 @@ int make_tmap_3d(CUtensorMap* map, const void* base, bool f64, uint64_t cols, ui
                  uint64_t frames, uint64_t row_pitch_elems, uint64_t frame_stride_elems,
                  uint32_t box_cols, uint32_t box_rows);
 
+// Opt a kernel into `smem` bytes of dynamic shared memory on the CURRENT device, once per
+// device (the attribute is per device context; `mask` is the caller's per-kernel bitset).
+template <typename Kernel>
+inline void ensure_smem_attr(Kernel kernel, int smem, unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !((mask >> dev) & 1ull)) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    mask |= 1ull << dev;
+  }
+}
+
 // ------------------------------------------------------------- device helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

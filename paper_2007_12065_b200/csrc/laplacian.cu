@@ -134,11 +134,8 @@ template <int H>
 int launch_one(const CUtensorMap& tin, const CUtensorMap& tout, uint32_t* vmask, long long vm_fs,
                int wpr, int F, int M, int N, float lam, cudaStream_t st) {
   using T = LapTile<H>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(laplacian_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
-    attr_set = true;
-  }
+  static unsigned long long attr_mask = 0;
+  ensure_smem_attr(laplacian_kernel<H>, T::SMEM, attr_mask);
   dim3 grid((N + kLapTW - 1) / kLapTW, (M + kLapTH - 1) / kLapTH, F);
   laplacian_kernel<H><<<grid, kLapNT, T::SMEM, st>>>(tin, tout, vmask, vm_fs, wpr, M, N, lam);
   return check_launch("laplacian_kernel");
