@@ -22,7 +22,7 @@
 //     reference's "off-grid neighbours are skipped"): the point tile (centroids are
 //     recomputed from points every iteration: 12 B/point instead of 24 B/quad of
 //     stored centroids) and, after iteration 1, the previous normal tile;
-//   * a pack step turns each halo quad into 4 float4 planes (conflict-free LDS.128):
+//   * a pack step turns each halo quad into 3 float4 planes (conflict-free LDS.128):
 //     per triangle n' = n*sqrt(B), c' = c*sqrt(A) with B, A the exponent scales
 //     pre-multiplied by log2(e), so  w = ex2(-(|c'_i - c'_j|^2 + |n'_i - n'_j|^2)).
 //     Missing / NaN-normal triangles carry n' = 0, c' = 1e18, so their weight to any
@@ -46,10 +46,16 @@ namespace {
 // pair-symmetric persistent kernel below (half the weights, but 121 registers -> 2 CTAs
 // per SM; measured 3.24 vs 2.77 ms per 8 x 1080p x 5 iterations on B200, kept for A/B).
 static const bool g_bil_direct = std::getenv("OPCFE_BILATERAL_SYM") == nullptr;
+// OPCFE_BILATERAL_WS=1 selects the warp-specialised persistent kernel (A/B: measured
+// 2.85 vs 2.43 ms for the direct kernel at 4 CTAs/SM, 8 x 1080p x 5 iterations)
+static const bool g_bil_ws = std::getenv("OPCFE_BILATERAL_WS") != nullptr;
 
 constexpr int kBilTQW = 32;  // interior quads per tile row (= one warp)
 constexpr int kBilTQH = 16;  // interior quad rows per tile (2 per thread)
 constexpr int kBilNT = 256;
+// resident CTAs per SM the register budget targets: k = 3 fits 4 x 55 KB of smem (64
+// registers), larger windows are smem-limited to 3 (80 registers)
+constexpr int bil_min_blocks(int h) { return h == 1 ? 4 : 3; }
 
 enum BilMode : int {
   kFromPoints = 0,     // iteration 1: normals + centroids from the point grid
@@ -72,7 +78,7 @@ struct BilTile {
   static constexpr int NQ = QW * QH;      // quads in the pack
   static constexpr int PTS_F = ((PW * 3 * PH) + 31) / 32 * 32;
   static constexpr int FC_F = ((QW * 6 * QH) + 31) / 32 * 32;
-  static constexpr int PACK_F = 16 * NQ;  // 4 float4 planes
+  static constexpr int PACK_F = 12 * NQ;  // 3 float4 planes (pack_quad)
   static constexpr int OUT_F = kBilTQW * 6 * kBilTQH;
   static_assert(QW * 6 <= 256 && PW * 3 <= 256 && PH <= 256, "TMA box extent must be <= 256");
   static_assert((QW * 6) % 4 == 0, "FC box rows must be 16-B multiples");
@@ -99,6 +105,9 @@ struct BilArgs {
   float* out_mesh;   // scatter destination: per frame [cap][3]
   long long out_fs;  // floats per frame
   long long n_out;   // rows per frame available in out_mesh (bounds check)
+  const float* raw_n;  // this launch's input FC normals (modes 1, 2): "unchanged" outputs
+  int raw_pitch;       // floats per FC quad row
+  long long raw_fs;    // floats per frame
 };
 
 // FC normal for the bilateral input: edges and cross product in fp64 (exact edge
@@ -130,12 +139,8 @@ __device__ __forceinline__ void unit_normal_fast(const float* pa, const float* p
 }
 
 struct Tri {
-  float nx, ny, nz, S, cx, cy, cz;
+  float nx, ny, nz, cx, cy, cz;
 };
-
-__device__ __forceinline__ Tri tri_from(const float4& n, const float4& c) {
-  return Tri{n.x, n.y, n.z, n.w, c.x, c.y, c.z};
-}
 
 // log2 of the weight between two packed triangles: -(|dc'|^2 + |dn'|^2).  Both terms
 // from differences: the dot form |n_i|^2 + |n_j|^2 - 2 n_i.n_j cancels catastrophically
@@ -151,8 +156,36 @@ __device__ __forceinline__ float neg_log2w(const Tri& i, const Tri& j) {
   return fmaf(-ez, ez, e);
 }
 
+// pack one quad (both triangles) into 3 float4 planes (conflict-free LDS.128):
+//   P0 = (n0'xyz, c0'x)  P1 = (c0'yz, n1'xy)  P2 = (n1'z, c1'xyz)
+// n' = n*sqrt(B), c' = c*sqrt(A); a triangle with a NaN normal or centroid is encoded as
+// n' = 0, c' = 1e18 (its weight to / from any valid triangle underflows to exactly 0).
+__device__ __forceinline__ void pack_quad(float4* pk, int nq, int q, const float* n,
+                                          const float* cc, float sA, float sB) {
+  float v[12];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const bool ok = !(isnan(n[3 * k]) || isnan(n[3 * k + 1]) || isnan(n[3 * k + 2]) ||
+                      isnan(cc[3 * k]) || isnan(cc[3 * k + 1]) || isnan(cc[3 * k + 2]));
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      v[6 * k + j] = ok ? n[3 * k + j] * sB : 0.f;
+      v[6 * k + 3 + j] = ok ? cc[3 * k + j] * sA : 1e18f;
+    }
+  }
+  pk[q] = make_float4(v[0], v[1], v[2], v[3]);
+  pk[nq + q] = make_float4(v[4], v[5], v[6], v[7]);
+  pk[2 * nq + q] = make_float4(v[8], v[9], v[10], v[11]);
+}
+
+__device__ __forceinline__ void load_quad(const float4* pk, int nq, int q, Tri* t) {
+  const float4 a0 = pk[q], a1 = pk[nq + q], a2 = pk[2 * nq + q];
+  t[0] = Tri{a0.x, a0.y, a0.z, a0.w, a1.x, a1.y};
+  t[1] = Tri{a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+}
+
 template <int H, int MODE, bool SCATTER>
-__global__ void __launch_bounds__(kBilNT, 3)
+__global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     bilateral_kernel(const __grid_constant__ CUtensorMap tpts, const __grid_constant__ CUtensorMap tnrm,
                      const __grid_constant__ CUtensorMap tcen, const __grid_constant__ CUtensorMap tout,
                      BilArgs a) {
@@ -166,7 +199,7 @@ __global__ void __launch_bounds__(kBilNT, 3)
   if (MODE != kNormalsCentBuf) { pts_s = p; p += T::PTS_F; }
   if (MODE != kFromPoints) { nrm_s = p; p += T::FC_F; }
   if (MODE == kNormalsCentBuf) { cen_s = p; p += T::FC_F; }
-  float4* pk = reinterpret_cast<float4*>(p);  // planes: [0] n0',S0 [1] c0' [2] n1',S1 [3] c1'
+  float4* pk = reinterpret_cast<float4*>(p);  // 3 planes, see pack_quad
   p += T::PACK_F;
   float* out_s = (MODE == kFromPoints) ? p : nrm_s;
   uint64_t& bar = *barp;
@@ -229,18 +262,7 @@ __global__ void __launch_bounds__(kBilNT, 3)
         }
       }
     }
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const bool ok = !(isnan(n[3 * k]) || isnan(n[3 * k + 1]) || isnan(n[3 * k + 2]) ||
-                        isnan(cc[3 * k]) || isnan(cc[3 * k + 1]) || isnan(cc[3 * k + 2]));
-      const float nx = ok ? n[3 * k] * sB : 0.f, ny = ok ? n[3 * k + 1] * sB : 0.f,
-                  nz = ok ? n[3 * k + 2] * sB : 0.f;
-      const float S = nx * nx + ny * ny + nz * nz;
-      pk[(2 * k) * T::NQ + q] = make_float4(nx, ny, nz, S);
-      pk[(2 * k + 1) * T::NQ + q] = ok ? make_float4(cc[3 * k] * sA, cc[3 * k + 1] * sA,
-                                                     cc[3 * k + 2] * sA, 0.f)
-                                       : make_float4(1e18f, 1e18f, 1e18f, 0.f);
-    }
+    pack_quad(pk, T::NQ, q, n, cc, sA, sB);
   }
   __syncthreads();
 
@@ -257,11 +279,7 @@ __global__ void __launch_bounds__(kBilNT, 3)
   }
   Tri own[2][2];
 #pragma unroll
-  for (int o = 0; o < 2; ++o) {
-    const int q = (R0 + o) * T::QW + C;
-    own[o][0] = tri_from(pk[q], pk[T::NQ + q]);
-    own[o][1] = tri_from(pk[2 * T::NQ + q], pk[3 * T::NQ + q]);
-  }
+  for (int o = 0; o < 2; ++o) load_quad(pk, T::NQ, (R0 + o) * T::QW + C, own[o]);
   float acc[2][2][4];  // [own quad][triangle][x, y, z, wsum]
 #pragma unroll
   for (int o = 0; o < 2; ++o)
@@ -274,9 +292,8 @@ __global__ void __launch_bounds__(kBilNT, 3)
   for (int dr = -H; dr <= H + 1; ++dr) {
 #pragma unroll
     for (int dc = -H; dc <= H; ++dc) {
-      const int q = (R0 + dr) * T::QW + C + dc;
-      const Tri nb[2] = {tri_from(pk[q], pk[T::NQ + q]),
-                         tri_from(pk[2 * T::NQ + q], pk[3 * T::NQ + q])};
+      Tri nb[2];
+      load_quad(pk, T::NQ, (R0 + dr) * T::QW + C + dc, nb);
 #pragma unroll
       for (int o = 0; o < 2; ++o) {
         const int du = dr - o;
@@ -379,10 +396,305 @@ int launch_bil(const CUtensorMap& tp, const CUtensorMap& tn, const CUtensorMap& 
   return check_launch("bilateral_kernel");
 }
 
+// ============================================================================
+// Warp-specialised persistent kernel (default).  The direct kernel above loses ~30 % of
+// its issue slots to CTA-phase bubbles: TMA wait at CTA start, the pack phase's last
+// partial round in front of a __syncthreads, the store at the end (ncu: 74 % issue-
+// active).  Here each persistent CTA has
+//   * 4 PRODUCER warps: wait for the TMA tile, pack it (pre-scaled, sentinel-encoded,
+//     3 float4 planes) into one of TWO pack buffers, release it through an mbarrier
+//     ("full"), and immediately TMA-load the next tile into the (now dead) input tiles;
+//   * 8 CONSUMER warps: wait "full", weigh and accumulate 2 quads per thread, release the
+//     pack ("empty"), and TMA-store / scatter the results,
+// so packing and loading tile i+1 overlap the compute of tile i.  The input tiles are
+// dead once packed, so consumers never see them: an output left unchanged (missing /
+// isolated / |acc| <= 1e-30) re-reads its input normal from global memory (modes 1, 2)
+// or is n'/sqrt(B) (<= 1 ulp of the FC normal; NaN where c' carries the sentinel).
+// ============================================================================
+constexpr int kWsCons = kBilNT;          // consumer threads (8 warps)
+constexpr int kWsProd = 128;             // producer threads (4 warps)
+constexpr int kWsThreads = kWsCons + kWsProd;
+
+template <int H, int MODE>
+constexpr int ws_smem_bytes() {
+  using T = BilTile<H>;
+  return (((MODE != kNormalsCentBuf) ? T::PTS_F : 0) + ((MODE != kFromPoints) ? T::FC_F : 0) +
+          ((MODE == kNormalsCentBuf) ? T::FC_F : 0) + 2 * T::PACK_F + T::OUT_F) *
+             4 +
+         64 + kSmemSlack;
+}
+
+template <int H, int MODE, bool SCATTER>
+__global__ void __launch_bounds__(kWsThreads, 2)
+    bilateral_ws_kernel(const __grid_constant__ CUtensorMap tpts,
+                        const __grid_constant__ CUtensorMap tnrm,
+                        const __grid_constant__ CUtensorMap tcen,
+                        const __grid_constant__ CUtensorMap tout, BilArgs a) {
+  using T = BilTile<H>;
+  constexpr int NQ = T::NQ;
+  extern __shared__ __align__(16) char smem_raw[];
+  uint64_t* tma_bar;
+  float* p = reinterpret_cast<float*>(smem_aligned_base(smem_raw, &tma_bar));
+  float* pts_s = nullptr;
+  float* nrm_s = nullptr;
+  float* cen_s = nullptr;
+  if (MODE != kNormalsCentBuf) { pts_s = p; p += T::PTS_F; }
+  if (MODE != kFromPoints) { nrm_s = p; p += T::FC_F; }
+  if (MODE == kNormalsCentBuf) { cen_s = p; p += T::FC_F; }
+  float4* const packs = reinterpret_cast<float4*>(p);  // 2 buffers x 3 planes x NQ
+  p += 2 * T::PACK_F;
+  float* out_s = p;
+  p += T::OUT_F;
+  uint64_t* full = reinterpret_cast<uint64_t*>(p);  // [2]
+  uint64_t* empty = full + 2;                       // [2]
+
+  const int Mq = a.M - 1, Nq = a.N - 1;
+  const int tiles_x = (Nq + kBilTQW - 1) / kBilTQW, tiles_y = (Mq + kBilTQH - 1) / kBilTQH;
+  const int n_tiles = tiles_x * tiles_y * a.F;
+  auto tile_origin = [&](int tile, int& q0, int& u0, int& f) {
+    q0 = (tile % tiles_x) * kBilTQW;
+    u0 = ((tile / tiles_x) % tiles_y) * kBilTQH;
+    f = tile / (tiles_x * tiles_y);
+  };
+  auto issue = [&](int tile) {
+    int q0, u0, f;
+    tile_origin(tile, q0, u0, f);
+    uint32_t bytes = 0;
+    if (MODE != kNormalsCentBuf) bytes += T::PW * 3 * T::PH * 4;
+    if (MODE != kFromPoints) bytes += T::QW * 6 * T::QH * 4;
+    if (MODE == kNormalsCentBuf) bytes += T::QW * 6 * T::QH * 4;
+    mbar_expect_tx(tma_bar, bytes);
+    if (MODE != kNormalsCentBuf) tma_load_3d(pts_s, &tpts, tma_bar, (q0 - T::LP) * 3, u0 - H, f);
+    if (MODE != kFromPoints) tma_load_3d(nrm_s, &tnrm, tma_bar, (q0 - T::LQ) * 6, u0 - H, f);
+    if (MODE == kNormalsCentBuf) tma_load_3d(cen_s, &tcen, tma_bar, (q0 - T::LQ) * 6, u0 - H, f);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(tma_bar, 1);
+    mbar_init(&full[0], kWsProd);
+    mbar_init(&full[1], kWsProd);
+    mbar_init(&empty[0], kWsCons);
+    mbar_init(&empty[1], kWsCons);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const float sA = a.sA, sB = a.sB;
+
+  if (threadIdx.x >= kWsCons) {
+    // ------------------------------------------------------------ producer warps
+    const int pt = threadIdx.x - kWsCons;
+    if (pt == 0 && (int)blockIdx.x < n_tiles) issue(blockIdx.x);
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      const int s = it & 1;
+      float4* pk = packs + s * 3 * NQ;
+      mbar_wait(tma_bar, it & 1);                              // input tile landed
+      if (it >= 2) mbar_wait(&empty[s], ((it >> 1) - 1) & 1);  // pack s released
+      for (int q = pt; q < NQ; q += kWsProd) {
+        const int r = q / T::QW, c = q % T::QW;
+        float n[6], cc[6];
+        if (MODE == kNormalsCentBuf) {
+#pragma unroll
+          for (int j = 0; j < 6; ++j) {
+            n[j] = nrm_s[q * 6 + j];
+            cc[j] = cen_s[q * 6 + j];
+          }
+        } else {
+          const float* P1 = pts_s + (r * T::PW + c + T::PSHIFT) * 3;
+          const float* P2 = P1 + 3;
+          const float* P4 = P1 + T::PW * 3;
+          const float* P3 = P4 + 3;
+          const float* tri[2][3] = {{P3, P2, P1}, {P1, P4, P3}};
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const float *pa = tri[k][0], *pb = tri[k][1], *pc = tri[k][2];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) cc[3 * k + j] = ((pa[j] + pb[j]) + pc[j]) * (1.0f / 3.0f);
+            if (MODE == kFromPoints) unit_normal_fast(pa, pb, pc, n + 3 * k);
+          }
+          if (MODE == kNormalsBuf) {
+#pragma unroll
+            for (int j = 0; j < 6; ++j) n[j] = nrm_s[q * 6 + j];
+          }
+        }
+        pack_quad(pk, NQ, q, n, cc, sA, sB);
+      }
+      named_bar_sync(2, kWsProd);  // every producer is done reading the input tiles
+      if (pt == 0 && tile + (int)gridDim.x < n_tiles) issue(tile + gridDim.x);
+      mbar_arrive(&full[s]);
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumer warps
+  const int tx = threadIdx.x % kBilTQW, ty = threadIdx.x / kBilTQW;  // ty in [0, 8)
+  const int R0 = 2 * ty + H, C = tx + T::LQ;                         // pack pos of quad 0
+  const float inv_sB = 1.0f / sB;
+  const float thr = 1e-30f * sB;
+  int it = 0;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+    const int s = it & 1;
+    const float4* pk = packs + s * 3 * NQ;
+    int q0, u0, f;
+    tile_origin(tile, q0, u0, f);
+    mbar_wait(&full[s], (it >> 1) & 1);
+    auto load2 = [&](int q, Tri* t) { load_quad(pk, NQ, q, t); };
+    Tri own[2][2];
+    load2(R0 * T::QW + C, own[0]);
+    load2((R0 + 1) * T::QW + C, own[1]);
+    float acc[2][2][3];
+#pragma unroll
+    for (int o = 0; o < 2; ++o)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) acc[o][k][0] = acc[o][k][1] = acc[o][k][2] = 0.f;
+#pragma unroll
+    for (int dr = -H; dr <= H + 1; ++dr) {
+#pragma unroll
+      for (int dc = -H; dc <= H; ++dc) {
+        Tri nb[2];
+        load2((R0 + dr) * T::QW + C + dc, nb);
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          const int du = dr - o;
+          if (du < -H || du > H) continue;
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              if (du == 0 && dc == 0 && kk == k) continue;
+              const float w = ex2_approx(neg_log2w(own[o][k], nb[kk]));
+              acc[o][k][0] = fmaf(nb[kk].nx, w, acc[o][k][0]);
+              acc[o][k][1] = fmaf(nb[kk].ny, w, acc[o][k][1]);
+              acc[o][k][2] = fmaf(nb[kk].nz, w, acc[o][k][2]);
+            }
+          }
+        }
+      }
+    }
+    mbar_arrive(&empty[s]);  // pack s may be refilled (all reads above are done)
+
+    float res[2][6];
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        float* r = &res[o][3 * k];
+        const Tri& t = own[o][k];
+        const bool valid = t.cx != 1e18f;
+        // |acc| > 1e-30 (wsum > 0 implied), underflow-safe: s * |acc/s|, s = max |acc_i|
+        const float ax = acc[o][k][0], ay = acc[o][k][1], az = acc[o][k][2];
+        const float sc = fmaxf(fabsf(ax), fmaxf(fabsf(ay), fabsf(az)));
+        bool upd = false;
+        if (valid && sc > 0.f) {
+          const float is = rcp_approx(sc);
+          const float mx = ax * is, my = ay * is, mz = az * is;
+          const float len = sqrtf(mx * mx + my * my + mz * mz);
+          if (len * sc > thr) {
+            const float il = 1.0f / len;
+            r[0] = mx * il;
+            r[1] = my * il;
+            r[2] = mz * il;
+            upd = true;
+          }
+        }
+        if (!upd) {  // unchanged (rare): the input normal as given
+          if (MODE == kFromPoints) {
+            // n'/sqrt(B) (<= 1 ulp of the FC normal); invalid <=> NaN normal in this mode
+            r[0] = valid ? t.nx * inv_sB : __int_as_float(0x7fc00000);
+            r[1] = valid ? t.ny * inv_sB : __int_as_float(0x7fc00000);
+            r[2] = valid ? t.nz * inv_sB : __int_as_float(0x7fc00000);
+          } else {
+            const int u = u0 + 2 * ty + o, v = q0 + tx;
+            r[0] = r[1] = r[2] = __int_as_float(0x7fc00000);
+            if (u < Mq && v < Nq) {
+              const float* g = a.raw_n + f * a.raw_fs + (long long)u * a.raw_pitch + 6 * v + 3 * k;
+              r[0] = g[0];
+              r[1] = g[1];
+              r[2] = g[2];
+            }
+          }
+        }
+      }
+    }
+    if (SCATTER) {
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        const int u = u0 + 2 * ty + o, v = q0 + tx;
+        if (u < Mq && v < Nq) {
+          const long long g = 2ll * ((long long)u * Nq + v);
+          const longlong2 tm = *reinterpret_cast<const longlong2*>(a.trimap + f * a.tm_fs + g);
+          float* dst = a.out_mesh + f * a.out_fs;
+          if (tm.x >= 0 && tm.x < a.n_out) {
+            dst[3 * tm.x] = res[o][0];
+            dst[3 * tm.x + 1] = res[o][1];
+            dst[3 * tm.x + 2] = res[o][2];
+          }
+          if (tm.y >= 0 && tm.y < a.n_out) {
+            dst[3 * tm.y] = res[o][3];
+            dst[3 * tm.y + 1] = res[o][4];
+            dst[3 * tm.y + 2] = res[o][5];
+          }
+        }
+      }
+    } else {
+      if (threadIdx.x == 0) tma_store_wait_read();  // previous out tile has left smem
+      named_bar_sync(1, kWsCons);
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        float* dst = out_s + ((2 * ty + o) * kBilTQW + tx) * 6;
+#pragma unroll
+        for (int j = 0; j < 6; ++j) dst[j] = res[o][j];
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, kWsCons);
+      if (threadIdx.x == 0) {
+        tma_store_3d(&tout, out_s, q0 * 6, u0, f);
+        tma_store_commit();
+      }
+    }
+  }
+  if (threadIdx.x == 0) tma_store_wait_read();
+}
+
+template <int H, int MODE, bool SCATTER>
+int launch_ws(const CUtensorMap& tp, const CUtensorMap& tn, const CUtensorMap& tc,
+              const CUtensorMap& to, const BilArgs& a, int F, cudaStream_t st) {
+  constexpr int smem = ws_smem_bytes<H, MODE>();
+  static unsigned long long attr_mask = 0;
+  ensure_smem_attr(bilateral_ws_kernel<H, MODE, SCATTER>, smem, attr_mask);
+  static int resident = 0, sms = 0;
+  if (resident == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, bilateral_ws_kernel<H, MODE, SCATTER>,
+                                                  kWsThreads, smem);
+    if (resident < 1) resident = 1;
+  }
+  const int Mq = a.M - 1, Nq = a.N - 1;
+  const long long tiles = (long long)((Nq + kBilTQW - 1) / kBilTQW) *
+                          ((Mq + kBilTQH - 1) / kBilTQH) * F;
+  const int grid = (int)std::min<long long>(tiles, (long long)sms * resident);  // persistent
+  bilateral_ws_kernel<H, MODE, SCATTER><<<grid, kWsThreads, smem, st>>>(tp, tn, tc, to, a);
+  return check_launch("bilateral_ws_kernel");
+}
+
 template <int H>
 int launch_any(int mode, bool scatter, const CUtensorMap& tp, const CUtensorMap& tn,
                const CUtensorMap& tc, const CUtensorMap& to, const BilArgs& a, int F,
                cudaStream_t st) {
+  if (g_bil_ws) {
+    switch (mode) {
+      case kFromPoints:
+        return scatter ? launch_ws<H, kFromPoints, true>(tp, tn, tc, to, a, F, st)
+                       : launch_ws<H, kFromPoints, false>(tp, tn, tc, to, a, F, st);
+      case kNormalsBuf:
+        return scatter ? launch_ws<H, kNormalsBuf, true>(tp, tn, tc, to, a, F, st)
+                       : launch_ws<H, kNormalsBuf, false>(tp, tn, tc, to, a, F, st);
+      default:
+        return scatter ? launch_ws<H, kNormalsCentBuf, true>(tp, tn, tc, to, a, F, st)
+                       : launch_ws<H, kNormalsCentBuf, false>(tp, tn, tc, to, a, F, st);
+    }
+  }
   switch (mode) {
     case kFromPoints:
       return scatter ? launch_bil<H, kFromPoints, true>(tp, tn, tc, to, a, F, st)
@@ -890,6 +1202,8 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   a.out_mesh = out_mesh;
   a.out_fs = 3ll * out_rows;
   a.n_out = out_rows;
+  a.raw_pitch = fcp;
+  a.raw_fs = (long long)fc_fs;
 
   // it0 reads (points | arrays) and writes A; it_k reads A/B and writes B/A; the last
   // iteration scatters to mesh order (trimap) or stores to out_fc.
@@ -899,6 +1213,7 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
     const int mode = from_arrays ? kNormalsCentBuf
                                  : ((it == 0 && !resume) ? kFromPoints : kNormalsBuf);
     const CUtensorMap* dst = last ? &st_fin : ((it % 2 == 0) ? &st_a : &st_b);
+    a.raw_n = (it == 0) ? normals_in : (((it - 1) % 2 == 0) ? buf_a : buf_b);
     rc = sym ? launch_sym_any(mode, last && scatter, m_pts, *src_n, m_cin, *dst, a, F, st)
              : launch_h(h, mode, last && scatter, m_pts, *src_n, m_cin, *dst, a, F, st);
     if (rc) return rc;
