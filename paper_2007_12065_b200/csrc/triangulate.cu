@@ -22,9 +22,11 @@
 //     status words (one warp inspects 32 predecessors per step); rows u-1 / u+1 bases
 //     follow from the counts, so every twin index (which needs trimap of the rows above
 //     and below) is computed in the same pass -- trimap is never read back.
-//   * Triangles and twins (int64, 24 B each) are staged in shared memory per 256-quad
-//     chunk and written out as contiguous, fully coalesced 8-B streams; trimap pairs
-//     are written as 16-B stores.
+//   * Per row segment (up to 8192 quads), one block scan of the packed per-group counts
+//     of rows u-1 | u | u+1 gives every 32-quad group its prefixes; each warp then emits
+//     its groups with no further block barrier: triangles and twins (int64, 24 B each)
+//     are staged per warp in shared memory and written out as contiguous, fully
+//     coalesced 8-B streams; trimap pairs are written as 16-B stores.
 // Integer outputs are bit-exact by construction (deterministic GID-order ranks).
 #include "common.cuh"
 #include "opcfe_internal.h"
@@ -35,7 +37,7 @@ namespace {
 
 constexpr int kTriNT = 256;
 constexpr int kTriWarps = kTriNT / 32;
-constexpr int kChunk = kTriNT;  // quads per chunk (one per thread)
+constexpr int kSegGroups = kTriNT;  // 32-quad groups per scan segment (one per thread)
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagInc = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
@@ -124,13 +126,13 @@ __device__ __forceinline__ void emit_extras(const TriArgs& a, int f, long long t
   }
 }
 
-__global__ void __launch_bounds__(kTriNT, 4) triangulate_kernel(TriArgs a) {
+template <bool EXTRAS>
+__global__ void __launch_bounds__(kTriNT, EXTRAS ? 2 : 4) triangulate_kernel(TriArgs a) {
   __shared__ unsigned long long red[kTriWarps];
-  __shared__ uint32_t wtot[kTriWarps];
   __shared__ long long s_base;
   __shared__ unsigned long long s_tot;
-  __shared__ int64_t tris_s[2 * kChunk * 3];
-  __shared__ int64_t he_s[2 * kChunk * 3];
+  __shared__ unsigned long long gpre[kSegGroups];     // packed per-group exclusive prefixes
+  __shared__ int64_t stage[kTriWarps][2][3 * 64];     // per-warp tris / twins staging
 
   const int u = blockIdx.x;
   const int f = blockIdx.y;
@@ -189,98 +191,127 @@ __global__ void __launch_bounds__(kTriNT, 4) triangulate_kernel(TriArgs a) {
       s_tot = t;
     }
   }
-  __syncthreads();
-  const long long base_cur = s_base;
-  const long long tot_cur = (long long)(s_tot & 0xffffffffull);
-  const long long base_prev = base_cur - (long long)(s_tot >> 32);
-  const long long base_next = base_cur + tot_cur;
+  // (the barrier at the top of the segment loop publishes s_base / s_tot)
 
-  // ---- 3. chunks of 256 quads: bit algebra per warp, block scan over warps, emission
+  // ---- 3. segments of up to kSegGroups 32-quad groups: packed group counts of rows
+  // u-1 | u | u+1 (21 bits each), block exclusive scan, then every warp emits its groups
+  // independently (ranks by popc, per-warp staging, no block barrier per group).
   const long long fG = (long long)f * a.G;
   int64_t* trimap = a.trimap + fG;
   int64_t* tris = a.tris + fG * 3;
   int64_t* he = a.he ? a.he + fG * 3 : nullptr;
   const int N = a.N;
   const uint32_t lt = (1u << lane) - 1u;
+  constexpr unsigned long long F21 = (1ull << 21) - 1;
+  auto group_bits = [&](int g, QuadBits& qp, QuadBits& qc, QuadBits& qn) {
+    const PtBits pu = pt_bits(vm + (long long)u * a.wpr, g, a.wpr);
+    const PtBits pd = pt_bits(vm + (long long)(u + 1) * a.wpr, g, a.wpr);
+    qc = quad_bits(pu, pd);
+    qp = QuadBits{};
+    qn = QuadBits{};
+    if (u > 0) qp = quad_bits(pt_bits(vm + (long long)(u - 1) * a.wpr, g, a.wpr), pu);
+    if (u + 1 < Mq) qn = quad_bits(pd, pt_bits(vm + (long long)(u + 2) * a.wpr, g, a.wpr));
+  };
+  long long base_cur = 0, base_prev = 0, base_next = 0;
   long long carry_p = 0, carry_c = 0, carry_n = 0;
-  for (int c0 = 0; c0 < Nq; c0 += kChunk) {
-    const int g = (c0 >> 5) + warp;  // this warp's 32-quad group
-    const int v = 32 * g + lane;
-    QuadBits qc{}, qp{}, qn{};
-    if (g < groups) {
-      const PtBits pu = pt_bits(vm + (long long)u * a.wpr, g, a.wpr);
-      const PtBits pd = pt_bits(vm + (long long)(u + 1) * a.wpr, g, a.wpr);
-      qc = quad_bits(pu, pd);
-      if (u > 0) qp = quad_bits(pt_bits(vm + (long long)(u - 1) * a.wpr, g, a.wpr), pu);
-      if (u + 1 < Mq) qn = quad_bits(pd, pt_bits(vm + (long long)(u + 2) * a.wpr, g, a.wpr));
+  for (int s0 = 0; s0 < groups; s0 += kSegGroups) {
+    const int ng = min(kSegGroups, groups - s0);
+    unsigned long long x = 0;  // this thread's group (one per thread: kSegGroups == kTriNT)
+    if (threadIdx.x < ng) {
+      QuadBits qp, qc, qn;
+      group_bits(s0 + threadIdx.x, qp, qc, qn);
+      x = (unsigned long long)(__popc(qp.f) + __popc(qp.s)) |
+          ((unsigned long long)(__popc(qc.f) + __popc(qc.s)) << 21) |
+          ((unsigned long long)(__popc(qn.f) + __popc(qn.s)) << 42);
     }
-    // per-warp totals of rows u-1 / u / u+1, packed 3 x 10 bits (<= 64 each)
-    if (lane == 0) {
-      wtot[warp] = (__popc(qp.f) + __popc(qp.s)) | ((__popc(qc.f) + __popc(qc.s)) << 10) |
-                   ((__popc(qn.f) + __popc(qn.s)) << 20);
+    // block exclusive scan of the packed counts (fields never carry: <= 2 * 8192)
+    unsigned long long inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
     }
+    __syncthreads();  // previous segment's gpre / red reads are done; s_base published
+    if (lane == 31) red[warp] = inc;
     __syncthreads();
-    uint32_t woff = 0, ctot = 0;
+    unsigned long long woff = 0, stot = 0;
 #pragma unroll
     for (int w = 0; w < kTriWarps; ++w) {
-      const uint32_t x = wtot[w];
-      woff += (w < warp) ? x : 0u;
-      ctot += x;
+      const unsigned long long r = red[w];
+      woff += (w < warp) ? r : 0ull;
+      stot += r;
     }
-    const uint32_t bf = (qc.f >> lane) & 1u, bs = (qc.s >> lane) & 1u;
-    const long long loc_c = ((woff >> 10) & 1023u) + __popc(qc.f & lt) + __popc(qc.s & lt);
-    const long long pre_c = carry_c + loc_c;
-    const long long pre_p = carry_p + (woff & 1023u) + __popc(qp.f & lt) + __popc(qp.s & lt);
-    const long long pre_n = carry_n + ((woff >> 20) & 1023u) + __popc(qn.f & lt) + __popc(qn.s & lt);
-    if (v < Nq) {
-      const long long gid = 2ll * ((long long)u * Nq + v);
-      const long long t0 = base_cur + pre_c;
-      const long long t1 = t0 + bf;
-      *reinterpret_cast<longlong2*>(trimap + gid) = make_longlong2(bf ? t0 : -1ll, bs ? t1 : -1ll);
-      const int64_t i1 = (int64_t)u * N + v, i2 = i1 + 1, i4 = i1 + N, i3 = i4 + 1;
-      const int l0 = (int)loc_c, l1 = l0 + (int)bf;
-      if (bf) {
-        tris_s[3 * l0] = i3;
-        tris_s[3 * l0 + 1] = i2;
-        tris_s[3 * l0 + 2] = i1;
-        if (he) {
-          he_s[3 * l0] = ((qc.sr >> lane) & 1u)
-                             ? 3 * (t0 + bf + bs + ((qc.fr >> lane) & 1u)) + 0 : -1;
-          he_s[3 * l0 + 1] = ((qp.s >> lane) & 1u)
-                                 ? 3 * (base_prev + pre_p + ((qp.f >> lane) & 1u)) + 1 : -1;
-          he_s[3 * l0 + 2] = bs ? 3 * t1 + 2 : -1;
-        }
-        if (a.normals || a.lflag) emit_extras(a, f, t0, i3, i2, i1);
-      }
-      if (bs) {
-        tris_s[3 * l1] = i1;
-        tris_s[3 * l1 + 1] = i4;
-        tris_s[3 * l1 + 2] = i3;
-        if (he) {
-          const uint32_t lf = (qc.fl >> lane) & 1u, ls = (qc.sl >> lane) & 1u;
-          he_s[3 * l1] = lf ? 3 * (t0 - lf - ls) + 0 : -1;
-          he_s[3 * l1 + 1] = ((qn.f >> lane) & 1u) ? 3 * (base_next + pre_n) + 1 : -1;
-          he_s[3 * l1 + 2] = bf ? 3 * t0 + 2 : -1;
-        }
-        if (a.normals || a.lflag) emit_extras(a, f, t1, i1, i4, i3);
-      }
+    gpre[threadIdx.x] = woff + inc - x;
+    if (s0 == 0) {
+      base_cur = s_base;
+      const long long tot_cur = (long long)(s_tot & 0xffffffffull);
+      base_prev = base_cur - (long long)(s_tot >> 32);
+      base_next = base_cur + tot_cur;
     }
     __syncthreads();
-    // coalesced copy-out of this chunk's triangles [base_cur + carry_c, + n)
-    const int n = (int)((ctot >> 10) & 1023u);
-    const long long t_first = base_cur + carry_c;
-    int64_t* tdst = tris + 3 * t_first;
-    for (int i = threadIdx.x; i < 3 * n; i += kTriNT) tdst[i] = tris_s[i];
-    if (he) {
-      int64_t* hdst = he + 3 * t_first;
-      for (int i = threadIdx.x; i < 3 * n; i += kTriNT) hdst[i] = he_s[i];
+
+    int64_t* st_t = stage[warp][0];
+    int64_t* st_h = stage[warp][1];
+    for (int gl = warp; gl < ng; gl += kTriWarps) {
+      const int g = s0 + gl;
+      const int v = 32 * g + lane;
+      QuadBits qp, qc, qn;
+      group_bits(g, qp, qc, qn);
+      const unsigned long long pre = gpre[gl];
+      const uint32_t bf = (qc.f >> lane) & 1u, bs = (qc.s >> lane) & 1u;
+      const int l0 = __popc(qc.f & lt) + __popc(qc.s & lt), l1 = l0 + (int)bf;  // warp-local
+      const long long t_first = base_cur + carry_c + (long long)((pre >> 21) & F21);
+      const long long pre_p = carry_p + (long long)(pre & F21) + __popc(qp.f & lt) + __popc(qp.s & lt);
+      const long long pre_n = carry_n + (long long)((pre >> 42) & F21) + __popc(qn.f & lt) +
+                              __popc(qn.s & lt);
+      if (v < Nq) {
+        const long long gid = 2ll * ((long long)u * Nq + v);
+        const long long t0 = t_first + l0;
+        const long long t1 = t0 + bf;
+        *reinterpret_cast<longlong2*>(trimap + gid) = make_longlong2(bf ? t0 : -1ll, bs ? t1 : -1ll);
+        const int64_t i1 = (int64_t)u * N + v, i2 = i1 + 1, i4 = i1 + N, i3 = i4 + 1;
+        if (bf) {
+          st_t[3 * l0] = i3;
+          st_t[3 * l0 + 1] = i2;
+          st_t[3 * l0 + 2] = i1;
+          if (he) {
+            st_h[3 * l0] = ((qc.sr >> lane) & 1u)
+                               ? 3 * (t0 + bf + bs + ((qc.fr >> lane) & 1u)) + 0 : -1;
+            st_h[3 * l0 + 1] = ((qp.s >> lane) & 1u)
+                                   ? 3 * (base_prev + pre_p + ((qp.f >> lane) & 1u)) + 1 : -1;
+            st_h[3 * l0 + 2] = bs ? 3 * t1 + 2 : -1;
+          }
+          if (EXTRAS) emit_extras(a, f, t0, i3, i2, i1);
+        }
+        if (bs) {
+          st_t[3 * l1] = i1;
+          st_t[3 * l1 + 1] = i4;
+          st_t[3 * l1 + 2] = i3;
+          if (he) {
+            const uint32_t lf = (qc.fl >> lane) & 1u, ls = (qc.sl >> lane) & 1u;
+            st_h[3 * l1] = lf ? 3 * (t0 - lf - ls) + 0 : -1;
+            st_h[3 * l1 + 1] = ((qn.f >> lane) & 1u) ? 3 * (base_next + pre_n) + 1 : -1;
+            st_h[3 * l1 + 2] = bf ? 3 * t0 + 2 : -1;
+          }
+          if (EXTRAS) emit_extras(a, f, t1, i1, i4, i3);
+        }
+      }
+      __syncwarp();
+      // contiguous, coalesced copy-out of this group's triangles [t_first, + n)
+      const int n3 = 3 * (__popc(qc.f) + __popc(qc.s));
+      int64_t* tdst = tris + 3 * t_first;
+      for (int i = lane; i < n3; i += 32) tdst[i] = st_t[i];
+      if (he) {
+        int64_t* hdst = he + 3 * t_first;
+        for (int i = lane; i < n3; i += 32) hdst[i] = st_h[i];
+      }
+      __syncwarp();  // staging reused by the warp's next group
     }
-    carry_p += ctot & 1023u;
-    carry_c += n;
-    carry_n += (ctot >> 20) & 1023u;
-    __syncthreads();  // wtot / staging reused by the next chunk
+    carry_p += (long long)(stot & F21);
+    carry_c += (long long)((stot >> 21) & F21);
+    carry_n += (long long)((stot >> 42) & F21);
   }
-  if (u == Mq - 1 && threadIdx.x == 0) a.ntri[f] = base_cur + tot_cur;
+  if (u == Mq - 1 && threadIdx.x == 0) a.ntri[f] = base_cur + (long long)(s_tot & 0xffffffffull);
 }
 
 // Twins from an arbitrary trimap (drop-in extract_halfedges_opc(trimap, M, N),
@@ -344,7 +375,10 @@ int triangulate(const uint32_t* vmask, int F, int M, int N, int64_t* trimap, int
   if (cudaMemsetAsync(ws, 0, triangulate_workspace_bytes(F, M), st) != cudaSuccess)
     return check_launch("triangulate: status reset");
   dim3 grid(M - 1, F);
-  triangulate_kernel<<<grid, kTriNT, 0, st>>>(a);
+  if (normals || lflag)
+    triangulate_kernel<true><<<grid, kTriNT, 0, st>>>(a);
+  else
+    triangulate_kernel<false><<<grid, kTriNT, 0, st>>>(a);
   return check_launch("triangulate_kernel");
 }
 
