@@ -130,6 +130,175 @@ __global__ void __launch_bounds__(kLapNT)
   }
 }
 
+// ---------------------------------------------------------------------------------
+// kernel_size 3 (the default): column-strip kernel.  A thread owns one column of a
+// 32 x 64 tile and walks 8 consecutive rows down it with a 3 x 3 register window, so
+//   * each row of the window is loaded from shared memory once (3 points per output
+//     point instead of 9);
+//   * the vertical pair (u,v)-(u+1,v) is weighed once: its d/|d| and 1/|d| enter row u
+//     directly and row u+1 negated (d_up = -d_down and w are exact), i.e. 7 rsqrt per
+//     point instead of 8.
+// Accumulation order stays the reference's (du outer, dv inner).
+constexpr int kL3TW = 32;           // tile columns (one warp)
+constexpr int kL3RS = 8;            // rows per thread
+constexpr int kL3TH = 8 * kL3RS;    // tile rows (8 warps)
+constexpr int kL3L = 4;             // left halo (points): 16-B aligned box start
+constexpr int kL3BW = 40;           // box width (points) >= L + 32 + 1, multiple of 4
+constexpr int kL3BH = kL3TH + 2;
+constexpr int kL3InF = (kL3BW * 3 * kL3BH + 31) / 32 * 32;
+constexpr int kL3OutF = kL3TW * 3 * kL3TH;
+constexpr int kL3Smem = (kL3InF + kL3OutF) * 4 + kSmemSlack;
+
+struct Acc4 {
+  float x, y, z, w;
+};
+
+// weigh the pair (p -> q): d = q - p; valid iff |d|^2 >= FLT_MIN (false for NaN)
+__device__ __forceinline__ void lap_pair(const float* p, const float* q, Acc4& acc, float* dw_out) {
+  const float dx = q[0] - p[0], dy = q[1] - p[1], dz = q[2] - p[2];
+  const float d2 = dx * dx + dy * dy + dz * dz;
+  if (d2 >= 1.17549435e-38f) {
+    const float w = rsqrt_approx(d2);
+    acc.x = fmaf(dx, w, acc.x);
+    acc.y = fmaf(dy, w, acc.y);
+    acc.z = fmaf(dz, w, acc.z);
+    acc.w += w;
+    if (dw_out) {
+      dw_out[0] = -dx * w;
+      dw_out[1] = -dy * w;
+      dw_out[2] = -dz * w;
+      dw_out[3] = w;
+    }
+  } else if (dw_out) {
+    dw_out[0] = dw_out[1] = dw_out[2] = dw_out[3] = 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(256, 4)
+    laplacian3_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+                      uint32_t* __restrict__ vmask, long long vm_fs, int wpr, int M, int N,
+                      float lam) {
+  extern __shared__ __align__(16) char smem_raw[];
+  uint64_t* barp;
+  float* smem = reinterpret_cast<float*>(smem_aligned_base(smem_raw, &barp));
+  float* in_s = smem;
+  float* out_s = smem + kL3InF;
+  uint64_t& bar = *barp;
+
+  const int v0 = blockIdx.x * kL3TW;
+  const int u0 = blockIdx.y * kL3TH;
+  const int f = blockIdx.z;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, kL3BW * 3 * kL3BH * 4);
+    tma_load_3d(in_s, &tin, &bar, (v0 - kL3L) * 3, u0 - 1, f);
+  }
+  mbar_wait(&bar, 0);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane, v = v0 + c;
+  const int r0 = warp * kL3RS;  // first tile row of this thread
+  const bool col_in = v > 0 && v < N - 1;
+  // window rows: box row of tile row r is r + 1
+  auto ld3 = [&](int br, float (*dst)[3]) {
+    const float* q = in_s + (br * kL3BW + c + kL3L - 1) * 3;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) dst[j / 3][j % 3] = q[j];
+  };
+  float A[3][3], B[3][3], Cr[3][3];
+  ld3(r0, A);      // tile row r0 - 1
+  ld3(r0 + 1, B);  // tile row r0
+  float carry[4];  // the up-pair contribution to the current row (from the row above)
+  {
+    Acc4 dummy{0.f, 0.f, 0.f, 0.f};
+    lap_pair(A[1], B[1], dummy, carry);  // pair (r0-1 -> r0): carry = its share for r0
+  }
+#pragma unroll
+  for (int i = 0; i < kL3RS; ++i) {
+    const int r = r0 + i, u = u0 + r;
+    ld3(r + 2, Cr);  // tile row r + 1
+    const float* p = B[1];
+    const bool fin = finite3f(p[0], p[1], p[2]);  // off-grid reads are NaN-filled -> false
+    if (vmask != nullptr) {
+      const uint32_t bits = __ballot_sync(0xffffffffu, fin);
+      if (lane == 0 && u < M && v0 < N) vmask[f * vm_fs + (long long)u * wpr + (v0 >> 5)] = bits;
+    }
+    Acc4 acc{0.f, 0.f, 0.f, 0.f};
+    float down[4];
+    lap_pair(p, A[0], acc, nullptr);
+    acc.x += carry[0];  // (-1, 0): weighed by the row above
+    acc.y += carry[1];
+    acc.z += carry[2];
+    acc.w += carry[3];
+    lap_pair(p, A[2], acc, nullptr);
+    lap_pair(p, B[0], acc, nullptr);
+    lap_pair(p, B[2], acc, nullptr);
+    lap_pair(p, Cr[0], acc, nullptr);
+    lap_pair(p, Cr[1], acc, down);
+    lap_pair(p, Cr[2], acc, nullptr);
+    float ox = p[0], oy = p[1], oz = p[2];
+    if (fin && col_in && u > 0 && u < M - 1 && acc.w > 0.f) {
+      const float s = lam * rcp_approx(acc.w);
+      ox = p[0] + s * acc.x;
+      oy = p[1] + s * acc.y;
+      oz = p[2] + s * acc.z;
+    }
+    float* po = out_s + (r * kL3TW + c) * 3;
+    po[0] = ox;
+    po[1] = oy;
+    po[2] = oz;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) carry[j] = down[j];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        A[k][j] = B[k][j];
+        B[k][j] = Cr[k][j];
+      }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(&tout, out_s, v0 * 3, u0, f);
+    tma_store_commit_and_wait();
+  }
+}
+
+int run_k3(const float* in, float* out, float* tmp, uint32_t* vmask, int F, int M, int N, int pitch,
+           float lam, int iters, cudaStream_t st) {
+  const uint64_t fs = (uint64_t)M * pitch;
+  CUtensorMap m_in, ld_out, st_out, ld_tmp, st_tmp;
+  int rc;
+  if ((rc = make_tmap_3d(&m_in, in, false, 3ull * N, M, F, pitch, fs, kL3BW * 3, kL3BH))) return rc;
+  if ((rc = make_tmap_3d(&ld_out, out, false, 3ull * N, M, F, pitch, fs, kL3BW * 3, kL3BH))) return rc;
+  if ((rc = make_tmap_3d(&st_out, out, false, 3ull * N, M, F, pitch, fs, kL3TW * 3, kL3TH))) return rc;
+  if (iters > 1) {
+    if ((rc = make_tmap_3d(&ld_tmp, tmp, false, 3ull * N, M, F, pitch, fs, kL3BW * 3, kL3BH))) return rc;
+    if ((rc = make_tmap_3d(&st_tmp, tmp, false, 3ull * N, M, F, pitch, fs, kL3TW * 3, kL3TH))) return rc;
+  }
+  static unsigned long long attr_mask = 0;
+  ensure_smem_attr(laplacian3_kernel, kL3Smem, attr_mask);
+  const int wpr = (N + 31) / 32;
+  const long long vm_fs = (long long)M * wpr;
+  dim3 grid((N + kL3TW - 1) / kL3TW, (M + kL3TH - 1) / kL3TH, F);
+  bool to_out = (iters % 2) == 1;
+  const CUtensorMap* src = &m_in;
+  for (int it = 0; it < iters; ++it) {
+    const CUtensorMap* dst = to_out ? &st_out : &st_tmp;
+    laplacian3_kernel<<<grid, 256, kL3Smem, st>>>(*src, *dst, it == 0 ? vmask : nullptr, vm_fs, wpr,
+                                                  M, N, lam);
+    if ((rc = check_launch("laplacian3_kernel"))) return rc;
+    src = to_out ? &ld_out : &ld_tmp;
+    to_out = !to_out;
+  }
+  return OK;
+}
+
 template <int H>
 int launch_one(const CUtensorMap& tin, const CUtensorMap& tout, uint32_t* vmask, long long vm_fs,
                int wpr, int F, int M, int N, float lam, cudaStream_t st) {
@@ -180,7 +349,7 @@ int laplacian(const float* in, float* out, float* tmp, uint32_t* vmask, int F, i
     return fail(ERR_INVALID, "laplacian: row pitch must be >= 3N floats and a multiple of 4");
   if (iters > 1 && tmp == nullptr) return fail(ERR_INVALID, "laplacian: tmp buffer required");
   switch (ksize / 2) {
-    case 1: return run_h<1>(in, out, tmp, vmask, F, M, N, pitch, lam, iters, st);
+    case 1: return run_k3(in, out, tmp, vmask, F, M, N, pitch, lam, iters, st);
     case 2: return run_h<2>(in, out, tmp, vmask, F, M, N, pitch, lam, iters, st);
     case 3: return run_h<3>(in, out, tmp, vmask, F, M, N, pitch, lam, iters, st);
     case 4: return run_h<4>(in, out, tmp, vmask, F, M, N, pitch, lam, iters, st);

@@ -14,7 +14,7 @@ timeout 600 $CMD > gpurun_out/${TAG}_plain.json 2> gpurun_out/${TAG}_plain.err |
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/${TAG}_launches.csv $CMD > /dev/null 2> gpurun_out/${TAG}_launches.err
 # warm-up launches: 3 steps x 16 kernels; capture step 4's kernels
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:laplacian_kernel \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:laplacian \
   -s 35 -c 1 -o gpurun_out/${TAG}_lap $CMD > gpurun_out/${TAG}_ncu_lap.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:triangulate_kernel \
   -s 3 -c 1 -o gpurun_out/${TAG}_tri $CMD > gpurun_out/${TAG}_ncu_tri.log 2>&1
