@@ -12,7 +12,8 @@ import subprocess
 import threading
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libopcfe.so")
+# OPCFE_LIB: an alternative in-tree build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("OPCFE_LIB") or os.path.join(PKG_DIR, "lib", "libopcfe.so")
 
 OPCFE_OK = 0
 OPCFE_ERR_INVALID = -1

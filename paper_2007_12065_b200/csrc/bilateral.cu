@@ -57,10 +57,13 @@ namespace opcfe {
 namespace {
 
 constexpr int kBilTQW = 32;  // interior quads per tile row (= one warp)
-constexpr int kBilTQH = 16;  // interior quad rows per tile (2 per thread)
+#ifndef OPCFE_BIL_TQH
+#define OPCFE_BIL_TQH 8
+#endif
+constexpr int kBilTQH = OPCFE_BIL_TQH;  // interior quad rows per tile (A/B: -DOPCFE_BIL_TQH)
 constexpr int kQPT = 2;                         // interior quads per thread (vertical)
 constexpr int kBilNT = kBilTQW * kBilTQH / kQPT;  // threads per CTA
-constexpr int kBilMinBlocks = kQPT == 1 ? 2 : 3;  // 64 / 80 registers
+constexpr int kBilMinBlocks = 65536 / (80 * kBilNT);  // 80 registers per thread
 
 enum BilMode : int {
   kFromPoints = 0,     // iteration 1: normals + centroids from the point grid
