@@ -124,7 +124,7 @@ class FrontEnd:
 
     @staticmethod
     def _count_launches(lap, bil, src_kind):
-        n = 1                                                   # triangulate
+        n = 3                                                   # triangulate: count, scan, emit
         n += lap.iterations if lap else 0
         if not lap or src_kind != 0:
             n += 1                                              # stage-in
