@@ -47,7 +47,7 @@ const char* opcfe_last_error(void);
 int opcfe_points_pitch(int N);
 int opcfe_fc_pitch(int N);
 size_t opcfe_vmask_words(int F, int M, int N); /* 1 validity bit per point, ceil(N/32) words/row */
-size_t opcfe_triangulate_workspace(int F, int M, int N);
+size_t opcfe_triangulate_workspace(int F, int M, int N); /* row prefixes: F x M int64 */
 
 /* Source grid (any f32/f64 layout with xyz contiguous) -> padded fp32 grid + validity bits.
  * Replaces the dtype coercion np.asarray(opc, dtype=float64) at smoothing.py:55 / mesh.py:65

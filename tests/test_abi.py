@@ -51,7 +51,7 @@ def test_layout_helpers():
         q = L.opcfe_fc_pitch(N)
         assert q >= 6 * (N - 1) and q % 4 == 0 and q - 6 * (N - 1) < 4
     assert L.opcfe_vmask_words(2, 5, 33) == 2 * 5 * 2
-    assert L.opcfe_triangulate_workspace(3, 10, 7) == 3 * 9 * 8
+    assert L.opcfe_triangulate_workspace(3, 10, 7) == 3 * 10 * 8  # row prefixes [F][M] int64
     p = _lib.FrontEndParams(10, 3, 1.0, 5, 3, 0.1, 0.15, -1.0)
     ws = L.opcfe_front_end_workspace(2, 1080, 1920, ctypes.byref(p), 0, L.opcfe_points_pitch(1920))
     grid = 2 * 1080 * 5760 * 4
