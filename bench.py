@@ -177,6 +177,14 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def load_fp32_peak():
+    p = os.path.join(REPO, "profiles", "fp32_peak.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)["fp32_lane_ops_per_s"], "measured (profiles/fp32_peak.json)"
+    return 148 * 128 * 1.965e9, "nominal 128 FP32 lanes/clk/SM at 1965 MHz"
+
+
 def load_traffic():
     p = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(p):
@@ -288,6 +296,19 @@ def run_ours(args, rank, world, local_rank):
                    "GBps": round(b / (ms / 1e3) / 1e9, 1),
                    "frac": round(b / (ms / 1e3) / 1e9 / peak, 3), "launches_per_step": n}
                for k, (b, ms, n) in per_kernel.items()}
+    # the bilateral is FP32-bound ("near the FP32/MUFU ridge"): its FP32
+    # lane-ops (34 directed pairs per quad at k=3, 15 lane-ops each) vs the FMA pipe
+    h = BIL[2] // 2
+    pairs_per_quad = 2 * (2 * (2 * h + 1) ** 2 - 1)
+    fp32_ops = F * (M - 1) * (N - 1) * pairs_per_quad * 15
+    fp32_peak, fp32_src = load_fp32_peak()
+    fp32_ach = fp32_ops / (stage_ms["bilateral"] / BIL[3] / 1e3)
+    compute = {"kernel": "bilateral_kernel", "pipe": "fp32 (FMA)",
+               "achieved": round(fp32_ach / 1e12, 2), "peak": round(fp32_peak / 1e12, 2),
+               "unit": "T lane-ops/s", "frac": round(fp32_ach / fp32_peak, 4),
+               "ops_per_launch": fp32_ops, "peak_source": fp32_src,
+               "note": f"{pairs_per_quad} directed pairs per quad x 15 FP32 lane-ops "
+                       "(6 differences, 6 squared-distance, 3 accumulate) + 1 MUFU ex2"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_reference(steps=3, warmup=0, budget_s=25.0)
@@ -303,7 +324,8 @@ def run_ours(args, rank, world, local_rank):
                      "traffic": traffic, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_pl,
                      "note": "algorithmic bytes per SURVEY.md 8d (unfused); fusion can make "
-                             "achieved exceed DRAM traffic"},
+                             "achieved exceed DRAM traffic",
+                     "compute": compute},
         "kernels": kernels,
         "stage_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
         "frame_hbm_frac": round(ab["frame_total"] * F / (max_ms / args.steps / 1e3) / 1e9 / peak, 4),
