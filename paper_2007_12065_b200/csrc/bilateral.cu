@@ -315,37 +315,76 @@ __global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
     }
     __syncthreads();
 
-    // ---- kQPT vertically adjacent interior quads per thread
-    OwnTri own[kQPT][2];
+    // ---- two vertically adjacent interior quads per thread: a (o = 0) above b (o = 1)
+    static_assert(kQPT == 2, "the in-thread symmetric pairs below assume 2 quads / thread");
+    const Quad2 qa = load_quad2(pk, T::NQ, R0 * T::QW + C);
+    const Quad2 qb = load_quad2(pk, T::NQ, (R0 + 1) * T::QW + C);
+    const OwnTri own[2][2] = {{own_tri(qa, 0), own_tri(qa, 1)}, {own_tri(qb, 0), own_tri(qb, 1)}};
+    f2_t acc[2][2][3];  // [own quad][own triangle][x, y, z] x (kk = 0, kk = 1) lanes
 #pragma unroll
-    for (int o = 0; o < kQPT; ++o) {
-      const Quad2 q = load_quad2(pk, T::NQ, (R0 + o) * T::QW + C);
-      own[o][0] = own_tri(q, 0);
-      own[o][1] = own_tri(q, 1);
-    }
-    f2_t acc[kQPT][2][3];  // [own quad][own triangle][x, y, z] x (kk = 0, kk = 1) lanes
-#pragma unroll
-    for (int o = 0; o < kQPT; ++o)
+    for (int o = 0; o < 2; ++o)
 #pragma unroll
       for (int k = 0; k < 2; ++k) acc[o][k][0] = acc[o][k][1] = acc[o][k][2] = 0ull;
 
+    // (1) pairs inside the thread, weighed once: w(i,j) = w(j,i).
+    //   intra-quad (tri 0, tri 1) of a and of b: one scalar weight each
 #pragma unroll
-    for (int dr = -H; dr <= H + kQPT - 1; ++dr) {
+    for (int o = 0; o < 2; ++o) {
+      const Quad2& q = o == 0 ? qa : qb;
+      const OwnTri& t0 = own[o][0];
+      const OwnTri& t1 = own[o][1];
+      const float dx = t1.cx - t0.cx, dy = t1.cy - t0.cy, dz = t1.cz - t0.cz;
+      const float ex = t1.nx - t0.nx, ey = t1.ny - t0.ny, ez = t1.nz - t0.nz;
+      float e = dx * dx;
+      e = fmaf(dy, dy, e);
+      e = fmaf(dz, dz, e);
+      e = fmaf(ex, ex, e);
+      e = fmaf(ey, ey, e);
+      e = fmaf(ez, ez, e);
+      const float w = ex2_approx(-e);
+      const f2_t w_to1 = f2(w, 0.f), w_to0 = f2(0.f, w);  // tri 1 <- tri 0 (lane kk = 0), ...
+      acc[o][1][0] = fma2(q.nx, w_to1, acc[o][1][0]);
+      acc[o][1][1] = fma2(q.ny, w_to1, acc[o][1][1]);
+      acc[o][1][2] = fma2(q.nz, w_to1, acc[o][1][2]);
+      acc[o][0][0] = fma2(q.nx, w_to0, acc[o][0][0]);
+      acc[o][0][1] = fma2(q.ny, w_to0, acc[o][0][1]);
+      acc[o][0][2] = fma2(q.nz, w_to0, acc[o][0][2]);
+    }
+    //   vertical a-b: a's triangle k against b's pair (lanes kk), shared with b
+    {
+      f2_t wv[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const f2_t sd = dist2(own[0][k], qb);
+        wv[k] = f2(ex2_approx(-f2lo(sd)), ex2_approx(-f2hi(sd)));
+        acc[0][k][0] = fma2(qb.nx, wv[k], acc[0][k][0]);
+        acc[0][k][1] = fma2(qb.ny, wv[k], acc[0][k][1]);
+        acc[0][k][2] = fma2(qb.nz, wv[k], acc[0][k][2]);
+      }
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {  // b's triangle kk <- a's pair (lanes k)
+        const f2_t w = kk == 0 ? f2(f2lo(wv[0]), f2lo(wv[1])) : f2(f2hi(wv[0]), f2hi(wv[1]));
+        acc[1][kk][0] = fma2(qa.nx, w, acc[1][kk][0]);
+        acc[1][kk][1] = fma2(qa.ny, w, acc[1][kk][1]);
+        acc[1][kk][2] = fma2(qa.nz, w, acc[1][kk][2]);
+      }
+    }
+
+    // (2) every other quad of the two windows
+#pragma unroll
+    for (int dr = -H; dr <= H + 1; ++dr) {
 #pragma unroll
       for (int dc = -H; dc <= H; ++dc) {
+        if (dc == 0 && (dr == 0 || dr == 1)) continue;  // a and b themselves: (1)
         const Quad2 nb = load_quad2(pk, T::NQ, (R0 + dr) * T::QW + C + dc);
 #pragma unroll
-        for (int o = 0; o < kQPT; ++o) {
+        for (int o = 0; o < 2; ++o) {
           const int du = dr - o;
           if (du < -H || du > H) continue;
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
-            const f2_t s = dist2(own[o][k], nb);
-            float w0 = ex2_approx(-f2lo(s)), w1 = ex2_approx(-f2hi(s));
-            if (du == 0 && dc == 0) {  // self pair excluded
-              if (k == 0) w0 = 0.f; else w1 = 0.f;
-            }
-            const f2_t w = f2(w0, w1);
+            const f2_t sd = dist2(own[o][k], nb);
+            const f2_t w = f2(ex2_approx(-f2lo(sd)), ex2_approx(-f2hi(sd)));
             acc[o][k][0] = fma2(nb.nx, w, acc[o][k][0]);
             acc[o][k][1] = fma2(nb.ny, w, acc[o][k][1]);
             acc[o][k][2] = fma2(nb.nz, w, acc[o][k][2]);
