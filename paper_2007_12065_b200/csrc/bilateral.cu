@@ -63,7 +63,10 @@ constexpr int kBilTQW = 32;  // interior quads per tile row (= one warp)
 constexpr int kBilTQH = OPCFE_BIL_TQH;  // interior quad rows per tile (A/B: -DOPCFE_BIL_TQH)
 constexpr int kQPT = 2;                         // interior quads per thread (vertical)
 constexpr int kBilNT = kBilTQW * kBilTQH / kQPT;  // threads per CTA
-constexpr int kBilMinBlocks = 65536 / (80 * kBilNT);  // 80 registers per thread
+#ifndef OPCFE_BIL_REGS
+#define OPCFE_BIL_REGS 80
+#endif
+constexpr int kBilMinBlocks = 65536 / (OPCFE_BIL_REGS * kBilNT);  // register budget per thread
 
 enum BilMode : int {
   kFromPoints = 0,     // iteration 1: normals + centroids from the point grid
@@ -180,19 +183,22 @@ __device__ __forceinline__ f2_t bc2(float x) { return f2(x, x); }
 
 // pack one quad (both triangles) into 3 float4 planes of (tri 0, tri 1) lane pairs:
 //   P0 = (c'x0, c'x1, c'y0, c'y1)  P1 = (c'z0, c'z1, n'x0, n'x1)  P2 = (n'y0, n'y1, n'z0, n'z1)
-// n' = n*sqrt(B), c' = c*sqrt(A); a triangle with a NaN normal or centroid is encoded as
-// n' = 0, c' = 1e18 (its weight to / from any valid triangle underflows to exactly 0).
+// n' = n*sqrt(B); `cs` are the centroids already scaled (c' = c*sqrt(A)); a triangle with
+// a NaN normal or centroid is encoded as n' = 0, c' = 1e18 (its weight to / from any
+// valid triangle underflows to exactly 0).  One NaN test per triangle: on the sum of its
+// six values (an infinite value either yields NaN or a zero weight downstream).
 __device__ __forceinline__ void pack_quad(float4* pk, int nq, int q, const float* n,
-                                          const float* cc, float sA, float sB) {
+                                          const float* cs, float sB) {
   float c2[2][3], n2[2][3];
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-    const bool ok = !(isnan(n[3 * k]) || isnan(n[3 * k + 1]) || isnan(n[3 * k + 2]) ||
-                      isnan(cc[3 * k]) || isnan(cc[3 * k + 1]) || isnan(cc[3 * k + 2]));
+    const float t = ((n[3 * k] + n[3 * k + 1]) + (n[3 * k + 2] + cs[3 * k])) +
+                    (cs[3 * k + 1] + cs[3 * k + 2]);
+    const bool ok = !isnan(t);
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       n2[k][j] = ok ? n[3 * k + j] * sB : 0.f;
-      c2[k][j] = ok ? cc[3 * k + j] * sA : 1e18f;
+      c2[k][j] = ok ? cs[3 * k + j] : 1e18f;
     }
   }
   pk[q] = make_float4(c2[0][0], c2[1][0], c2[0][1], c2[1][1]);
@@ -271,7 +277,7 @@ __global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
     if (MODE != kFromPoints) tma_load_3d(nrm_s, &tnrm, &bar, (q0 - T::LQ) * 6, u0 - H, f);
     if (MODE == kNormalsCentBuf) tma_load_3d(cen_s, &tcen, &bar, (q0 - T::LQ) * 6, u0 - H, f);
   }
-  const float sA = a.sA, sB = a.sB;
+  const float sA = a.sA, sB = a.sB, sA3 = a.sA * (1.0f / 3.0f);
   const int tx = threadIdx.x % kBilTQW, ty = threadIdx.x / kBilTQW;
   const int R0 = kQPT * ty + H, C = tx + T::LQ;  // pack position of the thread's quad 0
   mbar_wait(&bar, 0);
@@ -279,27 +285,29 @@ __global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
     // ---- pack every halo quad into the 3 planes (scaled + sentinel-encoded)
     for (int q = threadIdx.x; q < T::NQ; q += kBilNT) {
       const int r = q / T::QW, c = q % T::QW;
-      float n[6], cc[6];
+      float n[6], cc[6];  // cc: scaled centroids c' = c * sqrt(A)
       if (MODE == kNormalsCentBuf) {
 #pragma unroll
         for (int j = 0; j < 6; ++j) {
           n[j] = nrm_s[q * 6 + j];
-          cc[j] = cen_s[q * 6 + j];
+          cc[j] = cen_s[q * 6 + j] * sA;
         }
       } else {
         const float* P1 = pts_s + (r * T::PW + c + T::PSHIFT) * 3;
         const float* P2 = P1 + 3;
         const float* P4 = P1 + T::PW * 3;
         const float* P3 = P4 + 3;
-        const float* tri[2][3] = {{P3, P2, P1}, {P1, P4, P3}};
+        // triangles (p3, p2, p1) and (p1, p4, p3) share p1 + p3
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          const float *pa = tri[k][0], *pb = tri[k][1], *pc = tri[k][2];
-#pragma unroll
-          for (int j = 0; j < 3; ++j) cc[3 * k + j] = ((pa[j] + pb[j]) + pc[j]) * (1.0f / 3.0f);
-          if (MODE == kFromPoints) unit_normal_fast(pa, pb, pc, n + 3 * k);
+        for (int j = 0; j < 3; ++j) {
+          const float s13 = P1[j] + P3[j];
+          cc[j] = (s13 + P2[j]) * sA3;
+          cc[3 + j] = (s13 + P4[j]) * sA3;
         }
-        if (MODE == kNormalsBuf) {
+        if (MODE == kFromPoints) {
+          unit_normal_fast(P3, P2, P1, n);
+          unit_normal_fast(P1, P4, P3, n + 3);
+        } else {
 #pragma unroll
           for (int j = 0; j < 6; ++j) n[j] = nrm_s[q * 6 + j];
         }
@@ -311,7 +319,7 @@ __global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
           }
         }
       }
-      pack_quad(pk, T::NQ, q, n, cc, sA, sB);
+      pack_quad(pk, T::NQ, q, n, cc, sB);
     }
     __syncthreads();
 
@@ -414,11 +422,12 @@ __global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
         if (valid && s > 0.f) {
           const float is = rcp_approx(s);  // a common scale: cancels in the normalisation
           const float mx = ax * is, my = ay * is, mz = az * is;
-          // IEEE sqrt + reciprocal (~1.5 ulp): the stored normals feed the next iteration's
-          // weights, so rounding here compounds over the iterations
-          const float len = sqrtf(mx * mx + my * my + mz * mz);
-          if (len * s > thr) {
-            const float il = 1.0f / len;
+          // |m|^2 in [1, 3]: MUFU rsqrt + one Newton step (~1 ulp, like IEEE sqrt + divide,
+          // whose slow-path checks cost ~8 % of the kernel's instructions)
+          const float l2 = mx * mx + my * my + mz * mz;
+          float il = rsqrt_approx(l2);
+          il = il * fmaf(-0.5f * l2, il * il, 1.5f);
+          if (l2 * il * s > thr) {
             r[0] = mx * il;
             r[1] = my * il;
             r[2] = mz * il;
