@@ -274,6 +274,38 @@ def run_ours(args, rank, world, local_rank):
                        "(CUDA graph per frame) -> D2H of smoothed grid, trimap, triangles, "
                        "halfedges, normals into pinned host buffers; frame i+1's H2D + compute "
                        "overlap frame i's D2H on separate streams"}
+        # ---- the same, starting from frame FILES (binary PLY with "comment grid M N",
+        # written here to local /tmp): paper_2007_12065_b200.io.FrameFileReader loads the
+        # next batch into a pinned double buffer while HostPipeline runs the current one
+        e2e_files = None
+        if not args.no_e2e_files:
+            import tempfile
+            from paper_2007_12065_b200 import io as fio
+            tmp = tempfile.mkdtemp(prefix=f"opcfe_bench_r{rank}_")
+            try:
+                paths = []
+                for f in range(F):
+                    paths.append(os.path.join(tmp, f"frame{f}.ply"))
+                    fio.write_ply(paths[-1], host[f].numpy().reshape(-1, 3), binary=True,
+                                  grid=(M, N))
+                seq = paths * e2e_steps
+                reader = fio.FrameFileReader(seq, batch=F)
+                barrier()
+                e0.record(stream)
+                for batch in reader:
+                    pipe.run(batch)
+                e1.record(stream)
+                barrier()
+                tf = D.max_over_ranks(e0.elapsed_time(e1), dev)
+                e2e_files = {"value": world * len(seq) / (tf / 1e3), "unit": "frames/s",
+                             "file_bytes_per_step": int(F * M * N * 24), "steps": e2e_steps,
+                             "path": "FrameFileReader (native PLY reader, pread into pinned "
+                                     "buffers, next batch loaded during this one) -> "
+                                     "HostPipeline.run as in e2e; files in the page cache"}
+            finally:
+                import shutil
+                shutil.rmtree(tmp, ignore_errors=True)
+        e2e["from_files"] = e2e_files
         del pipe
 
     if rank != 0:
@@ -344,6 +376,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--frames", type=int, default=8, help="frames per GPU per step")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e-files", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -7,7 +7,7 @@ sm_100a CUDA kernels behind a C ABI (include/opcfe.h, lib/libopcfe.so).
 There is no CPU fallback.
 """
 
-from . import _kernels, accumulator, synthetic
+from . import _kernels, accumulator, io, synthetic
 from ._kernels import ACTIVE as kernel_backend
 from .accumulator import find_cell_indices, integrate_normals
 from .frontend import FrontEnd, FrontEndResult, HostPipeline, front_end
@@ -27,5 +27,5 @@ __all__ = [
     "gid_to_uvk", "mesh_from_opc", "UNASSIGNED", "MAX_GROUPS", "group_assignment",
     "max_edge_mask", "BilateralParams",
     "LaplacianParams", "bilateral_filter_opc", "bilateral_opc", "compute_fc_triangle_data",
-    "laplacian_filter_opc", "laplacian_opc",
+    "laplacian_filter_opc", "laplacian_opc", "io",
 ]

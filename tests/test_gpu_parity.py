@@ -594,3 +594,40 @@ def test_host_pipeline_matches_device_engine(fe):
         assert teq(res.normals[f, :T], ref.normals[f, :T].cpu())
     assert pipe.h2d_bytes == host.numel() * 8 and pipe.d2h_bytes > 0
 
+
+
+def test_frames_from_files_through_host_pipeline(fe, tmp_path):
+    """OPC ingestion -> front end: grid-text and binary-PLY frame files read by the native
+    loader into pinned batches (FrameFileReader) give exactly the device engine's result
+    on the in-memory frames (the loader is bit-exact, so the whole path is)."""
+    from paper_2007_12065_b200 import io as fio
+    frames = fe.synthetic.config_c5_frames(4)[:, :70, :110]
+    M, N = frames.shape[1:3]
+    paths = []
+    for f in range(4):
+        if f % 2:
+            paths.append(tmp_path / f"f{f}.ply")
+            fio.write_ply(paths[-1], frames[f].reshape(-1, 3), binary=True, grid=(M, N))
+        else:
+            paths.append(tmp_path / f"f{f}.grid")
+            with open(paths[-1], "w") as fh:
+                fh.write(f"{M} {N}\n")
+                np.savetxt(fh, frames[f].reshape(-1, 3), fmt="%.17g")
+    lap, bil = fe.LaplacianParams(1.0, 3, 2), fe.BilateralParams(0.1, 0.15, 3, 2)
+    pipe = fe.HostPipeline(M, N, laplacian=lap, bilateral=bil)
+    _, ref = _engine_run(fe, frames, lap, bil, frames=4, dtype=torch.float64)
+    f0 = 0
+    for batch in fio.FrameFileReader(paths, batch=3):
+        assert batch.is_pinned()
+        res = pipe.run(batch)
+        torch.cuda.synchronize()
+        for j in range(batch.shape[0]):
+            f = f0 + j
+            T = ref.n_tri[f]
+            assert res.n_tri[j] == T
+            assert teq(res.points[j], ref.points[f].cpu())
+            assert teq(res.triangles[j, :T], ref.triangles[f, :T].cpu())
+            assert teq(res.halfedges[j, :3 * T], ref.halfedges[f, :3 * T].cpu())
+            assert teq(res.normals[j, :T], ref.normals[f, :T].cpu())
+        f0 += batch.shape[0]
+    assert f0 == 4
