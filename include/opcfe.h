@@ -145,6 +145,26 @@ int opcfe_group_assignment(const void* normals, int is_f64, long long T, int F,
 int opcfe_max_edge_mask(const void* points, int is_f64, const int64_t* triangles,
                         long long n_tri, double l_max, uint8_t* flag, opcfe_stream_t stream);
 
+/* Region growing over twin edges.  n_tri < 2^31.
+ * opcfe_grow_segment replaces _kernels.grow_segment (_native.pyx:170-222): the connected
+ * component of `seed` among triangles with groups == label, visited == 0 and (ptp_max > 0)
+ * all vertices within ptp_max of the plane (anchor, normal) -- host double[3] each --
+ * written SORTED to members (device [n_tri]); *n_members (device) = its size; members are
+ * marked in visited.  opcfe_segment_components: for every triangle the minimum index of
+ * its same-label twin-connected component (-1 where groups == 255) and, optionally, the
+ * component size at its root: with ptp_max == 0 the segments of
+ * segmentation.region_growing_task (segmentation.py:117-170) are exactly these
+ * components (seed = root).  ws: opcfe_segments_workspace(n_tri) bytes. */
+size_t opcfe_segments_workspace(long long n_tri);
+int opcfe_grow_segment(const int64_t* triangles, const int64_t* halfedges, const double* points,
+                       const uint8_t* groups, uint8_t* visited, long long n_tri, long long seed,
+                       int label, const double* anchor, const double* normal, double ptp_max,
+                       int64_t* members, int64_t* n_members, void* ws, size_t ws_bytes,
+                       opcfe_stream_t stream);
+int opcfe_segment_components(const int64_t* halfedges, const uint8_t* groups, long long n_tri,
+                             int64_t* component, int64_t* size, void* ws, size_t ws_bytes,
+                             opcfe_stream_t stream);
+
 /* The organized branch of pipeline.run_scene (pipeline.py:125-134), all frames in one
  * call: [stage-in] -> Laplacian -> triangulation + twins -> bilateral (normals in mesh
  * order) [-> l_max flag]. */

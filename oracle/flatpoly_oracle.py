@@ -343,3 +343,63 @@ def front_end(opc, laplacian=None, bilateral=None, l_max=None):
         mesh["lmax_mask"] = max_edge_mask(mesh["points"], mesh["triangles"], l_max)
     mesh["smoothed"] = opc
     return mesh
+
+
+def grow_segment(triangles, halfedges, points, groups, visited, seed, label, anchor, normal,
+                 ptp_max):
+    """Region growing from one seed: _native.pyx:170-222 (explicit stack, the native
+    backend's order; the member SET is order independent).  `visited` is updated in
+    place; returns the sorted member indices."""
+    tris = np.asarray(triangles, dtype=np.int64).reshape(-1, 3)
+    he = np.asarray(halfedges, dtype=np.int64)
+    pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+    ax, ay, az = (float(x) for x in anchor)
+    nx, ny, nz = (float(x) for x in normal)
+    check = ptp_max > 0.0
+    visited[seed] = 1
+    stack, members = [int(seed)], [int(seed)]
+    while stack:
+        t = stack.pop()
+        for e in range(3 * t, 3 * t + 3):
+            tw = int(he[e])
+            if tw < 0:
+                continue
+            c = tw // 3
+            if groups[c] != label or visited[c]:
+                continue
+            if check:
+                ok = True
+                for k in range(3):
+                    p = pts[tris[c, k]]
+                    d = (p[0] - ax) * nx + (p[1] - ay) * ny + (p[2] - az) * nz
+                    if abs(d) > ptp_max:
+                        ok = False
+                        break
+                if not ok:
+                    continue
+            visited[c] = 1
+            stack.append(c)
+            members.append(c)
+    return np.sort(np.asarray(members, dtype=np.int64))
+
+
+def grow_segments(points, triangles, halfedges, groups, label, dominant_normal, ptp_max,
+                  tri_min):
+    """The triangle_indices of region_growing_task's kept segments for one label
+    (segmentation.py:117-151): seeds ascending, anchor = seed centroid (numpy mean),
+    kept when >= tri_min triangles."""
+    pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+    tris = np.asarray(triangles, dtype=np.int64).reshape(-1, 3)
+    groups = np.asarray(groups)
+    visited = np.zeros(len(tris), dtype=np.uint8)
+    dn = np.asarray(dominant_normal, dtype=np.float64)
+    out = []
+    for seed in np.nonzero(groups == label)[0]:
+        if visited[seed]:
+            continue
+        anchor = pts[tris[seed]].mean(axis=0)
+        m = grow_segment(tris, halfedges, pts, groups, visited, int(seed), int(groups[seed]),
+                         anchor, dn, ptp_max)
+        if len(m) >= tri_min:
+            out.append(m)
+    return out

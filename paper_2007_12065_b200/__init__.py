@@ -14,7 +14,8 @@ from .frontend import FrontEnd, FrontEndResult, HostPipeline, front_end
 from .geometry import DegenerateInputError, triangle_normals
 from .mesh import (HalfEdgeMesh, compute_normals, extract_halfedges_opc, extract_triangles_opc,
                    extract_tri_mesh_from_organized_point_cloud, gid_of, gid_to_uvk, mesh_from_opc)
-from .segmentation import MAX_GROUPS, UNASSIGNED, group_assignment, max_edge_mask
+from .segmentation import (MAX_GROUPS, UNASSIGNED, SegmentationParams, extract_planar_segment,
+                           group_assignment, grow_segments, max_edge_mask)
 from .smoothing import (BilateralParams, LaplacianParams, bilateral_filter_opc, bilateral_opc,
                         compute_fc_triangle_data, laplacian_filter_opc, laplacian_opc)
 
@@ -25,7 +26,8 @@ __all__ = [
     "triangle_normals", "HalfEdgeMesh", "compute_normals", "extract_halfedges_opc",
     "extract_triangles_opc", "extract_tri_mesh_from_organized_point_cloud", "gid_of",
     "gid_to_uvk", "mesh_from_opc", "UNASSIGNED", "MAX_GROUPS", "group_assignment",
-    "max_edge_mask", "BilateralParams",
+    "max_edge_mask", "SegmentationParams", "extract_planar_segment", "grow_segments",
+    "BilateralParams",
     "LaplacianParams", "bilateral_filter_opc", "bilateral_opc", "compute_fc_triangle_data",
     "laplacian_filter_opc", "laplacian_opc", "io",
 ]

@@ -48,5 +48,24 @@ def find_cells(query_normals, ids_sorted, cell_normals, neighbors, slope, interc
     return Q.give(DeviceAccumulator(ga).search(Q.dev.to(torch.float64)))
 
 
-def grow_segment(*args, **kwargs):  # pragma: no cover - outside the OPC front-end hot path
-    raise NotImplementedError("grow_segment (region growing) is outside this build's scope")
+def grow_segment(triangles, halfedges, points, groups, visited, seed, label, anchor, normal,
+                 ptp_max):
+    """Same contract as _kernels.grow_segment (_native.pyx:170-222 / _fallback.py:47-80):
+    the sorted members of the seed's segment; `visited` (uint8 [n_tri]) is updated in
+    place -- a NumPy array on the host or a torch tensor on the device."""
+    import numpy as np
+    host = isinstance(visited, np.ndarray)
+    dev = torch.device("cuda")
+    G = Staged(groups, float_only=False).dev.to(torch.uint8)
+    HE = Staged(halfedges, float_only=False).dev.to(torch.int64)
+    check = float(ptp_max) > 0.0
+    T = Staged(triangles, float_only=False).dev.to(torch.int64).reshape(-1, 3).contiguous() \
+        if check else None
+    P = Staged(points).dev.to(torch.float64).reshape(-1, 3).contiguous() if check else None
+    V = torch.from_numpy(np.ascontiguousarray(visited)).to(dev) if host else visited
+    m = _ops.grow_segment(T, HE, P, G, V, int(seed), int(label), np.asarray(anchor, np.float64),
+                          np.asarray(normal, np.float64), float(ptp_max))
+    if host:
+        visited[...] = V.cpu().numpy()
+        return m.cpu().numpy()
+    return m

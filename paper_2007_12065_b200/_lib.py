@@ -29,7 +29,8 @@ EXPORTS = (
     "opcfe_laplacian",
     "opcfe_triangulate", "opcfe_halfedges_from_trimap", "opcfe_fc_data", "opcfe_bilateral",
     "opcfe_triangle_normals", "opcfe_find_cells", "opcfe_group_assignment", "opcfe_max_edge_mask", "opcfe_front_end_workspace",
-    "opcfe_front_end", "opcfe_front_end_profiled",
+    "opcfe_front_end", "opcfe_front_end_profiled", "opcfe_segments_workspace",
+    "opcfe_grow_segment", "opcfe_segment_components",
 )
 
 
@@ -102,6 +103,9 @@ def _declare(L):
         "opcfe_max_edge_mask": (i, [vp, i, vp, ll, d, vp, vp]),
         "opcfe_find_cells": (i, [vp, ll, ll, vp, vp, vp, ll, d, d, ll, ll, vp, vp, vp]),
         "opcfe_group_assignment": (i, [vp, i, ll, i, vp, vp, i, d, vp, vp, vp]),
+        "opcfe_segments_workspace": (sz, [ll]),
+        "opcfe_grow_segment": (i, [vp, vp, vp, vp, vp, ll, ll, i, vp, vp, d, vp, vp, vp, sz, vp]),
+        "opcfe_segment_components": (i, [vp, vp, ll, vp, vp, vp, sz, vp]),
         "opcfe_front_end_workspace": (sz, [i, i, i, ctypes.POINTER(FrontEndParams), i, i]),
         "opcfe_front_end": (i, [i, i, i, ctypes.POINTER(FrontEndParams),
                                 ctypes.POINTER(FrontEndIO), vp, sz, vp]),

@@ -184,3 +184,41 @@ def max_edge_mask(points: torch.Tensor, triangles: torch.Tensor, l_max: float):
                                               out.data_ptr(), stream()),
                "max_edge_mask")
     return out.bool()
+
+
+# ------------------------------------------------------------------ region growing
+def _seg_ws(n_tri: int, device) -> torch.Tensor:
+    nb = int(_lib.lib().opcfe_segments_workspace(n_tri))
+    return torch.empty((max(nb, 1),), dtype=torch.uint8, device=device)
+
+
+def grow_segment(triangles, halfedges, points, groups, visited, seed: int, label: int,
+                 anchor, normal, ptp_max: float):
+    """Device tensors in; sorted int64 members (device) out; `visited` updated in place."""
+    import ctypes
+    n = int(groups.shape[0])
+    ws = _seg_ws(n, groups.device)
+    members = torch.empty((n,), dtype=torch.int64, device=groups.device)
+    cnt = torch.empty((1,), dtype=torch.int64, device=groups.device)
+    a = (ctypes.c_double * 3)(*[float(x) for x in anchor])
+    nn = (ctypes.c_double * 3)(*[float(x) for x in normal])
+    _lib.check(_lib.lib().opcfe_grow_segment(ptr(triangles), halfedges.data_ptr(), ptr(points),
+                                             groups.data_ptr(), visited.data_ptr(), n, int(seed),
+                                             int(label), a, nn, float(ptp_max),
+                                             members.data_ptr(), cnt.data_ptr(), ws.data_ptr(),
+                                             ws.numel(), stream()),
+               "grow_segment")
+    return members[: int(cnt.item())]
+
+
+def segment_components(halfedges, groups, with_size: bool = True):
+    """(component root = min index or -1, size at the root) per triangle (device)."""
+    n = int(groups.shape[0])
+    ws = _seg_ws(n, groups.device)
+    comp = torch.empty((n,), dtype=torch.int64, device=groups.device)
+    size = torch.empty((n,), dtype=torch.int64, device=groups.device) if with_size else None
+    _lib.check(_lib.lib().opcfe_segment_components(halfedges.data_ptr(), groups.data_ptr(), n,
+                                                   comp.data_ptr(), ptr(size), ws.data_ptr(),
+                                                   ws.numel(), stream()),
+               "segment_components")
+    return comp, size

@@ -206,6 +206,25 @@ int opcfe_max_edge_mask(const void* points, int is_f64, const int64_t* triangles
   return max_edge_mask(points, is_f64 != 0, triangles, n_tri, l_max, flag, S(stream));
 }
 
+size_t opcfe_segments_workspace(long long n_tri) {
+  return n_tri < 1 ? 0 : segments_workspace_bytes(n_tri);
+}
+
+int opcfe_grow_segment(const int64_t* triangles, const int64_t* halfedges, const double* points,
+                       const uint8_t* groups, uint8_t* visited, long long n_tri, long long seed,
+                       int label, const double* anchor, const double* normal, double ptp_max,
+                       int64_t* members, int64_t* n_members, void* ws, size_t ws_bytes,
+                       opcfe_stream_t stream) {
+  return grow_segment(triangles, halfedges, points, groups, visited, n_tri, seed, label, anchor,
+                      normal, ptp_max, members, n_members, ws, ws_bytes, S(stream));
+}
+
+int opcfe_segment_components(const int64_t* halfedges, const uint8_t* groups, long long n_tri,
+                             int64_t* component, int64_t* size, void* ws, size_t ws_bytes,
+                             opcfe_stream_t stream) {
+  return segment_components(halfedges, groups, n_tri, component, size, ws, ws_bytes, S(stream));
+}
+
 size_t opcfe_front_end_workspace(int F, int M, int N, const opcfe_front_end_params* p,
                                  int src_kind, int src_pitch) {
   if (!p || F < 1 || M < 2 || N < 2) return 0;

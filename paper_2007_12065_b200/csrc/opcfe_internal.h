@@ -40,4 +40,13 @@ int group_assignment(const void* normals, bool f64, long long T, int F, const in
 int max_edge_mask(const void* pts, bool f64, const int64_t* tris, long long T, double l_max,
                   uint8_t* flag, cudaStream_t st);
 
+size_t segments_workspace_bytes(long long n_tri);
+int grow_segment(const int64_t* tris, const int64_t* he, const double* pts,
+                 const uint8_t* groups, uint8_t* visited, long long n_tri, long long seed,
+                 int label, const double* anchor, const double* normal, double ptp_max,
+                 int64_t* members, int64_t* n_members, void* ws, size_t ws_bytes,
+                 cudaStream_t st);
+int segment_components(const int64_t* he, const uint8_t* groups, long long n_tri, int64_t* comp,
+                       int64_t* size, void* ws, size_t ws_bytes, cudaStream_t st);
+
 }  // namespace opcfe

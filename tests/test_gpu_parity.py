@@ -10,6 +10,8 @@ Fused fp32 pipeline: per-stage parity on identical inputs -- each oracle stage c
 the GPU's fp32 intermediate (upcast to f64) -- plus end-to-end bit-exact topology.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -631,3 +633,78 @@ def test_frames_from_files_through_host_pipeline(fe, tmp_path):
             assert teq(res.normals[j, :T], ref.normals[f, :T].cpu())
         f0 += batch.shape[0]
     assert f0 == 4
+
+
+SEG_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "segments.npz")
+
+
+def _seg_golden():
+    with np.load(SEG_PATH) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("scene", ["room", "frag"])
+@pytest.mark.parametrize("ptp", [0.0, 0.01])
+@pytest.mark.parametrize("device_mesh", [False, True])
+def test_golden_region_growing(fe, scene, ptp, device_mesh):
+    """grow_segments (union-find components on the GPU) == the reference's
+    region_growing_task membership for every label: same segments, same order, same
+    sorted members (tests/golden/make_segments_golden.py), NumPy and device meshes."""
+    g = _seg_golden()
+    mesh = fe.HalfEdgeMesh(points=g[f"{scene}_points"], triangles=g[f"{scene}_triangles"],
+                           halfedges=g[f"{scene}_halfedges"])
+    groups = g[f"{scene}_groups"]
+    if device_mesh:
+        mesh = fe.HalfEdgeMesh(points=torch.from_numpy(mesh.points).cuda(),
+                               triangles=torch.from_numpy(mesh.triangles).cuda(),
+                               halfedges=torch.from_numpy(mesh.halfedges).cuda())
+        groups = torch.from_numpy(groups).cuda()
+    params = fe.SegmentationParams(l_max=0.08, ang_min=0.9, ptp_max=ptp,
+                                   tri_min=int(g[f"{scene}_tri_min"]))
+    for lab in range(len(g["dominant"])):
+        got = fe.grow_segments(mesh, groups, lab, g["dominant"][lab], params)
+        key = f"{scene}_ptp{ptp:g}_label{lab}"
+        exp = np.split(g[key + "_members"], np.cumsum(g[key + "_lengths"])[:-1]) \
+            if len(g[key + "_lengths"]) else []
+        assert len(got) == len(exp), (lab, len(got), len(exp))
+        for a, b in zip(got, exp):
+            a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
+            assert np.array_equal(a, b)
+
+
+def test_grow_segment_kernel_drop_in(fe):
+    """_kernels.grow_segment == the oracle's (== _native.pyx:170-222) on single seeds:
+    same sorted members, same visited updates, rejected triangles stay seedable."""
+    from paper_2007_12065_b200 import _kernels
+    g = _seg_golden()
+    pts, tris, he, groups = (g["frag_points"], g["frag_triangles"], g["frag_halfedges"],
+                             g["frag_groups"])
+    rng = np.random.default_rng(3)
+    for ptp in (0.0, 0.004, 0.02):
+        v_ref = np.zeros(len(tris), np.uint8)
+        v_gpu = np.zeros(len(tris), np.uint8)
+        cands = np.nonzero(groups != 255)[0]
+        for seed in rng.choice(cands, 25, replace=False):
+            if v_ref[seed]:
+                continue
+            lab = int(groups[seed])
+            anchor = pts[tris[seed]].mean(axis=0)
+            nrm = g["dominant"][lab]
+            a = fo.grow_segment(tris, he, pts, groups, v_ref, int(seed), lab, anchor, nrm, ptp)
+            b = _kernels.grow_segment(tris, he, pts, groups, v_gpu, int(seed), lab, anchor, nrm,
+                                      ptp)
+            assert np.array_equal(a, b) and np.array_equal(v_ref, v_gpu)
+
+
+def test_extract_planar_segment(fe):
+    g = _seg_golden()
+    mesh = fe.HalfEdgeMesh(points=g["room_points"], triangles=g["room_triangles"],
+                           halfedges=g["room_halfedges"])
+    groups = g["room_groups"]
+    seed = int(np.nonzero(groups == 2)[0][0])
+    visited = np.zeros(len(groups), np.uint8)
+    m = fe.extract_planar_segment(seed, mesh, groups, g["dominant"][2], 0.01, visited)
+    v2 = np.zeros(len(groups), np.uint8)
+    exp = fo.grow_segment(mesh.triangles, mesh.halfedges, mesh.points, groups, v2, seed, 2,
+                          mesh.points[mesh.triangles[seed]].mean(axis=0), g["dominant"][2], 0.01)
+    assert np.array_equal(m, exp) and np.array_equal(visited, v2) and len(m) > 100

@@ -4,6 +4,8 @@ The golden files were produced by the real reference (tests/golden/make_golden.p
 These tests run without a GPU.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -157,3 +159,33 @@ def test_lidar_front_end():
     assert np.array_equal(r["triangles"], g["triangles"])
     assert np.array_equal(r["halfedges"], g["halfedges"])
     assert same_f64(r["normals"], g["mesh_normals"])
+
+
+SEG_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "segments.npz")
+
+
+def seg_golden():
+    with np.load(SEG_PATH) as z:
+        return {k: z[k] for k in z.files}
+
+
+def seg_expected(g, scene, ptp, lab):
+    key = f"{scene}_ptp{ptp:g}_label{lab}"
+    return np.split(g[key + "_members"], np.cumsum(g[key + "_lengths"])[:-1]) \
+        if len(g[key + "_lengths"]) else []
+
+
+@pytest.mark.parametrize("scene", ["room", "frag"])
+@pytest.mark.parametrize("ptp", [0.0, 0.01])
+def test_region_growing_oracle(scene, ptp):
+    """oracle.grow_segments == the reference's region_growing_task membership
+    (tests/golden/make_segments_golden.py), every label, planarity check off and on."""
+    g = seg_golden()
+    for lab in range(len(g["dominant"])):
+        got = fo.grow_segments(g[f"{scene}_points"], g[f"{scene}_triangles"],
+                               g[f"{scene}_halfedges"], g[f"{scene}_groups"], lab,
+                               g["dominant"][lab], ptp, int(g[f"{scene}_tri_min"]))
+        exp = seg_expected(g, scene, ptp, lab)
+        assert len(got) == len(exp)
+        for a, b in zip(got, exp):
+            assert np.array_equal(a, b)
