@@ -100,8 +100,9 @@ def main(tag):
         lines.append(f"| top stalls (cycles per issue) | "
                      f"{', '.join(f'{k} {v:.2f}' for k, v in d['stalls'].items())} |")
         lines.append("")
-        rb = float(d["dram__bytes_read.sum"][0]) * (1e6 if d["dram__bytes_read.sum"][1] == "Mbyte" else 1)
-        wb = float(d["dram__bytes_write.sum"][0]) * (1e6 if d["dram__bytes_write.sum"][1] == "Mbyte" else 1)
+        unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rb = float(d["dram__bytes_read.sum"][0]) * unit[d["dram__bytes_read.sum"][1]]
+        wb = float(d["dram__bytes_write.sum"][0]) * unit[d["dram__bytes_write.sum"][1]]
         traffic[kname] = {"dram_bytes_per_launch_per_frame": (rb + wb) / FRAMES,
                           "dram_read_bytes": rb, "dram_write_bytes": wb, "frames": FRAMES,
                           "capture": f"profiles/{tag}_summary.md"}
