@@ -152,6 +152,10 @@ constexpr int kL3Warps = OPCFE_LAP_WARPS;  // warps per CTA (stacked vertically)
 constexpr int kL3NT = 32 * kL3Warps;
 constexpr int kL3RS = OPCFE_LAP_RS;        // rows per thread
 constexpr int kL3TH = kL3Warps * kL3RS;    // tile rows
+#ifndef OPCFE_LAP_UNROLL
+#define OPCFE_LAP_UNROLL 8
+#endif
+constexpr int kL3Unroll = OPCFE_LAP_UNROLL;  // rows per unrolled loop body (code size)
 constexpr int kL3L = 4;             // left halo (points): 16-B aligned box start
 constexpr int kL3BW = 40;           // box width (points) >= L + 32 + 1, multiple of 4
 constexpr int kL3BH = kL3TH + 2;
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
     Acc4 dummy{0.f, 0.f, 0.f, 0.f};
     lap_pair(A[1], B[1], dummy, carry);  // pair (r0-1 -> r0): carry = its share for r0
   }
-#pragma unroll
+#pragma unroll kL3Unroll
   for (int i = 0; i < kL3RS; ++i) {
     const int r = r0 + i, u = u0 + r;
     ld3(r + 2, Cr);  // tile row r + 1
