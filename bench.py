@@ -213,7 +213,8 @@ def run_ours(args, rank, world, local_rank):
     eng.src.copy_(frames)
     del frames
     stream = torch.cuda.current_stream(dev)
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    prof_steps = max(1, min(args.steps, 20))
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(prof_steps)]
     for row in ev:                                  # materialise the cudaEvent_t handles
         for e in row:
             e.record(stream)
@@ -224,8 +225,10 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # the measured step: opcfe_front_end as a user calls it (the triangulation overlaps
+    # the Laplacian / bilateral on a side stream)
     for _ in range(args.warmup):
-        eng.launch_profiled(ev[0])
+        eng.launch()
     barrier()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -233,10 +236,17 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         t_start.record(stream)
         for k in range(args.steps):
-            eng.launch_profiled(ev[k])
+            eng.launch()
         t_end.record(stream)
         barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
+    # per-stage device times: opcfe_front_end_profiled runs the stages back to back with
+    # stage-boundary events (the reference's _Timer stages), on separate steps
+    for _ in range(2):
+        eng.launch_profiled(ev[0])
+    for k in range(prof_steps):
+        eng.launch_profiled(ev[k])
+    torch.cuda.synchronize()
     stage = {"stage_in": [], "laplacian": [], "triangulate": [], "bilateral": []}
     for row in ev:
         stage["stage_in"].append(row[0].elapsed_time(row[1]))
@@ -360,6 +370,8 @@ def run_ours(args, rank, world, local_rank):
                      "compute": compute},
         "kernels": kernels,
         "stage_ms_per_step": {k: round(v, 4) for k, v in stage_ms.items()},
+        "stage_note": "stage times from opcfe_front_end_profiled (stages back to back); the "
+                      "timed step overlaps the triangulation with the other stages",
         "frame_hbm_frac": round(ab["frame_total"] * F / (max_ms / args.steps / 1e3) / 1e9 / peak, 4),
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
         "clocks": clk.summary(), "n_tri_per_frame": T,

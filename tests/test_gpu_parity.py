@@ -708,3 +708,38 @@ def test_extract_planar_segment(fe):
     exp = fo.grow_segment(mesh.triangles, mesh.halfedges, mesh.points, groups, v2, seed, 2,
                           mesh.points[mesh.triangles[seed]].mean(axis=0), g["dominant"][2], 0.01)
     assert np.array_equal(m, exp) and np.array_equal(visited, v2) and len(m) > 100
+
+
+@pytest.mark.parametrize("lap_it,src", [(0, torch.float32), (1, torch.float32), (2, torch.float32),
+                                        (3, torch.float64), (4, torch.float64)])
+def test_profiled_eager_and_graph_agree(fe, lap_it, src):
+    """opcfe_front_end_profiled (stage events), opcfe_front_end eagerly and under a CUDA
+    graph give identical outputs for odd / even Laplacian pass counts (the ping-pong
+    ends in the output buffer), staged f64 input and no Laplacian."""
+    frames = fe.synthetic.config_c5_frames(2)[:, :150, :230]
+    lap = fe.LaplacianParams(1.0, 3, lap_it) if lap_it else None
+    bil = fe.BilateralParams(0.1, 0.15, 3, 3)
+    outs = []
+    for mode in ("serial", "eager", "graph"):
+        eng = fe.FrontEnd(150, 230, 2, laplacian=lap, bilateral=bil, src_dtype=src,
+                          graph=mode == "graph")
+        eng.src.copy_(torch.from_numpy(frames).to(eng.src.dtype).cuda().reshape(eng.src.shape))
+        if mode == "serial":
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            for e in ev:
+                e.record()
+            eng.launch_profiled(ev)
+        else:
+            eng.launch()
+            eng.launch()   # graph: capture + replay
+        torch.cuda.synchronize()
+        r = eng.result()
+        outs.append((r.points.clone(), r.triangles.clone(), r.halfedges.clone(),
+                     r.normals.clone(), list(r.n_tri)))
+    for o in outs[1:]:
+        assert o[4] == outs[0][4]
+        assert teq(o[0], outs[0][0])
+        for f, T in enumerate(o[4]):        # live rows only (capacity rows are scratch)
+            assert teq(o[1][f, :T], outs[0][1][f, :T])
+            assert teq(o[2][f, :3 * T], outs[0][2][f, :3 * T])
+            assert teq(o[3][f, :T], outs[0][3][f, :T])
