@@ -89,7 +89,13 @@ struct BilTile {
   static constexpr int NQ = QW * QH;      // quads in the pack
   static constexpr int PTS_F = ((PW * 3 * PH) + 31) / 32 * 32;
   static constexpr int FC_F = ((QW * 6 * QH) + 31) / 32 * 32;
-  static constexpr int PACK_F = 12 * NQ;  // 3 float4 planes (pack_quad)
+  // 4 pack planes (pack_quad), each 128-B aligned so TMA can fill them directly:
+  //   C0 float4 (c'x0, c'x1, c'y0, c'y1)  C1 float2 (c'z0, c'z1)
+  //   N0 float4 (n'x0, n'x1, n'y0, n'y1)  N1 float2 (n'z0, n'z1)
+  static constexpr int P_C1 = (4 * NQ + 31) / 32 * 32;
+  static constexpr int P_N0 = P_C1 + (2 * NQ + 31) / 32 * 32;
+  static constexpr int P_N1 = P_N0 + (4 * NQ + 31) / 32 * 32;
+  static constexpr int PACK_F = P_N1 + (2 * NQ + 31) / 32 * 32;
   static constexpr int OUT_F = kBilTQW * 6 * kBilTQH;
   static_assert(QW * 6 <= 256 && PW * 3 <= 256 && PH <= 256, "TMA box extent must be <= 256");
   static_assert((QW * 6) % 4 == 0, "FC box rows must be 16-B multiples");
@@ -181,13 +187,27 @@ __device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
 // broadcast scalar operand (ptxas encodes it as a .F32 operand of FADD2 / FFMA2)
 __device__ __forceinline__ f2_t bc2(float x) { return f2(x, x); }
 
-// pack one quad (both triangles) into 3 float4 planes of (tri 0, tri 1) lane pairs:
-//   P0 = (c'x0, c'x1, c'y0, c'y1)  P1 = (c'z0, c'z1, n'x0, n'x1)  P2 = (n'y0, n'y1, n'z0, n'z1)
-// n' = n*sqrt(B); `cs` are the centroids already scaled (c' = c*sqrt(A)); a triangle with
-// a NaN normal or centroid is encoded as n' = 0, c' = 1e18 (its weight to / from any
-// valid triangle underflows to exactly 0).  One NaN test per triangle: on the sum of its
-// six values (an infinite value either yields NaN or a zero weight downstream).
-__device__ __forceinline__ void pack_quad(float4* pk, int nq, int q, const float* n,
+// the 4 pack planes (in shared memory, or the global packed FC arrays of the fused
+// pipeline): one quad = (triangle 0, triangle 1) lane pairs, 48 B
+struct Planes {
+  float4* c0;
+  float2* c1;
+  float4* n0;
+  float2* n1;
+};
+template <int H>
+__device__ __forceinline__ Planes planes_at(float* base) {
+  using T = BilTile<H>;
+  return Planes{reinterpret_cast<float4*>(base), reinterpret_cast<float2*>(base + T::P_C1),
+                reinterpret_cast<float4*>(base + T::P_N0),
+                reinterpret_cast<float2*>(base + T::P_N1)};
+}
+
+// pack one quad: n' = n*sqrt(B); `cs` are the centroids already scaled (c' = c*sqrt(A));
+// a triangle with a NaN normal or centroid is encoded as n' = 0, c' = 1e18 (its weight
+// to / from any valid triangle underflows to exactly 0).  One NaN test per triangle: on
+// the sum of its six values (an infinite value either yields NaN or a zero weight).
+__device__ __forceinline__ void pack_quad(const Planes& P, int q, const float* n,
                                           const float* cs, float sB) {
   float c2[2][3], n2[2][3];
 #pragma unroll
@@ -201,20 +221,22 @@ __device__ __forceinline__ void pack_quad(float4* pk, int nq, int q, const float
       c2[k][j] = ok ? cs[3 * k + j] : 1e18f;
     }
   }
-  pk[q] = make_float4(c2[0][0], c2[1][0], c2[0][1], c2[1][1]);
-  pk[nq + q] = make_float4(c2[0][2], c2[1][2], n2[0][0], n2[1][0]);
-  pk[2 * nq + q] = make_float4(n2[0][1], n2[1][1], n2[0][2], n2[1][2]);
+  P.c0[q] = make_float4(c2[0][0], c2[1][0], c2[0][1], c2[1][1]);
+  P.c1[q] = make_float2(c2[0][2], c2[1][2]);
+  P.n0[q] = make_float4(n2[0][0], n2[1][0], n2[0][1], n2[1][1]);
+  P.n1[q] = make_float2(n2[0][2], n2[1][2]);
 }
 
-// a neighbour quad as 6 packed (tri 0, tri 1) registers
+// a quad as 6 packed (tri 0, tri 1) registers: LDS.128 + LDS.64 + LDS.128 + LDS.64
 struct Quad2 {
   f2_t cx, cy, cz, nx, ny, nz;
 };
-__device__ __forceinline__ Quad2 load_quad2(const float4* pk, int nq, int q) {
-  const ulonglong2 a = reinterpret_cast<const ulonglong2*>(pk)[q];
-  const ulonglong2 b = reinterpret_cast<const ulonglong2*>(pk)[nq + q];
-  const ulonglong2 c = reinterpret_cast<const ulonglong2*>(pk)[2 * nq + q];
-  return Quad2{a.x, a.y, b.x, b.y, c.x, c.y};
+__device__ __forceinline__ Quad2 load_quad2(const Planes& P, int q) {
+  const ulonglong2 a = reinterpret_cast<const ulonglong2*>(P.c0)[q];
+  const f2_t cz = reinterpret_cast<const f2_t*>(P.c1)[q];
+  const ulonglong2 b = reinterpret_cast<const ulonglong2*>(P.n0)[q];
+  const f2_t nz = reinterpret_cast<const f2_t*>(P.n1)[q];
+  return Quad2{a.x, a.y, cz, b.x, b.y, nz};
 }
 
 // an own triangle, NEGATED (so differences are packed adds with a broadcast operand)
@@ -238,12 +260,182 @@ __device__ __forceinline__ f2_t dist2(const OwnTri& t, const Quad2& nb) {
   return fma2(ez, ez, s);
 }
 
-template <int H, int MODE, bool SCATTER>
+// Weigh one thread's two quads: a = pack row R0, b = R0 + 1, pack column C.  res holds
+// the filtered unit normals where upd[o][k]; qa / qb are the thread's own packed quads.
+template <int H>
+__device__ __forceinline__ void bil_weigh(const Planes& P, int R0, int C, float sB, Quad2& qa,
+                                          Quad2& qb, float res[2][6], bool upd[2][2]) {
+  using T = BilTile<H>;
+  qa = load_quad2(P, R0 * T::QW + C);
+  qb = load_quad2(P, (R0 + 1) * T::QW + C);
+  const OwnTri own[2][2] = {{own_tri(qa, 0), own_tri(qa, 1)}, {own_tri(qb, 0), own_tri(qb, 1)}};
+  f2_t acc[2][2][3];  // [own quad][own triangle][x, y, z] x (kk = 0, kk = 1) lanes
+#pragma unroll
+  for (int o = 0; o < 2; ++o)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) acc[o][k][0] = acc[o][k][1] = acc[o][k][2] = 0ull;
+
+  // (1) pairs inside the thread, weighed once: w(i,j) = w(j,i).
+  //   intra-quad (tri 0, tri 1) of a and of b: one scalar weight each
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+    const Quad2& q = o == 0 ? qa : qb;
+    const OwnTri& t0 = own[o][0];
+    const OwnTri& t1 = own[o][1];
+    const float dx = t1.cx - t0.cx, dy = t1.cy - t0.cy, dz = t1.cz - t0.cz;
+    const float ex = t1.nx - t0.nx, ey = t1.ny - t0.ny, ez = t1.nz - t0.nz;
+    float e = dx * dx;
+    e = fmaf(dy, dy, e);
+    e = fmaf(dz, dz, e);
+    e = fmaf(ex, ex, e);
+    e = fmaf(ey, ey, e);
+    e = fmaf(ez, ez, e);
+    const float w = ex2_approx(-e);
+    const f2_t w_to1 = f2(w, 0.f), w_to0 = f2(0.f, w);  // tri 1 <- tri 0 (lane kk = 0), ...
+    acc[o][1][0] = fma2(q.nx, w_to1, acc[o][1][0]);
+    acc[o][1][1] = fma2(q.ny, w_to1, acc[o][1][1]);
+    acc[o][1][2] = fma2(q.nz, w_to1, acc[o][1][2]);
+    acc[o][0][0] = fma2(q.nx, w_to0, acc[o][0][0]);
+    acc[o][0][1] = fma2(q.ny, w_to0, acc[o][0][1]);
+    acc[o][0][2] = fma2(q.nz, w_to0, acc[o][0][2]);
+  }
+  //   vertical a-b: a's triangle k against b's pair (lanes kk), shared with b
+  {
+    f2_t wv[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const f2_t sd = dist2(own[0][k], qb);
+      wv[k] = f2(ex2_approx(-f2lo(sd)), ex2_approx(-f2hi(sd)));
+      acc[0][k][0] = fma2(qb.nx, wv[k], acc[0][k][0]);
+      acc[0][k][1] = fma2(qb.ny, wv[k], acc[0][k][1]);
+      acc[0][k][2] = fma2(qb.nz, wv[k], acc[0][k][2]);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {  // b's triangle kk <- a's pair (lanes k)
+      const f2_t w = kk == 0 ? f2(f2lo(wv[0]), f2lo(wv[1])) : f2(f2hi(wv[0]), f2hi(wv[1]));
+      acc[1][kk][0] = fma2(qa.nx, w, acc[1][kk][0]);
+      acc[1][kk][1] = fma2(qa.ny, w, acc[1][kk][1]);
+      acc[1][kk][2] = fma2(qa.nz, w, acc[1][kk][2]);
+    }
+  }
+
+  // (2) every other quad of the two windows
+#pragma unroll
+  for (int dr = -H; dr <= H + 1; ++dr) {
+#pragma unroll
+    for (int dc = -H; dc <= H; ++dc) {
+      if (dc == 0 && (dr == 0 || dr == 1)) continue;  // a and b themselves: (1)
+      const Quad2 nb = load_quad2(P, (R0 + dr) * T::QW + C + dc);
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        const int du = dr - o;
+        if (du < -H || du > H) continue;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const f2_t sd = dist2(own[o][k], nb);
+          const f2_t w = f2(ex2_approx(-f2lo(sd)), ex2_approx(-f2hi(sd)));
+          acc[o][k][0] = fma2(nb.nx, w, acc[o][k][0]);
+          acc[o][k][1] = fma2(nb.ny, w, acc[o][k][1]);
+          acc[o][k][2] = fma2(nb.nz, w, acc[o][k][2]);
+        }
+      }
+    }
+  }
+
+  // underflow-safe normalisation: n = m/|m|, m = acc'/s; |acc| > 1e-30 <=> |m| s > 1e-30 sB.
+  // wsum is not accumulated: wsum == 0 implies acc == 0, so the reference's
+  // `wsum > 0 and |acc| > 1e-30` (_native.pyx:352-360) is just |acc| > 1e-30, here
+  // |acc'| > 1e-30 sqrt(B) evaluated underflow-safely as s * |acc'/s|, s = max |acc'_i|
+  const float thr = 1e-30f * sB;
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      float* r = &res[o][3 * k];
+      const bool valid = own[o][k].cx != -1e18f;  // not the pack sentinel
+      const float ax = f2lo(acc[o][k][0]) + f2hi(acc[o][k][0]);
+      const float ay = f2lo(acc[o][k][1]) + f2hi(acc[o][k][1]);
+      const float az = f2lo(acc[o][k][2]) + f2hi(acc[o][k][2]);
+      const float sc = fmaxf(fabsf(ax), fmaxf(fabsf(ay), fabsf(az)));
+      upd[o][k] = false;
+      r[0] = r[1] = r[2] = 0.f;
+      if (valid && sc > 0.f) {
+        const float is = rcp_approx(sc);  // a common scale: cancels in the normalisation
+        const float mx = ax * is, my = ay * is, mz = az * is;
+        // |m|^2 in [1, 3]: MUFU rsqrt + one Newton step (~1 ulp, like IEEE sqrt + divide,
+        // whose slow-path checks cost ~8 % of the kernel's instructions)
+        const float l2 = mx * mx + my * my + mz * mz;
+        float il = rsqrt_approx(l2);
+        il = il * fmaf(-0.5f * l2, il * il, 1.5f);
+        if (l2 * il * sc > thr) {
+          r[0] = mx * il;
+          r[1] = my * il;
+          r[2] = mz * il;
+          upd[o][k] = true;
+        }
+      }
+    }
+  }
+}
+
+// the fused pipeline's packed FC arrays in global memory (per frame, row-major quads):
+// C0 / N0 float4 [Mq][Nq], C1 / N1 float2 [Mq][Nq2] (Nq2 = Nq rounded up to even)
+struct PackedG {
+  float4* c0;
+  float2* c1;
+  float4* n0;
+  float2* n1;
+  long long s4, s2;    // row strides in quads (Nq, Nq2)
+  long long f4, f2s;   // frame strides in quads
+};
+
+__device__ __forceinline__ void store_packed_n(const PackedG& g, int f, int u, int v,
+                                               const float* res, const bool* upd,
+                                               const Quad2& own, float sB) {
+  // n' of the next iteration: the filtered normal * sqrt(B); unchanged -> the input n'
+  // (exactly, already scaled); invalid (sentinel) -> 0
+  float n[6];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float inx = k == 0 ? f2lo(own.nx) : f2hi(own.nx);
+    const float iny = k == 0 ? f2lo(own.ny) : f2hi(own.ny);
+    const float inz = k == 0 ? f2lo(own.nz) : f2hi(own.nz);
+    n[3 * k] = upd[k] ? res[3 * k] * sB : inx;
+    n[3 * k + 1] = upd[k] ? res[3 * k + 1] * sB : iny;
+    n[3 * k + 2] = upd[k] ? res[3 * k + 2] * sB : inz;
+  }
+  g.n0[f * g.f4 + (long long)u * g.s4 + v] = make_float4(n[0], n[3], n[1], n[4]);
+  g.n1[f * g.f2s + (long long)u * g.s2 + v] = make_float2(n[2], n[5]);
+}
+
+__device__ __forceinline__ void scatter_mesh(const BilArgs& a, int f, int u, int v,
+                                             const float* r) {
+  const int Nq = a.N - 1;
+  const long long g = 2ll * ((long long)u * Nq + v);
+  const longlong2 tm = *reinterpret_cast<const longlong2*>(a.trimap + f * a.tm_fs + g);
+  float* dst = a.out_mesh + f * a.out_fs;
+  if (tm.x >= 0 && tm.x < a.n_out) {
+    dst[3 * tm.x] = r[0];
+    dst[3 * tm.x + 1] = r[1];
+    dst[3 * tm.x + 2] = r[2];
+  }
+  if (tm.y >= 0 && tm.y < a.n_out) {
+    dst[3 * tm.y] = r[3];
+    dst[3 * tm.y + 1] = r[4];
+    dst[3 * tm.y + 2] = r[5];
+  }
+}
+
+// PACKOUT (mode 0, fused pipeline with >= 2 iterations): besides filtering, write the
+// packed centroid planes (constant for all later iterations) and the packed filtered
+// normals, so the later iterations (bilateral_packed_kernel) skip the pack phase.
+template <int H, int MODE, bool SCATTER, bool PACKOUT>
 __global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
     bilateral_kernel(const __grid_constant__ CUtensorMap tpts, const __grid_constant__ CUtensorMap tnrm,
                      const __grid_constant__ CUtensorMap tcen, const __grid_constant__ CUtensorMap tout,
-                     BilArgs a) {
+                     BilArgs a, PackedG pg) {
   using T = BilTile<H>;
+  static_assert(!PACKOUT || (MODE == kFromPoints && !SCATTER), "PACKOUT: mode 0, no scatter");
   extern __shared__ __align__(16) char smem_raw[];
   uint64_t* barp;
   float* p = reinterpret_cast<float*>(smem_aligned_base(smem_raw, &barp));
@@ -253,7 +445,7 @@ __global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
   if (MODE != kNormalsCentBuf) { pts_s = p; p += T::PTS_F; }
   if (MODE != kFromPoints) { nrm_s = p; p += T::FC_F; }
   if (MODE == kNormalsCentBuf) { cen_s = p; p += T::FC_F; }
-  float4* pk = reinterpret_cast<float4*>(p);  // 3 planes, see pack_quad
+  const Planes P = planes_at<H>(p);
   p += T::PACK_F;
   float* out_s = (MODE == kFromPoints) ? p : nrm_s;  // modes 1/2: aliases the FC tile
   uint64_t& bar = *barp;
@@ -281,218 +473,201 @@ __global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
   const int tx = threadIdx.x % kBilTQW, ty = threadIdx.x / kBilTQW;
   const int R0 = kQPT * ty + H, C = tx + T::LQ;  // pack position of the thread's quad 0
   mbar_wait(&bar, 0);
-  {
-    // ---- pack every halo quad into the 3 planes (scaled + sentinel-encoded)
-    for (int q = threadIdx.x; q < T::NQ; q += kBilNT) {
-      const int r = q / T::QW, c = q % T::QW;
-      float n[6], cc[6];  // cc: scaled centroids c' = c * sqrt(A)
-      if (MODE == kNormalsCentBuf) {
-#pragma unroll
-        for (int j = 0; j < 6; ++j) {
-          n[j] = nrm_s[q * 6 + j];
-          cc[j] = cen_s[q * 6 + j] * sA;
-        }
-      } else {
-        const float* P1 = pts_s + (r * T::PW + c + T::PSHIFT) * 3;
-        const float* P2 = P1 + 3;
-        const float* P4 = P1 + T::PW * 3;
-        const float* P3 = P4 + 3;
-        // triangles (p3, p2, p1) and (p1, p4, p3) share p1 + p3
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const float s13 = P1[j] + P3[j];
-          cc[j] = (s13 + P2[j]) * sA3;
-          cc[3 + j] = (s13 + P4[j]) * sA3;
-        }
-        if (MODE == kFromPoints) {
-          unit_normal_fast(P3, P2, P1, n);
-          unit_normal_fast(P1, P4, P3, n + 3);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 6; ++j) n[j] = nrm_s[q * 6 + j];
-        }
-        if (MODE == kFromPoints) {  // raw normals of interior quads: the "unchanged" output
-          const int ir = r - H, ic = c - T::LQ;
-          if (ir >= 0 && ir < kBilTQH && ic >= 0 && ic < kBilTQW) {
-#pragma unroll
-            for (int j = 0; j < 6; ++j) out_s[(ir * kBilTQW + ic) * 6 + j] = n[j];
-          }
-        }
-      }
-      pack_quad(pk, T::NQ, q, n, cc, sB);
-    }
-    __syncthreads();
 
-    // ---- two vertically adjacent interior quads per thread: a (o = 0) above b (o = 1)
-    static_assert(kQPT == 2, "the in-thread symmetric pairs below assume 2 quads / thread");
-    const Quad2 qa = load_quad2(pk, T::NQ, R0 * T::QW + C);
-    const Quad2 qb = load_quad2(pk, T::NQ, (R0 + 1) * T::QW + C);
-    const OwnTri own[2][2] = {{own_tri(qa, 0), own_tri(qa, 1)}, {own_tri(qb, 0), own_tri(qb, 1)}};
-    f2_t acc[2][2][3];  // [own quad][own triangle][x, y, z] x (kk = 0, kk = 1) lanes
+  // ---- pack every halo quad into the planes (scaled + sentinel-encoded)
+  for (int q = threadIdx.x; q < T::NQ; q += kBilNT) {
+    const int r = q / T::QW, c = q % T::QW;
+    float n[6], cc[6];  // cc: scaled centroids c' = c * sqrt(A)
+    if (MODE == kNormalsCentBuf) {
 #pragma unroll
-    for (int o = 0; o < 2; ++o)
-#pragma unroll
-      for (int k = 0; k < 2; ++k) acc[o][k][0] = acc[o][k][1] = acc[o][k][2] = 0ull;
-
-    // (1) pairs inside the thread, weighed once: w(i,j) = w(j,i).
-    //   intra-quad (tri 0, tri 1) of a and of b: one scalar weight each
-#pragma unroll
-    for (int o = 0; o < 2; ++o) {
-      const Quad2& q = o == 0 ? qa : qb;
-      const OwnTri& t0 = own[o][0];
-      const OwnTri& t1 = own[o][1];
-      const float dx = t1.cx - t0.cx, dy = t1.cy - t0.cy, dz = t1.cz - t0.cz;
-      const float ex = t1.nx - t0.nx, ey = t1.ny - t0.ny, ez = t1.nz - t0.nz;
-      float e = dx * dx;
-      e = fmaf(dy, dy, e);
-      e = fmaf(dz, dz, e);
-      e = fmaf(ex, ex, e);
-      e = fmaf(ey, ey, e);
-      e = fmaf(ez, ez, e);
-      const float w = ex2_approx(-e);
-      const f2_t w_to1 = f2(w, 0.f), w_to0 = f2(0.f, w);  // tri 1 <- tri 0 (lane kk = 0), ...
-      acc[o][1][0] = fma2(q.nx, w_to1, acc[o][1][0]);
-      acc[o][1][1] = fma2(q.ny, w_to1, acc[o][1][1]);
-      acc[o][1][2] = fma2(q.nz, w_to1, acc[o][1][2]);
-      acc[o][0][0] = fma2(q.nx, w_to0, acc[o][0][0]);
-      acc[o][0][1] = fma2(q.ny, w_to0, acc[o][0][1]);
-      acc[o][0][2] = fma2(q.nz, w_to0, acc[o][0][2]);
-    }
-    //   vertical a-b: a's triangle k against b's pair (lanes kk), shared with b
-    {
-      f2_t wv[2];
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const f2_t sd = dist2(own[0][k], qb);
-        wv[k] = f2(ex2_approx(-f2lo(sd)), ex2_approx(-f2hi(sd)));
-        acc[0][k][0] = fma2(qb.nx, wv[k], acc[0][k][0]);
-        acc[0][k][1] = fma2(qb.ny, wv[k], acc[0][k][1]);
-        acc[0][k][2] = fma2(qb.nz, wv[k], acc[0][k][2]);
-      }
-#pragma unroll
-      for (int kk = 0; kk < 2; ++kk) {  // b's triangle kk <- a's pair (lanes k)
-        const f2_t w = kk == 0 ? f2(f2lo(wv[0]), f2lo(wv[1])) : f2(f2hi(wv[0]), f2hi(wv[1]));
-        acc[1][kk][0] = fma2(qa.nx, w, acc[1][kk][0]);
-        acc[1][kk][1] = fma2(qa.ny, w, acc[1][kk][1]);
-        acc[1][kk][2] = fma2(qa.nz, w, acc[1][kk][2]);
-      }
-    }
-
-    // (2) every other quad of the two windows
-#pragma unroll
-    for (int dr = -H; dr <= H + 1; ++dr) {
-#pragma unroll
-      for (int dc = -H; dc <= H; ++dc) {
-        if (dc == 0 && (dr == 0 || dr == 1)) continue;  // a and b themselves: (1)
-        const Quad2 nb = load_quad2(pk, T::NQ, (R0 + dr) * T::QW + C + dc);
-#pragma unroll
-        for (int o = 0; o < 2; ++o) {
-          const int du = dr - o;
-          if (du < -H || du > H) continue;
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const f2_t sd = dist2(own[o][k], nb);
-            const f2_t w = f2(ex2_approx(-f2lo(sd)), ex2_approx(-f2hi(sd)));
-            acc[o][k][0] = fma2(nb.nx, w, acc[o][k][0]);
-            acc[o][k][1] = fma2(nb.ny, w, acc[o][k][1]);
-            acc[o][k][2] = fma2(nb.nz, w, acc[o][k][2]);
-          }
-        }
-      }
-    }
-
-    // underflow-safe normalisation: n = m/|m|, m = acc'/s; |acc| > 1e-30 <=> |m| s > 1e-30 sB
-    const float thr = 1e-30f * sB;
-    float res[kQPT][6];
-#pragma unroll
-    for (int o = 0; o < kQPT; ++o) {
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        float* r = &res[o][3 * k];
-        // own triangle valid <=> finite normal (and centroid): not the pack sentinel
-        const bool valid = own[o][k].cx != -1e18f;
-        // wsum is not accumulated: wsum == 0 implies acc == 0, so the reference's
-        // `wsum > 0 and |acc| > 1e-30` (_native.pyx:352-360) is just |acc| > 1e-30, here
-        // |acc'| > 1e-30 sqrt(B) evaluated underflow-safely as s * |acc'/s|, s = max |acc'_i|
-        const float ax = f2lo(acc[o][k][0]) + f2hi(acc[o][k][0]);
-        const float ay = f2lo(acc[o][k][1]) + f2hi(acc[o][k][1]);
-        const float az = f2lo(acc[o][k][2]) + f2hi(acc[o][k][2]);
-        const float s = fmaxf(fabsf(ax), fmaxf(fabsf(ay), fabsf(az)));
-        bool upd = false;
-        if (valid && s > 0.f) {
-          const float is = rcp_approx(s);  // a common scale: cancels in the normalisation
-          const float mx = ax * is, my = ay * is, mz = az * is;
-          // |m|^2 in [1, 3]: MUFU rsqrt + one Newton step (~1 ulp, like IEEE sqrt + divide,
-          // whose slow-path checks cost ~8 % of the kernel's instructions)
-          const float l2 = mx * mx + my * my + mz * mz;
-          float il = rsqrt_approx(l2);
-          il = il * fmaf(-0.5f * l2, il * il, 1.5f);
-          if (l2 * il * s > thr) {
-            r[0] = mx * il;
-            r[1] = my * il;
-            r[2] = mz * il;
-            upd = true;
-          }
-        }
-        if (!upd) {  // unchanged (missing / isolated / |acc| <= 1e-30): the input normal
-          const float* n = (MODE == kFromPoints)
-                               ? out_s + ((kQPT * ty + o) * kBilTQW + tx) * 6 + 3 * k
-                               : nrm_s + ((R0 + o) * T::QW + C) * 6 + 3 * k;
-          r[0] = n[0];
-          r[1] = n[1];
-          r[2] = n[2];
-        }
-      }
-    }
-
-    if (SCATTER) {
-#pragma unroll
-      for (int o = 0; o < kQPT; ++o) {
-        const int u = u0 + kQPT * ty + o, v = q0 + tx;
-        if (u < Mq && v < Nq) {
-          const long long g = 2ll * ((long long)u * Nq + v);
-          const longlong2 tm = *reinterpret_cast<const longlong2*>(a.trimap + f * a.tm_fs + g);
-          float* dst = a.out_mesh + f * a.out_fs;
-          if (tm.x >= 0 && tm.x < a.n_out) {
-            dst[3 * tm.x] = res[o][0];
-            dst[3 * tm.x + 1] = res[o][1];
-            dst[3 * tm.x + 2] = res[o][2];
-          }
-          if (tm.y >= 0 && tm.y < a.n_out) {
-            dst[3 * tm.y] = res[o][3];
-            dst[3 * tm.y + 1] = res[o][4];
-            dst[3 * tm.y + 2] = res[o][5];
-          }
-        }
+      for (int j = 0; j < 6; ++j) {
+        n[j] = nrm_s[q * 6 + j];
+        cc[j] = cen_s[q * 6 + j] * sA;
       }
     } else {
-      __syncthreads();  // every thread has read its raw normals (out tile aliases them)
+      const float* P1 = pts_s + (r * T::PW + c + T::PSHIFT) * 3;
+      const float* P2 = P1 + 3;
+      const float* P4 = P1 + T::PW * 3;
+      const float* P3 = P4 + 3;
+      // triangles (p3, p2, p1) and (p1, p4, p3) share p1 + p3
 #pragma unroll
-      for (int o = 0; o < kQPT; ++o) {
-        float* dst = out_s + ((kQPT * ty + o) * kBilTQW + tx) * 6;
+      for (int j = 0; j < 3; ++j) {
+        const float s13 = P1[j] + P3[j];
+        cc[j] = (s13 + P2[j]) * sA3;
+        cc[3 + j] = (s13 + P4[j]) * sA3;
+      }
+      if (MODE == kFromPoints) {
+        unit_normal_fast(P3, P2, P1, n);
+        unit_normal_fast(P1, P4, P3, n + 3);
+      } else {
 #pragma unroll
-        for (int j = 0; j < 6; ++j) dst[j] = res[o][j];
+        for (int j = 0; j < 6; ++j) n[j] = nrm_s[q * 6 + j];
       }
-      fence_proxy_async_smem();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tma_store_3d(&tout, out_s, q0 * 6, u0, f);
-        tma_store_commit_and_wait();
+      if (MODE == kFromPoints && !PACKOUT) {  // raw normals of interior quads: "unchanged"
+        const int ir = r - H, ic = c - T::LQ;
+        if (ir >= 0 && ir < kBilTQH && ic >= 0 && ic < kBilTQW) {
+#pragma unroll
+          for (int j = 0; j < 6; ++j) out_s[(ir * kBilTQW + ic) * 6 + j] = n[j];
+        }
       }
+    }
+    pack_quad(P, q, n, cc, sB);
+  }
+  __syncthreads();
+
+  static_assert(kQPT == 2, "bil_weigh handles 2 quads per thread");
+  Quad2 qa, qb;
+  float res[2][6];
+  bool upd[2][2];
+  bil_weigh<H>(P, R0, C, sB, qa, qb, res, upd);
+
+  if (PACKOUT) {
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      const int u = u0 + kQPT * ty + o, v = q0 + tx;
+      if (u < Mq && v < Nq) {
+        const Quad2& q = o == 0 ? qa : qb;
+        pg.c0[f * pg.f4 + (long long)u * pg.s4 + v] =
+            make_float4(f2lo(q.cx), f2hi(q.cx), f2lo(q.cy), f2hi(q.cy));
+        pg.c1[f * pg.f2s + (long long)u * pg.s2 + v] = make_float2(f2lo(q.cz), f2hi(q.cz));
+        store_packed_n(pg, f, u, v, res[o], upd[o], q, sB);
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int o = 0; o < kQPT; ++o) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      if (!upd[o][k]) {  // unchanged (missing / isolated / |acc| <= 1e-30): the input normal
+        float* r = &res[o][3 * k];
+        const float* n = (MODE == kFromPoints)
+                             ? out_s + ((kQPT * ty + o) * kBilTQW + tx) * 6 + 3 * k
+                             : nrm_s + ((R0 + o) * T::QW + C) * 6 + 3 * k;
+        r[0] = n[0];
+        r[1] = n[1];
+        r[2] = n[2];
+      }
+    }
+  }
+
+  if (SCATTER) {
+#pragma unroll
+    for (int o = 0; o < kQPT; ++o) {
+      const int u = u0 + kQPT * ty + o, v = q0 + tx;
+      if (u < Mq && v < Nq) scatter_mesh(a, f, u, v, res[o]);
+    }
+  } else {
+    __syncthreads();  // every thread has read its raw normals (out tile aliases them)
+#pragma unroll
+    for (int o = 0; o < kQPT; ++o) {
+      float* dst = out_s + ((kQPT * ty + o) * kBilTQW + tx) * 6;
+#pragma unroll
+      for (int j = 0; j < 6; ++j) dst[j] = res[o][j];
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma_store_3d(&tout, out_s, q0 * 6, u0, f);
+      tma_store_commit_and_wait();
     }
   }
 }
 
-template <int H, int MODE, bool SCATTER>
+// Iterations 2..B of the fused pipeline: the packed planes (constant centroids from
+// iteration 1, the previous iteration's packed normals) arrive by four TMA boxes straight
+// into the shared-memory planes -- no pack phase, no barrier after the load.  Off-grid
+// halo quads are zero-filled by TMA: their n' = 0, so whatever their weight, they add
+// nothing.  Unchanged outputs are the input n' exactly (scaled domain); the final scatter
+// unscales (n'/sqrt(B): <= 1 ulp of the unit normal; NaN for the sentinel).
+template <int H, bool SCATTER>
+__global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
+    bilateral_packed_kernel(const __grid_constant__ CUtensorMap tc0,
+                            const __grid_constant__ CUtensorMap tc1,
+                            const __grid_constant__ CUtensorMap tn0,
+                            const __grid_constant__ CUtensorMap tn1, BilArgs a, PackedG out) {
+  using T = BilTile<H>;
+  extern __shared__ __align__(16) char smem_raw[];
+  uint64_t* barp;
+  float* p = reinterpret_cast<float*>(smem_aligned_base(smem_raw, &barp));
+  const Planes P = planes_at<H>(p);
+  uint64_t& bar = *barp;
+  const int Mq = a.M - 1, Nq = a.N - 1;
+  const int q0 = blockIdx.x * kBilTQW;
+  const int u0 = blockIdx.y * kBilTQH;
+  const int f = blockIdx.z;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, T::QW * T::QH * 48);
+    const int x = q0 - T::LQ, y = u0 - H;
+    tma_load_3d(P.c0, &tc0, &bar, x * 4, y, f);
+    tma_load_3d(P.c1, &tc1, &bar, x * 2, y, f);
+    tma_load_3d(P.n0, &tn0, &bar, x * 4, y, f);
+    tma_load_3d(P.n1, &tn1, &bar, x * 2, y, f);
+  }
+  const float sB = a.sB;
+  const int tx = threadIdx.x % kBilTQW, ty = threadIdx.x / kBilTQW;
+  const int R0 = kQPT * ty + H, C = tx + T::LQ;
+  mbar_wait(&bar, 0);
+
+  Quad2 qa, qb;
+  float res[2][6];
+  bool upd[2][2];
+  bil_weigh<H>(P, R0, C, sB, qa, qb, res, upd);
+
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+    const int u = u0 + kQPT * ty + o, v = q0 + tx;
+    if (u >= Mq || v >= Nq) continue;
+    const Quad2& q = o == 0 ? qa : qb;
+    if (SCATTER) {
+      const float inv = 1.0f / sB;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (!upd[o][k]) {
+          const bool valid = (k == 0 ? f2lo(q.cx) : f2hi(q.cx)) != 1e18f;
+          const float qn = __int_as_float(0x7fc00000);
+          res[o][3 * k] = valid ? (k == 0 ? f2lo(q.nx) : f2hi(q.nx)) * inv : qn;
+          res[o][3 * k + 1] = valid ? (k == 0 ? f2lo(q.ny) : f2hi(q.ny)) * inv : qn;
+          res[o][3 * k + 2] = valid ? (k == 0 ? f2lo(q.nz) : f2hi(q.nz)) * inv : qn;
+        }
+      }
+      scatter_mesh(a, f, u, v, res[o]);
+    } else {
+      store_packed_n(out, f, u, v, res[o], upd[o], q, sB);
+    }
+  }
+}
+
+template <int H, int MODE, bool SCATTER, bool PACKOUT = false>
 int launch_bil(const CUtensorMap& tp, const CUtensorMap& tn, const CUtensorMap& tc,
-               const CUtensorMap& to, const BilArgs& a, int F, cudaStream_t st) {
+               const CUtensorMap& to, const BilArgs& a, int F, cudaStream_t st,
+               const PackedG& pg = PackedG{}) {
   constexpr int smem = bil_smem_bytes<H, MODE>();
   static unsigned long long attr_mask = 0;
-  ensure_smem_attr(bilateral_kernel<H, MODE, SCATTER>, smem, attr_mask);
+  ensure_smem_attr(bilateral_kernel<H, MODE, SCATTER, PACKOUT>, smem, attr_mask);
   const int Mq = a.M - 1, Nq = a.N - 1;
   dim3 grid((Nq + kBilTQW - 1) / kBilTQW, (Mq + kBilTQH - 1) / kBilTQH, F);
-  bilateral_kernel<H, MODE, SCATTER><<<grid, kBilNT, smem, st>>>(tp, tn, tc, to, a);
+  bilateral_kernel<H, MODE, SCATTER, PACKOUT><<<grid, kBilNT, smem, st>>>(tp, tn, tc, to, a, pg);
   return check_launch("bilateral_kernel");
+}
+
+template <int H, bool SCATTER>
+int launch_packed(const CUtensorMap* maps, const BilArgs& a, int F, const PackedG& out,
+                  cudaStream_t st) {
+  using T = BilTile<H>;
+  constexpr int smem = T::PACK_F * 4 + kSmemSlack;
+  static unsigned long long attr_mask = 0;
+  ensure_smem_attr(bilateral_packed_kernel<H, SCATTER>, smem, attr_mask);
+  const int Mq = a.M - 1, Nq = a.N - 1;
+  dim3 grid((Nq + kBilTQW - 1) / kBilTQW, (Mq + kBilTQH - 1) / kBilTQH, F);
+  bilateral_packed_kernel<H, SCATTER><<<grid, kBilNT, smem, st>>>(maps[0], maps[1], maps[2],
+                                                                   maps[3], a, out);
+  return check_launch("bilateral_packed_kernel");
 }
 
 template <int H>
@@ -524,6 +699,38 @@ int launch_h(int h, int mode, bool scatter, const CUtensorMap& tp, const CUtenso
   }
 }
 
+int launch_packout_h(int h, const CUtensorMap& tp, const BilArgs& a, int F, const PackedG& pg,
+                     cudaStream_t st) {
+  switch (h) {
+    case 1: return launch_bil<1, kFromPoints, false, true>(tp, tp, tp, tp, a, F, st, pg);
+    case 2: return launch_bil<2, kFromPoints, false, true>(tp, tp, tp, tp, a, F, st, pg);
+    case 3: return launch_bil<3, kFromPoints, false, true>(tp, tp, tp, tp, a, F, st, pg);
+    case 4: return launch_bil<4, kFromPoints, false, true>(tp, tp, tp, tp, a, F, st, pg);
+    default: return fail(ERR_UNSUPPORTED, "bilateral: kernel_size > 9 is not compiled in");
+  }
+}
+
+int launch_packed_h(int h, bool scatter, const CUtensorMap* maps, const BilArgs& a, int F,
+                    const PackedG& out, cudaStream_t st) {
+  switch (h) {
+    case 1: return scatter ? launch_packed<1, true>(maps, a, F, out, st)
+                           : launch_packed<1, false>(maps, a, F, out, st);
+    case 2: return scatter ? launch_packed<2, true>(maps, a, F, out, st)
+                           : launch_packed<2, false>(maps, a, F, out, st);
+    case 3: return scatter ? launch_packed<3, true>(maps, a, F, out, st)
+                           : launch_packed<3, false>(maps, a, F, out, st);
+    case 4: return scatter ? launch_packed<4, true>(maps, a, F, out, st)
+                           : launch_packed<4, false>(maps, a, F, out, st);
+    default: return fail(ERR_UNSUPPORTED, "bilateral: kernel_size > 9 is not compiled in");
+  }
+}
+
+// OPCFE_BILATERAL_PACKED=0 disables the packed-plane path of the fused pipeline (A/B)
+static const bool g_bil_packed = [] {
+  const char* v = std::getenv("OPCFE_BILATERAL_PACKED");
+  return v == nullptr || v[0] != '0';
+}();
+
 int box_q(int h) { return ((((h + 1) / 2 * 2) + kBilTQW + h + 1) / 2) * 2; }
 int box_p(int h) { return ((((h + 3) / 4 * 4) + kBilTQW + h + 1 + 3) / 4) * 4; }
 
@@ -532,7 +739,7 @@ int box_p(int h) { return ((((h + 3) / 4 * 4) + kBilTQW + h + 1 + 3) / 4) * 4; }
 int bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
               const float* centroids_in, float sigma_length, float sigma_angle, int ksize,
               int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
-              float* out_mesh, long long out_rows, cudaStream_t st) {
+              float* out_mesh, long long out_rows, cudaStream_t st, float* buf_c) {
   if (F < 1 || M < 2 || N < 2 || iters < 1 || ksize < 3 || (ksize % 2) == 0)
     return fail(ERR_INVALID, "bilateral: bad shape or parameters");
   if (!(sigma_length > 0.f) || !(sigma_angle > 0.f))
@@ -595,6 +802,50 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   a.out_mesh = out_mesh;
   a.out_fs = 3ll * out_rows;
   a.n_out = out_rows;
+
+  // Fused pipeline with >= 2 iterations and a third buffer: iteration 1 writes the packed
+  // planes (centroids once into C, normals into A); iterations 2..B read them by TMA with
+  // no pack phase (bilateral_packed_kernel), ping-ponging A / B; the last one scatters.
+  if (buf_c != nullptr && g_bil_packed && !from_arrays && !resume && scatter && iters >= 2) {
+    const long long Nq2 = (Nq + 1) & ~1ll;
+    auto planes_of = [&](float* b) {
+      PackedG g;
+      g.c0 = reinterpret_cast<float4*>(b);
+      g.c1 = reinterpret_cast<float2*>(b + 4ll * F * Mq * Nq);
+      g.n0 = g.c0;
+      g.n1 = g.c1;
+      g.s4 = Nq;
+      g.s2 = Nq2;
+      g.f4 = (long long)Mq * Nq;
+      g.f2s = (long long)Mq * Nq2;
+      return g;
+    };
+    const PackedG gc = planes_of(buf_c), ga = planes_of(buf_a);
+    const PackedG gb = buf_b ? planes_of(buf_b) : ga;
+    auto maps_of = [&](const PackedG& g, CUtensorMap* m4, CUtensorMap* m2) {
+      int r = make_tmap_3d(m4, g.c0, false, 4ull * Nq, Mq, F, 4ull * Nq, 4ull * Mq * Nq,
+                           QW * 4, QH, true);
+      if (!r) r = make_tmap_3d(m2, g.c1, false, 2ull * Nq, Mq, F, 2ull * Nq2, 2ull * Mq * Nq2,
+                               QW * 2, QH, true);
+      return r;
+    };
+    CUtensorMap mc[2], mna[2], mnb[2];
+    if ((rc = maps_of(gc, &mc[0], &mc[1])) || (rc = maps_of(ga, &mna[0], &mna[1])) ||
+        (rc = maps_of(gb, &mnb[0], &mnb[1])))
+      return rc;
+    PackedG out0 = ga;  // iteration 1: centroids -> C, normals -> A
+    out0.c0 = gc.c0;
+    out0.c1 = gc.c1;
+    if ((rc = launch_packout_h(h, m_pts, a, F, out0, st))) return rc;
+    for (int it = 1; it < iters; ++it) {
+      const bool last = it == iters - 1;
+      const bool from_a = (it % 2) == 1;
+      const CUtensorMap* nin = from_a ? mna : mnb;
+      const CUtensorMap maps[4] = {mc[0], mc[1], nin[0], nin[1]};
+      if ((rc = launch_packed_h(h, last, maps, a, F, from_a ? gb : ga, st))) return rc;
+    }
+    return OK;
+  }
 
   // it0 reads (points | arrays) and writes A; it_k reads A/B and writes B/A; the last
   // iteration scatters to mesh order (trimap) or stores to out_fc.

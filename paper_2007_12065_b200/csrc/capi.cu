@@ -34,7 +34,7 @@ static std::once_flag g_encode_once;
 
 int make_tmap_3d(CUtensorMap* map, const void* base, bool f64, uint64_t cols, uint64_t rows,
                  uint64_t frames, uint64_t row_pitch_elems, uint64_t frame_stride_elems,
-                 uint32_t box_cols, uint32_t box_rows) {
+                 uint32_t box_cols, uint32_t box_rows, bool zero_fill) {
   std::call_once(g_encode_once, [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -57,7 +57,7 @@ int make_tmap_3d(CUtensorMap* map, const void* base, bool f64, uint64_t cols, ui
       map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
       const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-      CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA);
+      zero_fill ? CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE : CU_TENSOR_MAP_FLOAT_OOB_FILL_NAN_REQUEST_ZERO_FMA);
   if (r != CUDA_SUCCESS) {
     char buf[160];
     snprintf(buf, sizeof buf, "cuTensorMapEncodeTiled failed (%d): dims %llu x %llu x %llu box %u x %u",
@@ -75,7 +75,8 @@ inline cudaStream_t S(opcfe_stream_t s) { return reinterpret_cast<cudaStream_t>(
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct FeLayout {
-  size_t vmask = 0, status = 0, staged = 0, lap_tmp = 0, bil_a = 0, bil_b = 0, total = 0;
+  size_t vmask = 0, status = 0, staged = 0, lap_tmp = 0, bil_a = 0, bil_b = 0, bil_c = 0,
+         total = 0;
   size_t vmask_b = 0, status_b = 0, staged_b = 0, lap_b = 0, bil_b_bytes = 0;
 };
 
@@ -105,6 +106,8 @@ FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src
   off += (p->bilateral_iterations > 1) ? align256(fc_bytes) : 0;
   L.bil_b = off;
   off += (p->bilateral_iterations > 2) ? align256(fc_bytes) : 0;
+  L.bil_c = off;  // packed centroid planes of the fused bilateral (>= 2 iterations)
+  off += (p->bilateral_iterations > 1) ? align256(fc_bytes) : 0;
   L.total = off + 256;
   return L;
 }
@@ -262,6 +265,7 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   float* lap_tmp = reinterpret_cast<float*>(base + L.lap_tmp);
   float* bil_a = reinterpret_cast<float*>(base + L.bil_a);
   float* bil_b = reinterpret_cast<float*>(base + L.bil_b);
+  float* bil_c = reinterpret_cast<float*>(base + L.bil_c);
   const cudaStream_t st = S(stream);
   const bool f64 = io->src_kind == 2;
   const long long rs = io->src_kind == 0 ? io->src_pitch : 3ll * N;
@@ -302,7 +306,7 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
                    p->bilateral_kernel_size, p->bilateral_iterations,
                    p->bilateral_iterations > 1 ? bil_a : nullptr,
                    p->bilateral_iterations > 2 ? bil_b : nullptr, nullptr, io->trimap, io->normals,
-                   2ll * (M - 1) * (N - 1), st);
+                   2ll * (M - 1) * (N - 1), st, p->bilateral_iterations > 1 ? bil_c : nullptr);
     if (rc) return rc;
   }
   // 4. group labels (segmentation.group_assignment) on the final normals

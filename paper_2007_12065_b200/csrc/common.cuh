@@ -39,9 +39,10 @@ inline int fc_pitch(int N) { return round_up(6 * (N - 1), 4); }    // floats per
 // (elements) and a frame stride (elements).  Out-of-bounds reads fill with NaN,
 // which is exactly the reference's "off-grid neighbour is skipped" rule
 // (_kernels/_fallback.py:94 pads with NaN).
+// zero_fill: out-of-bounds reads return 0 instead of NaN (packed bilateral planes).
 int make_tmap_3d(CUtensorMap* map, const void* base, bool f64, uint64_t cols, uint64_t rows,
                  uint64_t frames, uint64_t row_pitch_elems, uint64_t frame_stride_elems,
-                 uint32_t box_cols, uint32_t box_rows);
+                 uint32_t box_cols, uint32_t box_rows, bool zero_fill = false);
 
 // Opt a kernel into `smem` bytes of dynamic shared memory on the CURRENT device, once per
 // device (the attribute is per device context; `mask` is the caller's per-kernel bitset).

@@ -25,7 +25,8 @@ int halfedges_from_trimap(const int64_t* trimap, int M, int N, int64_t n_tri, in
 int bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
               const float* centroids_in, float sigma_length, float sigma_angle, int ksize,
               int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
-              float* out_mesh, long long out_rows, cudaStream_t st);
+              float* out_mesh, long long out_rows, cudaStream_t st,
+              float* buf_c = nullptr);  // fused pipeline: packed centroid planes (FC size)
 
 int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st);
 int triangle_normals(const void* pts, bool f64, const int64_t* tris, long long T, void* out,
