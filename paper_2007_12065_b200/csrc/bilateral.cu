@@ -63,10 +63,10 @@ constexpr int kBilTQW = 32;  // interior quads per tile row (= one warp)
 constexpr int kBilTQH = OPCFE_BIL_TQH;  // interior quad rows per tile (A/B: -DOPCFE_BIL_TQH)
 constexpr int kQPT = 2;                         // interior quads per thread (vertical)
 constexpr int kBilNT = kBilTQW * kBilTQH / kQPT;  // threads per CTA
-#ifndef OPCFE_BIL_REGS
-#define OPCFE_BIL_REGS 80
-#endif
-constexpr int kBilMinBlocks = 65536 / (OPCFE_BIL_REGS * kBilNT);  // register budget per thread
+// resident CTAs the register budget targets: k = 3 -> 7 (72 registers; its packed kernel
+// needs 17.7 KB of shared memory); larger windows have larger tiles (fewer CTAs by shared
+// memory anyway) and more registers live
+constexpr int bil_min_blocks(int h) { return h == 1 ? 7 : (h == 2 ? 5 : 4); }
 
 enum BilMode : int {
   kFromPoints = 0,     // iteration 1: normals + centroids from the point grid
@@ -430,7 +430,7 @@ __device__ __forceinline__ void scatter_mesh(const BilArgs& a, int f, int u, int
 // packed centroid planes (constant for all later iterations) and the packed filtered
 // normals, so the later iterations (bilateral_packed_kernel) skip the pack phase.
 template <int H, int MODE, bool SCATTER, bool PACKOUT>
-__global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
+__global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     bilateral_kernel(const __grid_constant__ CUtensorMap tpts, const __grid_constant__ CUtensorMap tnrm,
                      const __grid_constant__ CUtensorMap tcen, const __grid_constant__ CUtensorMap tout,
                      BilArgs a, PackedG pg) {
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
 // nothing.  Unchanged outputs are the input n' exactly (scaled domain); the final scatter
 // unscales (n'/sqrt(B): <= 1 ulp of the unit normal; NaN for the sentinel).
 template <int H, bool SCATTER>
-__global__ void __launch_bounds__(kBilNT, kBilMinBlocks)
+__global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     bilateral_packed_kernel(const __grid_constant__ CUtensorMap tc0,
                             const __grid_constant__ CUtensorMap tc1,
                             const __grid_constant__ CUtensorMap tn0,
