@@ -18,6 +18,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:lapl
   -s 35 -c 1 -o gpurun_out/${TAG}_lap $CMD > gpurun_out/${TAG}_ncu_lap.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:triangulate_kernel \
   -s 3 -c 1 -o gpurun_out/${TAG}_tri $CMD > gpurun_out/${TAG}_ncu_tri.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:bilateral_kernel \
-  -s 16 -c 1 -o gpurun_out/${TAG}_bil $CMD > gpurun_out/${TAG}_ncu_bil.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:bilateral_packed \
+  -s 12 -c 1 -o gpurun_out/${TAG}_bil $CMD > gpurun_out/${TAG}_ncu_bil.log 2>&1
 ls -la gpurun_out/${TAG}_*

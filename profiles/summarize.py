@@ -67,6 +67,8 @@ def launch_shares(path):
     for r in rows[hdr + 1:]:
         if len(r) > vi:
             name = r[ki].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
+            if name == "bilateral_packed_kernel":
+                name = "bilateral_kernel"  # one bench stage: iteration 1 + packed 2..B
             agg[name].append(float(r[vi].replace(",", "")))
     tot = sum(sum(v) for v in agg.values())
     return {k: (len(v), sum(v) / len(v), sum(v) / tot) for k, v in agg.items()}
