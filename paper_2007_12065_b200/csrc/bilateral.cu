@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
   bool upd[2][2];
   bil_weigh<H>(P, R0, C, sB, qa, qb, res, upd);
 
-  if (PACKOUT) {
+  if constexpr (PACKOUT) {
 #pragma unroll
     for (int o = 0; o < 2; ++o) {
       const int u = u0 + kQPT * ty + o, v = q0 + tx;
@@ -533,8 +533,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
         store_packed_n(pg, f, u, v, res[o], upd[o], q, sB);
       }
     }
-    return;
-  }
+  } else {
 #pragma unroll
   for (int o = 0; o < kQPT; ++o) {
 #pragma unroll
@@ -572,6 +571,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
       tma_store_commit_and_wait();
     }
   }
+  }  // !PACKOUT
 }
 
 // Iterations 2..B of the fused pipeline: the packed planes (constant centroids from
