@@ -188,6 +188,7 @@ __device__ __forceinline__ void lap_pair(const float* p, const float* q, Acc4& a
   }
 }
 
+template <bool VMASK>  // first pass: also emit the validity mask
 __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
     laplacian3_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
                       uint32_t* __restrict__ vmask, long long vm_fs, int wpr, int M, int N,
@@ -216,7 +217,15 @@ __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane, v = v0 + c;
   const int r0 = warp * kL3RS;  // first tile row of this thread
-  const bool col_in = v > 0 && v < N - 1;
+  // rows of this thread's strip that may move (interior row and column), one bit per row
+  uint32_t movable = 0;
+  if (v > 0 && v < N - 1) {
+#pragma unroll
+    for (int i = 0; i < kL3RS; ++i) {
+      const int u = u0 + r0 + i;
+      movable |= (u > 0 && u < M - 1) ? (1u << i) : 0u;
+    }
+  }
   // window rows: box row of tile row r is r + 1
   auto ld3 = [&](int br, float (*dst)[3]) {
     const float* q = in_s + (br * kL3BW + c + kL3L - 1) * 3;
@@ -237,7 +246,7 @@ __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
     ld3(r + 2, Cr);  // tile row r + 1
     const float* p = B[1];
     const bool fin = finite3f(p[0], p[1], p[2]);  // off-grid reads are NaN-filled -> false
-    if (vmask != nullptr) {
+    if (VMASK) {
       const uint32_t bits = __ballot_sync(0xffffffffu, fin);
       if (lane == 0 && u < M && v0 < N) vmask[f * vm_fs + (long long)u * wpr + (v0 >> 5)] = bits;
     }
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
     lap_pair(p, Cr[1], acc, down);
     lap_pair(p, Cr[2], acc, nullptr);
     float ox = p[0], oy = p[1], oz = p[2];
-    if (fin && col_in && u > 0 && u < M - 1 && acc.w > 0.f) {
+    if (fin && ((movable >> i) & 1u) && acc.w > 0.f) {
       const float s = lam * rcp_approx(acc.w);
       ox = p[0] + s * acc.x;
       oy = p[1] + s * acc.y;
@@ -296,7 +305,9 @@ int run_k3(const float* in, float* out, float* tmp, uint32_t* vmask, int F, int 
     if ((rc = make_tmap_3d(&st_tmp, tmp, false, 3ull * N, M, F, pitch, fs, kL3TW * 3, kL3TH))) return rc;
   }
   static unsigned long long attr_mask = 0;
-  ensure_smem_attr(laplacian3_kernel, kL3Smem, attr_mask);
+  static unsigned long long attr_mask_v = 0;
+  ensure_smem_attr(laplacian3_kernel<false>, kL3Smem, attr_mask);
+  ensure_smem_attr(laplacian3_kernel<true>, kL3Smem, attr_mask_v);
   const int wpr = (N + 31) / 32;
   const long long vm_fs = (long long)M * wpr;
   dim3 grid((N + kL3TW - 1) / kL3TW, (M + kL3TH - 1) / kL3TH, F);
@@ -304,7 +315,8 @@ int run_k3(const float* in, float* out, float* tmp, uint32_t* vmask, int F, int 
   const CUtensorMap* src = &m_in;
   for (int it = 0; it < iters; ++it) {
     const CUtensorMap* dst = to_out ? &st_out : &st_tmp;
-    laplacian3_kernel<<<grid, kL3NT, kL3Smem, st>>>(*src, *dst, it == 0 ? vmask : nullptr, vm_fs, wpr,
+    auto kern = (it == 0 && vmask != nullptr) ? laplacian3_kernel<true> : laplacian3_kernel<false>;
+    kern<<<grid, kL3NT, kL3Smem, st>>>(*src, *dst, it == 0 ? vmask : nullptr, vm_fs, wpr,
                                                   M, N, lam);
     if ((rc = check_launch("laplacian3_kernel"))) return rc;
     src = to_out ? &ld_out : &ld_tmp;
