@@ -36,21 +36,65 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 METRIC = "frames/sec (HBM GB/s vs roofline) for smooth+mesh of 1080p organized PC, 1/2/4/8 GPU"
-LAP = (1.0, 3, 10)
-BIL = (0.1, 0.15, 3, 5)
-M, N = 1080, 1920
 
 
-def config_dict(frames):
-    return {"workload": "C4: 1080x1920 organized cloud (room scene), 10 Laplacian + 5 bilateral "
-                        "iterations, full mesh + half-edge twins",
-            "frames_per_gpu_per_step": frames, "grid": [M, N],
-            "laplacian": {"lam": LAP[0], "kernel_size": LAP[1], "iterations": LAP[2]},
-            "bilateral": {"sigma_length": BIL[0], "sigma_angle": BIL[1], "kernel_size": BIL[2],
-                          "iterations": BIL[3]},
-            "l2": f"inputs larger than L2: {frames} x 24.9 MB fp32 per step per GPU; "
-                  "outputs/workspace ~0.45 GB per frame",
-            "outputs": "smoothed grid fp32, triangles/trimap/halfedges int64, normals fp32"}
+class Workload:
+    """One of BASELINE.json's configs.  C4 (the metric's config) is the default bench
+    line; the others are secondary lines (`--workload`), C5 strong-scales a fixed batch."""
+
+    def __init__(self, name, desc, M, N, lap, bil, l_max, base, frames, total=None,
+                 dropout=0.0):
+        self.name, self.desc, self.M, self.N = name, desc, M, N
+        self.lap, self.bil, self.l_max, self.base = lap, bil, l_max, base
+        self.frames, self.total, self.dropout = frames, total, dropout
+
+
+def _base(name):
+    def make():
+        from paper_2007_12065_b200 import synthetic
+        return getattr(synthetic, name)()
+    return make
+
+
+WORKLOADS = {
+    "C4": Workload("C4", "C4: 1080x1920 organized cloud (room scene), 10 Laplacian + 5 bilateral "
+                         "iterations, full mesh + half-edge twins",
+                   1080, 1920, (1.0, 3, 10), (0.1, 0.15, 3, 5), None, _base("config_c4"), 16),
+    "C1": Workload("C1", "C1: 250x250 room scene, 1 Laplacian + 1 bilateral iteration",
+                   250, 250, (1.0, 3, 1), (0.1, 0.15, 3, 1), None, _base("config_c1"), 256),
+    "C2": Workload("C2", "C2: 480x640 RealSense-sized room crop (2 % dropout), 3 Laplacian + 2 "
+                         "bilateral iterations, mesh + normals",
+                   480, 640, (1.0, 3, 3), (0.1, 0.15, 3, 2), None, _base("config_c2"), 64),
+    "C3": Workload("C3", "C3: 64x1024 LiDAR range image with NaN gaps, 5 Laplacian iterations, "
+                         "l_max = 0.5 mask, mesh + twins + normals",
+                   64, 1024, (1.0, 3, 5), None, 0.5, _base("config_c3"), 512),
+    "C5": Workload("C5", "C5: batch of 512 frames at 480x640 (C2 base + per-frame 2 mm noise + "
+                         "2 % dropout) split over the GPUs, full front-end per frame",
+                   480, 640, (1.0, 3, 3), (0.1, 0.15, 3, 2), None,
+                   lambda: __import__("paper_2007_12065_b200.synthetic", fromlist=["x"])
+                   .room_scene(n=640, noise=0.002, seed=2)[80:560, :].copy(),
+                   512, total=512, dropout=0.02),
+}
+WL = WORKLOADS["C4"]
+
+
+def config_dict(frames, wl=None):
+    wl = wl or WL
+    per = frames * wl.M * wl.N * 12
+    return {"workload": wl.desc,
+            "frames_per_gpu_per_step": frames, "grid": [wl.M, wl.N],
+            "laplacian": ({"lam": wl.lap[0], "kernel_size": wl.lap[1], "iterations": wl.lap[2]}
+                          if wl.lap else None),
+            "bilateral": ({"sigma_length": wl.bil[0], "sigma_angle": wl.bil[1],
+                           "kernel_size": wl.bil[2], "iterations": wl.bil[3]} if wl.bil else None),
+            **({"l_max": wl.l_max} if wl.l_max is not None else {}),
+            **({"total_frames_per_step": wl.total} if wl.total else {}),
+            "l2": (f"inputs larger than L2: {frames} x {wl.M * wl.N * 12 / 1e6:.1f} MB fp32 "
+                   f"= {per / 1e6:.0f} MB per step per GPU" if per > 126e6 else
+                   f"inputs {per / 1e6:.0f} MB per step per GPU: L2-resident (126 MB L2), "
+                   "flagged per SURVEY.md 8d"),
+            "outputs": "smoothed grid fp32, triangles/trimap/halfedges int64, normals fp32"
+                       + (", l_max flags u8" if wl.l_max is not None else "")}
 
 
 # ------------------------------------------------------------------ clocks
@@ -102,15 +146,16 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm
-def cpu_reference(steps, warmup, budget_s=None):
+def cpu_reference(steps, warmup, budget_s=None, wl=None):
     """Time the reference's own CPU implementation on this host (bounded sample)."""
     import numpy as np
     from oracle import ref_frontend
-    from paper_2007_12065_b200 import synthetic
-    frame = synthetic.config_c4()
+    wl = wl or WL
+    frame = wl.base()
     cores = len(os.sched_getaffinity(0))
-    rows = 136                                  # ~1/8 frame per task
-    pool = ref_frontend.ReferencePool(frame, cores, rows, LAP, BIL)
+    # 1080p: ~1/8 frame (136-row strip) per task; small configs: one whole frame per task
+    rows = 136 if wl.M >= 1000 else wl.M
+    pool = ref_frontend.ReferencePool(frame, cores, rows, wl.lap, wl.bil)
     try:
         for _ in range(warmup):
             pool.step()
@@ -124,26 +169,30 @@ def cpu_reference(steps, warmup, budget_s=None):
     finally:
         pool.close()
     total = sum(times)
+    what = (f"a {rows}x{wl.N} row strip of the {wl.name} frame ({rows / wl.M:.3f} frame)"
+            if rows < wl.M else f"one {wl.M}x{wl.N} {wl.name} frame")
     return {"value": credit / total, "unit": "frames/s", "cores": cores,
             "kind": ref_frontend.kind(),
-            "sample": f"{len(times)} steps x {cores} processes, each a {rows}x{N} row strip of "
-                      f"the C4 frame ({rows / M:.3f} frame) through laplacian_filter (reference "
-                      "Cython) -> triangles/twins/normals (NumPy, as the reference) -> FC data "
-                      "-> bilateral_iterate (reference Cython) -> gather; single-threaded "
-                      "math per process",
+            "sample": f"{len(times)} steps x {cores} processes, each {what} through "
+                      "laplacian_filter (reference Cython) -> triangles/twins/normals (NumPy, "
+                      "as the reference)"
+                      + (" -> FC data -> bilateral_iterate (reference Cython) -> gather"
+                         if wl.bil else "")
+                      + "; single-threaded math per process",
             "ms_per_step": 1e3 * total / len(times), "steps_timed": len(times),
             "np_version": np.__version__}
 
 
-def run_reference(args, rank, world):
+def run_reference(args, rank, world, wl):
     if rank != 0:
         return 0
-    cb = cpu_reference(args.steps, args.warmup)
+    cb = cpu_reference(args.steps, args.warmup, wl=wl)
     line = {"metric": METRIC, "value": cb["value"], "unit": "frames/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": cb["steps_timed"], "warmup": args.warmup,
-            "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong" if wl.total else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args.frames),
+            "config": config_dict(args.frames, wl),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -152,19 +201,25 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
-def algorithmic_bytes(frames, T):
+def algorithmic_bytes(frames, T, wl=None):
     """SURVEY.md 8d per-frame algorithmic bytes (fp32 AoS, int64 indices, per pass)."""
-    P = M * N
-    Q = (M - 1) * (N - 1)
+    wl = wl or WL
+    P = wl.M * wl.N
+    Q = (wl.M - 1) * (wl.N - 1)
     G = 2 * Q
+    lap_it = wl.lap[2] if wl.lap else 0
+    bil_it = wl.bil[3] if wl.bil else 0
+    # triangulation: points in, trimap (+ its read-back for twins), triangles + twins out;
+    # + the l_max flags (T bytes); without bilateral the mesh-order normals (12T) too
+    tri = 12 * P + 16 * G + 48 * T + (T if wl.l_max is not None else 0) + (0 if wl.bil else 12 * T)
+    # bilateral stage: FC normals+centroids (12P + 48Q) + 72Q per iteration +
+    # mesh-order gather (12G + 12T); per launch = stage / iterations
+    bil = ((12 * P + 48 * Q) + bil_it * 72 * Q + 12 * G + 12 * T) if wl.bil else 0
     return {
         "laplacian_per_launch": frames * 24 * P,
-        "triangulate_per_launch": frames * (12 * P + 16 * G + 48 * T),
-        # bilateral stage: FC normals+centroids (12P + 48Q) + 72Q per iteration +
-        # mesh-order gather (12G + 12T); per launch = stage / iterations
-        "bilateral_stage": frames * ((12 * P + 48 * Q) + BIL[3] * 72 * Q + 12 * G + 12 * T),
-        "frame_total": (24 * P * LAP[2] + 12 * P + 16 * G + 48 * T
-                        + (12 * P + 48 * Q) + BIL[3] * 72 * Q + 12 * G + 12 * T),
+        "triangulate_per_launch": frames * tri,
+        "bilateral_stage": frames * bil,
+        "frame_total": 24 * P * lap_it + tri + bil,
     }
 
 
@@ -193,8 +248,7 @@ def load_traffic():
     return {}
 
 
-def run_ours(args, rank, world, local_rank):
-    import numpy as np
+def run_ours(args, rank, world, local_rank, wl):
     import torch
     import torch.distributed as dist
 
@@ -203,13 +257,23 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    F = args.frames
-    base = torch.from_numpy(fe.synthetic.config_c4()).to(dev, torch.float32)
+    M, N = wl.M, wl.N
+    lap_p = fe.LaplacianParams(*wl.lap) if wl.lap else None
+    bil_p = fe.BilateralParams(*wl.bil) if wl.bil else None
+    if wl.total:          # a fixed batch split over the ranks (strong scaling)
+        lo, hi = D.shard_range(wl.total, world, rank)
+        F = hi - lo
+    else:                 # F frames per GPU per step (weak scaling)
+        F = args.frames
+    base = torch.from_numpy(wl.base()).to(dev, torch.float32)
     g = torch.Generator(device=dev)
     g.manual_seed(1000 + rank)
     frames = base.unsqueeze(0) + 0.002 * torch.randn((F, M, N, 3), generator=g, device=dev)
-    eng = fe.FrontEnd(M, N, F, laplacian=fe.LaplacianParams(*LAP),
-                      bilateral=fe.BilateralParams(*BIL), src_dtype=torch.float32, graph=False)
+    if wl.dropout:
+        drop = torch.rand((F, M, N, 1), generator=g, device=dev) < wl.dropout
+        frames.masked_fill_(drop, float("nan"))
+    eng = fe.FrontEnd(M, N, F, laplacian=lap_p, bilateral=bil_p, l_max=wl.l_max,
+                      src_dtype=torch.float32, graph=False)
     eng.src.copy_(frames)
     del frames
     stream = torch.cuda.current_stream(dev)
@@ -257,14 +321,13 @@ def run_ours(args, rank, world, local_rank):
     T = int(eng.n_tri[0].item())
     # max over ranks (device time)
     max_ms = D.max_over_ranks(elapsed_ms, dev)
-    value = world * F * args.steps / (max_ms / 1e3)
+    value = (wl.total if wl.total else world * F) * args.steps / (max_ms / 1e3)
 
     # ---------------- e2e through the host API (pinned f64 host frames -> outputs on host)
     e2e = None
     if not args.no_e2e:
-        pipe = fe.HostPipeline(M, N, laplacian=fe.LaplacianParams(*LAP),
-                               bilateral=fe.BilateralParams(*BIL), src_dtype=torch.float64,
-                               device=dev)
+        pipe = fe.HostPipeline(M, N, laplacian=lap_p, bilateral=bil_p, l_max=wl.l_max,
+                               src_dtype=torch.float64, device=dev)
         FE = min(F, 8)  # e2e batch: 8 frames of pinned in/out buffers (~2.8 GB) suffice
         host = torch.empty((FE, M, N, 3), dtype=torch.float64, pin_memory=True)
         host.copy_(eng.src[:FE].double().cpu())
@@ -323,12 +386,14 @@ def run_ours(args, rank, world, local_rank):
         return 0
     # ---------------- roofline of the dominant kernel
     peak, peak_src = load_peaks()
-    ab = algorithmic_bytes(F, T)
-    per_kernel = {
-        "laplacian_kernel": (ab["laplacian_per_launch"], stage_ms["laplacian"] / LAP[2], LAP[2]),
-        "triangulate_kernel": (ab["triangulate_per_launch"], stage_ms["triangulate"], 1),
-        "bilateral_kernel": (ab["bilateral_stage"] / BIL[3], stage_ms["bilateral"] / BIL[3], BIL[3]),
-    }
+    ab = algorithmic_bytes(F, T, wl)
+    per_kernel = {"triangulate_kernel": (ab["triangulate_per_launch"], stage_ms["triangulate"], 1)}
+    if wl.lap:
+        per_kernel["laplacian_kernel"] = (ab["laplacian_per_launch"],
+                                          stage_ms["laplacian"] / wl.lap[2], wl.lap[2])
+    if wl.bil:
+        per_kernel["bilateral_kernel"] = (ab["bilateral_stage"] / wl.bil[3],
+                                          stage_ms["bilateral"] / wl.bil[3], wl.bil[3])
     share = {k: v[1] * v[2] for k, v in per_kernel.items()}
     dom = max(share, key=share.get)
     bytes_pl, ms_pl, _ = per_kernel[dom]
@@ -341,27 +406,29 @@ def run_ours(args, rank, world, local_rank):
                for k, (b, ms, n) in per_kernel.items()}
     # the bilateral is FP32-bound ("near the FP32/MUFU ridge"): its FP32
     # lane-ops (34 directed pairs per quad at k=3, 15 lane-ops each) vs the FMA pipe
-    h = BIL[2] // 2
-    pairs_per_quad = 2 * (2 * (2 * h + 1) ** 2 - 1)
-    fp32_ops = F * (M - 1) * (N - 1) * pairs_per_quad * 15
-    fp32_peak, fp32_src = load_fp32_peak()
-    fp32_ach = fp32_ops / (stage_ms["bilateral"] / BIL[3] / 1e3)
-    compute = {"kernel": "bilateral_kernel", "pipe": "fp32 (FMA)",
-               "achieved": round(fp32_ach / 1e12, 2), "peak": round(fp32_peak / 1e12, 2),
-               "unit": "T lane-ops/s", "frac": round(fp32_ach / fp32_peak, 4),
-               "ops_per_launch": fp32_ops, "peak_source": fp32_src,
-               "note": f"{pairs_per_quad} directed pairs per quad x 15 FP32 lane-ops "
-                       "(6 differences, 6 squared-distance, 3 accumulate) + 1 MUFU ex2"}
+    compute = None
+    if wl.bil:
+        h = wl.bil[2] // 2
+        pairs_per_quad = 2 * (2 * (2 * h + 1) ** 2 - 1)
+        fp32_ops = F * (M - 1) * (N - 1) * pairs_per_quad * 15
+        fp32_peak, fp32_src = load_fp32_peak()
+        fp32_ach = fp32_ops / (stage_ms["bilateral"] / wl.bil[3] / 1e3)
+        compute = {"kernel": "bilateral_kernel", "pipe": "fp32 (FMA)",
+                   "achieved": round(fp32_ach / 1e12, 2), "peak": round(fp32_peak / 1e12, 2),
+                   "unit": "T lane-ops/s", "frac": round(fp32_ach / fp32_peak, 4),
+                   "ops_per_launch": fp32_ops, "peak_source": fp32_src,
+                   "note": f"{pairs_per_quad} directed pairs per quad x 15 FP32 lane-ops "
+                           "(6 differences, 6 squared-distance, 3 accumulate) + 1 MUFU ex2"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference(steps=3, warmup=0, budget_s=25.0)
+        cb = cpu_reference(steps=3, warmup=0, budget_s=25.0, wl=wl)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     launches = eng.kernel_launches * args.steps
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic", "config": config_dict(F),
+        "higher_is_better": True, "scaling": "strong" if wl.total else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(F, wl),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": traffic, "peak_source": peak_src,
@@ -387,7 +454,10 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--frames", type=int, default=16, help="frames per GPU per step")
+    ap.add_argument("--frames", type=int, default=None,
+                    help="frames per GPU per step (default: the workload's; C5: 512 / N)")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C4",
+                    help="BASELINE.json config (C4 = the metric's config, the default line)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-e2e-files", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -397,15 +467,18 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
+    wl = WORKLOADS[args.workload]
+    if args.frames is None:
+        args.frames = wl.frames
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, rank, world, wl)
     if world > 1:
         import torch.distributed as dist
         import torch
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        return run_ours(args, rank, world, local_rank)
+        return run_ours(args, rank, world, local_rank, wl)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
 #include <string>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -34,6 +35,21 @@ int check_launch(const char* what);
 inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 inline int points_pitch(int N) { return round_up(3 * N, 4); }      // floats per grid row
 inline int fc_pitch(int N) { return round_up(6 * (N - 1), 4); }    // floats per FC quad row
+
+// The l_max test without square roots, bit-exact: IEEE sqrt is correctly rounded, hence
+// monotone, so {s : fl(sqrt(s)) <= l} is an interval (-inf, t] and
+//   fl(sqrt(s)) > l  <=>  s > t   for every s >= 0 (NaN s: false on both sides).
+// t is found next to fl(l*l) by stepping one ulp at a time (at most a few steps).
+inline double sq_threshold(double l) {
+  if (std::isnan(l)) return l;                 // every comparison false
+  if (l < 0.0) return -1.0;                    // every s >= 0 passes
+  if (std::isinf(l)) return l;                 // nothing passes
+  double t = l * l;
+  while (std::sqrt(t) > l) t = std::nextafter(t, -INFINITY);
+  for (double n = std::nextafter(t, INFINITY); std::sqrt(n) <= l; n = std::nextafter(t, INFINITY))
+    t = n;
+  return t;
+}
 
 // TMA descriptor for a 3-D fp32/fp64 tensor [F][rows][cols] with a row pitch
 // (elements) and a frame stride (elements).  Out-of-bounds reads fill with NaN,
@@ -218,10 +234,19 @@ __device__ __forceinline__ double centroid_f64(double a, double b, double c) {
   return __ddiv_rn(dadd(dadd(a, b), c), 3.0);
 }
 
-__device__ __forceinline__ double edge_len_f64(double px, double py, double pz, double qx,
-                                               double qy, double qz) {
+// squared edge length (dx^2 + dy^2) + dz^2 in numpy's order (the operand of
+// np.linalg.norm's sqrt); compared against sq_threshold(l_max) instead of taking the root
+__device__ __forceinline__ double edge_len2_f64(double px, double py, double pz, double qx,
+                                                double qy, double qz) {
   const double dx = dsub(qx, px), dy = dsub(qy, py), dz = dsub(qz, pz);
-  return __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
+  return dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
+}
+
+// np.maximum(|ab|, np.maximum(|bc|, |ca|)) > l_max (segmentation.py:59-67,73) from the
+// squared lengths and thr = sq_threshold(l_max); a NaN edge makes the maximum NaN -> false
+__device__ __forceinline__ bool longest_edge_exceeds(double sab, double sbc, double sca,
+                                                     double thr) {
+  return !(isnan(sab) || isnan(sbc) || isnan(sca)) && fmax(sab, fmax(sbc, sca)) > thr;
 }
 
 __device__ __forceinline__ bool finite3f(float x, float y, float z) {

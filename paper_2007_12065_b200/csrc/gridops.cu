@@ -90,18 +90,16 @@ __global__ void tri_normals_kernel(const S* __restrict__ pts, const int64_t* __r
 
 template <typename S>
 __global__ void max_edge_kernel(const S* __restrict__ pts, const int64_t* __restrict__ tris,
-                                long long T, double l_max, uint8_t* __restrict__ flag) {
+                                long long T, double l2_thr, uint8_t* __restrict__ flag) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   const S* a = pts + tris[3 * t] * 3;
   const S* b = pts + tris[3 * t + 1] * 3;
   const S* c = pts + tris[3 * t + 2] * 3;
-  const double lab = edge_len_f64(ld(a), ld(a + 1), ld(a + 2), ld(b), ld(b + 1), ld(b + 2));
-  const double lbc = edge_len_f64(ld(b), ld(b + 1), ld(b + 2), ld(c), ld(c + 1), ld(c + 2));
-  const double lca = edge_len_f64(ld(c), ld(c + 1), ld(c + 2), ld(a), ld(a + 1), ld(a + 2));
-  const double m = (isnan(lbc) || isnan(lca)) ? lbc + lca : fmax(lbc, lca);
-  const double e = (isnan(lab) || isnan(m)) ? lab + m : fmax(lab, m);
-  flag[t] = (uint8_t)(e > l_max);
+  flag[t] = (uint8_t)longest_edge_exceeds(
+      edge_len2_f64(ld(a), ld(a + 1), ld(a + 2), ld(b), ld(b + 1), ld(b + 2)),
+      edge_len2_f64(ld(b), ld(b + 1), ld(b + 2), ld(c), ld(c + 1), ld(c + 2)),
+      edge_len2_f64(ld(c), ld(c + 1), ld(c + 2), ld(a), ld(a + 1), ld(a + 2)), l2_thr);
 }
 
 
@@ -228,12 +226,13 @@ int group_assignment(const void* normals, bool f64, long long T, int F, const in
 int max_edge_mask(const void* pts, bool f64, const int64_t* tris, long long T, double l_max,
                   uint8_t* flag, cudaStream_t st) {
   if (T <= 0) return OK;
+  const double thr = sq_threshold(l_max);
   if (f64)
     max_edge_kernel<double><<<blocks_for(T, 256), 256, 0, st>>>(static_cast<const double*>(pts),
-                                                                tris, T, l_max, flag);
+                                                                tris, T, thr, flag);
   else
     max_edge_kernel<float><<<blocks_for(T, 256), 256, 0, st>>>(static_cast<const float*>(pts),
-                                                               tris, T, l_max, flag);
+                                                               tris, T, thr, flag);
   return check_launch("max_edge_kernel");
 }
 

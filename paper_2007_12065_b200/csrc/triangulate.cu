@@ -58,7 +58,7 @@ struct TriArgs {
   long long pts_fs;
   float* normals;
   uint8_t* lflag;
-  double l_max;
+  double l2_thr;  // sq_threshold(l_max)
 };
 
 // validity bits of point row r around the 32-point group starting at v0 = 32*word
@@ -91,13 +91,18 @@ __device__ __forceinline__ QuadBits quad_bits(const PtBits& t, const PtBits& b) 
   return q;
 }
 
-__device__ __forceinline__ void emit_extras(const TriArgs& a, int f, long long t, int64_t ia,
+// normals / l_max flag of triangle t (vertex ids ia, ib, ic in point rows u and u + 1)
+__device__ __forceinline__ void emit_extras(const TriArgs& a, int f, int u, long long t, int64_t ia,
                                             int64_t ib, int64_t ic) {
-  const int N = a.N;
-  const float* P = a.pts + f * a.pts_fs;
-  const float* pa = P + (ia / N) * a.pitch + (ia % N) * 3;
-  const float* pb = P + (ib / N) * a.pitch + (ib % N) * 3;
-  const float* pc = P + (ic / N) * a.pitch + (ic % N) * 3;
+  const long long r0 = (long long)u * a.N;
+  const float* P = a.pts + f * a.pts_fs + (long long)u * a.pitch;
+  auto at = [&](int64_t id) {  // no division: the row is u or u + 1
+    const bool lo = id >= r0 + a.N;
+    return P + (lo ? a.pitch : 0) + (id - r0 - (lo ? a.N : 0)) * 3;
+  };
+  const float* pa = at(ia);
+  const float* pb = at(ib);
+  const float* pc = at(ic);
   const double ax = pa[0], ay = pa[1], az = pa[2];
   const double bx = pb[0], by = pb[1], bz = pb[2];
   const double cx = pc[0], cy = pc[1], cz = pc[2];
@@ -110,18 +115,17 @@ __device__ __forceinline__ void emit_extras(const TriArgs& a, int f, long long t
     o[2] = (float)nz;
   }
   if (a.lflag != nullptr) {
-    const double lab = edge_len_f64(ax, ay, az, bx, by, bz);
-    const double lbc = edge_len_f64(bx, by, bz, cx, cy, cz);
-    const double lca = edge_len_f64(cx, cy, cz, ax, ay, az);
-    // np.maximum(lab, np.maximum(lbc, lca)) > l_max ; NaN propagates -> False
-    const double m = (isnan(lbc) || isnan(lca)) ? lbc + lca : fmax(lbc, lca);
-    const double e = (isnan(lab) || isnan(m)) ? lab + m : fmax(lab, m);
-    a.lflag[f * a.G + t] = (uint8_t)(e > a.l_max);
+    a.lflag[f * a.G + t] = (uint8_t)longest_edge_exceeds(
+        edge_len2_f64(ax, ay, az, bx, by, bz), edge_len2_f64(bx, by, bz, cx, cy, cz),
+        edge_len2_f64(cx, cy, cz, ax, ay, az), a.l2_thr);
   }
 }
 
+#ifndef OPCFE_TRI_XBLOCKS
+#define OPCFE_TRI_XBLOCKS 4  // 64 registers (measured: 2 -> 1.55, 3 -> 1.29, 4 -> 1.19 ms, C3)
+#endif
 template <bool EXTRAS>
-__global__ void __launch_bounds__(kTriNT, EXTRAS ? 2 : 4) triangulate_kernel(TriArgs a) {
+__global__ void __launch_bounds__(kTriNT, EXTRAS ? OPCFE_TRI_XBLOCKS : 4) triangulate_kernel(TriArgs a) {
   __shared__ unsigned long long red[kTriWarps];
   __shared__ unsigned long long gpre[kSegGroups];     // packed per-group exclusive prefixes
   __shared__ int64_t stage[kTriWarps][2][3 * 64];     // per-warp tris / twins staging
@@ -218,7 +222,6 @@ __global__ void __launch_bounds__(kTriNT, EXTRAS ? 2 : 4) triangulate_kernel(Tri
                                    ? 3 * (base_prev + pre_p + ((qp.f >> lane) & 1u)) + 1 : -1;
             st_h[3 * l0 + 2] = bs ? 3 * t1 + 2 : -1;
           }
-          if (EXTRAS) emit_extras(a, f, t0, i3, i2, i1);
         }
         if (bs) {
           st_t[3 * l1] = i1;
@@ -230,7 +233,6 @@ __global__ void __launch_bounds__(kTriNT, EXTRAS ? 2 : 4) triangulate_kernel(Tri
             st_h[3 * l1 + 1] = ((qn.f >> lane) & 1u) ? 3 * (base_next + pre_n) + 1 : -1;
             st_h[3 * l1 + 2] = bf ? 3 * t0 + 2 : -1;
           }
-          if (EXTRAS) emit_extras(a, f, t1, i1, i4, i3);
         }
       }
       __syncwarp();
@@ -238,6 +240,10 @@ __global__ void __launch_bounds__(kTriNT, EXTRAS ? 2 : 4) triangulate_kernel(Tri
       const int n3 = 3 * (__popc(qc.f) + __popc(qc.s));
       int64_t* tdst = tris + 3 * t_first;
       for (int i = lane; i < n3; i += 32) tdst[i] = st_t[i];
+      if (EXTRAS) {  // dense over the group's staged triangles (no divergent per-quad calls)
+        for (int i = lane; 3 * i < n3; i += 32)
+          emit_extras(a, f, u, t_first + i, st_t[3 * i], st_t[3 * i + 1], st_t[3 * i + 2]);
+      }
       if (he) {
         int64_t* hdst = he + 3 * t_first;
         for (int i = lane; i < n3; i += 32) hdst[i] = st_h[i];
@@ -364,7 +370,7 @@ int triangulate(const uint32_t* vmask, int F, int M, int N, int64_t* trimap, int
   a.pts_fs = (long long)M * pitch;
   a.normals = normals;
   a.lflag = lflag;
-  a.l_max = l_max;
+  a.l2_thr = sq_threshold(l_max);
   tri_count_kernel<<<dim3((M - 1 + 7) / 8, F), 256, 0, st>>>(vmask, a.vm_fs, a.wpr, M, N, row_base);
   if (int rc = check_launch("tri_count_kernel")) return rc;
   tri_scan_kernel<<<F, 1024, 0, st>>>(row_base, M, ntri);

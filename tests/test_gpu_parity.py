@@ -465,6 +465,46 @@ def test_lmax_mask_golden(fe):
     assert np.all(fe.max_edge_mask(mesh, 0.5)) and not np.any(fe.max_edge_mask(mesh, 2.0))
 
 
+def _np_lmax(pts, tris, l_max):
+    """segmentation.py:59-67,73: np.maximum of the three np.linalg.norm edge lengths > l_max"""
+    a, b, c = pts[tris[:, 0]], pts[tris[:, 1]], pts[tris[:, 2]]
+    e = np.maximum(np.linalg.norm(b - a, axis=1),
+                   np.maximum(np.linalg.norm(c - b, axis=1), np.linalg.norm(a - c, axis=1)))
+    with np.errstate(invalid="ignore"):
+        return e > l_max
+
+
+def test_lmax_threshold_at_exact_edge_lengths(fe):
+    """The kernels compare squared lengths against sq_threshold(l_max) (no sqrt): l_max
+    set to an exact edge length, one ulp either side, 0, negative, inf, NaN vertices."""
+    rng = np.random.default_rng(77)
+    pts = rng.normal(scale=0.3, size=(400, 3))
+    pts[5] = np.nan
+    tris = rng.integers(0, 400, size=(2000, 3))
+    tris[:40, 1] = tris[:40, 0]                       # zero-length edges
+    mesh = fe.HalfEdgeMesh(points=pts, triangles=tris, halfedges=None)
+    lens = np.linalg.norm(pts[tris[:, 1]] - pts[tris[:, 0]], axis=1)
+    cands = [0.0, -1.0, np.inf, 1e-300, 1e300]
+    for L in lens[np.isfinite(lens)][:60]:
+        cands += [L, np.nextafter(L, 0), np.nextafter(L, np.inf)]
+    for l_max in cands:
+        assert np.array_equal(fe.max_edge_mask(mesh, l_max), _np_lmax(pts, tris, l_max)), l_max
+    # the fused fp32 front end: l_max = exact edge lengths of the fp32 grid
+    opc = grid_opc(24, 31) * 0.05 + rng.normal(scale=0.02, size=(24, 31, 3))
+    opc[rng.random((24, 31)) < 0.1] = np.nan
+    opc = opc.astype(np.float32)
+    for k in range(4):
+        sm = opc.astype(np.float64)
+        tris_r, _, _ = c_oracle.triangulate(sm)
+        p = sm.reshape(-1, 3)
+        L = float(np.linalg.norm(p[tris_r[7 * k, 1]] - p[tris_r[7 * k, 0]]))
+        for l_max in (L, np.nextafter(L, 0), np.nextafter(L, np.inf)):
+            _, res = _engine_run(fe, opc, None, None, l_max=l_max)
+            T = res.n_tri[0]
+            assert np.array_equal(res.lmax_mask[0, :T].cpu().numpy().astype(bool),
+                                  _np_lmax(p, tris_r, l_max)), (k, l_max)
+
+
 def test_compute_normals_any_mesh(fe):
     rng = np.random.default_rng(12345)
     pts = rng.normal(size=(30, 3))
