@@ -783,3 +783,66 @@ def test_profiled_eager_and_graph_agree(fe, lap_it, src):
             assert teq(o[1][f, :T], outs[0][1][f, :T])
             assert teq(o[2][f, :3 * T], outs[0][2][f, :3 * T])
             assert teq(o[3][f, :T], outs[0][3][f, :T])
+
+
+def test_large_frame_topology_closed_form(fe):
+    """A 4000 x 6000 frame (24 M points, 48 M GIDs) through the fused front end, checked on
+    the device against the closed forms of SURVEY.md Appendix A (size-independent
+    properties of the reference's algorithm, mesh.py:58-135): validity from the smoothed
+    grid's NaN mask, trimap = cumsum - 1, triangles (p3,p2,p1) / (p1,p4,p3) in GID
+    order, twins 3*trimap[nbr] + k, every twin an involution, unit normals, and the l_max
+    flag against fp64 edge lengths."""
+    M, N = 4000, 6000
+    g = torch.Generator(device="cuda").manual_seed(5)
+    u = torch.arange(M, device="cuda", dtype=torch.float32)[:, None].expand(M, N)
+    v = torch.arange(N, device="cuda", dtype=torch.float32)[None, :].expand(M, N)
+    opc = torch.stack([v * 2e-3, -u * 2e-3, 0.3 * torch.sin(u * 1e-3) * torch.cos(v * 7e-4)], -1)
+    opc = opc + 5e-4 * torch.randn((M, N, 3), generator=g, device="cuda")
+    opc[torch.rand((M, N), generator=g, device="cuda") < 0.02] = float("nan")
+    eng = fe.FrontEnd(M, N, 1, laplacian=fe.LaplacianParams(1.0, 3, 2),
+                      bilateral=fe.BilateralParams(0.1, 0.15, 3, 2), l_max=4e-3)
+    res = eng.run(opc[None])
+    torch.cuda.synchronize()
+    pts = res.points[0]
+    ok = torch.isfinite(pts).all(-1)
+    assert torch.equal(ok, torch.isfinite(opc).all(-1))           # NaN mask invariance
+    p1, p2, p3, p4 = ok[:-1, :-1], ok[:-1, 1:], ok[1:, 1:], ok[1:, :-1]
+    valid = torch.stack([p1 & p2 & p3, p1 & p3 & p4], -1).reshape(-1)
+    T = int(valid.sum())
+    assert res.n_tri[0] == T
+    trimap = torch.where(valid, torch.cumsum(valid, 0) - 1, torch.full_like(valid, -1, dtype=torch.int64))
+    assert torch.equal(res.trimap[0], trimap)
+    gid = torch.nonzero(valid).squeeze(1)
+    q, k = gid // 2, gid % 2
+    qu, qv = q // (N - 1), q % (N - 1)
+    i1 = qu * N + qv
+    i2, i4 = i1 + 1, i1 + N
+    i3 = i4 + 1
+    tris = torch.where((k == 0)[:, None], torch.stack([i3, i2, i1], 1), torch.stack([i1, i4, i3], 1))
+    assert torch.equal(res.triangles[0, :T], tris)
+    # twins: k = 0 -> [(u,v+1,1), (u-1,v,1), (u,v,0+1)]; k = 1 -> [(u,v-1,0), (u+1,v,0), (u,v,0)]
+    tm = trimap.view(M - 1, N - 1, 2)
+    def nbr(du, dv, kk):
+        uu, vv = qu + du, qv + dv
+        inside = (uu >= 0) & (uu < M - 1) & (vv >= 0) & (vv < N - 1)
+        t = tm[uu.clamp(0, M - 2), vv.clamp(0, N - 2), kk]
+        return torch.where(inside & (t >= 0), t, torch.full_like(t, -1))
+    first = k == 0
+    e0 = torch.where(first, nbr(0, 1, 1), nbr(0, -1, 0))
+    e1 = torch.where(first, nbr(-1, 0, 1), nbr(1, 0, 0))
+    e2 = torch.where(first, nbr(0, 0, 1), nbr(0, 0, 0))
+    he = torch.stack([torch.where(e >= 0, 3 * e + j, e) for j, e in enumerate((e0, e1, e2))], 1)
+    got = res.halfedges[0, :3 * T]
+    assert torch.equal(got, he.reshape(-1))
+    linked = got >= 0
+    assert torch.equal(got[got[linked]], torch.nonzero(linked).squeeze(1))
+    n = res.normals[0, :T]
+    assert torch.isfinite(n).all() and (n.norm(dim=1) - 1).abs().max() < 1e-6
+    P = pts.reshape(-1, 3).double()
+    a, b, c = P[tris[:, 0]], P[tris[:, 1]], P[tris[:, 2]]
+    def norm(d):  # np.linalg.norm's order: sqrt((dx^2 + dy^2) + dz^2)
+        return ((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2]).sqrt()
+    e = torch.maximum(norm(b - a), torch.maximum(norm(c - b), norm(a - c)))
+    flag = res.lmax_mask[0, :T].bool()
+    assert 0 < int(flag.sum()) < T
+    assert torch.equal(flag, e > 4e-3)
