@@ -169,40 +169,6 @@ __device__ __forceinline__ void fc_normals_quad(const float* P1, const float* P2
                  e1s[1] * d13[0] - e1s[0] * d13[1], n + 3);
 }
 
-// ---- packed fp32x2 (one b64 register pair = lanes (lo, hi)); .rn, denormals kept
-typedef unsigned long long f2_t;
-__device__ __forceinline__ f2_t f2(float lo, float hi) {
-  f2_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ float f2lo(f2_t r) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
-  return lo;
-}
-__device__ __forceinline__ float f2hi(f2_t r) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r));
-  return hi;
-}
-__device__ __forceinline__ f2_t add2(f2_t a, f2_t b) {
-  f2_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
-  f2_t r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
-  f2_t r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-// broadcast scalar operand (ptxas encodes it as a .F32 operand of FADD2 / FFMA2)
-__device__ __forceinline__ f2_t bc2(float x) { return f2(x, x); }
 
 // the 4 pack planes (in shared memory, or the global packed FC arrays of the fused
 // pipeline): one quad = (triangle 0, triangle 1) lane pairs, 48 B

@@ -163,6 +163,25 @@ constexpr int kL3InF = (kL3BW * 3 * kL3BH + 31) / 32 * 32;
 constexpr int kL3OutF = kL3TW * 3 * kL3TH;
 constexpr int kL3Smem = (kL3InF + kL3OutF) * 4 + kSmemSlack;
 
+// Invalid points between passes 1 and L of the packed pipeline (all three components):
+// |sentinel - p|^2 overflows to +inf for any in-contract vertex p, so MUFU.RSQ gives an
+// exact 0 weight and d * w = 0 -- no per-pair validity test, no NaN in packed lanes.
+// A vertex whose three components carry the same non-finite bits b (the usual all-NaN
+// dropout, any payload, or inf) is encoded losslessly: exponent field 2^100, mantissa and
+// sign of b; the last pass rebuilds b with no memory access.  Any other non-finite vertex
+// (partial NaN, mixed payloads) becomes 2^101 and the last pass reloads it from the
+// pass-1 input.  Either way it comes back exactly as given.
+constexpr uint32_t kLapSentExp = 0x71800000u;     // 2^100
+constexpr float kLapSentRestore = 2.5353012e30f;  // 2^101
+constexpr float kLapValidMax = 1e29f;             // |x| below: a real vertex
+
+__device__ __forceinline__ float lap_encode_invalid(const float* p) {
+  const uint32_t b = __float_as_uint(p[0]);
+  if (__float_as_uint(p[1]) == b && __float_as_uint(p[2]) == b && (b & 0x7f800000u) == 0x7f800000u)
+    return __uint_as_float(kLapSentExp | (b & 0x807fffffu));
+  return kLapSentRestore;
+}
+
 struct Acc4 {
   float x, y, z, w;
 };
@@ -188,7 +207,10 @@ __device__ __forceinline__ void lap_pair(const float* p, const float* q, Acc4& a
   }
 }
 
-template <bool VMASK>  // first pass: also emit the validity mask
+// VMASK: first pass, also emit the validity mask.  ENC: more passes follow on the packed
+// kernel -- write invalid points (any non-finite component) as the sentinel (see
+// laplacian3p_kernel); the last packed pass restores them from the input.
+template <bool VMASK, bool ENC>
 __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
     laplacian3_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
                       uint32_t* __restrict__ vmask, long long vm_fs, int wpr, int M, int N,
@@ -270,6 +292,7 @@ __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
       oy = p[1] + s * acc.y;
       oz = p[2] + s * acc.z;
     }
+    if (ENC && !fin) ox = oy = oz = lap_encode_invalid(p);
     float* po = out_s + (r * kL3TW + c) * 3;
     po[0] = ox;
     po[1] = oy;
@@ -292,6 +315,207 @@ __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
   }
 }
 
+// ---------------------------------------------------------------------------------
+// kernel_size 3, passes 2..L: packed FP32x2 on a sentinel-encoded grid.  The two lanes of
+// every packed register are two output rows of the thread's column (the top and bottom
+// halves of its strip), so each neighbour pair is weighed for both rows by one FADD2 /
+// FFMA2 stream (3 sub, 3 for |d|^2, 2 MUFU rsqrt, 3 accumulate, 1 weight sum: 12 issue
+// slots for two points, against 12 per point in the scalar pass).  Invalid points carry the sentinel
+// (pass 1 writes it), whose weight is exactly 0 with no test; a coincident neighbour
+// (|d| = 0 -> w = inf) makes the weight sum non-finite and that point is recomputed by
+// the exact scalar rule (lap_pair: skip |d|^2 < FLT_MIN).  Neighbour order per lane is
+// the reference's (du outer, dv inner).  The last pass (LAST) writes invalid points back
+// exactly as given (see lap_encode_invalid).
+// Off-grid halo cells (TMA NaN fill) are only read by ring points, which never move.
+#ifndef OPCFE_LAPP_BLOCKS
+#define OPCFE_LAPP_BLOCKS 14
+#endif
+template <bool LAST>
+__global__ void __launch_bounds__(kL3NT, OPCFE_LAPP_BLOCKS)
+    laplacian3p_kernel(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+                       const float* __restrict__ orig, long long orig_fs, int pitch, int M, int N,
+                       float lam) {
+  static_assert(kL3RS % 2 == 0, "rows are processed in pairs");
+  extern __shared__ __align__(16) char smem_raw[];
+  uint64_t* barp;
+  float* smem = reinterpret_cast<float*>(smem_aligned_base(smem_raw, &barp));
+  float* in_s = smem;
+  float* out_s = smem + kL3InF;
+  uint64_t& bar = *barp;
+
+  const int v0 = blockIdx.x * kL3TW;
+  const int u0 = blockIdx.y * kL3TH;
+  const int f = blockIdx.z;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, kL3BW * 3 * kL3BH * 4);
+    tma_load_3d(in_s, &tin, &bar, (v0 - kL3L) * 3, u0 - 1, f);
+  }
+  mbar_wait(&bar, 0);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = lane, v = v0 + c;
+  const int r0 = warp * kL3RS;
+  uint32_t movable = 0;
+  if (v > 0 && v < N - 1) {
+#pragma unroll
+    for (int i = 0; i < kL3RS; ++i) {
+      const int u = u0 + r0 + i;
+      movable |= (u > 0 && u < M - 1) ? (1u << i) : 0u;
+    }
+  }
+  // 3 points of box row br around the thread's column
+  auto ld3 = [&](int br, float (*dst)[3]) {
+    const float* q = in_s + (br * kL3BW + c + kL3L - 1) * 3;
+#pragma unroll
+    for (int j = 0; j < 9; ++j) dst[j / 3][j % 3] = q[j];
+  };
+  // exact scalar rule for one point (box row br): the rare coincident-neighbour case
+  auto slow = [&](int br, float* o) {
+    const float* p = in_s + (br * kL3BW + c + kL3L) * 3;
+    Acc4 acc{0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int du = -1; du <= 1; ++du)
+#pragma unroll 1
+      for (int dv = -1; dv <= 1; ++dv)
+        if (du != 0 || dv != 0) lap_pair(p, p + (du * kL3BW + dv) * 3, acc, nullptr);
+    o[0] = p[0];
+    o[1] = p[1];
+    o[2] = p[2];
+    if (acc.w > 0.f) {
+      const float s = lam * rcp_approx(acc.w);
+      o[0] = p[0] + s * acc.x;
+      o[1] = p[1] + s * acc.y;
+      o[2] = p[2] + s * acc.z;
+    }
+  };
+  // Packed rows Q(q) = (tile row r0+q, tile row r0+q+HS): lane lo walks the top half of the
+  // strip, lane hi the bottom half, so the up / centre / down rows of both lanes are the
+  // packed registers Q(q-1), Q(q), Q(q+1) -- every row is loaded into exactly one lane
+  // (no duplication), and the down pair of step q is the up pair of step q+1 in both lanes
+  // (weighed once, carried negated).  [column][xyz]
+  constexpr int HS = kL3RS / 2;
+  auto ldq = [&](int q, f2_t (&dst)[3][3]) {
+    const float* a = in_s + ((r0 + q + 1) * kL3BW + c + kL3L - 1) * 3;
+    const float* b = a + HS * kL3BW * 3;
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) dst[j][k] = f2(a[3 * j + k], b[3 * j + k]);
+  };
+  f2_t Qm[3][3], Q0[3][3], Qp[3][3];
+  ldq(-1, Qm);
+  ldq(0, Q0);
+  f2_t cdx = 0ull, cdy = 0ull, cdz = 0ull, cw = 0ull;  // down pair of the previous step: d*w, w
+#pragma unroll
+  for (int q = 0; q < HS; ++q) {
+    ldq(q + 1, Qp);
+    const f2_t px = Q0[1][0], py = Q0[1][1], pz = Q0[1][2];
+    f2_t ax = 0ull, ay = 0ull, az = 0ull, aw = 0ull;
+    auto nb = [&](const f2_t* n) {
+      const f2_t dx = sub2(n[0], px), dy = sub2(n[1], py), dz = sub2(n[2], pz);
+      f2_t d2 = mul2(dx, dx);
+      d2 = fma2(dy, dy, d2);
+      d2 = fma2(dz, dz, d2);
+      const f2_t w = f2(rsqrt_approx(f2lo(d2)), rsqrt_approx(f2hi(d2)));
+      ax = fma2(dx, w, ax);
+      ay = fma2(dy, w, ay);
+      az = fma2(dz, w, az);
+      aw = add2(aw, w);
+    };
+    // the reference's order: du = -1 (dv = -1, 0, 1), du = 0 (dv = -1, 1), du = 1 (...)
+    nb(Qm[0]);
+    if (q == 0) {
+      nb(Qm[1]);
+    } else {  // up pair = the previous step's down pair, negated
+      ax = sub2(ax, cdx);
+      ay = sub2(ay, cdy);
+      az = sub2(az, cdz);
+      aw = add2(aw, cw);
+    }
+    nb(Qm[2]);
+    nb(Q0[0]);
+    nb(Q0[2]);
+    nb(Qp[0]);
+    {
+      const f2_t dx = sub2(Qp[1][0], px), dy = sub2(Qp[1][1], py), dz = sub2(Qp[1][2], pz);
+      f2_t d2 = mul2(dx, dx);
+      d2 = fma2(dy, dy, d2);
+      d2 = fma2(dz, dz, d2);
+      cw = f2(rsqrt_approx(f2lo(d2)), rsqrt_approx(f2hi(d2)));
+      cdx = mul2(dx, cw);
+      cdy = mul2(dy, cw);
+      cdz = mul2(dz, cw);
+      ax = add2(ax, cdx);
+      ay = add2(ay, cdy);
+      az = add2(az, cdz);
+      aw = add2(aw, cw);
+    }
+    nb(Qp[2]);
+    const f2_t sc = f2(lam * rcp_approx(f2lo(aw)), lam * rcp_approx(f2hi(aw)));
+    const f2_t ox2 = fma2(sc, ax, px), oy2 = fma2(sc, ay, py), oz2 = fma2(sc, az, pz);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int r = r0 + q + k * HS;  // tile row of this lane
+      const float p0 = k ? f2hi(px) : f2lo(px), p1 = k ? f2hi(py) : f2lo(py),
+                  p2 = k ? f2hi(pz) : f2lo(pz);
+      const float ws = k ? f2hi(aw) : f2lo(aw);
+      float o[3] = {p0, p1, p2};
+      const bool valid = fabsf(p0) < kLapValidMax;  // in-contract coordinates are < 1e19
+      if (valid && ((movable >> (q + k * HS)) & 1u)) {
+        if (ws <= 3.402823466e38f) {  // finite (no coincident neighbour)
+          if (ws > 0.f) {
+            o[0] = k ? f2hi(ox2) : f2lo(ox2);
+            o[1] = k ? f2hi(oy2) : f2lo(oy2);
+            o[2] = k ? f2hi(oz2) : f2lo(oz2);
+          }
+        } else {
+          slow(r + 1, o);
+        }
+      }
+      if (LAST && !valid) {  // back to the caller's values (lap_encode_invalid)
+        const uint32_t e = __float_as_uint(p0);
+        if ((e & 0x7f800000u) == kLapSentExp) {
+          o[0] = o[1] = o[2] = __uint_as_float((e & 0x807fffffu) | 0x7f800000u);
+        } else {
+          const int u = u0 + r;
+          if (u < M && v < N) {
+            const float* gp = orig + f * orig_fs + (long long)u * pitch + v * 3;
+            o[0] = gp[0];
+            o[1] = gp[1];
+            o[2] = gp[2];
+          }
+        }
+      }
+      float* po = out_s + (r * kL3TW + c) * 3;
+      po[0] = o[0];
+      po[1] = o[1];
+      po[2] = o[2];
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        Qm[j][k] = Q0[j][k];
+        Q0[j][k] = Qp[j][k];
+      }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma_store_3d(&tout, out_s, v0 * 3, u0, f);
+    tma_store_commit_and_wait();
+  }
+}
+
+#ifndef OPCFE_LAP_PACKED
+#define OPCFE_LAP_PACKED 1
+#endif
+
 int run_k3(const float* in, float* out, float* tmp, uint32_t* vmask, int F, int M, int N, int pitch,
            float lam, int iters, cudaStream_t st) {
   const uint64_t fs = (uint64_t)M * pitch;
@@ -304,21 +528,36 @@ int run_k3(const float* in, float* out, float* tmp, uint32_t* vmask, int F, int 
     if ((rc = make_tmap_3d(&ld_tmp, tmp, false, 3ull * N, M, F, pitch, fs, kL3BW * 3, kL3BH))) return rc;
     if ((rc = make_tmap_3d(&st_tmp, tmp, false, 3ull * N, M, F, pitch, fs, kL3TW * 3, kL3TH))) return rc;
   }
-  static unsigned long long attr_mask = 0;
-  static unsigned long long attr_mask_v = 0;
-  ensure_smem_attr(laplacian3_kernel<false>, kL3Smem, attr_mask);
-  ensure_smem_attr(laplacian3_kernel<true>, kL3Smem, attr_mask_v);
+  static unsigned long long attr_mask[6] = {0, 0, 0, 0, 0, 0};
+  ensure_smem_attr(laplacian3_kernel<false, false>, kL3Smem, attr_mask[0]);
+  ensure_smem_attr(laplacian3_kernel<true, false>, kL3Smem, attr_mask[1]);
+  ensure_smem_attr(laplacian3_kernel<false, true>, kL3Smem, attr_mask[2]);
+  ensure_smem_attr(laplacian3_kernel<true, true>, kL3Smem, attr_mask[3]);
+  ensure_smem_attr(laplacian3p_kernel<false>, kL3Smem, attr_mask[4]);
+  ensure_smem_attr(laplacian3p_kernel<true>, kL3Smem, attr_mask[5]);
   const int wpr = (N + 31) / 32;
   const long long vm_fs = (long long)M * wpr;
   dim3 grid((N + kL3TW - 1) / kL3TW, (M + kL3TH - 1) / kL3TH, F);
   bool to_out = (iters % 2) == 1;
   const CUtensorMap* src = &m_in;
+  // pass 1: scalar (reads the caller's NaN-marked grid, emits the mask); with more passes
+  // it writes the sentinel encoding and passes 2..L run packed (the last restores `in`)
+  const bool packed = OPCFE_LAP_PACKED && iters > 1;
   for (int it = 0; it < iters; ++it) {
     const CUtensorMap* dst = to_out ? &st_out : &st_tmp;
-    auto kern = (it == 0 && vmask != nullptr) ? laplacian3_kernel<true> : laplacian3_kernel<false>;
-    kern<<<grid, kL3NT, kL3Smem, st>>>(*src, *dst, it == 0 ? vmask : nullptr, vm_fs, wpr,
-                                                  M, N, lam);
-    if ((rc = check_launch("laplacian3_kernel"))) return rc;
+    if (it == 0 || !packed) {
+      auto kern = (it == 0 && vmask != nullptr)
+                      ? (packed ? laplacian3_kernel<true, true> : laplacian3_kernel<true, false>)
+                      : (packed && it == 0 ? laplacian3_kernel<false, true>
+                                           : laplacian3_kernel<false, false>);
+      kern<<<grid, kL3NT, kL3Smem, st>>>(*src, *dst, it == 0 ? vmask : nullptr, vm_fs, wpr, M,
+                                         N, lam);
+      if ((rc = check_launch("laplacian3_kernel"))) return rc;
+    } else {
+      auto kern = (it == iters - 1) ? laplacian3p_kernel<true> : laplacian3p_kernel<false>;
+      kern<<<grid, kL3NT, kL3Smem, st>>>(*src, *dst, in, (long long)fs, pitch, M, N, lam);
+      if ((rc = check_launch("laplacian3p_kernel"))) return rc;
+    }
     src = to_out ? &ld_out : &ld_tmp;
     to_out = !to_out;
   }

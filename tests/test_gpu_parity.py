@@ -846,3 +846,42 @@ def test_large_frame_topology_closed_form(fe):
     flag = res.lmax_mask[0, :T].bool()
     assert 0 < int(flag.sum()) < T
     assert torch.equal(flag, e > 4e-3)
+
+
+@pytest.mark.parametrize("iters", [1, 2, 3, 6])
+def test_laplacian_invalid_vertices_bit_identical(fe, iters):
+    """Passes 2..L run on a sentinel-encoded grid (laplacian.cu); every non-finite vertex
+    must still come back exactly as given (_fallback.py:111-115: a centre with a NaN
+    component is copied) -- canonical NaN, partial NaN, other NaN payloads, -NaN -- and
+    must not leak into its neighbours."""
+    rng = np.random.default_rng(iters)
+    M, N = 37, 52
+    opc = (grid_opc(M, N) * 0.01 + rng.normal(scale=0.002, size=(M, N, 3))).astype(np.float32)
+    bits = opc.view(np.uint32)
+    cells = rng.choice(M * N, size=70, replace=False)
+    kinds = []
+    for i, cell in enumerate(cells):
+        u, v = divmod(int(cell), N)
+        kind = i % 7
+        if kind == 0:
+            bits[u, v, :] = 0x7fc00000                      # canonical NaN
+        elif kind == 5:
+            bits[u, v, :] = 0x7fffffff                      # the GPU's arithmetic NaN
+        elif kind == 6:
+            bits[u, v, :] = [0x7fc00000, 0x7fc00001, 0x7fc00000]  # mixed payloads
+        elif kind == 1:
+            bits[u, v, 1] = 0x7fc00000                      # partial NaN
+        elif kind == 2:
+            bits[u, v, :] = 0x7fc00123                      # NaN payload
+        elif kind == 3:
+            bits[u, v, :] = 0xffc00000                      # -NaN
+        else:
+            bits[u, v, 2] = 0x7fa00000                      # partial signalling NaN
+        kinds.append((u, v))
+    lap = fe.LaplacianParams(1.0, 3, iters)
+    _, res = _engine_run(fe, opc, lap, None)
+    got = res.points[0].cpu().numpy()
+    for u, v in kinds:
+        assert np.array_equal(got[u, v].view(np.uint32), opc[u, v].view(np.uint32)), (u, v)
+    ref = c_oracle.laplacian_filter(opc.astype(np.float64), 1.0, 3, iters)
+    assert_vertices_close(got, ref)
