@@ -885,3 +885,20 @@ def test_laplacian_invalid_vertices_bit_identical(fe, iters):
         assert np.array_equal(got[u, v].view(np.uint32), opc[u, v].view(np.uint32)), (u, v)
     ref = c_oracle.laplacian_filter(opc.astype(np.float64), 1.0, 3, iters)
     assert_vertices_close(got, ref)
+
+
+@pytest.mark.parametrize("iters", [2, 5])
+def test_laplacian_coincident_neighbours(fe, iters):
+    """Duplicated vertices (|d| = 0: the reference skips the pair, _native.pyx:262-266).
+    The packed passes see w = inf there and recompute that point by the scalar rule."""
+    rng = np.random.default_rng(11 + iters)
+    M, N = 40, 70
+    opc = (grid_opc(M, N) * 0.01 + rng.normal(scale=0.002, size=(M, N, 3))).astype(np.float32)
+    for u, v in rng.integers(1, [M - 2, N - 2], size=(40, 2)):
+        opc[u, v + 1] = opc[u, v]                        # right neighbour coincident
+        opc[u + 1, v] = opc[u, v]                        # and the one below
+    opc[5:9, 10:14] = opc[5, 10]                         # a 4x4 block of one point
+    opc[rng.random((M, N)) < 0.03] = np.nan
+    _, res = _engine_run(fe, opc, fe.LaplacianParams(1.0, 3, iters), None)
+    ref = c_oracle.laplacian_filter(opc.astype(np.float64), 1.0, 3, iters)
+    assert_vertices_close(res.points[0].cpu().numpy(), ref)
