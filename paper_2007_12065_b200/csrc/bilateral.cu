@@ -66,7 +66,10 @@ constexpr int kBilNT = kBilTQW * kBilTQH / kQPT;  // threads per CTA
 // resident CTAs the register budget targets: k = 3 -> 7 (72 registers; its packed kernel
 // needs 17.7 KB of shared memory); larger windows have larger tiles (fewer CTAs by shared
 // memory anyway) and more registers live
-constexpr int bil_min_blocks(int h) { return h == 1 ? 7 : (h == 2 ? 5 : 4); }
+#ifndef OPCFE_BIL_BLOCKS3
+#define OPCFE_BIL_BLOCKS3 7
+#endif
+constexpr int bil_min_blocks(int h) { return h == 1 ? OPCFE_BIL_BLOCKS3 : (h == 2 ? 5 : 4); }
 
 enum BilMode : int {
   kFromPoints = 0,     // iteration 1: normals + centroids from the point grid
