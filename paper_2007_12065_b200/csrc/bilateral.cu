@@ -125,6 +125,9 @@ struct BilArgs {
   float* out_mesh;   // scatter destination: per frame [cap][3]
   long long out_fs;  // floats per frame
   long long n_out;   // rows per frame available in out_mesh (bounds check)
+  const float* pts;  // point grid (packed scatter: exact rebuild of unchanged normals)
+  int pitch;
+  long long pts_fs;
 };
 
 // FC normals of a quad's two triangles (p3, p2, p1) and (p1, p4, p3) for the bilateral
@@ -610,15 +613,30 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     if (u >= Mq || v >= Nq) continue;
     const Quad2& q = o == 0 ? qa : qb;
     if (SCATTER) {
-      const float inv = 1.0f / sB;
+      // unchanged triangles return this iteration's input normal, held here only as
+      // n' = fl(n * sqrt(B)).  A valid triangle no iteration has moved (isolated, or
+      // |acc| <= 1e-30 throughout -- the usual case) has n = its FC normal: rebuilt from
+      // the points with iteration 1's arithmetic and accepted when it reproduces n'
+      // exactly; otherwise n' / sqrt(B) (<= 1 ulp).  Rare path (global point loads).
+      if (!upd[o][0] || !upd[o][1]) {
+        const float* P1 = a.pts + f * a.pts_fs + (long long)u * a.pitch + 3 * v;
+        float raw[6];
+        fc_normals_quad(P1, P1 + 3, P1 + a.pitch + 3, P1 + a.pitch, raw);
+        const float inv = 1.0f / sB;
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        if (!upd[o][k]) {
-          const bool valid = (k == 0 ? f2lo(q.cx) : f2hi(q.cx)) != 1e18f;
-          const float qn = __int_as_float(0x7fc00000);
-          res[o][3 * k] = valid ? (k == 0 ? f2lo(q.nx) : f2hi(q.nx)) * inv : qn;
-          res[o][3 * k + 1] = valid ? (k == 0 ? f2lo(q.ny) : f2hi(q.ny)) * inv : qn;
-          res[o][3 * k + 2] = valid ? (k == 0 ? f2lo(q.nz) : f2hi(q.nz)) * inv : qn;
+        for (int k = 0; k < 2; ++k) {
+          if (!upd[o][k]) {
+            const bool valid = (k == 0 ? f2lo(q.cx) : f2hi(q.cx)) != 1e18f;
+            const float n0 = k == 0 ? f2lo(q.nx) : f2hi(q.nx);
+            const float n1 = k == 0 ? f2lo(q.ny) : f2hi(q.ny);
+            const float n2 = k == 0 ? f2lo(q.nz) : f2hi(q.nz);
+            const float* rk = raw + 3 * k;
+            const bool same = rk[0] * sB == n0 && rk[1] * sB == n1 && rk[2] * sB == n2;
+            const float qn = __int_as_float(0x7fc00000);
+            res[o][3 * k] = valid ? (same ? rk[0] : n0 * inv) : qn;
+            res[o][3 * k + 1] = valid ? (same ? rk[1] : n1 * inv) : qn;
+            res[o][3 * k + 2] = valid ? (same ? rk[2] : n2 * inv) : qn;
+          }
         }
       }
       scatter_mesh(a, f, u, v, res[o]);
@@ -787,6 +805,9 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   a.out_mesh = out_mesh;
   a.out_fs = 3ll * out_rows;
   a.n_out = out_rows;
+  a.pts = pts;
+  a.pitch = pitch;
+  a.pts_fs = (long long)M * pitch;
 
   // Fused pipeline with >= 2 iterations and a third buffer: iteration 1 writes the packed
   // planes (centroids once into C, normals into A); iterations 2..B read them by TMA with
