@@ -929,3 +929,38 @@ def test_front_end_randomised(fe, seed):
     l_max = float(rng.uniform(0.001, 0.05)) if rng.random() < 0.5 else None
     _, res = _engine_run(fe, opc, lap, bil, l_max)
     _per_stage_check(fe, opc, lap, bil, l_max, res)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_drop_in_api_randomised(fe, seed):
+    """The reference-facing functions on random float64 grids (odd shapes, NaN, duplicated
+    vertices) against the NumPy restatement of the reference (oracle/flatpoly_oracle.py):
+    topology and fp64 normals / FC data bit-exact, Laplacian and bilateral within 1e-5."""
+    rng = np.random.default_rng(500 + seed)
+    M, N = int(rng.integers(5, 90)), int(rng.integers(5, 90))
+    opc = grid_opc(M, N) * rng.uniform(0.003, 0.03)
+    opc[..., 2] = rng.normal(0, 0.005, (M, N))
+    opc += rng.normal(scale=rng.uniform(0, 0.003), size=opc.shape)
+    opc[rng.integers(0, M), :] = opc[rng.integers(0, M), :]       # a duplicated row
+    opc[rng.random((M, N)) < rng.uniform(0, 0.3)] = np.nan
+    k = int(rng.choice([3, 5]))
+    lp = fe.LaplacianParams(float(rng.uniform(0.2, 1.0)), k, int(rng.integers(1, 5)))
+    sm = fe.laplacian_filter_opc(opc, lp)
+    assert sm.dtype == np.float64 and sm.shape == opc.shape
+    assert_vertices_close(sm, fo.laplacian_filter(opc, lp.lam, lp.kernel_size, lp.iterations))
+    tris, trimap = fe.extract_triangles_opc(sm)
+    rt, rtm = fo.extract_triangles_opc(sm)
+    assert np.array_equal(tris, rt) and np.array_equal(trimap, rtm)
+    assert np.array_equal(fe.extract_halfedges_opc(trimap, M, N),
+                          fo.extract_halfedges_opc(rtm, M, N))
+    mesh = fe.mesh_from_opc(sm)
+    assert same(mesh.normals, fo.triangle_normals(sm.reshape(-1, 3), rt))
+    cen, nrm = fe.compute_fc_triangle_data(sm)
+    rc, rn = fo.compute_fc_triangle_data(sm)
+    assert same(cen, rc) and same(nrm, rn)
+    bp = fe.BilateralParams(float(rng.uniform(0.03, 0.2)), float(rng.uniform(0.1, 0.4)),
+                            int(rng.choice([3, 5])), 1)
+    got = fe.bilateral_filter_opc(sm, bp, trimap)
+    ref = fo.bilateral_filter_opc(sm, bp.sigma_length, bp.sigma_angle, bp.kernel_size,
+                                  bp.iterations)
+    assert_normals_close(got, ref)
