@@ -618,24 +618,34 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
       // |acc| <= 1e-30 throughout -- the usual case) has n = its FC normal: rebuilt from
       // the points with iteration 1's arithmetic and accepted when it reproduces n'
       // exactly; otherwise n' / sqrt(B) (<= 1 ulp).  Rare path (global point loads).
-      if (!upd[o][0] || !upd[o][1]) {
+      const float inv = 1.0f / sB;
+      bool rebuild = false;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (!upd[o][k]) {
+          const bool valid = (k == 0 ? f2lo(q.cx) : f2hi(q.cx)) != 1e18f;  // not a sentinel
+          const float qn = __int_as_float(0x7fc00000);
+          res[o][3 * k] = valid ? (k == 0 ? f2lo(q.nx) : f2hi(q.nx)) * inv : qn;
+          res[o][3 * k + 1] = valid ? (k == 0 ? f2lo(q.ny) : f2hi(q.ny)) * inv : qn;
+          res[o][3 * k + 2] = valid ? (k == 0 ? f2lo(q.nz) : f2hi(q.nz)) * inv : qn;
+          rebuild |= valid;
+        }
+      }
+      if (rebuild) {  // rare: a valid triangle left unchanged
         const float* P1 = a.pts + f * a.pts_fs + (long long)u * a.pitch + 3 * v;
         float raw[6];
         fc_normals_quad(P1, P1 + 3, P1 + a.pitch + 3, P1 + a.pitch, raw);
-        const float inv = 1.0f / sB;
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          if (!upd[o][k]) {
-            const bool valid = (k == 0 ? f2lo(q.cx) : f2hi(q.cx)) != 1e18f;
-            const float n0 = k == 0 ? f2lo(q.nx) : f2hi(q.nx);
-            const float n1 = k == 0 ? f2lo(q.ny) : f2hi(q.ny);
-            const float n2 = k == 0 ? f2lo(q.nz) : f2hi(q.nz);
-            const float* rk = raw + 3 * k;
-            const bool same = rk[0] * sB == n0 && rk[1] * sB == n1 && rk[2] * sB == n2;
-            const float qn = __int_as_float(0x7fc00000);
-            res[o][3 * k] = valid ? (same ? rk[0] : n0 * inv) : qn;
-            res[o][3 * k + 1] = valid ? (same ? rk[1] : n1 * inv) : qn;
-            res[o][3 * k + 2] = valid ? (same ? rk[2] : n2 * inv) : qn;
+          const float n0 = k == 0 ? f2lo(q.nx) : f2hi(q.nx);
+          const float n1 = k == 0 ? f2lo(q.ny) : f2hi(q.ny);
+          const float n2 = k == 0 ? f2lo(q.nz) : f2hi(q.nz);
+          const float* rk = raw + 3 * k;
+          if (!upd[o][k] && (k == 0 ? f2lo(q.cx) : f2hi(q.cx)) != 1e18f &&
+              rk[0] * sB == n0 && rk[1] * sB == n1 && rk[2] * sB == n2) {
+            res[o][3 * k] = rk[0];
+            res[o][3 * k + 1] = rk[1];
+            res[o][3 * k + 2] = rk[2];
           }
         }
       }
