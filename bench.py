@@ -70,9 +70,7 @@ WORKLOADS = {
                    64, 1024, (1.0, 3, 5), None, 0.5, _base("config_c3"), 512),
     "C5": Workload("C5", "C5: batch of 512 frames at 480x640 (C2 base + per-frame 2 mm noise + "
                          "2 % dropout) split over the GPUs, full front-end per frame",
-                   480, 640, (1.0, 3, 3), (0.1, 0.15, 3, 2), None,
-                   lambda: __import__("paper_2007_12065_b200.synthetic", fromlist=["x"])
-                   .room_scene(n=640, noise=0.002, seed=2)[80:560, :].copy(),
+                   480, 640, (1.0, 3, 3), (0.1, 0.15, 3, 2), None, _base("config_c5_base"),
                    512, total=512, dropout=0.02),
 }
 WL = WORKLOADS["C4"]

@@ -118,10 +118,15 @@ def config_c4(seed=4):
     return room_scene(n=1920, noise=0.002, seed=seed)[420:1500, :].copy()
 
 
+def config_c5_base():
+    """C5 base frame: the C2 crop before dropout (per-frame noise + dropout are added)."""
+    return room_scene(n=640, noise=0.002, seed=2)[80:560, :].copy()
+
+
 def config_c5_frames(count, base=None, start=0):
     """C5 frames: C2 base + per-frame N(0, 2 mm) noise + 2 % dropout (configs[4])."""
     if base is None:
-        base = room_scene(n=640, noise=0.002, seed=2)[80:560, :]
+        base = config_c5_base()
     out = np.empty((count,) + base.shape)
     for i in range(count):
         g = np.random.default_rng(1000 + start + i)
