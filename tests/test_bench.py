@@ -41,3 +41,17 @@ def test_algorithmic_bytes_match_survey_table():
     assert abs(ab["laplacian_per_launch"] * 10 / 1e6 - 497.7) < 0.5
     assert abs(ab["triangulate_per_launch"] / 1e6 - 289.9) < 0.5
     assert abs(ab["frame_total"] / 1e6 - 1756.7) < 1.0
+
+
+def test_algorithmic_bytes_other_configs():
+    sys.path.insert(0, REPO)
+    import bench
+    # 140.0 MB / frame (lap 22.1, FC 18.4, bil 44.1, tri 41.1, gather 14.3)
+    ab = bench.algorithmic_bytes(1, 575884, bench.WORKLOADS["C2"])
+    assert abs(ab["frame_total"] / 1e6 - 140.0) < 0.5
+    assert abs(ab["triangulate_per_launch"] / 1e6 - 41.1) < 0.1
+    # C3: no bilateral -> triangulation carries the l_max flags (T) and the normals (12T)
+    ab = bench.algorithmic_bytes(1, 91991, bench.WORKLOADS["C3"])
+    assert ab["bilateral_stage"] == 0
+    assert abs(ab["triangulate_per_launch"] / 1e6 - (7.26 + 0.09 + 1.10)) < 0.02
+    assert bench.WORKLOADS["C5"].total == 512
