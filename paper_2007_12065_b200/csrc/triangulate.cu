@@ -9,8 +9,9 @@
 //   * twins (mesh.py:129-134): edge k links edge k of the neighbour
 //       first  e0 -> (u,v+1,1)  e1 -> (u-1,v,1)  e2 -> (u,v,1)
 //       second e0 -> (u,v-1,0)  e1 -> (u+1,v,0)  e2 -> (u,v,0)
-//   * optional fused extras: mesh-order normals (geometry.py:134-147, fp64 math)
-//     and the l_max longest-edge flag (segmentation.py:59-67,73, fp64 math).
+//   * optional extras: mesh-order normals (geometry.py:134-147, fp64 math) and the
+//     l_max longest-edge flag (segmentation.py:59-67,73, fp64 math), by a 4th launch
+//     per quad (quad_extras_kernel) once trimap exists.
 //
 // B200 mapping: three launches, none of which waits on another CTA.
 //   1. tri_count_kernel: one warp per quad row counts its valid triangles (popc of the
@@ -53,12 +54,6 @@ struct TriArgs {
   int64_t* tris;
   int64_t* he;
   const long long* row_base;  // [F][M]: exclusive prefix of row u's triangles; [Mq] = total
-  const float* pts;
-  int pitch;
-  long long pts_fs;
-  float* normals;
-  uint8_t* lflag;
-  double l2_thr;  // sq_threshold(l_max)
 };
 
 // validity bits of point row r around the 32-point group starting at v0 = 32*word
@@ -91,41 +86,84 @@ __device__ __forceinline__ QuadBits quad_bits(const PtBits& t, const PtBits& b) 
   return q;
 }
 
-// normals / l_max flag of triangle t (vertex ids ia, ib, ic in point rows u and u + 1)
-__device__ __forceinline__ void emit_extras(const TriArgs& a, int f, int u, long long t, int64_t ia,
-                                            int64_t ib, int64_t ic) {
-  const long long r0 = (long long)u * a.N;
-  const float* P = a.pts + f * a.pts_fs + (long long)u * a.pitch;
-  auto at = [&](int64_t id) {  // no division: the row is u or u + 1
-    const bool lo = id >= r0 + a.N;
-    return P + (lo ? a.pitch : 0) + (id - r0 - (lo ? a.N : 0)) * 3;
-  };
-  const float* pa = at(ia);
-  const float* pb = at(ib);
-  const float* pc = at(ic);
-  const double ax = pa[0], ay = pa[1], az = pa[2];
-  const double bx = pb[0], by = pb[1], bz = pb[2];
-  const double cx = pc[0], cy = pc[1], cz = pc[2];
-  if (a.normals != nullptr) {
-    double nx, ny, nz;
-    unit_normal_f64(ax, ay, az, bx, by, bz, cx, cy, cz, nx, ny, nz);
-    float* o = a.normals + (f * a.G + t) * 3;
-    o[0] = (float)nx;
-    o[1] = (float)ny;
-    o[2] = (float)nz;
+// Normals + l_max flags per QUAD, after the triangulation (which then runs its lean
+// variant): one thread loads the quad's 4 points (coalesced) and converts them to fp64
+// once; the two triangles (p3,p2,p1) and (p1,p4,p3) share the diagonal p1 - p3, so 5
+// edge vectors serve 6 edges.  Results go to mesh order through trimap.  The arithmetic
+// is numpy's (geometry.py:134-147; segmentation.py:59-67,73), so normals are
+// float32(reference) exactly and the flags bit-exact (see sq_threshold).
+__device__ __forceinline__ void normal_from_edges_f64(const double* e1, const double* e2,
+                                                      float* o) {
+  const double x = dsub(dmul(e1[1], e2[2]), dmul(e1[2], e2[1]));
+  const double y = dsub(dmul(e1[2], e2[0]), dmul(e1[0], e2[2]));
+  const double z = dsub(dmul(e1[0], e2[1]), dmul(e1[1], e2[0]));
+  const double n = __dsqrt_rn(dadd(dadd(dmul(x, x), dmul(y, y)), dmul(z, z)));
+  if (n > 0.0) {
+    o[0] = (float)__ddiv_rn(x, n);
+    o[1] = (float)__ddiv_rn(y, n);
+    o[2] = (float)__ddiv_rn(z, n);
+  } else {
+    o[0] = o[1] = o[2] = __int_as_float(0x7fc00000);
   }
-  if (a.lflag != nullptr) {
-    a.lflag[f * a.G + t] = (uint8_t)longest_edge_exceeds(
-        edge_len2_f64(ax, ay, az, bx, by, bz), edge_len2_f64(bx, by, bz, cx, cy, cz),
-        edge_len2_f64(cx, cy, cz, ax, ay, az), a.l2_thr);
+}
+__device__ __forceinline__ double len2_f64(const double* d) {
+  return dadd(dadd(dmul(d[0], d[0]), dmul(d[1], d[1])), dmul(d[2], d[2]));
+}
+
+__global__ void __launch_bounds__(128) quad_extras_kernel(const float* __restrict__ pts, int pitch,
+                                                          long long pts_fs, int M, int N,
+                                                          const int64_t* __restrict__ trimap,
+                                                          long long G, float* __restrict__ normals,
+                                                          uint8_t* __restrict__ lflag,
+                                                          double l2_thr) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  const int u = blockIdx.y, f = blockIdx.z;
+  const int Nq = N - 1;
+  if (v >= Nq) return;
+  const long long gid = 2ll * ((long long)u * Nq + v);
+  const longlong2 tm = *reinterpret_cast<const longlong2*>(trimap + f * G + gid);
+  if (tm.x < 0 && tm.y < 0) return;
+  const float* P1 = pts + f * pts_fs + (long long)u * pitch + 3 * v;
+  const float* P4 = P1 + pitch;
+  double p1[3], p2[3], p3[3], p4[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    p1[j] = P1[j];
+    p2[j] = P1[3 + j];
+    p4[j] = P4[j];
+    p3[j] = P4[3 + j];
+  }
+  double d31[3], d13[3], e23[3], e14[3];  // p3 - p1, p1 - p3, p2 - p3, p4 - p1
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    d13[j] = dsub(p1[j], p3[j]);
+    d31[j] = -d13[j];  // exact: the same value numpy's p3 - p1 rounds to
+    e23[j] = dsub(p2[j], p3[j]);
+    e14[j] = dsub(p4[j], p1[j]);
+  }
+  if (tm.x >= 0) {  // (p3, p2, p1): e1 = p2 - p3, e2 = p1 - p3
+    if (normals) normal_from_edges_f64(e23, d13, normals + (f * G + tm.x) * 3);
+    if (lflag) {
+      double e12[3];  // c - b = p1 - p2
+#pragma unroll
+      for (int j = 0; j < 3; ++j) e12[j] = dsub(p1[j], p2[j]);
+      lflag[f * G + tm.x] =
+          (uint8_t)longest_edge_exceeds(len2_f64(e23), len2_f64(e12), len2_f64(d31), l2_thr);
+    }
+  }
+  if (tm.y >= 0) {  // (p1, p4, p3): e1 = p4 - p1, e2 = p3 - p1
+    if (normals) normal_from_edges_f64(e14, d31, normals + (f * G + tm.y) * 3);
+    if (lflag) {
+      double e43[3];  // c - b = p3 - p4
+#pragma unroll
+      for (int j = 0; j < 3; ++j) e43[j] = dsub(p3[j], p4[j]);
+      lflag[f * G + tm.y] =
+          (uint8_t)longest_edge_exceeds(len2_f64(e14), len2_f64(e43), len2_f64(d13), l2_thr);
+    }
   }
 }
 
-#ifndef OPCFE_TRI_XBLOCKS
-#define OPCFE_TRI_XBLOCKS 4  // 64 registers (measured: 2 -> 1.55, 3 -> 1.29, 4 -> 1.19 ms, C3)
-#endif
-template <bool EXTRAS>
-__global__ void __launch_bounds__(kTriNT, EXTRAS ? OPCFE_TRI_XBLOCKS : 4) triangulate_kernel(TriArgs a) {
+__global__ void __launch_bounds__(kTriNT, 4) triangulate_kernel(TriArgs a) {
   __shared__ unsigned long long red[kTriWarps];
   __shared__ unsigned long long gpre[kSegGroups];     // packed per-group exclusive prefixes
   __shared__ int64_t stage[kTriWarps][2][3 * 64];     // per-warp tris / twins staging
@@ -240,10 +278,6 @@ __global__ void __launch_bounds__(kTriNT, EXTRAS ? OPCFE_TRI_XBLOCKS : 4) triang
       const int n3 = 3 * (__popc(qc.f) + __popc(qc.s));
       int64_t* tdst = tris + 3 * t_first;
       for (int i = lane; i < n3; i += 32) tdst[i] = st_t[i];
-      if (EXTRAS) {  // dense over the group's staged triangles (no divergent per-quad calls)
-        for (int i = lane; 3 * i < n3; i += 32)
-          emit_extras(a, f, u, t_first + i, st_t[3 * i], st_t[3 * i + 1], st_t[3 * i + 2]);
-      }
       if (he) {
         int64_t* hdst = he + 3 * t_first;
         for (int i = lane; i < n3; i += 32) hdst[i] = st_h[i];
@@ -365,22 +399,20 @@ int triangulate(const uint32_t* vmask, int F, int M, int N, int64_t* trimap, int
   a.he = he;
   long long* row_base = static_cast<long long*>(ws);
   a.row_base = row_base;
-  a.pts = pts;
-  a.pitch = pitch;
-  a.pts_fs = (long long)M * pitch;
-  a.normals = normals;
-  a.lflag = lflag;
-  a.l2_thr = sq_threshold(l_max);
   tri_count_kernel<<<dim3((M - 1 + 7) / 8, F), 256, 0, st>>>(vmask, a.vm_fs, a.wpr, M, N, row_base);
   if (int rc = check_launch("tri_count_kernel")) return rc;
   tri_scan_kernel<<<F, 1024, 0, st>>>(row_base, M, ntri);
   if (int rc = check_launch("tri_scan_kernel")) return rc;
   dim3 grid(M - 1, F);
-  if (normals || lflag)
-    triangulate_kernel<true><<<grid, kTriNT, 0, st>>>(a);
-  else
-    triangulate_kernel<false><<<grid, kTriNT, 0, st>>>(a);
-  return check_launch("triangulate_kernel");
+  triangulate_kernel<<<grid, kTriNT, 0, st>>>(a);
+  if (int rc = check_launch("triangulate_kernel")) return rc;
+  if (normals || lflag) {
+    dim3 xg((N - 1 + 127) / 128, M - 1, F);
+    quad_extras_kernel<<<xg, 128, 0, st>>>(pts, pitch, (long long)M * pitch, M, N, trimap, a.G,
+                                            normals, lflag, sq_threshold(l_max));
+    return check_launch("quad_extras_kernel");
+  }
+  return OK;
 }
 
 int halfedges_from_trimap(const int64_t* trimap, int M, int N, int64_t n_tri, int64_t* he,
