@@ -92,18 +92,42 @@ __device__ __forceinline__ QuadBits quad_bits(const PtBits& t, const PtBits& b) 
 // edge vectors serve 6 edges.  Results go to mesh order through trimap.  The arithmetic
 // is numpy's (geometry.py:134-147; segmentation.py:59-67,73), so normals are
 // float32(reference) exactly and the flags bit-exact (see sq_threshold).
+// float32(fl64(c / fl64(sqrt(s)))) -- the reference's fp64 normal component rounded to
+// fp32 -- without the correctly rounded divide and square root: q = c * rsqrt(s) is
+// within a few ulp64 of fl64(c / n), so both round to the same fp32 value unless q lies
+// within 16 ulp64 of an fp32 rounding midpoint (probability ~6e-8) or in the fp32
+// subnormal range; those take the exact path.
+__device__ __forceinline__ float div_norm_to_f32(double c, double r, double s) {
+  const double q = c * r;
+  const long long b = __double_as_longlong(q);
+  const int low = (int)(b & 0x1fffffff) - 0x10000000;  // distance to the fp32 midpoint
+  if (low > 16 || low < -16) {
+    if (fabs(q) >= 2.4e-38) return (float)q;             // fp32 normal range
+    if (q == 0.0) return (float)q;
+  }
+  return (float)__ddiv_rn(c, __dsqrt_rn(s));
+}
+
 __device__ __forceinline__ void normal_from_edges_f64(const double* e1, const double* e2,
                                                       float* o) {
   const double x = dsub(dmul(e1[1], e2[2]), dmul(e1[2], e2[1]));
   const double y = dsub(dmul(e1[2], e2[0]), dmul(e1[0], e2[2]));
   const double z = dsub(dmul(e1[0], e2[1]), dmul(e1[1], e2[0]));
-  const double n = __dsqrt_rn(dadd(dadd(dmul(x, x), dmul(y, y)), dmul(z, z)));
-  if (n > 0.0) {
-    o[0] = (float)__ddiv_rn(x, n);
-    o[1] = (float)__ddiv_rn(y, n);
-    o[2] = (float)__ddiv_rn(z, n);
+  const double s = dadd(dadd(dmul(x, x), dmul(y, y)), dmul(z, z));
+  if (s >= 2.3e-308 && s <= 1.7e308) {  // normal range: rsqrt <= 1 ulp
+    const double r = rsqrt(s);
+    o[0] = div_norm_to_f32(x, r, s);
+    o[1] = div_norm_to_f32(y, r, s);
+    o[2] = div_norm_to_f32(z, r, s);
   } else {
-    o[0] = o[1] = o[2] = __int_as_float(0x7fc00000);
+    const double n = __dsqrt_rn(s);
+    if (n > 0.0) {
+      o[0] = (float)__ddiv_rn(x, n);
+      o[1] = (float)__ddiv_rn(y, n);
+      o[2] = (float)__ddiv_rn(z, n);
+    } else {
+      o[0] = o[1] = o[2] = __int_as_float(0x7fc00000);
+    }
   }
 }
 __device__ __forceinline__ double len2_f64(const double* d) {

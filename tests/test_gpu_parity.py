@@ -965,3 +965,25 @@ def test_drop_in_api_randomised(fe, seed):
     ref = fo.bilateral_filter_opc(sm, bp.sigma_length, bp.sigma_angle, bp.kernel_size,
                                   bp.iterations)
     assert_normals_close(got, ref)
+
+
+@pytest.mark.parametrize("scale", [1e-4, 1.0, 3e3])
+def test_front_end_normals_exact_at_scale(fe, scale):
+    """Mesh normals of the fp32 pipeline without bilateral are float32(reference fp64
+    normal) exactly (quad_extras_kernel: rsqrt + multiply, exact divide / sqrt only near
+    an fp32 rounding midpoint) -- 1.2 M triangles of random shapes per scale."""
+    rng = np.random.default_rng(int(scale * 1000) % 997)
+    M, N = 700, 900
+    opc = grid_opc(M, N) * scale * 0.01
+    opc += rng.normal(scale=scale * 0.006, size=opc.shape)
+    opc[rng.random((M, N)) < 0.05] = np.nan
+    opc = opc.astype(np.float32)
+    _, res = _engine_run(fe, opc, None, None, l_max=scale * 0.02)
+    T = res.n_tri[0]
+    sm = opc.astype(np.float64)
+    tris, _, _ = c_oracle.triangulate(sm)
+    assert T == len(tris) > 1_000_000
+    ref = c_oracle.triangle_normals(sm, tris).astype(np.float32)
+    assert same(res.normals[0, :T].cpu().numpy(), ref)
+    assert np.array_equal(res.lmax_mask[0, :T].cpu().numpy().astype(bool),
+                          c_oracle.max_edge_mask(sm, tris, scale * 0.02))
