@@ -446,9 +446,6 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
     uint32_t bytes = 0;
     if (MODE != kNormalsCentBuf) bytes += T::PW * 3 * T::PH * 4;
     if (MODE != kFromPoints) bytes += T::QW * 6 * T::QH * 4;
@@ -458,6 +455,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     if (MODE != kFromPoints) tma_load_3d(nrm_s, &tnrm, &bar, (q0 - T::LQ) * 6, u0 - H, f);
     if (MODE == kNormalsCentBuf) tma_load_3d(cen_s, &tcen, &bar, (q0 - T::LQ) * 6, u0 - H, f);
   }
+  __syncthreads();  // barrier initialised (and its loads issued) before anyone waits
   const float sA = a.sA, sB = a.sB, sA3 = a.sA * (1.0f / 3.0f);
   const int tx = threadIdx.x % kBilTQW, ty = threadIdx.x / kBilTQW;
   const int R0 = kQPT * ty + H, C = tx + T::LQ;  // pack position of the thread's quad 0
@@ -587,9 +585,6 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
     mbar_expect_tx(&bar, T::QW * T::QH * 48);
     const int x = q0 - T::LQ, y = u0 - H;
     tma_load_3d(P.c0, &tc0, &bar, x * 4, y, f);
@@ -597,6 +592,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     tma_load_3d(P.n0, &tn0, &bar, x * 4, y, f);
     tma_load_3d(P.n1, &tn1, &bar, x * 2, y, f);
   }
+  __syncthreads();  // barrier initialised (and its loads issued) before anyone waits
   const float sB = a.sB;
   const int tx = threadIdx.x % kBilTQW, ty = threadIdx.x / kBilTQW;
   const int R0 = kQPT * ty + H, C = tx + T::LQ;

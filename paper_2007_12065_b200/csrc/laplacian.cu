@@ -63,12 +63,10 @@ __global__ void __launch_bounds__(kLapNT)
     prefetch_tmap(&tout);
     mbar_init(&bar, 1);
     fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
     mbar_expect_tx(&bar, T::IN_FLOATS * 4);
     tma_load_3d(in_s, &tin, &bar, (v0 - T::L) * 3, u0 - H, f);
   }
+  __syncthreads();  // barrier initialised (and its loads issued) before anyone waits
   mbar_wait(&bar, 0);
 
   const int lane = threadIdx.x & 31;
@@ -228,12 +226,10 @@ __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
     mbar_expect_tx(&bar, kL3BW * 3 * kL3BH * 4);
     tma_load_3d(in_s, &tin, &bar, (v0 - kL3L) * 3, u0 - 1, f);
   }
+  __syncthreads();  // barrier initialised (and its loads issued) before anyone waits
   mbar_wait(&bar, 0);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -349,12 +345,10 @@ __global__ void __launch_bounds__(kL3NT, OPCFE_LAPP_BLOCKS)
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
     mbar_expect_tx(&bar, kL3BW * 3 * kL3BH * 4);
     tma_load_3d(in_s, &tin, &bar, (v0 - kL3L) * 3, u0 - 1, f);
   }
+  __syncthreads();  // barrier initialised (and its loads issued) before anyone waits
   mbar_wait(&bar, 0);
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
