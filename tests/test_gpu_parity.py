@@ -906,30 +906,47 @@ def test_laplacian_coincident_neighbours(fe, iters):
     assert_vertices_close(res.points[0].cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("seed", range(24))
+def _frame_view(res, f):
+    from paper_2007_12065_b200.frontend import FrontEndResult
+    sl = slice(f, f + 1)
+    return FrontEndResult(points=res.points[sl], triangles=res.triangles[sl],
+                          trimap=res.trimap[sl],
+                          halfedges=None if res.halfedges is None else res.halfedges[sl],
+                          normals=None if res.normals is None else res.normals[sl],
+                          lmax_mask=None if res.lmax_mask is None else res.lmax_mask[sl],
+                          n_tri=[res.n_tri[f]], grid_shape=res.grid_shape)
+
+
+@pytest.mark.parametrize("seed", range(40))
 def test_front_end_randomised(fe, seed):
-    """Randomised configurations through the fused front end, per-stage against the oracle:
-    odd shapes (tile edges, N % 4 != 0 -> staged input), NaN fractions up to 40 %,
-    duplicated vertices, Laplacian 0..6 passes (scalar / packed / last-pass restore),
-    kernel sizes 3 and 5, bilateral 0..3 iterations at random sigmas, random l_max."""
+    """Randomised configurations through the fused front end, per-stage against the oracle,
+    every frame of a 1..3-frame batch: odd shapes (tile edges, N % 4 != 0 -> staged
+    input), NaN fractions up to 40 %, duplicated vertices, Laplacian 0..6 passes (scalar /
+    packed / last-pass restore), kernel sizes 3, 5 and 7, bilateral 0..3 iterations at
+    random sigmas, random l_max."""
     rng = np.random.default_rng(1000 + seed)
     M, N = int(rng.integers(3, 170)), int(rng.integers(3, 170))
-    opc = grid_opc(M, N) * rng.uniform(0.002, 0.05)
-    opc[..., 2] = rng.normal(0, 0.01, (M, N)) + 0.2 * np.sin(np.arange(N) / 9.0)[None, :]
-    opc += rng.normal(scale=rng.uniform(0, 0.004), size=opc.shape)
-    for u, v in rng.integers(0, [max(1, M - 1), max(1, N - 1)], size=(int(rng.integers(0, 6)), 2)):
-        opc[u, min(v + 1, N - 1)] = opc[u, v]
-    opc[rng.random((M, N)) < rng.uniform(0, 0.4)] = np.nan
-    opc = opc.astype(np.float32)
-    k_lap = 3 if rng.random() < 0.7 else 5
+    F = int(rng.integers(1, 4))
+    frames = []
+    for f in range(F):
+        opc = grid_opc(M, N) * rng.uniform(0.002, 0.05)
+        opc[..., 2] = rng.normal(0, 0.01, (M, N)) + 0.2 * np.sin(np.arange(N) / 9.0)[None, :]
+        opc += rng.normal(scale=rng.uniform(0, 0.004), size=opc.shape)
+        for u, v in rng.integers(0, [max(1, M - 1), max(1, N - 1)],
+                                 size=(int(rng.integers(0, 6)), 2)):
+            opc[u, min(v + 1, N - 1)] = opc[u, v]
+        opc[rng.random((M, N)) < rng.uniform(0, 0.4)] = np.nan
+        frames.append(opc.astype(np.float32))
+    k_lap = int(rng.choice([3, 3, 3, 5, 7]))
     lap = fe.LaplacianParams(float(rng.uniform(0.3, 1.0)), k_lap, int(rng.integers(1, 7))) \
         if rng.random() < 0.85 and min(M, N) >= k_lap else None
-    k_bil = 3 if rng.random() < 0.7 else 5
+    k_bil = int(rng.choice([3, 3, 3, 5, 7]))
     bil = fe.BilateralParams(float(rng.uniform(0.02, 0.3)), float(rng.uniform(0.08, 0.5)), k_bil,
                              int(rng.integers(1, 4))) if rng.random() < 0.75 else None
     l_max = float(rng.uniform(0.001, 0.05)) if rng.random() < 0.5 else None
-    _, res = _engine_run(fe, opc, lap, bil, l_max)
-    _per_stage_check(fe, opc, lap, bil, l_max, res)
+    _, res = _engine_run(fe, np.stack(frames), lap, bil, l_max, frames=F)
+    for f in range(F):
+        _per_stage_check(fe, frames[f], lap, bil, l_max, _frame_view(res, f))
 
 
 @pytest.mark.parametrize("seed", range(12))
