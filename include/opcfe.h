@@ -68,7 +68,9 @@ int opcfe_unstage(const float* src, int pitch, int F, int M, int N, void* dst, i
  * (_kernels/__init__.py:29 -> _native.pyx:225 / _fallback.py:82) as called by
  * smoothing.laplacian_filter_opc (smoothing.py:53-58).  Result in `out`; `tmp` is the
  * ping-pong buffer (same size, needed when iterations > 1).  If vmask != NULL the
- * first pass also writes the point-validity bits of `in`. */
+ * first pass also writes the point-validity bits of `in`.  `in` must not alias `out` or
+ * `tmp`: with kernel_size 3 and iterations > 1 the last pass re-reads it to return
+ * partial-NaN vertices exactly as given. */
 int opcfe_laplacian(const float* in, float* out, float* tmp, uint32_t* vmask, int F, int M,
                     int N, int pitch, float lam, int kernel_size, int iterations,
                     opcfe_stream_t stream);
