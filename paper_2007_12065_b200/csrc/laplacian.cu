@@ -607,6 +607,8 @@ int laplacian(const float* in, float* out, float* tmp, uint32_t* vmask, int F, i
   if (pitch < 3 * N || (pitch % 4) != 0)
     return fail(ERR_INVALID, "laplacian: row pitch must be >= 3N floats and a multiple of 4");
   if (iters > 1 && tmp == nullptr) return fail(ERR_INVALID, "laplacian: tmp buffer required");
+  if (in == out || (iters > 1 && in == tmp))
+    return fail(ERR_INVALID, "laplacian: input must not alias the output or the ping-pong buffer");
   switch (ksize / 2) {
     case 1: return run_k3(in, out, tmp, vmask, F, M, N, pitch, lam, iters, st);
     case 2: return run_h<2>(in, out, tmp, vmask, F, M, N, pitch, lam, iters, st);

@@ -66,6 +66,9 @@ def test_errors_cross_the_abi_as_codes():
     rc = L.opcfe_laplacian(None, None, None, None, 1, 4, 4, 12, 1.0, 3, 1, None)
     assert rc == _lib.OPCFE_ERR_INVALID
     assert b"null" in L.opcfe_last_error()
+    buf = ctypes.c_void_p(0x1000)  # never dereferenced: the aliasing check comes first
+    rc = L.opcfe_laplacian(buf, buf, None, None, 1, 4, 4, 12, 1.0, 3, 1, None)
+    assert rc == _lib.OPCFE_ERR_INVALID and b"alias" in L.opcfe_last_error()
     rc = L.opcfe_triangulate(None, 1, 1, 5, None, None, None, None, None, 0, None, -1.0, None,
                              None, 0, None)
     assert rc == _lib.OPCFE_ERR_INVALID
