@@ -119,12 +119,14 @@ class FrontEnd:
             self.labels.data_ptr() if self.labels is not None else None)
         self._graph = None
         self._use_graph = graph
-        self.kernel_launches = self._count_launches(laplacian, bilateral, src_kind) + \
+        extras = (normals and bilateral is None) or l_max is not None
+        self.kernel_launches = self._count_launches(laplacian, bilateral, src_kind, extras) + \
             (1 if self.labels is not None else 0)
 
     @staticmethod
-    def _count_launches(lap, bil, src_kind):
+    def _count_launches(lap, bil, src_kind, extras=False):
         n = 3                                                   # triangulate: count, scan, emit
+        n += 1 if extras else 0                                 # quad_extras: normals / l_max
         n += lap.iterations if lap else 0
         if not lap or src_kind != 0:
             n += 1                                              # stage-in

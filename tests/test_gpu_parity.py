@@ -568,8 +568,8 @@ def test_front_end_fused_labels(fe):
                                     0.05, 0.96)
     lab = res.labels[0, :T].cpu().numpy()
     assert np.array_equal(lab, ref)
-    # laplacian 3 + triangulate (count, scan, emit) 3 + bilateral 2 + labels 1
-    assert 0 < (lab == 255).sum() < T and eng.kernel_launches == 3 + 3 + 2 + 1
+    # laplacian 3 + triangulate (count, scan, emit) 3 + l_max flags 1 + bilateral 2 + labels 1
+    assert 0 < (lab == 255).sum() < T and eng.kernel_launches == 3 + 3 + 1 + 2 + 1
 
 
 FASTGA = load_golden("fastga")
@@ -1004,3 +1004,45 @@ def test_front_end_normals_exact_at_scale(fe, scale):
     assert same(res.normals[0, :T].cpu().numpy(), ref)
     assert np.array_equal(res.lmax_mask[0, :T].cpu().numpy().astype(bool),
                           c_oracle.max_edge_mask(sm, tris, scale * 0.02))
+
+
+@pytest.mark.parametrize("cfg", ["lap+bil", "lap+lmax", "f64+bil+lmax", "nolap"])
+def test_kernel_launch_count_matches_graph(fe, cfg):
+    """bench.py's gpu_launches = FrontEnd.kernel_launches x steps: the count equals the
+    kernel nodes of the captured front-end graph, and every node is a libopcfe kernel."""
+    from cuda.bindings import driver as drv
+    M, N = 70, 96
+    opc = grid_opc(M, N) * 0.01
+    opc[5, 7] = np.nan
+    kw = dict(laplacian=fe.LaplacianParams(1.0, 3, 3), bilateral=fe.BilateralParams())
+    dtype = torch.float32
+    if cfg == "lap+lmax":
+        kw.update(bilateral=None, l_max=0.02)
+    elif cfg == "f64+bil+lmax":
+        kw.update(l_max=0.02)
+        dtype = torch.float64
+    elif cfg == "nolap":
+        kw.update(laplacian=None)
+    eng = fe.FrontEnd(M, N, 2, src_dtype=dtype, graph=False, **kw)
+    eng.src.copy_(torch.from_numpy(opc).to("cuda", dtype).expand(2, M, N, 3))
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        eng._launch(s)                                   # warm-up outside the capture
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph(keep_graph=True)
+    with torch.cuda.graph(g, stream=s):
+        eng._launch(s)
+    graph = drv.CUgraph(g.raw_cuda_graph())
+    err, _, n = drv.cuGraphGetNodes(graph, 0)
+    assert err == drv.CUresult.CUDA_SUCCESS
+    err, nodes, n = drv.cuGraphGetNodes(graph, n)
+    names = []
+    for node in nodes[:n]:
+        err, kind = drv.cuGraphNodeGetType(node)
+        if kind == drv.CUgraphNodeType.CU_GRAPH_NODE_TYPE_KERNEL:
+            err, params = drv.cuGraphKernelNodeGetParams(node)
+            err, name = drv.cuFuncGetName(params.func)
+            names.append(name.decode() if isinstance(name, bytes) else str(name))
+    assert len(names) == eng.kernel_launches, names
+    assert all("opcfe" in nm for nm in names), names
