@@ -20,4 +20,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:tria
   -s 3 -c 1 -o gpurun_out/${TAG}_tri $CMD > gpurun_out/${TAG}_ncu_tri.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:bilateral_packed \
   -s 12 -c 1 -o gpurun_out/${TAG}_bil $CMD > gpurun_out/${TAG}_ncu_bil.log 2>&1
+# bilateral iteration 1 (FC normals + pack + packed-plane writes)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"bilateral_kernel" \
+  -s 3 -c 1 -o gpurun_out/${TAG}_bil1 $CMD > gpurun_out/${TAG}_ncu_bil1.log 2>&1
 ls -la gpurun_out/${TAG}_*
