@@ -168,11 +168,16 @@ __device__ __forceinline__ void fc_normals_quad(const float* P1, const float* P2
     e1f[j] = (double)P2[j] - p3;
     e1s[j] = (double)P4[j] - p1;
   }
-  // first: cross(p2 - p3, p1 - p3); second: cross(p4 - p1, p3 - p1) = -cross(e1s, d13)
-  normalise_fast(e1f[1] * d13[2] - e1f[2] * d13[1], e1f[2] * d13[0] - e1f[0] * d13[2],
-                 e1f[0] * d13[1] - e1f[1] * d13[0], n);
-  normalise_fast(e1s[2] * d13[1] - e1s[1] * d13[2], e1s[0] * d13[2] - e1s[2] * d13[0],
-                 e1s[1] * d13[0] - e1s[0] * d13[1], n + 3);
+  // first: cross(p2 - p3, p1 - p3); second: cross(p4 - p1, p3 - p1) = -cross(e1s, d13).
+  // Products and differences rounded separately (numpy's np.cross, no FMA contraction): a
+  // triangle with two coincident vertices has an exactly zero cross product -> NaN normal,
+  // as in the reference (a contracted FMA leaves the rounding error of one product).
+  normalise_fast(dsub(dmul(e1f[1], d13[2]), dmul(e1f[2], d13[1])),
+                 dsub(dmul(e1f[2], d13[0]), dmul(e1f[0], d13[2])),
+                 dsub(dmul(e1f[0], d13[1]), dmul(e1f[1], d13[0])), n);
+  normalise_fast(dsub(dmul(e1s[2], d13[1]), dmul(e1s[1], d13[2])),
+                 dsub(dmul(e1s[0], d13[2]), dmul(e1s[2], d13[0])),
+                 dsub(dmul(e1s[1], d13[0]), dmul(e1s[0], d13[1])), n + 3);
 }
 
 

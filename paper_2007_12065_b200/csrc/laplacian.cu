@@ -185,19 +185,21 @@ struct Acc4 {
 };
 
 // weigh the pair (p -> q): d = q - p; valid iff |d|^2 >= FLT_MIN (false for NaN)
+// Every operation is spelled out (no compiler contraction choices) so the packed passes,
+// which run the same operations on FP32x2 registers, are bit-identical to this one.
 __device__ __forceinline__ void lap_pair(const float* p, const float* q, Acc4& acc, float* dw_out) {
-  const float dx = q[0] - p[0], dy = q[1] - p[1], dz = q[2] - p[2];
-  const float d2 = dx * dx + dy * dy + dz * dz;
+  const float dx = __fsub_rn(q[0], p[0]), dy = __fsub_rn(q[1], p[1]), dz = __fsub_rn(q[2], p[2]);
+  const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
   if (d2 >= 1.17549435e-38f) {
     const float w = rsqrt_approx(d2);
-    acc.x = fmaf(dx, w, acc.x);
-    acc.y = fmaf(dy, w, acc.y);
-    acc.z = fmaf(dz, w, acc.z);
-    acc.w += w;
+    acc.x = __fmaf_rn(dx, w, acc.x);
+    acc.y = __fmaf_rn(dy, w, acc.y);
+    acc.z = __fmaf_rn(dz, w, acc.z);
+    acc.w = __fadd_rn(acc.w, w);
     if (dw_out) {
-      dw_out[0] = -dx * w;
-      dw_out[1] = -dy * w;
-      dw_out[2] = -dz * w;
+      dw_out[0] = __fmul_rn(-dx, w);
+      dw_out[1] = __fmul_rn(-dy, w);
+      dw_out[2] = __fmul_rn(-dz, w);
       dw_out[3] = w;
     }
   } else if (dw_out) {
@@ -271,10 +273,10 @@ __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
     Acc4 acc{0.f, 0.f, 0.f, 0.f};
     float down[4];
     lap_pair(p, A[0], acc, nullptr);
-    acc.x += carry[0];  // (-1, 0): weighed by the row above
-    acc.y += carry[1];
-    acc.z += carry[2];
-    acc.w += carry[3];
+    acc.x = __fadd_rn(acc.x, carry[0]);  // (-1, 0): weighed by the row above
+    acc.y = __fadd_rn(acc.y, carry[1]);
+    acc.z = __fadd_rn(acc.z, carry[2]);
+    acc.w = __fadd_rn(acc.w, carry[3]);
     lap_pair(p, A[2], acc, nullptr);
     lap_pair(p, B[0], acc, nullptr);
     lap_pair(p, B[2], acc, nullptr);
@@ -283,10 +285,10 @@ __global__ void __launch_bounds__(kL3NT, 65536 / (64 * kL3NT))
     lap_pair(p, Cr[2], acc, nullptr);
     float ox = p[0], oy = p[1], oz = p[2];
     if (fin && ((movable >> i) & 1u) && acc.w > 0.f) {
-      const float s = lam * rcp_approx(acc.w);
-      ox = p[0] + s * acc.x;
-      oy = p[1] + s * acc.y;
-      oz = p[2] + s * acc.z;
+      const float s = __fmul_rn(lam, rcp_approx(acc.w));
+      ox = __fmaf_rn(s, acc.x, p[0]);
+      oy = __fmaf_rn(s, acc.y, p[1]);
+      oz = __fmaf_rn(s, acc.z, p[2]);
     }
     if (ENC && !fin) ox = oy = oz = lap_encode_invalid(p);
     float* po = out_s + (r * kL3TW + c) * 3;
@@ -375,16 +377,28 @@ __global__ void __launch_bounds__(kL3NT, OPCFE_LAPP_BLOCKS)
 #pragma unroll 1
     for (int du = -1; du <= 1; ++du)
 #pragma unroll 1
-      for (int dv = -1; dv <= 1; ++dv)
-        if (du != 0 || dv != 0) lap_pair(p, p + (du * kL3BW + dv) * 3, acc, nullptr);
+      for (int dv = -1; dv <= 1; ++dv) {
+        if (du == 0 && dv == 0) continue;
+        if (du == -1 && dv == 0) {  // the up pair: the scalar pass's carried form
+          float dw[4];
+          Acc4 dummy{0.f, 0.f, 0.f, 0.f};
+          lap_pair(p - kL3BW * 3, p, dummy, dw);  // weighed from the row above
+          acc.x = __fadd_rn(acc.x, dw[0]);
+          acc.y = __fadd_rn(acc.y, dw[1]);
+          acc.z = __fadd_rn(acc.z, dw[2]);
+          acc.w = __fadd_rn(acc.w, dw[3]);
+        } else {
+          lap_pair(p, p + (du * kL3BW + dv) * 3, acc, nullptr);
+        }
+      }
     o[0] = p[0];
     o[1] = p[1];
     o[2] = p[2];
     if (acc.w > 0.f) {
-      const float s = lam * rcp_approx(acc.w);
-      o[0] = p[0] + s * acc.x;
-      o[1] = p[1] + s * acc.y;
-      o[2] = p[2] + s * acc.z;
+      const float s = __fmul_rn(lam, rcp_approx(acc.w));
+      o[0] = __fmaf_rn(s, acc.x, p[0]);
+      o[1] = __fmaf_rn(s, acc.y, p[1]);
+      o[2] = __fmaf_rn(s, acc.z, p[2]);
     }
   };
   // Packed rows Q(q) = (tile row r0+q, tile row r0+q+HS): lane lo walks the top half of the
@@ -423,8 +437,18 @@ __global__ void __launch_bounds__(kL3NT, OPCFE_LAPP_BLOCKS)
     };
     // the reference's order: du = -1 (dv = -1, 0, 1), du = 0 (dv = -1, 1), du = 1 (...)
     nb(Qm[0]);
-    if (q == 0) {
-      nb(Qm[1]);
+    if (q == 0) {  // up pair, in the scalar pass's carried form: acc + fl(d * w)
+      const f2_t dx = sub2(Qm[1][0], px), dy = sub2(Qm[1][1], py), dz = sub2(Qm[1][2], pz);
+      f2_t d2 = mul2(dx, dx);
+      d2 = fma2(dy, dy, d2);
+      d2 = fma2(dz, dz, d2);
+      const float wl = rsqrt_approx(f2lo(d2)), wh = rsqrt_approx(f2hi(d2));
+      // scalar mul.rn products: ptxas contracts a packed mul2 feeding add2 into FFMA2
+      auto prod = [&](f2_t d) { return f2(__fmul_rn(f2lo(d), wl), __fmul_rn(f2hi(d), wh)); };
+      ax = add2(ax, prod(dx));
+      ay = add2(ay, prod(dy));
+      az = add2(az, prod(dz));
+      aw = add2(aw, f2(wl, wh));
     } else {  // up pair = the previous step's down pair, negated
       ax = sub2(ax, cdx);
       ay = sub2(ay, cdy);
@@ -441,13 +465,15 @@ __global__ void __launch_bounds__(kL3NT, OPCFE_LAPP_BLOCKS)
       d2 = fma2(dy, dy, d2);
       d2 = fma2(dz, dz, d2);
       cw = f2(rsqrt_approx(f2lo(d2)), rsqrt_approx(f2hi(d2)));
+      // accumulate with FMA exactly as the scalar pass does (lap_pair), so the packed passes
+      // are bit-identical to chained scalar passes; the carry is the rounded product
+      ax = fma2(dx, cw, ax);
+      ay = fma2(dy, cw, ay);
+      az = fma2(dz, cw, az);
+      aw = add2(aw, cw);
       cdx = mul2(dx, cw);
       cdy = mul2(dy, cw);
       cdz = mul2(dz, cw);
-      ax = add2(ax, cdx);
-      ay = add2(ay, cdy);
-      az = add2(az, cdz);
-      aw = add2(aw, cw);
     }
     nb(Qp[2]);
     const f2_t sc = f2(lam * rcp_approx(f2lo(aw)), lam * rcp_approx(f2hi(aw)));

@@ -351,8 +351,18 @@ def _per_stage_check(fe, opc, lap, bil, l_max=None, res=None):
     x32 = np.asarray(opc, dtype=np.float32).astype(np.float64)
     sm_gpu = res.points.cpu().numpy()[0].astype(np.float64)
     if lap is not None:
-        assert_vertices_close(sm_gpu, c_oracle.laplacian_filter(x32, lap.lam, lap.kernel_size,
-                                                                lap.iterations))
+        # per pass: every GPU pass within 1e-5 of one fp64 reference pass on the same input
+        # (chained fp32 vs chained fp64 is ill-conditioned where the 1/|d| weights collapse
+        # two vertices onto each other), and the fused L-pass result equals the chain of
+        # single passes bit for bit
+        cur = np.asarray(opc, dtype=np.float32)
+        one = fe.LaplacianParams(lap.lam, lap.kernel_size, 1)
+        for _ in range(lap.iterations):
+            g = np.asarray(fe.laplacian_filter_opc(cur, one), dtype=np.float32)
+            assert_vertices_close(g, c_oracle.laplacian_filter(cur.astype(np.float64), lap.lam,
+                                                               lap.kernel_size, 1))
+            cur = g
+        assert same(res.points.cpu().numpy()[0], cur)
     else:
         assert same(sm_gpu, x32)
     T = res.n_tri[0]
