@@ -128,7 +128,35 @@ struct BilArgs {
   const float* pts;  // point grid (packed scatter: exact rebuild of unchanged normals)
   int pitch;
   long long pts_fs;
+  char* cwin;        // fused pipeline: per-tile centroid windows [F][gy][gx] (see below)
+  long long wstride; // bytes per window
+  int gx, gy;        // tile grid (kBilTQW x kBilTQH quads per tile)
 };
+
+// Centroids are handled relative to a per-tile origin o (the box's centre value, else the
+// first finite one): an fp32 centroid far from the coordinate origin carries an absolute
+// rounding of |c| * 2^-24, which the weight exponent would see as a relative error
+// |c| h / sl^2 * 1.2e-7 (h the spacing) -- at 8.6 m with sl = 2 cm that broke the 1e-5
+// contract.  Relative to o, the rounding scales with the tile extent instead.  Halo quads
+// need the SAME origin, so the fused pipeline's iteration 1 stores each tile's whole packed
+// centroid window (tile + halo, ~1.4x the quads) and later iterations bulk-load their own
+// window: no re-basing, and the values equal what a pack from the points computes.
+template <int NT>
+__device__ __forceinline__ float3 tile_origin(const float* v, int count, int stride, int* s_first) {
+  if (threadIdx.x == 0) *s_first = 0x7fffffff;
+  __syncthreads();
+  for (int i = threadIdx.x; i < count; i += NT) {
+    const float* q = v + i * stride;
+    if (finite3f(q[0], q[1], q[2])) {
+      atomicMin(s_first, i);
+      break;
+    }
+  }
+  __syncthreads();
+  const int i = *s_first;
+  return i == 0x7fffffff ? make_float3(0.f, 0.f, 0.f)
+                         : make_float3(v[i * stride], v[i * stride + 1], v[i * stride + 2]);
+}
 
 // FC normals of a quad's two triangles (p3, p2, p1) and (p1, p4, p3) for the bilateral
 // input: edges and cross products in fp64 (exact edge differences of fp32 vertices; no
@@ -465,6 +493,18 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
   const int tx = threadIdx.x % kBilTQW, ty = threadIdx.x / kBilTQW;
   const int R0 = kQPT * ty + H, C = tx + T::LQ;  // pack position of the thread's quad 0
   mbar_wait(&bar, 0);
+  // tile origin: the box's centre value, or (rare, e.g. NaN there) the first finite one;
+  // every thread reads the same shared value, so the fallback branch is uniform
+  __shared__ int s_first;
+  float3 o;
+  {
+    const float* cp = (MODE == kNormalsCentBuf) ? cen_s + ((T::QH / 2) * T::QW + T::QW / 2) * 6
+                                                : pts_s + ((T::PH / 2) * T::PW + T::PW / 2) * 3;
+    o = make_float3(cp[0], cp[1], cp[2]);
+    if (!finite3f(o.x, o.y, o.z))
+      o = (MODE == kNormalsCentBuf) ? tile_origin<kBilNT>(cen_s, T::QW * T::QH * 2, 3, &s_first)
+                                    : tile_origin<kBilNT>(pts_s, T::PW * T::PH, 3, &s_first);
+  }
 
   // ---- pack every halo quad into the planes (scaled + sentinel-encoded)
   for (int q = threadIdx.x; q < T::NQ; q += kBilNT) {
@@ -474,19 +514,20 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
         n[j] = nrm_s[q * 6 + j];
-        cc[j] = cen_s[q * 6 + j] * sA;
+        cc[j] = (cen_s[q * 6 + j] - (j % 3 == 0 ? o.x : (j % 3 == 1 ? o.y : o.z))) * sA;
       }
     } else {
       const float* P1 = pts_s + (r * T::PW + c + T::PSHIFT) * 3;
       const float* P2 = P1 + 3;
       const float* P4 = P1 + T::PW * 3;
       const float* P3 = P4 + 3;
-      // triangles (p3, p2, p1) and (p1, p4, p3) share p1 + p3
+      // triangles (p3, p2, p1) and (p1, p4, p3) share p1 + p3; relative to the tile origin
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        const float s13 = P1[j] + P3[j];
-        cc[j] = (s13 + P2[j]) * sA3;
-        cc[3 + j] = (s13 + P4[j]) * sA3;
+        const float oj = j == 0 ? o.x : (j == 1 ? o.y : o.z);
+        const float s13 = (P1[j] - oj) + (P3[j] - oj);
+        cc[j] = (s13 + (P2[j] - oj)) * sA3;
+        cc[3 + j] = (s13 + (P4[j] - oj)) * sA3;
       }
       if (MODE == kFromPoints) {
         fc_normals_quad(P1, P2, P3, P4, n);
@@ -505,6 +546,14 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     pack_quad(P, q, n, cc, sB);
   }
   __syncthreads();
+  char* win = nullptr;
+  if (PACKOUT && threadIdx.x == 0) {  // the tile's centroid window, for iterations 2..B
+    win = a.cwin + (((long long)f * a.gy + blockIdx.y) * a.gx + blockIdx.x) * a.wstride;
+    fence_proxy_async_smem();
+    bulk_store(win, P.c0, T::NQ * 16);
+    bulk_store(win + T::NQ * 16, P.c1, T::NQ * 8);
+    tma_store_commit();
+  }
 
   static_assert(kQPT == 2, "bil_weigh handles 2 quads per thread");
   Quad2 qa, qb;
@@ -518,12 +567,11 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
       const int u = u0 + kQPT * ty + o, v = q0 + tx;
       if (u < Mq && v < Nq) {
         const Quad2& q = o == 0 ? qa : qb;
-        pg.c0[f * pg.f4 + (long long)u * pg.s4 + v] =
-            make_float4(f2lo(q.cx), f2hi(q.cx), f2lo(q.cy), f2hi(q.cy));
-        pg.c1[f * pg.f2s + (long long)u * pg.s2 + v] = make_float2(f2lo(q.cz), f2hi(q.cz));
         store_packed_n(pg, f, u, v, res[o], upd[o], q, sB);
       }
     }
+    if (threadIdx.x == 0) tma_store_wait_read();  // the window left shared memory
+    (void)win;
   } else {
 #pragma unroll
   for (int o = 0; o < kQPT; ++o) {
@@ -592,8 +640,9 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     fence_mbar_init();
     mbar_expect_tx(&bar, T::QW * T::QH * 48);
     const int x = q0 - T::LQ, y = u0 - H;
-    tma_load_3d(P.c0, &tc0, &bar, x * 4, y, f);
-    tma_load_3d(P.c1, &tc1, &bar, x * 2, y, f);
+    const char* win = a.cwin + (((long long)f * a.gy + blockIdx.y) * a.gx + blockIdx.x) * a.wstride;
+    bulk_load(P.c0, win, T::NQ * 16, &bar);
+    bulk_load(P.c1, win + T::NQ * 16, T::NQ * 8, &bar);
     tma_load_3d(P.n0, &tn0, &bar, x * 4, y, f);
     tma_load_3d(P.n1, &tn1, &bar, x * 2, y, f);
   }
@@ -750,6 +799,16 @@ int box_p(int h) { return ((((h + 3) / 4 * 4) + kBilTQW + h + 1 + 3) / 4) * 4; }
 
 }  // namespace
 
+// bytes of one tile's packed centroid window (C0 float4 + C1 float2 per box quad), 128-B rounded
+size_t centroid_window_bytes(int h) {
+  const int QW = box_q(h), QH = kBilTQH + 2 * h;
+  return ((size_t)QW * QH * 24 + 127) / 128 * 128;
+}
+size_t bilateral_buf_c_bytes(int F, int M, int N, int ksize) {
+  const size_t tiles = (size_t)((N - 1 + kBilTQW - 1) / kBilTQW) * ((M - 1 + kBilTQH - 1) / kBilTQH);
+  return (size_t)F * tiles * centroid_window_bytes(ksize / 2);
+}
+
 int bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
               const float* centroids_in, float sigma_length, float sigma_angle, int ksize,
               int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
@@ -819,6 +878,10 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   a.pts = pts;
   a.pitch = pitch;
   a.pts_fs = (long long)M * pitch;
+  a.gx = (Nq + kBilTQW - 1) / kBilTQW;
+  a.gy = (Mq + kBilTQH - 1) / kBilTQH;
+  a.wstride = (long long)centroid_window_bytes(h);
+  a.cwin = reinterpret_cast<char*>(buf_c);
 
   // Fused pipeline with >= 2 iterations and a third buffer: iteration 1 writes the packed
   // planes (centroids once into C, normals into A); iterations 2..B read them by TMA with
@@ -837,7 +900,7 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
       g.f2s = (long long)Mq * Nq2;
       return g;
     };
-    const PackedG gc = planes_of(buf_c), ga = planes_of(buf_a);
+    const PackedG ga = planes_of(buf_a);  // normals; centroids: per-tile windows in buf_c
     const PackedG gb = buf_b ? planes_of(buf_b) : ga;
     auto maps_of = [&](const PackedG& g, CUtensorMap* m4, CUtensorMap* m2) {
       int r = make_tmap_3d(m4, g.c0, false, 4ull * Nq, Mq, F, 4ull * Nq, 4ull * Mq * Nq,
@@ -846,19 +909,15 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
                                QW * 2, QH, true);
       return r;
     };
-    CUtensorMap mc[2], mna[2], mnb[2];
-    if ((rc = maps_of(gc, &mc[0], &mc[1])) || (rc = maps_of(ga, &mna[0], &mna[1])) ||
-        (rc = maps_of(gb, &mnb[0], &mnb[1])))
-      return rc;
-    PackedG out0 = ga;  // iteration 1: centroids -> C, normals -> A
-    out0.c0 = gc.c0;
-    out0.c1 = gc.c1;
-    if ((rc = launch_packout_h(h, m_pts, a, F, out0, st))) return rc;
+    CUtensorMap mna[2], mnb[2];
+    if ((rc = maps_of(ga, &mna[0], &mna[1])) || (rc = maps_of(gb, &mnb[0], &mnb[1]))) return rc;
+    // iteration 1: centroid windows -> buf_c, normals -> A
+    if ((rc = launch_packout_h(h, m_pts, a, F, ga, st))) return rc;
     for (int it = 1; it < iters; ++it) {
       const bool last = it == iters - 1;
       const bool from_a = (it % 2) == 1;
       const CUtensorMap* nin = from_a ? mna : mnb;
-      const CUtensorMap maps[4] = {mc[0], mc[1], nin[0], nin[1]};
+      const CUtensorMap maps[4] = {nin[0], nin[1], nin[0], nin[1]};  // [0], [1] unused
       if ((rc = launch_packed_h(h, last, maps, a, F, from_a ? gb : ga, st))) return rc;
     }
     return OK;

@@ -106,8 +106,10 @@ FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src
   off += (p->bilateral_iterations > 1) ? align256(fc_bytes) : 0;
   L.bil_b = off;
   off += (p->bilateral_iterations > 2) ? align256(fc_bytes) : 0;
-  L.bil_c = off;  // packed centroid planes of the fused bilateral (>= 2 iterations)
-  off += (p->bilateral_iterations > 1) ? align256(fc_bytes) : 0;
+  L.bil_c = off;  // packed centroid planes + tile origins of the fused bilateral (>= 2 it.)
+  off += (p->bilateral_iterations > 1)
+             ? align256(bilateral_buf_c_bytes(F, M, N, p->bilateral_kernel_size))
+             : 0;
   L.total = off + 256;
   return L;
 }

@@ -22,11 +22,15 @@ int triangulate(const uint32_t* vmask, int F, int M, int N, int64_t* trimap, int
 int halfedges_from_trimap(const int64_t* trimap, int M, int N, int64_t n_tri, int64_t* he,
                           cudaStream_t st);
 
+// fused-pipeline bilateral scratch `buf_c`: one packed centroid window (tile + halo, relative
+// to the tile's origin) per 32 x 8-quad tile
+size_t centroid_window_bytes(int h);
+size_t bilateral_buf_c_bytes(int F, int M, int N, int ksize);
 int bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
               const float* centroids_in, float sigma_length, float sigma_angle, int ksize,
               int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
               float* out_mesh, long long out_rows, cudaStream_t st,
-              float* buf_c = nullptr);  // fused pipeline: packed centroid planes (FC size)
+              float* buf_c = nullptr);  // fused pipeline: centroid windows (bilateral_buf_c_bytes)
 
 int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st);
 int triangle_normals(const void* pts, bool f64, const int64_t* tris, long long T, void* out,

@@ -1056,3 +1056,16 @@ def test_kernel_launch_count_matches_graph(fe, cfg):
             names.append(name.decode() if isinstance(name, bytes) else str(name))
     assert len(names) == eng.kernel_launches, names
     assert all("opcfe" in nm for nm in names), names
+
+
+@pytest.mark.parametrize("offset", [0.0, 50.0, 400.0])
+def test_bilateral_far_from_origin(fe, offset):
+    """A scene far from the coordinate origin with a small sigma_length: fp32 centroids
+    carry an absolute rounding ~|c| 2^-24, which tile-relative centroids keep out of the
+    weights (without them, 50 m at 13 mm spacing and sl = 2 cm broke 1e-5)."""
+    opc = fe.synthetic.room_scene(n=300, noise=0.002, seed=3)
+    opc = opc + np.array([offset, -0.5 * offset, 0.1 * offset])
+    lap = fe.LaplacianParams(1.0, 3, 2)
+    bil = fe.BilateralParams(0.02, 0.15, 3, 3)
+    _, res = _engine_run(fe, opc, lap, bil)
+    _per_stage_check(fe, opc, lap, bil, None, res)
