@@ -104,13 +104,15 @@ int opcfe_fc_data(const void* opc, int is_f64, int M, int N, void* centroids, vo
  *   pts != NULL, normals_in != NULL, centroids_in == NULL: continue filtering from the
  *     given FC normals (centroids from the grid): bilateral_iterate(.., k) followed by
  *     bilateral_iterate(.., m) equals bilateral_iterate(.., k + m) (_native.pyx:305);
- *   normals_in, centroids_in != NULL: FC arrays (padded rows) as given to
- *     _kernels.bilateral_iterate (_kernels/__init__.py:30).
+ *   normals_in, centroids_in != NULL: FC arrays as given to _kernels.bilateral_iterate
+ *     (_kernels/__init__.py:30): normals fp32 padded rows, centroids float64 contiguous
+ *     [F][M-1][N-1][2][3] (differences to a per-tile origin are taken in fp64, so the
+ *     centroid term keeps its precision far from the coordinate origin).
  * Output: out_mesh != NULL -> mesh order through trimap ([F][out_rows][3]);
  *         otherwise out_fc (FC layout, padded rows).
  * buf_a / buf_b: FC-sized ping-pong buffers (needed for iterations > 1 / > 2). */
 int opcfe_bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
-                    const float* centroids_in, float sigma_length, float sigma_angle,
+                    const double* centroids_in, float sigma_length, float sigma_angle,
                     int kernel_size, int iterations, float* buf_a, float* buf_b, float* out_fc,
                     const int64_t* trimap, float* out_mesh, long long out_rows,
                     opcfe_stream_t stream);

@@ -28,9 +28,8 @@ def bilateral_iterate(centroids, normals, sigma_length, sigma_angle, kernel_size
     Nn = Staged(normals)
     n = Nn.dev
     Mq, Nq = n.shape[:2]
-    c = C.dev.to(n.dtype)
     out = _ops.bilateral(1, Mq + 1, Nq + 1, sigma_length, sigma_angle, kernel_size, iterations,
-                         fc_normals=_ops.stage_fc(n), fc_centroids=_ops.stage_fc(c))
+                         fc_normals=_ops.stage_fc(n), fc_centroids=_ops.centroids_f64(C.dev))
     res = _ops.unstage_fc(out, 1, Mq, Nq, n.dtype, orig=n.unsqueeze(0).contiguous())[0]
     return Nn.give(res)
 

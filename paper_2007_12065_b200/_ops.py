@@ -143,6 +143,13 @@ def stage_fc(arr: torch.Tensor):
     return grid
 
 
+def centroids_f64(arr: torch.Tensor):
+    """(F?,Mq,Nq,2,3) -> contiguous float64 [F, Mq, Nq, 2, 3] (opcfe_bilateral's centroids)."""
+    if arr.dim() == 4:
+        arr = arr.unsqueeze(0)
+    return arr.to(torch.float64).contiguous()
+
+
 def unstage_fc(fc: torch.Tensor, F: int, Mq: int, Nq: int, dtype, orig=None):
     out = unstage(fc, F, Mq, 2 * Nq, dtype,
                   None if orig is None else orig.reshape(F, Mq, 2 * Nq, 3))

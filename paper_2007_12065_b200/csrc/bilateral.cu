@@ -110,7 +110,7 @@ template <int H, int MODE>
 constexpr int bil_smem_bytes() {
   using T = BilTile<H>;
   return (((MODE != kNormalsCentBuf) ? T::PTS_F : 0) + ((MODE != kFromPoints) ? T::FC_F : 0) +
-          ((MODE == kNormalsCentBuf) ? T::FC_F : 0) + T::PACK_F +
+          ((MODE == kNormalsCentBuf) ? 2 * T::FC_F : 0) + T::PACK_F +  // f64 centroid tile
           ((MODE == kFromPoints) ? T::OUT_F : 0)) *
              4 +
          kSmemSlack;
@@ -141,21 +141,25 @@ struct BilArgs {
 // need the SAME origin, so the fused pipeline's iteration 1 stores each tile's whole packed
 // centroid window (tile + halo, ~1.4x the quads) and later iterations bulk-load their own
 // window: no re-basing, and the values equal what a pack from the points computes.
-template <int NT>
-__device__ __forceinline__ float3 tile_origin(const float* v, int count, int stride, int* s_first) {
+template <int NT, typename S>
+__device__ __forceinline__ auto tile_origin(const S* v, int count, int stride, int* s_first) {
   if (threadIdx.x == 0) *s_first = 0x7fffffff;
   __syncthreads();
   for (int i = threadIdx.x; i < count; i += NT) {
-    const float* q = v + i * stride;
-    if (finite3f(q[0], q[1], q[2])) {
+    const S* q = v + i * stride;
+    if (isfinite(q[0]) && isfinite(q[1]) && isfinite(q[2])) {
       atomicMin(s_first, i);
       break;
     }
   }
   __syncthreads();
   const int i = *s_first;
-  return i == 0x7fffffff ? make_float3(0.f, 0.f, 0.f)
-                         : make_float3(v[i * stride], v[i * stride + 1], v[i * stride + 2]);
+  if constexpr (sizeof(S) == 8)
+    return i == 0x7fffffff ? make_double3(0.0, 0.0, 0.0)
+                           : make_double3(v[i * stride], v[i * stride + 1], v[i * stride + 2]);
+  else
+    return i == 0x7fffffff ? make_float3(0.f, 0.f, 0.f)
+                           : make_float3(v[i * stride], v[i * stride + 1], v[i * stride + 2]);
 }
 
 // FC normals of a quad's two triangles (p3, p2, p1) and (p1, p4, p3) for the bilateral
@@ -466,7 +470,8 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
   float* cen_s = nullptr;
   if (MODE != kNormalsCentBuf) { pts_s = p; p += T::PTS_F; }
   if (MODE != kFromPoints) { nrm_s = p; p += T::FC_F; }
-  if (MODE == kNormalsCentBuf) { cen_s = p; p += T::FC_F; }
+  if (MODE == kNormalsCentBuf) { cen_s = p; p += 2 * T::FC_F; }  // float64 centroid tile
+  const double* cen_d = reinterpret_cast<const double*>(cen_s);
   const Planes P = planes_at<H>(p);
   p += T::PACK_F;
   float* out_s = (MODE == kFromPoints) ? p : nrm_s;  // modes 1/2: aliases the FC tile
@@ -482,7 +487,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     uint32_t bytes = 0;
     if (MODE != kNormalsCentBuf) bytes += T::PW * 3 * T::PH * 4;
     if (MODE != kFromPoints) bytes += T::QW * 6 * T::QH * 4;
-    if (MODE == kNormalsCentBuf) bytes += T::QW * 6 * T::QH * 4;
+    if (MODE == kNormalsCentBuf) bytes += T::QW * 6 * T::QH * 8;
     mbar_expect_tx(&bar, bytes);
     if (MODE != kNormalsCentBuf) tma_load_3d(pts_s, &tpts, &bar, (q0 - T::LP) * 3, u0 - H, f);
     if (MODE != kFromPoints) tma_load_3d(nrm_s, &tnrm, &bar, (q0 - T::LQ) * 6, u0 - H, f);
@@ -497,13 +502,16 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
   // every thread reads the same shared value, so the fallback branch is uniform
   __shared__ int s_first;
   float3 o;
-  {
-    const float* cp = (MODE == kNormalsCentBuf) ? cen_s + ((T::QH / 2) * T::QW + T::QW / 2) * 6
-                                                : pts_s + ((T::PH / 2) * T::PW + T::PW / 2) * 3;
+  double3 od;  // MODE 2: float64 centroids, origin and differences in fp64
+  if constexpr (MODE == kNormalsCentBuf) {
+    const double* cp = cen_d + ((T::QH / 2) * T::QW + T::QW / 2) * 6;
+    od = make_double3(cp[0], cp[1], cp[2]);
+    if (!(isfinite(od.x) && isfinite(od.y) && isfinite(od.z)))
+      od = tile_origin<kBilNT>(cen_d, T::QW * T::QH * 2, 3, &s_first);
+  } else {
+    const float* cp = pts_s + ((T::PH / 2) * T::PW + T::PW / 2) * 3;
     o = make_float3(cp[0], cp[1], cp[2]);
-    if (!finite3f(o.x, o.y, o.z))
-      o = (MODE == kNormalsCentBuf) ? tile_origin<kBilNT>(cen_s, T::QW * T::QH * 2, 3, &s_first)
-                                    : tile_origin<kBilNT>(pts_s, T::PW * T::PH, 3, &s_first);
+    if (!finite3f(o.x, o.y, o.z)) o = tile_origin<kBilNT>(pts_s, T::PW * T::PH, 3, &s_first);
   }
 
   // ---- pack every halo quad into the planes (scaled + sentinel-encoded)
@@ -514,7 +522,8 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
 #pragma unroll
       for (int j = 0; j < 6; ++j) {
         n[j] = nrm_s[q * 6 + j];
-        cc[j] = (cen_s[q * 6 + j] - (j % 3 == 0 ? o.x : (j % 3 == 1 ? o.y : o.z))) * sA;
+        const double oj = j % 3 == 0 ? od.x : (j % 3 == 1 ? od.y : od.z);
+        cc[j] = (float)((cen_d[q * 6 + j] - oj) * (double)sA);
       }
     } else {
       const float* P1 = pts_s + (r * T::PW + c + T::PSHIFT) * 3;
@@ -810,7 +819,7 @@ size_t bilateral_buf_c_bytes(int F, int M, int N, int ksize) {
 }
 
 int bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
-              const float* centroids_in, float sigma_length, float sigma_angle, int ksize,
+              const double* centroids_in, float sigma_length, float sigma_angle, int ksize,
               int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
               float* out_mesh, long long out_rows, cudaStream_t st, float* buf_c) {
   if (F < 1 || M < 2 || N < 2 || iters < 1 || ksize < 3 || (ksize % 2) == 0)
@@ -847,7 +856,11 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
     return make_tmap_3d(m, b, false, 6ull * Nq, Mq, F, fcp, fc_fs, SW * 6, SH);
   };
   if (from_arrays) {
-    if ((rc = fc_load(&m_nin, normals_in)) || (rc = fc_load(&m_cin, centroids_in))) return rc;
+    if ((rc = fc_load(&m_nin, normals_in))) return rc;
+    // float64 centroids, contiguous [F][Mq][Nq][2][3] (rows of 6 Nq doubles: 16-B multiples)
+    if ((rc = make_tmap_3d(&m_cin, centroids_in, true, 6ull * Nq, Mq, F, 6ull * Nq,
+                           6ull * Nq * Mq, QW * 6, QH)))
+      return rc;
     m_pts = m_nin;
   } else {
     if ((rc = make_tmap_3d(&m_pts, pts, false, 3ull * N, M, F, pitch, (uint64_t)M * pitch,

@@ -174,7 +174,7 @@ int opcfe_fc_data(const void* opc, int is_f64, int M, int N, void* centroids, vo
 }
 
 int opcfe_bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
-                    const float* centroids_in, float sigma_length, float sigma_angle,
+                    const double* centroids_in, float sigma_length, float sigma_angle,
                     int kernel_size, int iterations, float* buf_a, float* buf_b, float* out_fc,
                     const int64_t* trimap, float* out_mesh, long long out_rows,
                     opcfe_stream_t stream) {

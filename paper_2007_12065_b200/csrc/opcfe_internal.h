@@ -27,7 +27,7 @@ int halfedges_from_trimap(const int64_t* trimap, int M, int N, int64_t n_tri, in
 size_t centroid_window_bytes(int h);
 size_t bilateral_buf_c_bytes(int F, int M, int N, int ksize);
 int bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
-              const float* centroids_in, float sigma_length, float sigma_angle, int ksize,
+              const double* centroids_in, float sigma_length, float sigma_angle, int ksize,
               int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
               float* out_mesh, long long out_rows, cudaStream_t st,
               float* buf_c = nullptr);  // fused pipeline: centroid windows (bilateral_buf_c_bytes)

@@ -109,7 +109,7 @@ def bilateral_filter_opc(opc, params: BilateralParams, trimap=None):
     n_out = int((tm >= 0).sum().item())
     out = _ops.bilateral(1, M, N, params.sigma_length, params.sigma_angle, params.kernel_size,
                          params.iterations, fc_normals=_ops.stage_fc(nrm),
-                         fc_centroids=_ops.stage_fc(cen), trimap=tm, out_rows=n_out)[0]
+                         fc_centroids=_ops.centroids_f64(cen), trimap=tm, out_rows=n_out)[0]
     return S.give(out.to(x.dtype))
 
 

@@ -1069,3 +1069,19 @@ def test_bilateral_far_from_origin(fe, offset):
     bil = fe.BilateralParams(0.02, 0.15, 3, 3)
     _, res = _engine_run(fe, opc, lap, bil)
     _per_stage_check(fe, opc, lap, bil, None, res)
+
+
+@pytest.mark.parametrize("offset", [0.0, 300.0])
+def test_drop_in_bilateral_far_from_origin(fe, offset):
+    """The float64 drop-in (_kernels.bilateral_iterate / bilateral_filter_opc) takes its
+    centroids in float64 and subtracts the tile origin in fp64, so a scene hundreds of
+    metres out keeps the 1e-5 contract at a small sigma_length."""
+    opc = fe.synthetic.room_scene(n=160, noise=0.002, seed=8) + np.array([offset, 0.3 * offset, 0.0])
+    bp = fe.BilateralParams(0.03, 0.2, 3, 2)
+    got = fe.bilateral_filter_opc(opc, bp)
+    ref = fo.bilateral_filter_opc(opc, bp.sigma_length, bp.sigma_angle, bp.kernel_size,
+                                  bp.iterations)
+    assert_normals_close(got, ref)
+    cen, nrm = fo.compute_fc_triangle_data(opc)
+    g1 = fe._kernels.bilateral_iterate(cen, nrm, 0.03, 0.2, 3, 1)
+    assert_normals_close(g1, fo.bilateral_iterate(cen, nrm, 0.03, 0.2, 3, 1))
