@@ -245,16 +245,22 @@ class FrontEnd:
 class HostPipeline:
     """End-to-end frames through host memory with copies overlapped across frames.
 
-    Two single-frame FrontEnd slots (each a CUDA graph) and three streams: frame i+1's
-    H2D and front end run while frame i's outputs stream back (D2H).  A frame's D2H is
-    sized by its own triangle count (one event wait per frame on the host), so exactly
-    the drop-in outputs travel: smoothed grid (fp32), trimap, triangles, halfedges
-    (int64) and normals (fp32), as mesh_from_opc + bilateral_filter_opc return them.
+    Two FrontEnd slots (each a CUDA graph over `frames_per_slot` frames) and three
+    streams: chunk i+1's H2D and front end run while chunk i's outputs stream back (D2H).
+    A frame's D2H is sized by its own triangle count (one event wait per chunk on the
+    host), so exactly the drop-in outputs travel: smoothed grid (fp32), trimap, triangles,
+    halfedges (int64) and normals (fp32), as mesh_from_opc + bilateral_filter_opc return
+    them.  Small frames go several to a slot (default: ~8 MB of input per slot), so the
+    per-chunk host wait and launch latency are amortised.
     """
 
     def __init__(self, M, N, laplacian=LaplacianParams(), bilateral=BilateralParams(),
-                 l_max=None, src_dtype=torch.float64, device=None):
-        self.slots = [FrontEnd(M, N, 1, laplacian=laplacian, bilateral=bilateral, l_max=l_max,
+                 l_max=None, src_dtype=torch.float64, device=None, frames_per_slot=None):
+        if frames_per_slot is None:
+            esz = torch.empty((), dtype=src_dtype).element_size()
+            frames_per_slot = max(1, min(16, (8 << 20) // (M * N * 3 * esz)))
+        self.k = k = int(frames_per_slot)
+        self.slots = [FrontEnd(M, N, k, laplacian=laplacian, bilateral=bilateral, l_max=l_max,
                                src_dtype=src_dtype, device=device, graph=True) for _ in range(2)]
         dev = self.slots[0].device
         self.M, self.N, self.G = M, N, self.slots[0].G
@@ -264,7 +270,7 @@ class HostPipeline:
         self.ev_h2d = [torch.cuda.Event() for _ in range(2)]
         self.ev_cmp = [torch.cuda.Event() for _ in range(2)]
         self.ev_d2h = [torch.cuda.Event() for _ in range(2)]
-        self.ntri_host = torch.empty((2,), dtype=torch.int64, pin_memory=True)
+        self.ntri_host = torch.empty((2, k), dtype=torch.int64, pin_memory=True)
         self._host = None
         self.kernel_launches = self.slots[0].kernel_launches
         for s in self.slots:   # capture both graphs up front
@@ -284,35 +290,42 @@ class HostPipeline:
             )
         return self._host
 
-    def _enqueue(self, src_host, i):
-        k = i % 2
-        eng = self.slots[k]
+    def _enqueue(self, src_host, c):
+        s = c % 2
+        eng = self.slots[s]
+        lo = c * self.k
+        n = min(self.k, src_host.shape[0] - lo)
         with torch.cuda.stream(self.s_h2d):
-            self.s_h2d.wait_event(self.ev_cmp[k])      # slot input consumed by frame i-2
-            eng.src.copy_(src_host[i:i + 1], non_blocking=True)
-            self.ev_h2d[k].record(self.s_h2d)
+            self.s_h2d.wait_event(self.ev_cmp[s])      # slot input consumed by chunk c-2
+            eng.src[:n].copy_(src_host[lo:lo + n], non_blocking=True)
+            self.ev_h2d[s].record(self.s_h2d)
         with torch.cuda.stream(self.s_cmp):
-            self.s_cmp.wait_event(self.ev_h2d[k])
-            self.s_cmp.wait_event(self.ev_d2h[k])      # slot outputs drained (frame i-2)
+            self.s_cmp.wait_event(self.ev_h2d[s])
+            self.s_cmp.wait_event(self.ev_d2h[s])      # slot outputs drained (chunk c-2)
             eng._graph.replay()
-            self.ntri_host[k].copy_(eng.n_tri[0], non_blocking=True)
-            self.ev_cmp[k].record(self.s_cmp)
+            self.ntri_host[s].copy_(eng.n_tri, non_blocking=True)
+            self.ev_cmp[s].record(self.s_cmp)
 
-    def _drain(self, H, i):
-        k = i % 2
-        eng = self.slots[k]
-        self.ev_cmp[k].synchronize()                    # n_tri of frame i is on the host
-        T = int(self.ntri_host[k])
+    def _drain(self, H, c, F):
+        s = c % 2
+        eng = self.slots[s]
+        lo = c * self.k
+        n = min(self.k, F - lo)
+        self.ev_cmp[s].synchronize()                    # the chunk's n_tri are on the host
+        nt = [int(t) for t in self.ntri_host[s, :n]]
+        b = 0
         with torch.cuda.stream(self.s_d2h):
-            self.s_d2h.wait_event(self.ev_cmp[k])
-            H["points"][i].copy_(eng.grid[0, :, :3 * self.N].unflatten(-1, (self.N, 3)),
-                                 non_blocking=True)
-            H["trimap"][i].copy_(eng.trimap[0], non_blocking=True)
-            H["triangles"][i, :T].copy_(eng.triangles[0, :T], non_blocking=True)
-            H["halfedges"][i, :3 * T].copy_(eng.halfedges[0, :3 * T], non_blocking=True)
-            H["normals"][i, :T].copy_(eng.normals[0, :T], non_blocking=True)
-            self.ev_d2h[k].record(self.s_d2h)
-        return T, (self.M * self.N * 12 + self.G * 8 + T * (24 + 24 + 12))
+            self.s_d2h.wait_event(self.ev_cmp[s])
+            H["points"][lo:lo + n].copy_(eng.grid[:n, :, :3 * self.N].unflatten(-1, (self.N, 3)),
+                                         non_blocking=True)
+            H["trimap"][lo:lo + n].copy_(eng.trimap[:n], non_blocking=True)
+            for j, T in enumerate(nt):
+                H["triangles"][lo + j, :T].copy_(eng.triangles[j, :T], non_blocking=True)
+                H["halfedges"][lo + j, :3 * T].copy_(eng.halfedges[j, :3 * T], non_blocking=True)
+                H["normals"][lo + j, :T].copy_(eng.normals[j, :T], non_blocking=True)
+                b += self.M * self.N * 12 + self.G * 8 + T * (24 + 24 + 12) + 8
+            self.ev_d2h[s].record(self.s_d2h)
+        return nt, b
 
     def run(self, src_host: torch.Tensor) -> FrontEndResult:
         """src_host: pinned (F, M, N, 3).  Returns pinned host outputs (valid until the next run)."""
@@ -320,14 +333,15 @@ class HostPipeline:
         H = self.host_outputs(F)
         for s in (self.s_h2d, self.s_cmp, self.s_d2h):
             s.wait_stream(torch.cuda.current_stream(self.slots[0].device))
+        chunks = (F + self.k - 1) // self.k
         nt, d2h = [], 0
         self._enqueue(src_host, 0)
-        for i in range(F):
-            if i + 1 < F:
-                self._enqueue(src_host, i + 1)
-            T, b = self._drain(H, i)
-            nt.append(T)
-            d2h += b + 8
+        for c in range(chunks):
+            if c + 1 < chunks:
+                self._enqueue(src_host, c + 1)
+            t, b = self._drain(H, c, F)
+            nt += t
+            d2h += b
         torch.cuda.current_stream(self.slots[0].device).wait_stream(self.s_d2h)
         self.h2d_bytes = src_host.numel() * src_host.element_size()
         self.d2h_bytes = d2h

@@ -626,17 +626,20 @@ def test_find_cells_large_vs_c_oracle(fe):
         assert got[i] in g["neighbors"][ref[i]]
 
 
-def test_host_pipeline_matches_device_engine(fe):
-    """HostPipeline (overlapped H2D / graph / D2H per frame) returns exactly what the
-    device engine computes, with D2H sized by each frame's triangle count."""
-    frames = fe.synthetic.config_c5_frames(3)[:, :90, :130]
+@pytest.mark.parametrize("per_slot", [None, 1, 2])
+def test_host_pipeline_matches_device_engine(fe, per_slot):
+    """HostPipeline (overlapped H2D / graph / D2H per chunk of frames) returns exactly what
+    the device engine computes, with D2H sized by each frame's triangle count -- one frame
+    per slot, two (a partial last chunk), and the default (all five in one slot)."""
+    frames = fe.synthetic.config_c5_frames(5)[:, :90, :130]
     lap, bil = fe.LaplacianParams(1.0, 3, 2), fe.BilateralParams(0.1, 0.15, 3, 2)
-    pipe = fe.HostPipeline(90, 130, laplacian=lap, bilateral=bil)
+    pipe = fe.HostPipeline(90, 130, laplacian=lap, bilateral=bil, frames_per_slot=per_slot)
     host = torch.from_numpy(frames).pin_memory()
     res = pipe.run(host)
+    res = pipe.run(host)                                 # reuse: slots and buffers recycled
     torch.cuda.synchronize()
-    _, ref = _engine_run(fe, frames, lap, bil, frames=3, dtype=torch.float64)
-    for f in range(3):
+    _, ref = _engine_run(fe, frames, lap, bil, frames=5, dtype=torch.float64)
+    for f in range(5):
         T = ref.n_tri[f]
         assert res.n_tri[f] == T
         assert teq(res.points[f], ref.points[f].cpu())
