@@ -406,9 +406,7 @@ __device__ __forceinline__ void bil_weigh(const Planes& P, int R0, int C, float 
 
 // the fused pipeline's packed FC arrays in global memory (per frame, row-major quads):
 // C0 / N0 float4 [Mq][Nq], C1 / N1 float2 [Mq][Nq2] (Nq2 = Nq rounded up to even)
-struct PackedG {
-  float4* c0;
-  float2* c1;
+struct PackedG {  // the packed normal planes N0 / N1 of the fused pipeline
   float4* n0;
   float2* n1;
   long long s4, s2;    // row strides in quads (Nq, Nq2)
@@ -555,9 +553,8 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     pack_quad(P, q, n, cc, sB);
   }
   __syncthreads();
-  char* win = nullptr;
   if (PACKOUT && threadIdx.x == 0) {  // the tile's centroid window, for iterations 2..B
-    win = a.cwin + (((long long)f * a.gy + blockIdx.y) * a.gx + blockIdx.x) * a.wstride;
+    char* win = a.cwin + (((long long)f * a.gy + blockIdx.y) * a.gx + blockIdx.x) * a.wstride;
     fence_proxy_async_smem();
     bulk_store(win, P.c0, T::NQ * 16);
     bulk_store(win + T::NQ * 16, P.c1, T::NQ * 8);
@@ -580,7 +577,6 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
       }
     }
     if (threadIdx.x == 0) tma_store_wait_read();  // the window left shared memory
-    (void)win;
   } else {
 #pragma unroll
   for (int o = 0; o < kQPT; ++o) {
@@ -903,10 +899,8 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
     const long long Nq2 = (Nq + 1) & ~1ll;
     auto planes_of = [&](float* b) {
       PackedG g;
-      g.c0 = reinterpret_cast<float4*>(b);
-      g.c1 = reinterpret_cast<float2*>(b + 4ll * F * Mq * Nq);
-      g.n0 = g.c0;
-      g.n1 = g.c1;
+      g.n0 = reinterpret_cast<float4*>(b);
+      g.n1 = reinterpret_cast<float2*>(b + 4ll * F * Mq * Nq);
       g.s4 = Nq;
       g.s2 = Nq2;
       g.f4 = (long long)Mq * Nq;
@@ -916,9 +910,9 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
     const PackedG ga = planes_of(buf_a);  // normals; centroids: per-tile windows in buf_c
     const PackedG gb = buf_b ? planes_of(buf_b) : ga;
     auto maps_of = [&](const PackedG& g, CUtensorMap* m4, CUtensorMap* m2) {
-      int r = make_tmap_3d(m4, g.c0, false, 4ull * Nq, Mq, F, 4ull * Nq, 4ull * Mq * Nq,
+      int r = make_tmap_3d(m4, g.n0, false, 4ull * Nq, Mq, F, 4ull * Nq, 4ull * Mq * Nq,
                            QW * 4, QH, true);
-      if (!r) r = make_tmap_3d(m2, g.c1, false, 2ull * Nq, Mq, F, 2ull * Nq2, 2ull * Mq * Nq2,
+      if (!r) r = make_tmap_3d(m2, g.n1, false, 2ull * Nq, Mq, F, 2ull * Nq2, 2ull * Mq * Nq2,
                                QW * 2, QH, true);
       return r;
     };
