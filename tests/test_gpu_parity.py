@@ -141,8 +141,11 @@ def test_acceptance05_random_grids(fe):
         check_twins(mesh.triangles, mesh.halfedges)
 
 
+# (3, 4099) / (5, 12003): rows of more than one 4096-quad scan segment of the row CTA
+# (triangulate.cu: carries between segments); (9000, 3): many 2-quad rows
 @pytest.mark.parametrize("shape", [(2, 1000), (1000, 2), (3, 3), (97, 33), (64, 1024),
-                                   (300, 257), (1080, 1920)])
+                                   (300, 257), (1080, 1920), (3, 4099), (5, 12003),
+                                   (9000, 3)])
 def test_topology_shapes(fe, shape):
     M, N = shape
     rng = np.random.default_rng(M * 7 + N)
@@ -1088,3 +1091,23 @@ def test_drop_in_bilateral_far_from_origin(fe, offset):
     cen, nrm = fo.compute_fc_triangle_data(opc)
     g1 = fe._kernels.bilateral_iterate(cen, nrm, 0.03, 0.2, 3, 1)
     assert_normals_close(g1, fo.bilateral_iterate(cen, nrm, 0.03, 0.2, 3, 1))
+
+
+@pytest.mark.parametrize("shape", [(6, 9001), (4100, 5)])
+def test_front_end_wide_and_tall(fe, shape):
+    """The fused front end on rows wider than one triangulation scan segment (4096 quads)
+    and on a tall 4-quad-wide grid (partial TMA boxes on every row), 2-frame batch,
+    per-stage against the oracle."""
+    M, N = shape
+    rng = np.random.default_rng(M + N)
+    frames = []
+    for _ in range(2):
+        opc = grid_opc(M, N) * 0.01
+        opc[..., 2] = rng.normal(0, 0.01, (M, N))
+        opc[rng.random((M, N)) < 0.1] = np.nan
+        frames.append(opc.astype(np.float32))
+    lap = fe.LaplacianParams(1.0, 3, 3)
+    bil = fe.BilateralParams(0.1, 0.15, 3, 2)
+    _, res = _engine_run(fe, np.stack(frames), lap, bil, 0.02, frames=2)
+    for f in range(2):
+        _per_stage_check(fe, frames[f], lap, bil, 0.02, _frame_view(res, f))
