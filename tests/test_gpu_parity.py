@@ -1111,3 +1111,21 @@ def test_front_end_wide_and_tall(fe, shape):
     _, res = _engine_run(fe, np.stack(frames), lap, bil, 0.02, frames=2)
     for f in range(2):
         _per_stage_check(fe, frames[f], lap, bil, 0.02, _frame_view(res, f))
+
+
+def test_front_end_many_frames(fe):
+    """A 300-frame batch of small distinct frames (C1-style batching): frame strides of
+    every stage, per-stage against the oracle on the first, last and 8 random frames."""
+    M, N, F = 20, 27, 300
+    rng = np.random.default_rng(300)
+    frames = []
+    for _ in range(F):
+        opc = grid_opc(M, N) * rng.uniform(0.005, 0.03)
+        opc[..., 2] = rng.normal(0, 0.01, (M, N))
+        opc[rng.random((M, N)) < rng.uniform(0, 0.3)] = np.nan
+        frames.append(opc.astype(np.float32))
+    lap = fe.LaplacianParams(0.8, 3, 2)
+    bil = fe.BilateralParams(0.05, 0.2, 3, 2)
+    _, res = _engine_run(fe, np.stack(frames), lap, bil, 0.03, frames=F)
+    for f in [0, F - 1] + [int(x) for x in rng.choice(np.arange(1, F - 1), 8, replace=False)]:
+        _per_stage_check(fe, frames[f], lap, bil, 0.03, _frame_view(res, f))
