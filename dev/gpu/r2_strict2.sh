@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests/test_gpu_strict.py -q --timeout 300 -p no:cacheprovider -s > gpurun_out/pytest_strict.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_strict.log
+grep -E "fast chain|FAILED|Error|passed|failed|rc=" gpurun_out/pytest_strict.log | tail -30

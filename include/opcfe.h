@@ -123,8 +123,6 @@ int opcfe_bilateral(const float* pts, int F, int M, int N, int pitch, const floa
 int opcfe_triangle_normals(const void* points, int is_f64, const int64_t* triangles,
                            long long n_tri, void* normals, opcfe_stream_t stream);
 
-/* Replaces the l_max half of segmentation.group_assignment (segmentation.py:59-67,73):
- * flag[t] = longest edge of triangle t > l_max (fp64 edge lengths). */
 /* Replaces _kernels.find_cells (_kernels/__init__.py:27 -> _native.pyx:120 /
  * _fallback.py:14-44) and, with counts != NULL, the bincount of
  * accumulator.integrate_normals (accumulator.py:157-173).  queries: n rows taken every
@@ -146,8 +144,43 @@ int opcfe_group_assignment(const void* normals, int is_f64, long long T, int F,
                            double ang_min, const uint8_t* lmax_flag, uint8_t* labels,
                            opcfe_stream_t stream);
 
+/* Replaces the l_max half of segmentation.group_assignment (segmentation.py:59-67,73):
+ * flag[t] = longest edge of triangle t > l_max (fp64 edge lengths). */
 int opcfe_max_edge_mask(const void* points, int is_f64, const int64_t* triangles,
                         long long n_tri, double l_max, uint8_t* flag, opcfe_stream_t stream);
+
+/* Compact (NON-reference) index output: int64 index rows -> int32.  Frame f's first
+ * n_rows[f] rows (all `rows` if n_rows == NULL) of `width` indices; strides in elements.
+ * The caller guarantees every value fits (grids with M*N and 6(M-1)(N-1) below 2^31). */
+int opcfe_narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int width,
+                         const int64_t* n_rows, long long src_frame_stride,
+                         long long dst_frame_stride, opcfe_stream_t stream);
+
+/* ---- strict precision: the reference's own fp64 arithmetic on its own layouts ----
+ * Grids (F, M, N, 3) and FC arrays (F, M-1, N-1, 2, 3) are contiguous float64; any odd
+ * kernel_size >= 3 (generic-window kernels).
+ *
+ * opcfe_laplacian_f64 replaces _kernels.laplacian_filter (_native.pyx:225-284,
+ * _fallback.py:82-117) BIT-EXACTLY: IEEE mul / add / sqrt / div in the reference's
+ * operation order (it is compiled with -ffp-contract=off, setup.py:24-26).  tmp: ping-pong
+ * buffer (iterations > 1); `in` must alias neither. */
+int opcfe_laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N,
+                        double lam, int kernel_size, int iterations, opcfe_stream_t stream);
+
+/* compute_fc_triangle_data (smoothing.py:61-88) of F frames, bit-exact. */
+int opcfe_fc_data_f64(const double* opc, int F, int M, int N, double* centroids, double* normals,
+                      opcfe_stream_t stream);
+
+/* Replaces _kernels.bilateral_iterate (_native.pyx:287-364, _fallback.py:120-166) on an
+ * (M-1) x (N-1) FC grid, and with trimap != NULL also bilateral_filter_opc's gather
+ * (smoothing.py:108-114: out_mesh[f][trimap[gid]] for trimap >= 0, out_rows rows per
+ * frame); otherwise out_fc.  Same arithmetic and accumulation order as the reference; exp()
+ * is CUDA's (<= 1 ulp, as the reference's two backends differ).  buf_a / buf_b: FC-sized
+ * ping-pong buffers (iterations > 1 / > 2). */
+int opcfe_bilateral_f64(const double* centroids, const double* normals, int F, int M, int N,
+                        double sigma_length, double sigma_angle, int kernel_size, int iterations,
+                        double* buf_a, double* buf_b, double* out_fc, const int64_t* trimap,
+                        double* out_mesh, long long out_rows, opcfe_stream_t stream);
 
 /* Region growing over twin edges.  n_tri < 2^31.
  * opcfe_grow_segment replaces _kernels.grow_segment (_native.pyx:170-222): the connected
@@ -175,18 +208,27 @@ int opcfe_segment_components(const int64_t* halfedges, const uint8_t* groups, lo
 typedef struct {
   int laplacian_iterations; /* 0 = no Laplacian */
   int laplacian_kernel_size;
-  float laplacian_lambda;
+  double laplacian_lambda;  /* double: the strict chain uses the caller's value as given */
   int bilateral_iterations; /* 0 = no bilateral: normals = triangle normals of the smoothed grid */
   int bilateral_kernel_size;
-  float sigma_length;
-  float sigma_angle;
+  double sigma_length;
+  double sigma_angle;
   double l_max; /* < 0: no l_max flag */
   /* group_assignment (segmentation.py:52-74) fused after the normals: device f64
    * [n_dominant][3] dominant normals, or NULL for no labels */
   const double* dominant_normals;
   int n_dominant;
   double ang_min;
+  /* OPCFE_PRECISION_FAST: fp32 kernels (+ the fp64 steps the 1e-5 contract needs);
+   * OPCFE_PRECISION_STRICT: the reference's fp64 chain (points / normals outputs are
+   * double: bit-exact Laplacian, FC data, topology; bilateral to <= a few ulp).
+   * Fast-precision stages whose kernel size exceeds the fp32 kernels (Laplacian > 17,
+   * bilateral > 9) run on the fp64 generic-window kernels, results rounded to fp32. */
+  int precision;
 } opcfe_front_end_params;
+
+#define OPCFE_PRECISION_FAST 0
+#define OPCFE_PRECISION_STRICT 1
 
 typedef struct {
   /* input: src_kind 0 = padded fp32 grid (src_pitch floats/row, frame stride M*src_pitch),
@@ -195,11 +237,12 @@ typedef struct {
   int src_kind;
   int src_pitch;
   /* outputs (device) */
-  float* points;      /* [F][M][pitch] smoothed grid, pitch = opcfe_points_pitch(N) */
+  void* points;       /* fast: float [F][M][pitch], pitch = opcfe_points_pitch(N);
+                         strict: double [F][M][N][3] */
   int64_t* trimap;    /* [F][G] */
   int64_t* triangles; /* [F][G][3] */
   int64_t* halfedges; /* [F][G][3] or NULL */
-  float* normals;     /* [F][G][3] or NULL */
+  void* normals;      /* [F][G][3] float (fast) / double (strict), or NULL */
   uint8_t* lmax_flag; /* [F][G] or NULL (needs l_max >= 0) */
   int64_t* n_tri;     /* [F] */
   uint8_t* labels;    /* [F][G] group labels (255 = unassigned) or NULL */

@@ -58,8 +58,12 @@ class Staged:
         self.is_f64 = self.dev.dtype == torch.float64
 
     def give(self, t: torch.Tensor):
-        """Return a device result in the caller's world (numpy host / torch device)."""
+        """Return a device result in the caller's world: NumPy callers get host arrays,
+        floating point as float64 like the reference (np.asarray(opc, dtype=float64),
+        smoothing.py:55); torch callers keep the device tensor."""
         if self.numpy:
+            if self.out_dtype is not None and t.is_floating_point():
+                t = t.to(self.out_dtype)
             return t.cpu().numpy()
         return t
 

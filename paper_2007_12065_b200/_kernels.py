@@ -23,11 +23,19 @@ def laplacian_filter(points, lam, kernel_size, iterations):
 
 
 def bilateral_iterate(centroids, normals, sigma_length, sigma_angle, kernel_size, iterations):
-    """Same contract as _kernels.bilateral_iterate (_native.pyx:287 / _fallback.py:120)."""
+    """Same contract as _kernels.bilateral_iterate (_native.pyx:287 / _fallback.py:120).
+
+    Precision as smoothing.resolve_precision (float64 normals: the reference's fp64
+    arithmetic by default)."""
+    from .smoothing import BILATERAL_MAX_K32, resolve_precision
     C = Staged(centroids)
     Nn = Staged(normals)
     n = Nn.dev
     Mq, Nq = n.shape[:2]
+    if resolve_precision(None, n.dtype) == "strict" or kernel_size > BILATERAL_MAX_K32:
+        out = _ops.bilateral_f64(C.dev.to(torch.float64), n.to(torch.float64), sigma_length,
+                                 sigma_angle, kernel_size, iterations)
+        return Nn.give(out.to(n.dtype))
     out = _ops.bilateral(1, Mq + 1, Nq + 1, sigma_length, sigma_angle, kernel_size, iterations,
                          fc_normals=_ops.stage_fc(n), fc_centroids=_ops.centroids_f64(C.dev))
     res = _ops.unstage_fc(out, 1, Mq, Nq, n.dtype, orig=n.unsqueeze(0).contiguous())[0]

@@ -31,7 +31,11 @@ EXPORTS = (
     "opcfe_triangle_normals", "opcfe_find_cells", "opcfe_group_assignment", "opcfe_max_edge_mask", "opcfe_front_end_workspace",
     "opcfe_front_end", "opcfe_front_end_profiled", "opcfe_segments_workspace",
     "opcfe_grow_segment", "opcfe_segment_components",
+    "opcfe_laplacian_f64", "opcfe_fc_data_f64", "opcfe_bilateral_f64", "opcfe_narrow_indices",
 )
+
+PRECISION_FAST = 0      # OPCFE_PRECISION_FAST
+PRECISION_STRICT = 1    # OPCFE_PRECISION_STRICT
 
 
 class FrontEndParams(ctypes.Structure):
@@ -39,15 +43,16 @@ class FrontEndParams(ctypes.Structure):
     _fields_ = [
         ("laplacian_iterations", ctypes.c_int),
         ("laplacian_kernel_size", ctypes.c_int),
-        ("laplacian_lambda", ctypes.c_float),
+        ("laplacian_lambda", ctypes.c_double),
         ("bilateral_iterations", ctypes.c_int),
         ("bilateral_kernel_size", ctypes.c_int),
-        ("sigma_length", ctypes.c_float),
-        ("sigma_angle", ctypes.c_float),
+        ("sigma_length", ctypes.c_double),
+        ("sigma_angle", ctypes.c_double),
         ("l_max", ctypes.c_double),
         ("dominant_normals", ctypes.c_void_p),
         ("n_dominant", ctypes.c_int),
         ("ang_min", ctypes.c_double),
+        ("precision", ctypes.c_int),
     ]
 
 
@@ -106,6 +111,10 @@ def _declare(L):
         "opcfe_segments_workspace": (sz, [ll]),
         "opcfe_grow_segment": (i, [vp, vp, vp, vp, vp, ll, ll, i, vp, vp, d, vp, vp, vp, sz, vp]),
         "opcfe_segment_components": (i, [vp, vp, ll, vp, vp, vp, sz, vp]),
+        "opcfe_narrow_indices": (i, [vp, vp, i, ll, i, vp, ll, ll, vp]),
+        "opcfe_laplacian_f64": (i, [vp, vp, vp, i, i, i, d, i, i, vp]),
+        "opcfe_fc_data_f64": (i, [vp, i, i, i, vp, vp, vp]),
+        "opcfe_bilateral_f64": (i, [vp, vp, i, i, i, d, d, i, i, vp, vp, vp, vp, vp, ll, vp]),
         "opcfe_front_end_workspace": (sz, [i, i, i, ctypes.POINTER(FrontEndParams), i, i]),
         "opcfe_front_end": (i, [i, i, i, ctypes.POINTER(FrontEndParams),
                                 ctypes.POINTER(FrontEndIO), vp, sz, vp]),

@@ -229,3 +229,64 @@ def segment_components(halfedges, groups, with_size: bool = True):
                                                    ws.numel(), stream()),
                "segment_components")
     return comp, size
+
+
+# ------------------------------------------------------------------ strict (fp64) kernels
+def laplacian_f64(x: torch.Tensor, lam: float, kernel_size: int, iterations: int,
+                  out: torch.Tensor | None = None):
+    """(F?, M, N, 3) float64 contiguous -> smoothed grid (same shape), the reference's own
+    fp64 arithmetic (opcfe_laplacian_f64: bit-exact), any odd kernel size."""
+    x = x.contiguous()
+    F, M, N = _frames(x)
+    out = torch.empty_like(x) if out is None else out
+    tmp = torch.empty_like(x) if iterations > 1 else None
+    _lib.check(_lib.lib().opcfe_laplacian_f64(x.data_ptr(), out.data_ptr(), ptr(tmp), F, M, N,
+                                              float(lam), int(kernel_size), int(iterations),
+                                              stream()),
+               "laplacian")
+    return out
+
+
+def fc_data_f64(x: torch.Tensor):
+    """(F?, M, N, 3) float64 -> centroids, normals (F?, M-1, N-1, 2, 3) float64 (bit-exact)."""
+    x = x.contiguous()
+    F, M, N = _frames(x)
+    shape = (M - 1, N - 1, 2, 3) if x.dim() == 3 else (F, M - 1, N - 1, 2, 3)
+    cen = torch.empty(shape, dtype=torch.float64, device=x.device)
+    nrm = torch.empty_like(cen)
+    _lib.check(_lib.lib().opcfe_fc_data_f64(x.data_ptr(), F, M, N, cen.data_ptr(), nrm.data_ptr(),
+                                            stream()),
+               "fc_data")
+    return cen, nrm
+
+
+def bilateral_f64(centroids: torch.Tensor, normals: torch.Tensor, sigma_length: float,
+                  sigma_angle: float, kernel_size: int, iterations: int, trimap=None,
+                  out_rows=None):
+    """FC arrays (F?, Mq, Nq, 2, 3) float64 -> filtered FC normals (same shape), or with
+    ``trimap`` ((F?, G) int64) the mesh-order normals (F?, out_rows, 3)
+    (opcfe_bilateral_f64: the reference's fp64 arithmetic, any odd kernel size)."""
+    batched = normals.dim() == 5
+    c = centroids.contiguous() if batched else centroids.contiguous().unsqueeze(0)
+    n = normals.contiguous() if batched else normals.contiguous().unsqueeze(0)
+    F, Mq, Nq = n.shape[:3]
+    buf_a = torch.empty_like(n) if iterations > 1 else None
+    buf_b = torch.empty_like(n) if iterations > 2 else None
+    out_fc = out_mesh = None
+    if trimap is not None:
+        out_mesh = torch.empty((F, int(out_rows), 3), dtype=torch.float64, device=n.device)
+        tm = trimap.reshape(F, -1).contiguous()
+        if tm.shape[1] != 2 * Mq * Nq:
+            from .geometry import DegenerateInputError
+            raise DegenerateInputError("trimap does not match the grid shape")
+    else:
+        out_fc = torch.empty_like(n)
+        tm = None
+    _lib.check(_lib.lib().opcfe_bilateral_f64(c.data_ptr(), n.data_ptr(), F, Mq + 1, Nq + 1,
+                                              float(sigma_length), float(sigma_angle),
+                                              int(kernel_size), int(iterations), ptr(buf_a),
+                                              ptr(buf_b), ptr(out_fc), ptr(tm), ptr(out_mesh),
+                                              int(out_rows or 0), stream()),
+               "bilateral")
+    res = out_mesh if trimap is not None else out_fc
+    return res if batched else res[0]

@@ -716,8 +716,9 @@ int launch_bil(const CUtensorMap& tp, const CUtensorMap& tn, const CUtensorMap& 
                const CUtensorMap& to, const BilArgs& a, int F, cudaStream_t st,
                const PackedG& pg = PackedG{}) {
   constexpr int smem = bil_smem_bytes<H, MODE>();
-  static unsigned long long attr_mask = 0;
-  ensure_smem_attr(bilateral_kernel<H, MODE, SCATTER, PACKOUT>, smem, attr_mask);
+  static std::atomic<unsigned long long> attr_mask{0};
+  if (const int rc = ensure_smem_attr(bilateral_kernel<H, MODE, SCATTER, PACKOUT>, smem, attr_mask))
+    return rc;
   const int Mq = a.M - 1, Nq = a.N - 1;
   dim3 grid((Nq + kBilTQW - 1) / kBilTQW, (Mq + kBilTQH - 1) / kBilTQH, F);
   bilateral_kernel<H, MODE, SCATTER, PACKOUT><<<grid, kBilNT, smem, st>>>(tp, tn, tc, to, a, pg);
@@ -729,8 +730,9 @@ int launch_packed(const CUtensorMap* maps, const BilArgs& a, int F, const Packed
                   cudaStream_t st) {
   using T = BilTile<H>;
   constexpr int smem = T::PACK_F * 4 + kSmemSlack;
-  static unsigned long long attr_mask = 0;
-  ensure_smem_attr(bilateral_packed_kernel<H, SCATTER>, smem, attr_mask);
+  static std::atomic<unsigned long long> attr_mask{0};
+  if (const int rc = ensure_smem_attr(bilateral_packed_kernel<H, SCATTER>, smem, attr_mask))
+    return rc;
   const int Mq = a.M - 1, Nq = a.N - 1;
   dim3 grid((Nq + kBilTQW - 1) / kBilTQW, (Mq + kBilTQH - 1) / kBilTQH, F);
   bilateral_packed_kernel<H, SCATTER><<<grid, kBilNT, smem, st>>>(maps[0], maps[1], maps[2],

@@ -78,6 +78,9 @@ struct FeLayout {
   size_t vmask = 0, status = 0, staged = 0, lap_tmp = 0, bil_a = 0, bil_b = 0, bil_c = 0,
          total = 0;
   size_t vmask_b = 0, status_b = 0, staged_b = 0, lap_b = 0, bil_b_bytes = 0;
+  // fp64 stages (strict precision, or kernel sizes beyond the fp32 kernels)
+  bool strict = false, lap64 = false, bil64 = false;
+  size_t g64_in = 0, g64_tmp = 0, g64_out = 0, fc_c = 0, fc_n = 0, fc_a = 0, fc_b = 0;
 };
 
 FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src_kind,
@@ -86,30 +89,44 @@ FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src
   const int pitch = points_pitch(N);
   const size_t grid_bytes = (size_t)F * M * pitch * sizeof(float);
   const size_t fc_bytes = (size_t)F * (M - 1) * fc_pitch(N) * sizeof(float);
+  const size_t g64 = (size_t)F * M * N * 3 * sizeof(double);
+  const size_t fc64 = (size_t)F * (M - 1) * (N - 1) * 6 * sizeof(double);
+  const bool lap = p->laplacian_iterations > 0;
+  const bool bil = p->bilateral_iterations > 0;
+  L.strict = p->precision == OPCFE_PRECISION_STRICT;
+  L.lap64 = lap && (L.strict || p->laplacian_kernel_size > kLapMaxK32);
+  L.bil64 = bil && (L.strict || p->bilateral_kernel_size > kBilMaxK32);
   L.vmask_b = (size_t)F * M * ((N + 31) / 32) * sizeof(uint32_t);
   L.status_b = triangulate_workspace_bytes(F, M);
-  const bool lap = p->laplacian_iterations > 0;
-  const bool need_stage = lap && !(src_kind == 0 && src_pitch == pitch);
+  const bool need_stage = lap && !L.lap64 && !(src_kind == 0 && src_pitch == pitch);
   L.staged_b = need_stage ? grid_bytes : 0;
-  L.lap_b = (lap && p->laplacian_iterations > 1) ? grid_bytes : 0;
+  L.lap_b = (lap && !L.lap64 && p->laplacian_iterations > 1) ? grid_bytes : 0;
   L.bil_b_bytes = fc_bytes;
+  const bool bil32 = bil && !L.bil64;
   size_t off = 0;
-  L.vmask = off;
-  off += align256(L.vmask_b);
-  L.status = off;
-  off += align256(L.status_b);
-  L.staged = off;
-  off += align256(L.staged_b);
-  L.lap_tmp = off;
-  off += align256(L.lap_b);
-  L.bil_a = off;
-  off += (p->bilateral_iterations > 1) ? align256(fc_bytes) : 0;
-  L.bil_b = off;
-  off += (p->bilateral_iterations > 2) ? align256(fc_bytes) : 0;
-  L.bil_c = off;  // packed centroid planes + tile origins of the fused bilateral (>= 2 it.)
-  off += (p->bilateral_iterations > 1)
-             ? align256(bilateral_buf_c_bytes(F, M, N, p->bilateral_kernel_size))
-             : 0;
+  auto take = [&](size_t& at, size_t bytes) {
+    at = off;
+    off += align256(bytes);
+  };
+  take(L.vmask, L.vmask_b);
+  take(L.status, L.status_b);
+  take(L.staged, L.staged_b);
+  take(L.lap_tmp, L.lap_b);
+  take(L.bil_a, (bil32 && p->bilateral_iterations > 1) ? fc_bytes : 0);
+  take(L.bil_b, (bil32 && p->bilateral_iterations > 2) ? fc_bytes : 0);
+  // packed centroid planes + tile origins of the fused bilateral (>= 2 it.)
+  take(L.bil_c, (bil32 && p->bilateral_iterations > 1)
+                    ? bilateral_buf_c_bytes(F, M, N, p->bilateral_kernel_size)
+                    : 0);
+  // fp64 grids: the source as f64 (unless it is f64 already), the Laplacian ping-pong,
+  // and (fast precision) the f64 smoothed grid the fp64 stages read
+  take(L.g64_in, ((L.strict || L.lap64) && src_kind != 2) ? g64 : 0);
+  take(L.g64_tmp, (L.lap64 && p->laplacian_iterations > 1) ? g64 : 0);
+  take(L.g64_out, (!L.strict && (L.lap64 || L.bil64)) ? g64 : 0);
+  take(L.fc_c, L.bil64 ? fc64 : 0);
+  take(L.fc_n, L.bil64 ? fc64 : 0);
+  take(L.fc_a, (L.bil64 && p->bilateral_iterations > 1) ? fc64 : 0);
+  take(L.fc_b, (L.bil64 && p->bilateral_iterations > 2) ? fc64 : 0);
   L.total = off + 256;
   return L;
 }
@@ -230,6 +247,34 @@ int opcfe_segment_components(const int64_t* halfedges, const uint8_t* groups, lo
   return segment_components(halfedges, groups, n_tri, component, size, ws, ws_bytes, S(stream));
 }
 
+int opcfe_narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int width,
+                         const int64_t* n_rows, long long src_frame_stride,
+                         long long dst_frame_stride, opcfe_stream_t stream) {
+  return narrow_indices(src, dst, F, rows, width, n_rows, src_frame_stride, dst_frame_stride,
+                        S(stream));
+}
+
+int opcfe_laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N,
+                        double lam, int kernel_size, int iterations, opcfe_stream_t stream) {
+  return laplacian_f64(in, out, tmp, F, M, N, lam, kernel_size, iterations, S(stream));
+}
+
+int opcfe_fc_data_f64(const double* opc, int F, int M, int N, double* centroids, double* normals,
+                      opcfe_stream_t stream) {
+  if (!opc || !centroids || !normals) return fail(ERR_INVALID, "fc_data_f64: null buffer");
+  return fc_data_f64(opc, F, M, N, centroids, normals, S(stream));
+}
+
+int opcfe_bilateral_f64(const double* centroids, const double* normals, int F, int M, int N,
+                        double sigma_length, double sigma_angle, int kernel_size, int iterations,
+                        double* buf_a, double* buf_b, double* out_fc, const int64_t* trimap,
+                        double* out_mesh, long long out_rows, opcfe_stream_t stream) {
+  if (M < 2 || N < 2) return fail(ERR_INVALID, "organized cloud must be at least 2 x 2");
+  return bilateral_f64(centroids, normals, F, M - 1, N - 1, sigma_length, sigma_angle,
+                       kernel_size, iterations, buf_a, buf_b, out_fc, trimap, out_mesh, false,
+                       out_rows, S(stream));
+}
+
 size_t opcfe_front_end_workspace(int F, int M, int N, const opcfe_front_end_params* p,
                                  int src_kind, int src_pitch) {
   if (!p || F < 1 || M < 2 || N < 2) return 0;
@@ -246,6 +291,11 @@ inline void mark(void* const* ev, int i, cudaStream_t st) {
 
 // ev (optional): 5 cudaEvent_t recorded at stage boundaries
 //   [0] start  [1] after stage-in  [2] after Laplacian  [3] after triangulation  [4] end
+//
+// Precision: OPCFE_PRECISION_FAST runs the fp32 kernels (fp64 where the contract needs it);
+// OPCFE_PRECISION_STRICT runs the reference's own fp64 arithmetic end to end (points and
+// normals outputs are then double).  A fast-precision stage whose kernel size is beyond the
+// fp32 kernels' compiled set runs on the fp64 generic-window kernels (results converted).
 int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
                    const opcfe_front_end_io* io, void* ws, size_t ws_bytes,
                    opcfe_stream_t stream, void* const* ev) {
@@ -257,6 +307,8 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   if (io->src_kind == 0 && (io->src_pitch < 3 * N || io->src_pitch % 4))
     return fail(ERR_INVALID, "front_end: src_pitch must be >= 3N and a multiple of 4");
   if (io->lmax_flag && p->l_max < 0) return fail(ERR_INVALID, "front_end: lmax_flag needs l_max");
+  if (p->precision != OPCFE_PRECISION_FAST && p->precision != OPCFE_PRECISION_STRICT)
+    return fail(ERR_INVALID, "front_end: bad precision");
   const int pitch = points_pitch(N);
   const FeLayout L = fe_layout(F, M, N, p, io->src_kind, io->src_pitch);
   if (!ws || ws_bytes < L.total) return fail(ERR_WORKSPACE, "front_end: workspace too small");
@@ -268,14 +320,52 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   float* bil_a = reinterpret_cast<float*>(base + L.bil_a);
   float* bil_b = reinterpret_cast<float*>(base + L.bil_b);
   float* bil_c = reinterpret_cast<float*>(base + L.bil_c);
+  double* g64_in = reinterpret_cast<double*>(base + L.g64_in);
+  double* g64_tmp = reinterpret_cast<double*>(base + L.g64_tmp);
+  double* g64_out = reinterpret_cast<double*>(base + L.g64_out);
   const cudaStream_t st = S(stream);
   const bool f64 = io->src_kind == 2;
   const long long rs = io->src_kind == 0 ? io->src_pitch : 3ll * N;
   const long long fs = (long long)M * rs;
+  const long long G = 2ll * (M - 1) * (N - 1);
+  const bool lap = p->laplacian_iterations > 0;
   int rc;
   mark(ev, 0, st);
+  // the source as contiguous f64 (fp64 Laplacian input / strict points)
+  const double* src64 = f64 ? static_cast<const double*>(io->src) : nullptr;
+  if (!f64 && (L.strict || L.lap64)) {
+    if ((rc = unstage(static_cast<const float*>(io->src), (int)rs, F, M, N, g64_in, true, nullptr,
+                      st)))
+      return rc;
+    src64 = g64_in;
+  }
   // 1. Laplacian (smoothing.laplacian_filter_opc, pipeline.py:127-129)
-  if (p->laplacian_iterations > 0) {
+  // points64: the smoothed grid as f64 for the fp64 stages (strict: the output itself)
+  double* points64 = L.strict ? static_cast<double*>(io->points) : nullptr;
+  if (L.strict) {
+    mark(ev, 1, st);
+    if (lap) {
+      if ((rc = laplacian_f64(src64, points64, g64_tmp, F, M, N, p->laplacian_lambda,
+                              p->laplacian_kernel_size, p->laplacian_iterations, st)))
+        return rc;
+    } else if (src64 != points64) {
+      if (cudaMemcpyAsync(points64, src64, (size_t)F * M * N * 3 * sizeof(double),
+                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return check_launch("front_end: copy");
+    }
+    // validity bits of the smoothed grid (the NaN mask is iteration-invariant)
+    if ((rc = stage_in(points64, true, 3ll * N, 3ll * N * M, F, M, N, nullptr, pitch, vmask, st)))
+      return rc;
+  } else if (L.lap64) {
+    mark(ev, 1, st);
+    if ((rc = laplacian_f64(src64, g64_out, g64_tmp, F, M, N, p->laplacian_lambda,
+                            p->laplacian_kernel_size, p->laplacian_iterations, st)))
+      return rc;
+    points64 = g64_out;
+    if ((rc = stage_in(g64_out, true, 3ll * N, 3ll * N * M, F, M, N,
+                       static_cast<float*>(io->points), pitch, vmask, st)))
+      return rc;
+  } else if (lap) {
     const float* lin;
     uint32_t* lap_vmask;
     if (L.staged_b == 0) {
@@ -287,36 +377,62 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
       lap_vmask = nullptr;
     }
     mark(ev, 1, st);
-    rc = laplacian(lin, io->points, lap_tmp, lap_vmask, F, M, N, pitch, p->laplacian_lambda,
-                   p->laplacian_kernel_size, p->laplacian_iterations, st);
+    rc = laplacian(lin, static_cast<float*>(io->points), lap_tmp, lap_vmask, F, M, N, pitch,
+                   (float)p->laplacian_lambda, p->laplacian_kernel_size, p->laplacian_iterations, st);
     if (rc) return rc;
   } else {
-    if ((rc = stage_in(io->src, f64, rs, fs, F, M, N, io->points, pitch, vmask, st))) return rc;
+    if ((rc = stage_in(io->src, f64, rs, fs, F, M, N, static_cast<float*>(io->points), pitch,
+                       vmask, st)))
+      return rc;
     mark(ev, 1, st);
   }
   mark(ev, 2, st);
-  // 2. mesh_from_opc (pipeline.py:130-131): triangles + trimap + twins [+ normals]
+  // 2. mesh_from_opc (pipeline.py:130-131): triangles + trimap + twins [+ normals, flags]
   const bool bil = p->bilateral_iterations > 0 && io->normals != nullptr;
-  rc = triangulate(vmask, F, M, N, io->trimap, io->triangles, io->halfedges, io->n_tri, io->points,
-                   pitch, bil ? nullptr : io->normals, p->l_max, io->lmax_flag, status, L.status_b,
-                   st);
+  const bool extras32 = !L.strict;  // fp32 grid: normals / flags fused with the triangulation
+  rc = triangulate(vmask, F, M, N, io->trimap, io->triangles, io->halfedges, io->n_tri,
+                   extras32 ? static_cast<const float*>(io->points) : nullptr, pitch,
+                   (extras32 && !bil) ? static_cast<float*>(io->normals) : nullptr, p->l_max,
+                   extras32 ? io->lmax_flag : nullptr, status, L.status_b, st);
   if (rc) return rc;
+  if (L.strict && (io->lmax_flag || (!bil && io->normals))) {
+    rc = tri_extras_f64(points64, F, M, N, io->triangles, io->n_tri, bil ? nullptr : io->normals,
+                        false, p->l_max, io->lmax_flag, st);
+    if (rc) return rc;
+  }
   mark(ev, 3, st);
   // 3. bilateral_filter_opc (pipeline.py:132-134), scattered to mesh order via trimap
-  if (bil) {
-    rc = bilateral(io->points, F, M, N, pitch, nullptr, nullptr, p->sigma_length, p->sigma_angle,
-                   p->bilateral_kernel_size, p->bilateral_iterations,
-                   p->bilateral_iterations > 1 ? bil_a : nullptr,
-                   p->bilateral_iterations > 2 ? bil_b : nullptr, nullptr, io->trimap, io->normals,
-                   2ll * (M - 1) * (N - 1), st, p->bilateral_iterations > 1 ? bil_c : nullptr);
+  if (bil && L.bil64) {
+    if (!points64) {  // fast precision, fp32 grid: its exact f64 image
+      if ((rc = unstage(static_cast<const float*>(io->points), pitch, F, M, N, g64_out, true,
+                        nullptr, st)))
+        return rc;
+      points64 = g64_out;
+    }
+    double* fc_c = reinterpret_cast<double*>(base + L.fc_c);
+    double* fc_n = reinterpret_cast<double*>(base + L.fc_n);
+    if ((rc = fc_data_f64(points64, F, M, N, fc_c, fc_n, st))) return rc;
+    rc = bilateral_f64(fc_c, fc_n, F, M - 1, N - 1, p->sigma_length,
+                       p->sigma_angle, p->bilateral_kernel_size, p->bilateral_iterations,
+                       reinterpret_cast<double*>(base + L.fc_a),
+                       reinterpret_cast<double*>(base + L.fc_b), nullptr, io->trimap, io->normals,
+                       !L.strict, G, st);
+    if (rc) return rc;
+  } else if (bil) {
+    rc = bilateral(static_cast<const float*>(io->points), F, M, N, pitch, nullptr, nullptr,
+                   (float)p->sigma_length, (float)p->sigma_angle, p->bilateral_kernel_size,
+                   p->bilateral_iterations, p->bilateral_iterations > 1 ? bil_a : nullptr,
+                   p->bilateral_iterations > 2 ? bil_b : nullptr, nullptr, io->trimap,
+                   static_cast<float*>(io->normals), G, st,
+                   p->bilateral_iterations > 1 ? bil_c : nullptr);
     if (rc) return rc;
   }
   // 4. group labels (segmentation.group_assignment) on the final normals
   if (p->dominant_normals && io->labels) {
     if (!io->normals) return fail(ERR_INVALID, "front_end: labels need normals");
-    rc = group_assignment(io->normals, false, 2ll * (M - 1) * (N - 1), F, io->n_tri,
-                          p->dominant_normals, p->n_dominant, p->ang_min,
-                          p->l_max >= 0 ? io->lmax_flag : nullptr, io->labels, st);
+    rc = group_assignment(io->normals, L.strict, G, F, io->n_tri, p->dominant_normals,
+                          p->n_dominant, p->ang_min, p->l_max >= 0 ? io->lmax_flag : nullptr,
+                          io->labels, st);
     if (rc) return rc;
   }
   mark(ev, 4, st);

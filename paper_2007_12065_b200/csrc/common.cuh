@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cmath>
 #include <string>
 
@@ -60,16 +61,22 @@ int make_tmap_3d(CUtensorMap* map, const void* base, bool f64, uint64_t cols, ui
                  uint64_t frames, uint64_t row_pitch_elems, uint64_t frame_stride_elems,
                  uint32_t box_cols, uint32_t box_rows, bool zero_fill = false);
 
-// Opt a kernel into `smem` bytes of dynamic shared memory on the CURRENT device, once per
-// device (the attribute is per device context; `mask` is the caller's per-kernel bitset).
+// Opt a kernel into `smem` bytes of dynamic shared memory on the CURRENT device.  The
+// attribute is per device context; `mask` (one per kernel) remembers the devices already
+// done (ids >= 64 set it on every call).  Returns OK or the CUDA error via fail().
 template <typename Kernel>
-inline void ensure_smem_attr(Kernel kernel, int smem, unsigned long long& mask) {
+inline int ensure_smem_attr(Kernel kernel, int smem, std::atomic<unsigned long long>& mask) {
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64 && !((mask >> dev) & 1ull)) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    mask |= 1ull << dev;
-  }
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(ERR_CUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+  const unsigned long long bit = dev < 64 ? (1ull << dev) : 0ull;
+  if (bit && (mask.load(std::memory_order_acquire) & bit)) return OK;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess)
+    return fail(ERR_CUDA, std::string("cudaFuncSetAttribute(MaxDynamicSharedMemorySize): ") +
+                              cudaGetErrorString(e));
+  if (bit) mask.fetch_or(bit, std::memory_order_acq_rel);
+  return OK;
 }
 
 // ------------------------------------------------------------- device helpers

@@ -164,9 +164,44 @@ __global__ void group_assign_kernel(const S* __restrict__ normals, long long T, 
   labels[row] = lab;
 }
 
+// int64 index arrays -> int32 (the compact, non-reference output mode): frame f's first
+// n_rows[f] rows (all `rows` when n_rows is NULL) of `width` indices each.  Values are
+// < 2^31 by the caller's check; -1 stays -1.  Streaming: 8 B in, 4 B out per index.
+__global__ void narrow_indices_kernel(const int64_t* __restrict__ src, int32_t* __restrict__ dst,
+                                      long long rows, int width, const int64_t* __restrict__ n_rows,
+                                      long long src_fs, long long dst_fs) {
+  const int f = blockIdx.y;
+  const long long n = (n_rows ? n_rows[f] : rows) * width;
+  const int64_t* s = src + f * src_fs;
+  int32_t* d = dst + f * dst_fs;
+  for (long long i = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x); i < n;
+       i += 2ll * gridDim.x * blockDim.x) {
+    const bool vec = reinterpret_cast<uintptr_t>(s + i) % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(d + i) % 8 == 0;
+    if (i + 1 < n && vec) {
+      const longlong2 x = *reinterpret_cast<const longlong2*>(s + i);
+      *reinterpret_cast<int2*>(d + i) = make_int2((int)x.x, (int)x.y);
+    } else {
+      d[i] = (int32_t)s[i];
+      if (i + 1 < n) d[i + 1] = (int32_t)s[i + 1];
+    }
+  }
+}
+
 inline unsigned blocks_for(long long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
 }  // namespace
+
+int narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int width,
+                   const int64_t* n_rows, long long src_fs, long long dst_fs, cudaStream_t st) {
+  if (F < 1 || rows < 0 || width < 1 || !src || !dst)
+    return fail(ERR_INVALID, "narrow_indices: bad arguments");
+  if (rows == 0) return OK;
+  const long long n = rows * width;
+  dim3 grid((unsigned)std::min<long long>(blocks_for((n + 1) / 2, 256), 148 * 8), F);
+  narrow_indices_kernel<<<grid, 256, 0, st>>>(src, dst, rows, width, n_rows, src_fs, dst_fs);
+  return check_launch("narrow_indices_kernel");
+}
 
 int stage_in(const void* src, bool f64, long long rs, long long fs, int F, int M, int N,
              float* dst, int pitch, uint32_t* vmask, cudaStream_t st) {

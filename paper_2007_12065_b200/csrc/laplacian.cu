@@ -548,13 +548,14 @@ int run_k3(const float* in, float* out, float* tmp, uint32_t* vmask, int F, int 
     if ((rc = make_tmap_3d(&ld_tmp, tmp, false, 3ull * N, M, F, pitch, fs, kL3BW * 3, kL3BH))) return rc;
     if ((rc = make_tmap_3d(&st_tmp, tmp, false, 3ull * N, M, F, pitch, fs, kL3TW * 3, kL3TH))) return rc;
   }
-  static unsigned long long attr_mask[6] = {0, 0, 0, 0, 0, 0};
-  ensure_smem_attr(laplacian3_kernel<false, false>, kL3Smem, attr_mask[0]);
-  ensure_smem_attr(laplacian3_kernel<true, false>, kL3Smem, attr_mask[1]);
-  ensure_smem_attr(laplacian3_kernel<false, true>, kL3Smem, attr_mask[2]);
-  ensure_smem_attr(laplacian3_kernel<true, true>, kL3Smem, attr_mask[3]);
-  ensure_smem_attr(laplacian3p_kernel<false>, kL3Smem, attr_mask[4]);
-  ensure_smem_attr(laplacian3p_kernel<true>, kL3Smem, attr_mask[5]);
+  static std::atomic<unsigned long long> attr_mask[6];
+  if ((rc = ensure_smem_attr(laplacian3_kernel<false, false>, kL3Smem, attr_mask[0])) ||
+      (rc = ensure_smem_attr(laplacian3_kernel<true, false>, kL3Smem, attr_mask[1])) ||
+      (rc = ensure_smem_attr(laplacian3_kernel<false, true>, kL3Smem, attr_mask[2])) ||
+      (rc = ensure_smem_attr(laplacian3_kernel<true, true>, kL3Smem, attr_mask[3])) ||
+      (rc = ensure_smem_attr(laplacian3p_kernel<false>, kL3Smem, attr_mask[4])) ||
+      (rc = ensure_smem_attr(laplacian3p_kernel<true>, kL3Smem, attr_mask[5])))
+    return rc;
   const int wpr = (N + 31) / 32;
   const long long vm_fs = (long long)M * wpr;
   dim3 grid((N + kL3TW - 1) / kL3TW, (M + kL3TH - 1) / kL3TH, F);
@@ -588,8 +589,8 @@ template <int H>
 int launch_one(const CUtensorMap& tin, const CUtensorMap& tout, uint32_t* vmask, long long vm_fs,
                int wpr, int F, int M, int N, float lam, cudaStream_t st) {
   using T = LapTile<H>;
-  static unsigned long long attr_mask = 0;
-  ensure_smem_attr(laplacian_kernel<H>, T::SMEM, attr_mask);
+  static std::atomic<unsigned long long> attr_mask{0};
+  if (const int rc = ensure_smem_attr(laplacian_kernel<H>, T::SMEM, attr_mask)) return rc;
   dim3 grid((N + kLapTW - 1) / kLapTW, (M + kLapTH - 1) / kLapTH, F);
   laplacian_kernel<H><<<grid, kLapNT, T::SMEM, st>>>(tin, tout, vmask, vm_fs, wpr, M, N, lam);
   return check_launch("laplacian_kernel");

@@ -33,6 +33,24 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
               float* buf_c = nullptr);  // fused pipeline: centroid windows (bilateral_buf_c_bytes)
 
 int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st);
+
+int narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int width,
+                   const int64_t* n_rows, long long src_fs, long long dst_fs, cudaStream_t st);
+
+// strict (fp64, reference operation order) kernels: strict.cu
+int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
+                  int ksize, int iters, cudaStream_t st);
+int bilateral_f64(const double* centroids, const double* normals_in, int F, int Mq, int Nq,
+                  double sigma_length, double sigma_angle, int ksize, int iters, double* buf_a,
+                  double* buf_b, double* out_fc, const int64_t* trimap, void* out_mesh,
+                  bool out_f32, long long out_rows, cudaStream_t st);
+int fc_data_f64(const double* opc, int F, int M, int N, double* cen, double* nrm, cudaStream_t st);
+int tri_extras_f64(const double* pts, int F, int M, int N, const int64_t* tris,
+                   const int64_t* n_tri, void* normals, bool normals_f32, double l_max,
+                   uint8_t* flag, cudaStream_t st);
+// largest kernel sizes of the fp32 kernels (beyond: the fp64 generic-window kernels)
+constexpr int kLapMaxK32 = 17;
+constexpr int kBilMaxK32 = 9;
 int triangle_normals(const void* pts, bool f64, const int64_t* tris, long long T, void* out,
                      cudaStream_t st);
 int find_cells(const double* queries, long long n, long long stride, const uint64_t* ids,

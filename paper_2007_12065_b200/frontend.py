@@ -30,12 +30,13 @@ from .smoothing import BilateralParams, LaplacianParams
 
 @dataclass
 class FrontEndResult:
-    """Device (or pinned host) outputs of one batch; rows beyond n_tri[f] are unused."""
-    points: torch.Tensor        # (F, M, N, 3) fp32 smoothed grid (view of the padded buffer)
+    """Device (or pinned host) outputs of one batch; rows beyond n_tri[f] are unused.
+    Float outputs are fp32 (precision "fast") or float64 (precision "strict")."""
+    points: torch.Tensor        # (F, M, N, 3) smoothed grid (fast: view of the padded buffer)
     triangles: torch.Tensor     # (F, G, 3) int64, GID order
     trimap: torch.Tensor        # (F, G) int64
     halfedges: torch.Tensor     # (F, 3G) int64 or None
-    normals: torch.Tensor       # (F, G, 3) fp32 (bilateral result, or triangle normals)
+    normals: torch.Tensor       # (F, G, 3) (bilateral result, or triangle normals)
     lmax_mask: torch.Tensor     # (F, G) uint8 or None
     n_tri: list = field(default_factory=list)
     grid_shape: tuple = None
@@ -55,15 +56,28 @@ class FrontEndResult:
 
 
 class FrontEnd:
-    """Batched organized front-end engine on one GPU."""
+    """Batched organized front-end engine on one GPU.
+
+    precision "fast" (default): fp32 kernels (+ the fp64 steps of the 1e-5 contract);
+    "strict": the reference's own fp64 chain (opcfe_front_end with
+    OPCFE_PRECISION_STRICT) -- float64 points and normals, bit-exact Laplacian and
+    topology, bilateral normals within a few ulp of the reference chain.
+    """
 
     def __init__(self, M: int, N: int, frames: int = 1,
                  laplacian: LaplacianParams | None = LaplacianParams(),
                  bilateral: BilateralParams | None = BilateralParams(),
                  l_max: float | None = None, halfedges: bool = True, normals: bool = True,
                  dominant_normals=None, ang_min: float = 0.95,
-                 src_dtype=torch.float32, device=None, graph: bool = True):
+                 src_dtype=torch.float32, device=None, graph: bool = True,
+                 precision: str = "fast", index_dtype=torch.int64):
         require_cuda()
+        if index_dtype not in (torch.int64, torch.int32):
+            raise ValueError("index_dtype must be torch.int64 (reference) or torch.int32")
+        if precision not in ("fast", "strict"):
+            raise ValueError(f"precision must be 'fast' or 'strict', got {precision!r}")
+        self.precision = precision
+        self.strict = strict = precision == "strict"
         if M < 2 or N < 2:
             from .geometry import DegenerateInputError
             raise DegenerateInputError("organized cloud must be at least 2 x 2")
@@ -87,6 +101,7 @@ class FrontEnd:
             bilateral.iterations if bilateral else 0, bilateral.kernel_size if bilateral else 3,
             bilateral.sigma_length if bilateral else 0.1, bilateral.sigma_angle if bilateral else 0.15,
             float(l_max) if l_max is not None else -1.0)
+        self.p.precision = _lib.PRECISION_STRICT if strict else _lib.PRECISION_FAST
         self.dn = None
         if dominant_normals is not None:   # fused group_assignment (segmentation.py:52-74)
             dn = torch.as_tensor(np.atleast_2d(np.asarray(dominant_normals, dtype=np.float64)))
@@ -96,11 +111,13 @@ class FrontEnd:
             self.p.dominant_normals = self.dn.data_ptr()
             self.p.n_dominant = self.dn.shape[0]
             self.p.ang_min = float(ang_min)
-        self.grid = torch.empty((frames, M, self.pitch), dtype=torch.float32, device=dev)
+        fdt = torch.float64 if strict else torch.float32
+        self.grid = torch.empty((frames, M, N, 3) if strict else (frames, M, self.pitch),
+                                dtype=fdt, device=dev)
         self.trimap = torch.empty((frames, G), dtype=torch.int64, device=dev)
         self.triangles = torch.empty((frames, G, 3), dtype=torch.int64, device=dev)
         self.halfedges = torch.empty((frames, 3 * G), dtype=torch.int64, device=dev) if halfedges else None
-        self.normals = torch.empty((frames, G, 3), dtype=torch.float32, device=dev) if normals else None
+        self.normals = torch.empty((frames, G, 3), dtype=fdt, device=dev) if normals else None
         self.lmax = torch.empty((frames, G), dtype=torch.uint8, device=dev) if l_max is not None else None
         self.n_tri = torch.empty((frames,), dtype=torch.int64, device=dev)
         self.labels = torch.empty((frames, G), dtype=torch.uint8, device=dev) \
@@ -117,28 +134,72 @@ class FrontEnd:
             self.lmax.data_ptr() if self.lmax is not None else None,
             self.n_tri.data_ptr(),
             self.labels.data_ptr() if self.labels is not None else None)
+        # compact (NON-reference) int32 copies of the index outputs, narrowed on the device
+        # after the chain (opcfe_narrow_indices) so that half the bytes cross PCIe
+        self.index_dtype = index_dtype
+        self.trimap32 = self.triangles32 = self.halfedges32 = None
+        if index_dtype == torch.int32:
+            if M * N >= 2 ** 31 or 3 * G >= 2 ** 31:
+                raise ValueError("int32 indices need M*N and 6(M-1)(N-1) below 2^31")
+            self.trimap32 = torch.empty((frames, G), dtype=torch.int32, device=dev)
+            self.triangles32 = torch.empty((frames, G, 3), dtype=torch.int32, device=dev)
+            self.halfedges32 = torch.empty((frames, 3 * G), dtype=torch.int32, device=dev) \
+                if halfedges else None
         self._graph = None
         self._use_graph = graph
         extras = (normals and bilateral is None) or l_max is not None
-        self.kernel_launches = self._count_launches(laplacian, bilateral, src_kind, extras) + \
-            (1 if self.labels is not None else 0)
+        self.kernel_launches = self._count_launches(laplacian, bilateral if normals else None,
+                                                    src_kind, extras, strict) + \
+            (1 if self.labels is not None else 0) + \
+            (0 if self.trimap32 is None else (3 if halfedges else 2))
 
     @staticmethod
-    def _count_launches(lap, bil, src_kind, extras=False):
+    def _count_launches(lap, bil, src_kind, extras=False, strict=False):
+        """Kernels one batch launches (mirrors front_end_impl in csrc/capi.cu)."""
+        from .smoothing import BILATERAL_MAX_K32, LAPLACIAN_MAX_K32
+        lap64 = lap is not None and (strict or lap.kernel_size > LAPLACIAN_MAX_K32)
+        bil64 = bil is not None and (strict or bil.kernel_size > BILATERAL_MAX_K32)
         n = 3                                                   # triangulate: count, scan, emit
-        n += 1 if extras else 0                                 # quad_extras: normals / l_max
-        n += lap.iterations if lap else 0
-        if not lap or src_kind != 0:
-            n += 1                                              # stage-in
-        n += bil.iterations if bil else 0
+        if strict or lap64:
+            n += 1 if src_kind != 2 else 0                      # source -> f64 (unstage)
+            n += lap.iterations if lap else 0                   # laplacian_f64
+            n += 1 if (lap or strict) else 0                    # validity bits (+ fp32 grid)
+            n += 1 if (strict and extras) else 0                # tri_extras_f64
+        else:
+            n += lap.iterations if lap else 0
+            if not lap or src_kind != 0:
+                n += 1                                          # stage-in
+        if not strict:
+            n += 1 if extras else 0                             # quad_extras: normals / l_max
+        if bil64:
+            n += 0 if (strict or lap64) else 1                  # fp32 grid -> f64 (unstage)
+            n += 1 + bil.iterations                             # fc_data_f64 + bilateral_f64
+        elif bil:
+            n += bil.iterations
         return n
 
     # ------------------------------------------------------------------ device
     def _launch(self, stream: torch.cuda.Stream):
-        rc = _lib.lib().opcfe_front_end(self.F, self.M, self.N, ctypes.byref(self.p),
-                                        ctypes.byref(self.io), self.ws.data_ptr(),
-                                        self.ws.numel(), stream.cuda_stream)
+        L = _lib.lib()
+        rc = L.opcfe_front_end(self.F, self.M, self.N, ctypes.byref(self.p),
+                               ctypes.byref(self.io), self.ws.data_ptr(), self.ws.numel(),
+                               stream.cuda_stream)
         _lib.check(rc, "front_end")
+        self._narrow(stream)
+
+    def _narrow(self, stream):
+        if self.trimap32 is None:
+            return
+        L, F, G, s = _lib.lib(), self.F, self.G, stream.cuda_stream
+        nt = self.n_tri.data_ptr()
+        _lib.check(L.opcfe_narrow_indices(self.trimap.data_ptr(), self.trimap32.data_ptr(), F,
+                                          G, 1, None, G, G, s), "narrow_indices")
+        _lib.check(L.opcfe_narrow_indices(self.triangles.data_ptr(), self.triangles32.data_ptr(),
+                                          F, G, 3, nt, 3 * G, 3 * G, s), "narrow_indices")
+        if self.halfedges32 is not None:
+            _lib.check(L.opcfe_narrow_indices(self.halfedges.data_ptr(),
+                                              self.halfedges32.data_ptr(), F, G, 3, nt, 3 * G,
+                                              3 * G, s), "narrow_indices")
 
     def _capture(self):
         s = torch.cuda.Stream(device=self.device)
@@ -171,6 +232,7 @@ class FrontEnd:
                                                  ctypes.byref(self.io), self.ws.data_ptr(),
                                                  self.ws.numel(), s.cuda_stream, arr)
         _lib.check(rc, "front_end_profiled")
+        self._narrow(s)
 
     def run(self, src: torch.Tensor | None = None) -> FrontEndResult:
         """Process the batch in self.src (or copy `src` (F,M,N,3) into it first)."""
@@ -179,8 +241,25 @@ class FrontEnd:
         self.launch()
         return self.result()
 
+    def device_outputs(self) -> dict:
+        """name -> (device tensor (F, ...), rows-per-triangle: 0 = fixed size) of every
+        output this engine produces, index arrays in self.index_dtype."""
+        c = self.index_dtype == torch.int32
+        out = {"points": (self.points_view(), 0),
+               "trimap": (self.trimap32 if c else self.trimap, 0),
+               "triangles": (self.triangles32 if c else self.triangles, 1),
+               "halfedges": (self.halfedges32 if c else self.halfedges, 3),
+               "normals": (self.normals, 1), "lmax": (self.lmax, 1), "labels": (self.labels, 1)}
+        return {k: v for k, v in out.items() if v[0] is not None}
+
+    def points_view(self) -> torch.Tensor:
+        """The smoothed grid as (F, M, N, 3) (fast: a view of the padded fp32 rows)."""
+        if self.strict:
+            return self.grid
+        return self.grid[..., :3 * self.N].unflatten(-1, (self.N, 3))
+
     def result(self) -> FrontEndResult:
-        pts = self.grid[..., :3 * self.N].unflatten(-1, (self.N, 3))
+        pts = self.points_view()
         return FrontEndResult(points=pts, triangles=self.triangles, trimap=self.trimap,
                               halfedges=self.halfedges, normals=self.normals,
                               lmax_mask=self.lmax, n_tri=self.n_tri.tolist(), labels=self.labels,
@@ -192,12 +271,13 @@ class FrontEnd:
         if not hasattr(self, "_host"):
             F, M, N, G = self.F, self.M, self.N, self.G
             pin = dict(pin_memory=True)
+            fdt = self.grid.dtype
             self._host = dict(
-                points=torch.empty((F, M, N, 3), dtype=torch.float32, **pin),
+                points=torch.empty((F, M, N, 3), dtype=fdt, **pin),
                 trimap=torch.empty((F, G), dtype=torch.int64, **pin),
                 triangles=torch.empty((F, G, 3), dtype=torch.int64, **pin),
                 halfedges=torch.empty((F, 3 * G), dtype=torch.int64, **pin) if self.halfedges is not None else None,
-                normals=torch.empty((F, G, 3), dtype=torch.float32, **pin) if self.normals is not None else None,
+                normals=torch.empty((F, G, 3), dtype=fdt, **pin) if self.normals is not None else None,
                 lmax=torch.empty((F, G), dtype=torch.uint8, **pin) if self.lmax is not None else None,
                 n_tri=torch.empty((F,), dtype=torch.int64, **pin),
             )
@@ -218,10 +298,10 @@ class FrontEnd:
         cur.synchronize()                                        # data-dependent sizes
         nt = H["n_tri"].tolist()
         d2h = 8 * self.F
-        pts = self.grid[..., :3 * self.N].unflatten(-1, (self.N, 3))
-        H["points"].copy_(pts, non_blocking=True)
+        H["points"].copy_(self.points_view(), non_blocking=True)
         H["trimap"].copy_(self.trimap, non_blocking=True)
-        d2h += H["points"].numel() * 4 + H["trimap"].numel() * 8
+        fsz = self.grid.element_size()
+        d2h += H["points"].numel() * fsz + H["trimap"].numel() * 8
         for f, T in enumerate(nt):
             H["triangles"][f, :T].copy_(self.triangles[f, :T], non_blocking=True)
             d2h += 24 * T
@@ -230,7 +310,7 @@ class FrontEnd:
                 d2h += 24 * T
             if H["normals"] is not None:
                 H["normals"][f, :T].copy_(self.normals[f, :T], non_blocking=True)
-                d2h += 12 * T
+                d2h += 3 * fsz * T
             if H["lmax"] is not None:
                 H["lmax"][f, :T].copy_(self.lmax[f, :T], non_blocking=True)
                 d2h += T
@@ -248,21 +328,47 @@ class HostPipeline:
     Two FrontEnd slots (each a CUDA graph over `frames_per_slot` frames) and three
     streams: chunk i+1's H2D and front end run while chunk i's outputs stream back (D2H).
     A frame's D2H is sized by its own triangle count (one event wait per chunk on the
-    host), so exactly the drop-in outputs travel: smoothed grid (fp32), trimap, triangles,
-    halfedges (int64) and normals (fp32), as mesh_from_opc + bilateral_filter_opc return
-    them.  Small frames go several to a slot (default: ~8 MB of input per slot), so the
-    per-chunk host wait and launch latency are amortised.
+    host), so only live rows travel.  Small frames go several to a slot (default: ~8 MB
+    of input per slot), so the per-chunk host wait and launch latency are amortised.
+
+    outputs      which results come back (default: the drop-in set mesh_from_opc +
+                 bilateral_filter_opc return -- smoothed grid, trimap, triangles,
+                 halfedges, normals; also "lmax" (needs l_max) and "labels" (needs
+                 dominant_normals)).  Unrequested outputs are not copied.
+    index_dtype  torch.int64 (the reference's dtype) or torch.int32 -- compact,
+                 NON-reference indices narrowed on the device (half the index bytes).
+    precision    "fast" (fp32 outputs) or "strict" (float64, the reference's chain).
     """
 
+    DROPIN = ("points", "trimap", "triangles", "halfedges", "normals")
+    NAMES = DROPIN + ("lmax", "labels")
+
     def __init__(self, M, N, laplacian=LaplacianParams(), bilateral=BilateralParams(),
-                 l_max=None, src_dtype=torch.float64, device=None, frames_per_slot=None):
+                 l_max=None, src_dtype=torch.float64, device=None, frames_per_slot=None,
+                 precision: str = "fast", outputs=DROPIN, index_dtype=torch.int64,
+                 dominant_normals=None, ang_min: float = 0.95):
+        outputs = tuple(outputs)
+        bad = [o for o in outputs if o not in self.NAMES]
+        if bad:
+            raise ValueError(f"unknown outputs {bad}; choose from {self.NAMES}")
+        if "lmax" in outputs and l_max is None:
+            raise ValueError("the lmax output needs l_max")
+        if "labels" in outputs and dominant_normals is None:
+            raise ValueError("the labels output needs dominant_normals")
         if frames_per_slot is None:
             esz = torch.empty((), dtype=src_dtype).element_size()
             frames_per_slot = max(1, min(16, (8 << 20) // (M * N * 3 * esz)))
         self.k = k = int(frames_per_slot)
+        self.outputs = outputs
         self.slots = [FrontEnd(M, N, k, laplacian=laplacian, bilateral=bilateral, l_max=l_max,
-                               src_dtype=src_dtype, device=device, graph=True) for _ in range(2)]
+                               halfedges="halfedges" in outputs,
+                               normals="normals" in outputs or "labels" in outputs,
+                               dominant_normals=dominant_normals, ang_min=ang_min,
+                               src_dtype=src_dtype, device=device, graph=True,
+                               precision=precision, index_dtype=index_dtype)
+                      for _ in range(2)]
         dev = self.slots[0].device
+        self.device = dev
         self.M, self.N, self.G = M, N, self.slots[0].G
         self.s_h2d = torch.cuda.Stream(device=dev)
         self.s_cmp = torch.cuda.Stream(device=dev)
@@ -279,15 +385,13 @@ class HostPipeline:
 
     def host_outputs(self, F):
         if self._host is None or self._host["points"].shape[0] < F:
-            M, N, G = self.M, self.N, self.G
-            pin = dict(pin_memory=True)
-            self._host = dict(
-                points=torch.empty((F, M, N, 3), dtype=torch.float32, **pin),
-                trimap=torch.empty((F, G), dtype=torch.int64, **pin),
-                triangles=torch.empty((F, G, 3), dtype=torch.int64, **pin),
-                halfedges=torch.empty((F, 3 * G), dtype=torch.int64, **pin),
-                normals=torch.empty((F, G, 3), dtype=torch.float32, **pin),
-            )
+            # only the requested outputs (points is always sized for the batch bookkeeping)
+            dev_out = self.slots[0].device_outputs()
+            self._host = {}
+            for name in set(self.outputs) | {"points"}:
+                t = dev_out[name][0]
+                self._host[name] = torch.empty((F,) + tuple(t.shape[1:]), dtype=t.dtype,
+                                                pin_memory=True)
         return self._host
 
     def _enqueue(self, src_host, c):
@@ -313,26 +417,30 @@ class HostPipeline:
         n = min(self.k, F - lo)
         self.ev_cmp[s].synchronize()                    # the chunk's n_tri are on the host
         nt = [int(t) for t in self.ntri_host[s, :n]]
-        b = 0
+        dev_out = eng.device_outputs()
+        b = 8 * n
         with torch.cuda.stream(self.s_d2h):
             self.s_d2h.wait_event(self.ev_cmp[s])
-            H["points"][lo:lo + n].copy_(eng.grid[:n, :, :3 * self.N].unflatten(-1, (self.N, 3)),
-                                         non_blocking=True)
-            H["trimap"][lo:lo + n].copy_(eng.trimap[:n], non_blocking=True)
-            for j, T in enumerate(nt):
-                H["triangles"][lo + j, :T].copy_(eng.triangles[j, :T], non_blocking=True)
-                H["halfedges"][lo + j, :3 * T].copy_(eng.halfedges[j, :3 * T], non_blocking=True)
-                H["normals"][lo + j, :T].copy_(eng.normals[j, :T], non_blocking=True)
-                b += self.M * self.N * 12 + self.G * 8 + T * (24 + 24 + 12) + 8
+            for name in self.outputs:
+                t, per_tri = dev_out[name]
+                if per_tri == 0:                        # fixed-size per frame
+                    H[name][lo:lo + n].copy_(t[:n], non_blocking=True)
+                    b += t[:n].numel() * t.element_size()
+                    continue
+                for j, T in enumerate(nt):
+                    rows = per_tri * T
+                    H[name][lo + j, :rows].copy_(t[j, :rows], non_blocking=True)
+                    b += t[j, :rows].numel() * t.element_size()
             self.ev_d2h[s].record(self.s_d2h)
         return nt, b
 
     def run(self, src_host: torch.Tensor) -> FrontEndResult:
-        """src_host: pinned (F, M, N, 3).  Returns pinned host outputs (valid until the next run)."""
+        """src_host: pinned (F, M, N, 3).  Returns pinned host outputs (valid until the
+        next run); every copy has completed when run() returns."""
         F = src_host.shape[0]
         H = self.host_outputs(F)
         for s in (self.s_h2d, self.s_cmp, self.s_d2h):
-            s.wait_stream(torch.cuda.current_stream(self.slots[0].device))
+            s.wait_stream(torch.cuda.current_stream(self.device))
         chunks = (F + self.k - 1) // self.k
         nt, d2h = [], 0
         self._enqueue(src_host, 0)
@@ -342,30 +450,69 @@ class HostPipeline:
             t, b = self._drain(H, c, F)
             nt += t
             d2h += b
-        torch.cuda.current_stream(self.slots[0].device).wait_stream(self.s_d2h)
+        torch.cuda.current_stream(self.device).wait_stream(self.s_d2h)
+        self.s_d2h.synchronize()                        # host buffers complete
         self.h2d_bytes = src_host.numel() * src_host.element_size()
         self.d2h_bytes = d2h
-        return FrontEndResult(points=H["points"][:F], triangles=H["triangles"][:F],
-                              trimap=H["trimap"][:F], halfedges=H["halfedges"][:F],
-                              normals=H["normals"][:F], lmax_mask=None, n_tri=nt,
-                              grid_shape=(self.M, self.N))
+        get = lambda k: H[k][:F] if k in self.outputs else None
+        return FrontEndResult(points=get("points"), triangles=get("triangles"),
+                              trimap=get("trimap"), halfedges=get("halfedges"),
+                              normals=get("normals"), lmax_mask=get("lmax"), n_tri=nt,
+                              grid_shape=(self.M, self.N), labels=get("labels"))
+
+
+_ENGINES: "OrderedDict[tuple, FrontEnd]" = None
+_ENGINES_MAX = 4
+
+
+def cached_engine(M, N, laplacian, bilateral, l_max, src_dtype, precision, frames=1,
+                  dominant_normals=None, ang_min=0.95, device=None) -> FrontEnd:
+    """A FrontEnd for these shapes / parameters, reused across calls (buffers, workspace
+    and TMA descriptors are built once; small LRU per process)."""
+    from collections import OrderedDict
+    global _ENGINES
+    if _ENGINES is None:
+        _ENGINES = OrderedDict()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    dn_key = None if dominant_normals is None else \
+        np.asarray(dominant_normals, dtype=np.float64).tobytes()
+    key = (M, N, frames, laplacian and (laplacian.lam, laplacian.kernel_size, laplacian.iterations),
+           bilateral and (bilateral.sigma_length, bilateral.sigma_angle, bilateral.kernel_size,
+                          bilateral.iterations),
+           l_max, src_dtype, precision, dn_key, ang_min, dev)
+    eng = _ENGINES.get(key)
+    if eng is None:
+        eng = FrontEnd(M, N, frames, laplacian=laplacian, bilateral=bilateral, l_max=l_max,
+                       dominant_normals=dominant_normals, ang_min=ang_min, src_dtype=src_dtype,
+                       device=dev, graph=False, precision=precision)
+        _ENGINES[key] = eng
+        while len(_ENGINES) > _ENGINES_MAX:
+            _ENGINES.popitem(last=False)
+    else:
+        _ENGINES.move_to_end(key)
+    return eng
 
 
 def front_end(opc, laplacian: LaplacianParams | None = None,
-              bilateral: BilateralParams | None = None, l_max: float | None = None):
+              bilateral: BilateralParams | None = None, l_max: float | None = None,
+              precision: str | None = None):
     """Single-frame organized front-end (pipeline.py:125-134) on the GPU.
 
     Returns (smoothed grid, HalfEdgeMesh, l_max mask or None); NumPy in ->
     NumPy out (float arrays as float64 like the reference), torch in -> torch.
+    Precision as smoothing.resolve_precision (float64 input: the reference's fp64
+    chain by default).  Engines are cached per shape and parameters.
     """
+    from .smoothing import resolve_precision
     is_np = not isinstance(opc, torch.Tensor)
     src = torch.from_numpy(np.ascontiguousarray(opc, dtype=np.float64)) if is_np else opc
+    if src.dtype not in (torch.float32, torch.float64):
+        src = src.to(torch.float64)
     src = src.to("cuda").contiguous()
     M, N = src.shape[:2]
-    eng = FrontEnd(M, N, 1, laplacian=laplacian, bilateral=bilateral, l_max=l_max,
-                   src_dtype=src.dtype if src.dtype in (torch.float32, torch.float64) else torch.float64,
-                   graph=False)
-    res = eng.run(src.unsqueeze(0).to(eng.src.dtype))
+    prec = resolve_precision(precision, src.dtype)
+    eng = cached_engine(M, N, laplacian, bilateral, l_max, src.dtype, prec)
+    res = eng.run(src.unsqueeze(0))
     mesh = res.mesh(0)
     if is_np:
         conv = lambda t, dt=None: None if t is None else (t.cpu().numpy() if dt is None
@@ -376,5 +523,11 @@ def front_end(opc, laplacian: LaplacianParams | None = None,
                             trimap=conv(mesh.trimap), grid_shape=(M, N))
         mask = None if res.lmax_mask is None else conv(res.lmax_mask[0, :mesh.num_triangles]).astype(bool)
         return smoothed, mesh, mask
+    # torch callers: copies, so the next call on the cached engine cannot alias them
+    cl = lambda t: None if t is None else t.clone()
+    pts = res.points[0].clone()
+    mesh = HalfEdgeMesh(points=pts.reshape(-1, 3), triangles=cl(mesh.triangles),
+                        halfedges=cl(mesh.halfedges), normals=cl(mesh.normals),
+                        trimap=cl(mesh.trimap), grid_shape=(M, N))
     mask = None if res.lmax_mask is None else res.lmax_mask[0, :len(mesh.triangles)].bool()
-    return res.points[0], mesh, mask
+    return pts, mesh, mask

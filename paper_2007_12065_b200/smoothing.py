@@ -4,16 +4,28 @@ Laplacian vertex smoothing and bilateral normal smoothing on the image-space
 grid, as sm_100a kernels behind libopcfe.  Same dataclasses, validation,
 function names and errors as the reference (smoothing.py:22-114).
 
-Precision (north-star contract): arithmetic is fp32 with the fp64 steps the
-contract needs (FC normal edges/cross products, l_max edge lengths).  For
-float64 input the outputs are float64; vertices / normals the filters leave
-unchanged (outer ring, NaN and isolated vertices, unchanged normals) come back
-bit-identical, moved ones are within 1e-5 (norm-wise relative) of the fp64
-reference.
+Precision (``precision=`` argument, or the process default from
+:func:`set_precision` / the ``OPCFE_PRECISION`` environment variable):
+
+* ``"strict"`` -- the reference's own fp64 arithmetic in its operation order
+  (``opcfe_laplacian_f64`` / ``opcfe_bilateral_f64``): the Laplacian and the FC
+  data are bit-identical to the reference, the bilateral normals differ only by
+  exp()'s last-ulp rounding, so chained results stay within ~1e-15 of the
+  reference chain.  Any odd kernel size.
+* ``"fast"`` -- fp32 kernels with the fp64 steps the north-star's 1e-5 contract
+  needs (FC normal edges / cross products, l_max edge lengths); vertices /
+  normals the filters leave unchanged come back bit-identical, moved ones are
+  within 1e-5 per stage.  Kernel sizes beyond the fp32 kernels' compiled set
+  (Laplacian > 17, bilateral > 9) run on the fp64 kernels.
+* ``"auto"`` (default) -- strict for float64 input (what the reference computes
+  in), fast for float32.
+
+NumPy callers get float64 arrays back, as from the reference.
 """
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -56,22 +68,55 @@ class BilateralParams:
             raise ValueError("iterations must be >= 1")
 
 
-def _laplacian_staged(S: Staged, lam, kernel_size, iterations):
+PRECISIONS = ("auto", "fast", "strict")
+LAPLACIAN_MAX_K32 = 17   # fp32 kernels' compiled kernel sizes (kLapMaxK32 / kBilMaxK32)
+BILATERAL_MAX_K32 = 9
+_precision = os.environ.get("OPCFE_PRECISION", "auto")
+if _precision not in PRECISIONS:
+    raise ValueError(f"OPCFE_PRECISION must be one of {PRECISIONS}, got {_precision!r}")
+
+
+def set_precision(precision: str) -> None:
+    """Process-wide default precision of the drop-in functions ("auto" | "fast" | "strict")."""
+    global _precision
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}, got {precision!r}")
+    _precision = precision
+
+
+def get_precision() -> str:
+    return _precision
+
+
+def resolve_precision(precision, dtype) -> str:
+    """"fast" or "strict" for an input of `dtype` (None = the process default)."""
+    p = _precision if precision is None else precision
+    if p not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}, got {p!r}")
+    if p == "auto":
+        return "strict" if dtype == torch.float64 else "fast"
+    return p
+
+
+def _laplacian_staged(S: Staged, lam, kernel_size, iterations, precision=None):
     x = S.dev
     M, N = x.shape[:2]
+    if resolve_precision(precision, x.dtype) == "strict" or kernel_size > LAPLACIAN_MAX_K32:
+        res = _ops.laplacian_f64(x.to(torch.float64), lam, kernel_size, iterations)
+        return S.give(res.to(x.dtype))
     grid, _ = _ops.stage_in(x, want_points=True, want_mask=False)
     out = _ops.laplacian(grid, 1, M, N, lam, kernel_size, iterations)
     res = _ops.unstage(out, 1, M, N, x.dtype, orig=x.unsqueeze(0))[0]
     return S.give(res)
 
 
-def laplacian_filter_opc(opc, params: LaplacianParams):
+def laplacian_filter_opc(opc, params: LaplacianParams, precision: str | None = None):
     """Smooth an (M, N, 3) organized cloud; border ring and NaNs are untouched (smoothing.py:53-58)."""
     S = Staged(opc)
     x = S.dev
     if x.dim() != 3 or min(x.shape[:2]) < params.kernel_size:
         raise DegenerateInputError("grid smaller than the filter kernel")
-    return _laplacian_staged(S, params.lam, params.kernel_size, params.iterations)
+    return _laplacian_staged(S, params.lam, params.kernel_size, params.iterations, precision)
 
 
 def compute_fc_triangle_data(opc):
@@ -87,26 +132,44 @@ def compute_fc_triangle_data(opc):
     return S.give(cen), S.give(nrm)
 
 
-def bilateral_filter_opc(opc, params: BilateralParams, trimap=None):
+def _trimap_of(S: Staged, trimap, M: int, N: int) -> torch.Tensor:
+    """The GID map as a 16-B aligned int64 device vector of 2(M-1)(N-1) entries (given, or
+    from the triangulation kernel)."""
+    if trimap is None:
+        _, vmask = _ops.stage_in(S.dev, want_points=False, want_mask=True)
+        return _ops.triangulate(vmask, 1, M, N, halfedges=False)["trimap"][0]
+    tm = Staged(trimap, float_only=False).dev.to(torch.int64).reshape(-1).contiguous()
+    if tm.numel() != 2 * (M - 1) * (N - 1):
+        # the reference's flat[trimap >= 0] fails the same way (smoothing.py:111-113)
+        raise IndexError(f"trimap has {tm.numel()} entries; the grid has "
+                         f"{2 * (M - 1) * (N - 1)} fully-connected triangles")
+    if tm.data_ptr() % 16:
+        tm = tm.clone()
+    return tm
+
+
+def bilateral_filter_opc(opc, params: BilateralParams, trimap=None, precision: str | None = None):
     """Bilaterally smoothed unit normals for the valid mesh of an OPC (smoothing.py:91-114).
 
-    FC centroids/normals are computed in fp64 from the caller's vertices and
-    filtered in fp32; the last pass scatters straight into mesh order through
-    the GID map (given, or computed by the triangulation kernel).
+    FC centroids/normals are computed in fp64 from the caller's vertices (bit-exact) and
+    filtered in fp64 (strict) or fp32 (fast); the last pass scatters straight into mesh
+    order through the GID map (given, or computed by the triangulation kernel).
     """
     S = Staged(opc)
     x = S.dev
     if x.dim() != 3 or min(x.shape[:2]) < 2:
         raise DegenerateInputError("organized cloud must be at least 2 x 2")
     M, N = x.shape[:2]
-    cen, nrm = _ops.fc_data(x)
-    if trimap is None:
-        _, vmask = _ops.stage_in(x, want_points=False, want_mask=True)
-        r = _ops.triangulate(vmask, 1, M, N, halfedges=False)
-        tm = r["trimap"][0]
-    else:
-        tm = Staged(trimap, float_only=False).dev.to(torch.int64).reshape(-1).contiguous()
+    tm = _trimap_of(S, trimap, M, N)
     n_out = int((tm >= 0).sum().item())
+    strict = resolve_precision(precision, x.dtype) == "strict"
+    if strict or params.kernel_size > BILATERAL_MAX_K32:
+        cen, nrm = _ops.fc_data_f64(x.to(torch.float64))
+        out = _ops.bilateral_f64(cen, nrm, params.sigma_length, params.sigma_angle,
+                                 params.kernel_size, params.iterations, trimap=tm,
+                                 out_rows=n_out)
+        return S.give(out.to(x.dtype))
+    cen, nrm = _ops.fc_data(x)
     out = _ops.bilateral(1, M, N, params.sigma_length, params.sigma_angle, params.kernel_size,
                          params.iterations, fc_normals=_ops.stage_fc(nrm),
                          fc_centroids=_ops.centroids_f64(cen), trimap=tm, out_rows=n_out)[0]

@@ -6,6 +6,7 @@ Bars (north-star + SURVEY.md 8c precision contract):
   * Laplacian vertices: per vertex |g - r| <= 1e-5 * max(|r|, rms|r|) (norm-wise
     relative); unchanged vertices (ring, NaN, isolated) bit-identical;
   * bilateral normals (unit vectors): per triangle |g - r| <= 1e-5; NaN masks equal.
+Drop-in calls run with precision "fast" here (module fixture).
 Fused fp32 pipeline: per-stage parity on identical inputs -- each oracle stage consumes
 the GPU's fp32 intermediate (upcast to f64) -- plus end-to-end bit-exact topology.
 """
@@ -30,6 +31,17 @@ TOL = 1e-5
 def fe():
     import paper_2007_12065_b200 as m
     return m
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _fast_precision():
+    """This module checks the fp32 ("fast") drop-in path against the 1e-5 contract; the
+    strict fp64 path (the float64 default) is checked in test_gpu_strict.py."""
+    from paper_2007_12065_b200 import smoothing
+    old = smoothing.get_precision()
+    smoothing.set_precision("fast")
+    yield
+    smoothing.set_precision(old)
 
 
 def same(a, b):

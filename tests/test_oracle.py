@@ -189,3 +189,33 @@ def test_region_growing_oracle(scene, ptp):
         assert len(got) == len(exp)
         for a, b in zip(got, exp):
             assert np.array_equal(a, b)
+
+
+# ---------------------------------------------- chains (tests/golden/make_chain_golden.py)
+CHAIN = load_golden("chain")
+
+
+@pytest.mark.parametrize("case", sorted(CHAIN))
+def test_c_oracle_chain_pinned(case):
+    """The C oracle's fp64 chain (laplacian -> mesh -> bilateral, pipeline.py:125-134)
+    equals the reference's own chain: smoothed grid and topology bit-exact, normals to
+    exp()'s last ulp (the GPU strict chain is checked against both)."""
+    g = CHAIN[case]
+    lap = tuple(g["lap"][:1]) + tuple(int(x) for x in g["lap"][1:])
+    bil = None
+    if g["bil"].size:
+        b = g["bil"]
+        bil = (float(b[0]), float(b[1]), int(b[2]), int(b[3]))
+    r = c_oracle.front_end(g["opc"], lap, bil)
+    sm = r["smoothed"]
+    assert np.array_equal(np.isnan(sm), np.isnan(g["smoothed"]))
+    assert np.array_equal(np.nan_to_num(sm), np.nan_to_num(g["smoothed"]))
+    assert np.array_equal(r["trimap"], g["trimap"].astype(np.int64))
+    assert int((r["halfedges"] >= 0).sum()) == int(g["n_halfedges_linked"][0])
+    n, ref = r["normals"], g["normals"]
+    assert np.array_equal(np.isnan(n), np.isnan(ref))
+    ok = ~np.isnan(ref).any(1)
+    assert np.max(np.linalg.norm(n[ok] - ref[ok], axis=1)) <= 1e-13
+    l_max, ang = (float(x) for x in g["seg"])
+    lab = c_oracle.group_assignment(r["points"], r["triangles"], n, g["dominant"], l_max, ang)
+    assert np.array_equal(lab, g["labels"])
