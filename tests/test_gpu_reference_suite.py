@@ -1,0 +1,79 @@
+"""The reference's OWN test suite, run through libopcfe from the reference's side.
+
+integration/install.py installs the unmodified reference (baseline/_ref, built by
+baseline/install_ref.sh from /root/reference/pkg) plus the libopcfe backend
+(integration/flatpoly/_kernels/_opcfe.py: ctypes over include/opcfe.h, no torch) and
+the maintainer's patch (integration/flatpoly_cuda.patch: the FLATPOLY_CUDA branch of
+_kernels/__init__.py:9-30, mesh / FC functions routed to the backend).  With
+FLATPOLY_CUDA=1 the reference's own tests -- tests/test_kernels.py (compiled backend vs
+the NumPy fallback), test_smoothing.py, test_mesh.py, test_segmentation.py and
+test_acceptance.py -- then exercise the GPU kernels through the C ABI.
+
+Deselected: acceptance #06 / #07 / #10 run the polygon stage, which needs the real
+Shapely (absent from this image; tests/golden/_stubs has an import stub only) -- they
+fail identically on the stock reference here.
+"""
+
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(REPO, "baseline", "_ref")
+LIB = os.path.join(REPO, "paper_2007_12065_b200", "lib", "libopcfe.so")
+STUBS = os.path.join(REPO, "tests", "golden", "_stubs")
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device"),
+              pytest.mark.skipif(not os.path.isdir(os.path.join(REF, "flatpoly")),
+                                 reason="baseline/_ref missing (run baseline/install_ref.sh)")]
+
+FILES = ["tests/test_kernels.py", "tests/test_smoothing.py", "tests/test_mesh.py",
+         "tests/test_segmentation.py", "tests/test_acceptance.py"]
+DESELECT = ["tests/test_acceptance.py::test_06_room_benchmark",
+            "tests/test_acceptance.py::test_07_thread_determinism",
+            "tests/test_acceptance.py::test_10_buffer_geometry"]
+
+
+@pytest.fixture(scope="module")
+def installed(tmp_path_factory):
+    dest = str(tmp_path_factory.mktemp("flatpoly_cuda"))
+    subprocess.run([sys.executable, os.path.join(REPO, "integration", "install.py"), dest],
+                   check=True)
+    return dest
+
+
+def _env(dest, mode="1"):
+    env = dict(os.environ, FLATPOLY_CUDA=mode, OPCFE_LIB=LIB,
+               PYTHONPATH=os.pathsep.join([dest, STUBS]))
+    env.pop("FLATPOLY_PURE", None)
+    return env
+
+
+def test_backend_is_libopcfe(installed):
+    code = ("from flatpoly import _kernels, mesh\n"
+            "import numpy as np\n"
+            "assert _kernels.ACTIVE == 'cuda', _kernels.ACTIVE\n"
+            "assert _kernels.laplacian_filter.__module__ == 'flatpoly._kernels._opcfe'\n"
+            "mesh.mesh_from_opc(np.zeros((4, 4, 3)))\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "assert 'libopcfe.so' in maps, 'libopcfe not mapped'\n"
+            "print('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=installed, env=_env(installed),
+                       capture_output=True, text=True)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_reference_suite_through_libopcfe(installed):
+    args = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", *FILES]
+    for d in DESELECT:
+        args += ["--deselect", d]
+    r = subprocess.run(args, cwd=installed, env=_env(installed), capture_output=True, text=True,
+                       timeout=1200)
+    tail = "\n".join(r.stdout.splitlines()[-25:])
+    print(tail)
+    assert r.returncode == 0, tail + r.stderr[-2000:]
+    assert " passed" in tail and "failed" not in tail
