@@ -144,22 +144,26 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm
-def cpu_reference(steps, warmup, budget_s=None, wl=None):
-    """Time the reference's own CPU implementation on this host (bounded sample)."""
+def cpu_reference(steps, warmup, budget_s=None, wl=None, want_sample=False):
+    """Time the reference's own CPU implementation on this host: one whole frame per
+    process per step (small frames: several per task so a step is >= ~0.5 s), stopping
+    early once `budget_s` of timed work is done.  With want_sample, worker 0's outputs
+    of the first timed step are returned for the chained-parity check."""
     import numpy as np
     from oracle import ref_frontend
     wl = wl or WL
     frame = wl.base()
     cores = len(os.sched_getaffinity(0))
-    # 1080p: ~1/8 frame (136-row strip) per task; small configs: one whole frame per task
-    rows = 136 if wl.M >= 1000 else wl.M
-    pool = ref_frontend.ReferencePool(frame, cores, rows, wl.lap, wl.bil)
+    per_task = max(1, int(round(0.5 / _ref_frame_seconds(wl))))
+    pool = ref_frontend.ReferencePool(frame, cores, wl.lap, wl.bil, frames_per_task=per_task)
+    sample = None
     try:
         for _ in range(warmup):
             pool.step()
-        times, credit = [], 0.0
-        for _ in range(steps):
-            dt, fr = pool.step()
+        times, credit = [], 0
+        for k in range(steps):
+            dt, fr, smp = pool.step(want_sample=want_sample and k == 0)
+            sample = sample or smp
             times.append(dt)
             credit += fr
             if budget_s is not None and sum(times) > budget_s:
@@ -167,35 +171,90 @@ def cpu_reference(steps, warmup, budget_s=None, wl=None):
     finally:
         pool.close()
     total = sum(times)
-    what = (f"a {rows}x{wl.N} row strip of the {wl.name} frame ({rows / wl.M:.3f} frame)"
-            if rows < wl.M else f"one {wl.M}x{wl.N} {wl.name} frame")
     return {"value": credit / total, "unit": "frames/s", "cores": cores,
             "kind": ref_frontend.kind(),
-            "sample": f"{len(times)} steps x {cores} processes, each {what} through "
-                      "laplacian_filter (reference Cython) -> triangles/twins/normals (NumPy, "
-                      "as the reference)"
-                      + (" -> FC data -> bilateral_iterate (reference Cython) -> gather"
-                         if wl.bil else "")
-                      + "; single-threaded math per process",
+            "sample": f"{len(times)} timed steps (+{warmup} warm-up) x {cores} processes, each "
+                      f"{per_task} whole {wl.M}x{wl.N} {wl.name} frame(s) per step through "
+                      f"{ref_frontend.path_name()}; single-threaded math per process; "
+                      f"CPU: {ref_frontend.cpu_model()}",
+            "cpu_model": ref_frontend.cpu_model(),
             "ms_per_step": 1e3 * total / len(times), "steps_timed": len(times),
-            "np_version": np.__version__}
+            "frames_per_step": cores * per_task, "np_version": np.__version__}, sample
+
+
+def _ref_frame_seconds(wl):
+    """Rough single-core seconds per frame of the reference, used
+    only to size a step; C4 ~12 s, scaling with points and iterations."""
+    P = wl.M * wl.N
+    lap = wl.lap[2] if wl.lap else 0
+    bil = wl.bil[3] if wl.bil else 0
+    return P * (0.075e-6 * lap + 0.86e-6 * bil + 1.5e-6)
 
 
 def run_reference(args, rank, world, wl):
     if rank != 0:
         return 0
-    cb = cpu_reference(args.steps, args.warmup, wl=wl)
+    # whole frames cost ~12 s of CPU each at C4: warm-up capped at 1 step, timed steps
+    # stop after ~150 s so the default --steps 200 run ends within a few minutes
+    cb, _ = cpu_reference(args.steps, min(args.warmup, 1), budget_s=150.0, wl=wl)
     line = {"metric": METRIC, "value": cb["value"], "unit": "frames/s", "impl": "reference",
-            "n_gpus": args.gpus, "steps": cb["steps_timed"], "warmup": args.warmup,
+            "n_gpus": args.gpus, "steps": cb["steps_timed"], "warmup": min(args.warmup, 1),
             "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
             "scaling": "strong" if wl.total else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(args.frames, wl),
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "steps_note": f"--steps {args.steps} requested; whole-frame steps stop after 150 s "
+                          "of timed work (steps = the steps actually timed)"}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def chained_parity(sample, wl, dev):
+    """GPU chain vs the reference's OWN chain on the same whole frame (worker 0's output of
+    the cpu_baseline leg): fast (fp32) and strict (fp64) precision."""
+    import numpy as np
+    import torch
+
+    import paper_2007_12065_b200 as fe
+    base = wl.base()
+    M, N = base.shape[:2]
+    ref_sm, ref_n, ref_tm = sample["smoothed"], sample["normals"], sample["trimap"]
+    ok = np.isfinite(ref_sm).all(2)
+    out = {"frame": f"{wl.name} base frame {M}x{N} (the cpu_baseline leg's worker 0)"}
+    for prec in ("fast", "strict"):
+        eng = fe.FrontEnd(M, N, 1, laplacian=fe.LaplacianParams(*wl.lap) if wl.lap else None,
+                          bilateral=fe.BilateralParams(*wl.bil) if wl.bil else None,
+                          l_max=wl.l_max, src_dtype=torch.float64, device=dev, graph=False,
+                          precision=prec)
+        res = eng.run(torch.from_numpy(base).to(dev).unsqueeze(0))
+        torch.cuda.synchronize(dev)
+        T = res.n_tri[0]
+        sm = res.points[0].cpu().numpy().astype(np.float64)
+        tm = res.trimap[0].cpu().numpy()
+        he_linked = int((res.halfedges[0, :3 * T] >= 0).sum().item())
+        g_n = res.normals[0, :T].cpu().numpy().astype(np.float64)
+        verr = np.linalg.norm(sm[ok] - ref_sm[ok], axis=1) / \
+            np.maximum(np.linalg.norm(ref_sm[ok], axis=1), 1e-300)
+        nok = ~np.isnan(ref_n).any(1)
+        nerr = np.linalg.norm(g_n[nok] - ref_n[nok], axis=1) if T == len(ref_n) else None
+        q = lambda e: None if e is None or e.size == 0 else float(np.quantile(e, 0.999))
+        out[prec] = {
+            "topology_exact": bool(np.array_equal(tm, ref_tm) and
+                                   he_linked == sample["n_halfedges_linked"]),
+            "smoothed_bit_exact": bool(np.array_equal(np.nan_to_num(sm), np.nan_to_num(ref_sm))
+                                       and np.array_equal(np.isnan(sm), np.isnan(ref_sm))),
+            "smoothed_rel": {"max": float(verr.max()) if verr.size else 0.0, "p99.9": q(verr),
+                             "n_over_1e-5": int((verr > 1e-5).sum()), "n": int(verr.size)},
+            "normals_abs": None if nerr is None else {
+                "max": float(nerr.max()) if nerr.size else 0.0, "p99.9": q(nerr),
+                "n_over_1e-5": int((nerr > 1e-5).sum()), "n": int(nerr.size)},
+        }
+        del eng, res
+        torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------------ our arm
@@ -244,6 +303,78 @@ def load_traffic():
         with open(p) as f:
             return json.load(f)
     return {}
+
+
+def strict_throughput(fe, wl, eng_fast, args, dev):
+    """Device-resident frames/s of the STRICT chain (the reference's fp64 arithmetic) on
+    the same frames as the fast line (eng_fast.src), CUDA events on the launching stream."""
+    import torch
+    F = eng_fast.F
+    eng = fe.FrontEnd(wl.M, wl.N, F, laplacian=fe.LaplacianParams(*wl.lap) if wl.lap else None,
+                      bilateral=fe.BilateralParams(*wl.bil) if wl.bil else None, l_max=wl.l_max,
+                      src_dtype=eng_fast.src.dtype, device=dev, graph=False, precision="strict")
+    eng.src.copy_(eng_fast.src)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(2):
+        eng.launch()
+    steps = 5
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    a.record(stream)
+    for _ in range(steps):
+        eng.launch()
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = a.elapsed_time(b) / steps
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    for e in ev:                                    # materialise the cudaEvent_t handles
+        e.record(stream)
+    eng.launch_profiled(ev)
+    torch.cuda.synchronize(dev)
+    stage = {"stage_in": ev[0].elapsed_time(ev[1]), "laplacian": ev[1].elapsed_time(ev[2]),
+             "triangulate": ev[2].elapsed_time(ev[3]), "bilateral": ev[3].elapsed_time(ev[4])}
+    out = {"value": F / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms, "frames_per_step": F,
+           "steps": steps, "dtype": "f64", "gpu_launches_per_step": eng.kernel_launches,
+           "stage_ms_per_step": {k: round(v, 4) for k, v in stage.items()},
+           "what": "precision='strict': the reference's fp64 chain (bit-exact Laplacian, FC "
+                   "data and topology; bilateral to exp()'s last ulp), float64 outputs"}
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
+def dropin_e2e(fe, wl, frame, dev, frames=3):
+    """pipeline.py:125-134 unchanged, through the drop-in API (NumPy float64 in, NumPy
+    out, one frame per call), host wall clock around each whole frame."""
+    import numpy as np
+    import torch
+    frame = np.ascontiguousarray(frame, dtype=np.float64)
+    lp = fe.LaplacianParams(*wl.lap) if wl.lap else None
+    bp = fe.BilateralParams(*wl.bil) if wl.bil else None
+
+    def one():
+        sm = fe.laplacian_filter_opc(frame, lp) if lp else frame
+        mesh = fe.mesh_from_opc(sm)
+        if bp:
+            mesh.normals = fe.bilateral_filter_opc(sm, bp, mesh.trimap)
+        return sm, mesh
+
+    one()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(frames):
+        sm, mesh = one()
+    dt = (time.perf_counter() - t0) / frames
+    T = mesh.num_triangles
+    h2d = 3 * frame.nbytes + mesh.trimap.nbytes     # opc to each call + the trimap
+    d2h = sm.nbytes + mesh.triangles.nbytes + mesh.halfedges.nbytes + mesh.trimap.nbytes + \
+        24 * T * (2 if bp else 1)
+    from paper_2007_12065_b200 import smoothing
+    return {"value": 1.0 / dt, "unit": "frames/s", "frames": frames,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "precision": smoothing.resolve_precision(None, torch.float64),
+            "path": "laplacian_filter_opc -> mesh_from_opc -> bilateral_filter_opc on NumPy "
+                    "float64 (pageable) arrays, one frame per call, host wall clock"}
 
 
 def run_ours(args, rank, world, local_rank, wl):
@@ -379,6 +510,30 @@ def run_ours(args, rank, world, local_rank, wl):
                 shutil.rmtree(tmp, ignore_errors=True)
         e2e["from_files"] = e2e_files
         del pipe
+        # ---- compact (NON-reference) output modes: int32 indices narrowed on the device,
+        # optionally only a subset of the outputs
+        for key, outs in (("compact", fe.HostPipeline.DROPIN),
+                          ("selected", ("points", "triangles", "normals"))):
+            p2 = fe.HostPipeline(M, N, laplacian=lap_p, bilateral=bil_p, l_max=wl.l_max,
+                                 src_dtype=torch.float64, device=dev, outputs=outs,
+                                 index_dtype=torch.int32)
+            p2.run(host)
+            barrier()
+            e0.record(stream)
+            for _ in range(e2e_steps):
+                p2.run(host)
+            e1.record(stream)
+            barrier()
+            tc = D.max_over_ranks(e0.elapsed_time(e1), dev)
+            e2e[key] = {"value": world * FE * e2e_steps / (tc / 1e3), "unit": "frames/s",
+                        "h2d_bytes_per_step": int(p2.h2d_bytes),
+                        "d2h_bytes_per_step": int(p2.d2h_bytes), "outputs": list(outs),
+                        "index_dtype": "int32 (non-reference)"}
+            del p2
+        # ---- the unchanged pipeline.py:125-134 sequence through the drop-in API: NumPy f64
+        # in and out, one frame per call (default precision: strict for float64 input)
+        if not args.no_e2e_dropin:
+            e2e["dropin"] = dropin_e2e(fe, wl, host[0].numpy(), dev)
 
     if rank != 0:
         return 0
@@ -417,10 +572,15 @@ def run_ours(args, rank, world, local_rank, wl):
                    "ops_per_launch": fp32_ops, "peak_source": fp32_src,
                    "note": f"{pairs_per_quad} directed pairs per quad x 15 FP32 lane-ops "
                            "(6 differences, 6 squared-distance, 3 accumulate) + 1 MUFU ex2"}
-    cpu = None
+    strict = None
+    if not args.no_strict:
+        strict = strict_throughput(fe, wl, eng, args, dev)
+    cpu = parity = None
     if world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference(steps=3, warmup=0, budget_s=25.0, wl=wl)
+        cb, sample = cpu_reference(steps=1, warmup=0, budget_s=25.0, wl=wl, want_sample=True)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        if sample is not None:
+            parity = {"chained": chained_parity(sample, wl, dev)}
     launches = eng.kernel_launches * args.steps
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
@@ -440,6 +600,7 @@ def run_ours(args, rank, world, local_rank, wl):
                       "timed step runs the same launches on one stream (opcfe_front_end)",
         "frame_hbm_frac": round(ab["frame_total"] * F / (max_ms / args.steps / 1e3) / 1e9 / peak, 4),
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+        "parity": parity, "strict": strict,
         "clocks": clk.summary(), "n_tri_per_frame": T,
     }
     print(json.dumps(line), flush=True)
@@ -459,6 +620,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-e2e-files", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e-dropin", action="store_true")
+    ap.add_argument("--no-strict", action="store_true",
+                    help="skip the strict (fp64 reference-chain) device throughput leg")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -1,35 +1,62 @@
-"""The REFERENCE's own CPU front-end, for the CPU baseline -- TEST/BENCH INFRASTRUCTURE ONLY.
+"""The REFERENCE's own CPU front-end, timed for the CPU baseline -- BENCH INFRASTRUCTURE ONLY.
 
-Sequence of pipeline.run_scene's organized branch (pipeline.py:125-134):
-    laplacian_filter_opc -> mesh_from_opc -> bilateral_filter_opc
-with the reference's compiled kernels (oracle/_ref/_native.so, built by
-oracle/build_ref.sh from /root/reference/pkg/src/flatpoly/_kernels/_native.pyx
-with the reference's own flags) for the two hot loops -- laplacian_filter
-(_native.pyx:225) and bilateral_iterate (_native.pyx:287) -- and the NumPy
-restatement in flatpoly_oracle for the parts the reference itself runs in NumPy
-(triangles / twins / normals / FC data / gather, mesh.py + smoothing.py).
+The stock code path: the unmodified reference package installed in baseline/_ref
+(baseline/install_ref.sh: pip install of /root/reference/pkg, its Cython kernels built
+by its own setup.py) running the organized branch of pipeline.run_scene
+(pipeline.py:125-134) through its public API, one WHOLE frame per process:
 
-If oracle/_ref is missing (reference not built), the C restatement
-(oracle/opc_oracle.c) is used and the baseline is reported as kind "port".
-Only bench.py's cpu_baseline / --impl reference legs call this.
+    sm   = smoothing.laplacian_filter_opc(opc, LaplacianParams)         (smoothing.py:53)
+    mesh = mesh.mesh_from_opc(sm)                                        (mesh.py:167)
+    mesh.normals = smoothing.bilateral_filter_opc(sm, BilateralParams, mesh.trimap)
+
+The reference has no intra-frame parallelism (its _native.pyx loops are serial), so its
+best multi-core mode is one frame per process.  Math libraries
+are single-threaded per process.
+
+If baseline/_ref is missing, the reference's compiled kernels alone (oracle/_ref,
+oracle/build_ref.sh) with the NumPy restatement around them are used ("reference-
+kernels"), else the C restatement ("port").  Only bench.py's cpu_baseline /
+--impl reference legs call this.
 """
 
 from __future__ import annotations
 
 import importlib.util
 import os
+import sys
 import time
 
 import numpy as np
 
-from . import flatpoly_oracle as fo
-
 _HERE = os.path.dirname(os.path.abspath(__file__))
+_REPO = os.path.dirname(_HERE)
+REF_DIR = os.path.join(_REPO, "baseline", "_ref")
+STUBS = os.path.join(_REPO, "tests", "golden", "_stubs")   # shapely import stub
+_FLATPOLY = None
 _NATIVE = None
 
 
+def flatpoly():
+    """The installed reference package (baseline/_ref), native backend, or None."""
+    global _FLATPOLY
+    if _FLATPOLY is None and os.path.isdir(os.path.join(REF_DIR, "flatpoly")):
+        for p in (STUBS, REF_DIR):
+            if p not in sys.path:
+                sys.path.insert(0, p)
+        os.environ.pop("FLATPOLY_PURE", None)
+        os.environ.pop("FLATPOLY_CUDA", None)
+        import flatpoly as fp
+        import flatpoly.mesh  # noqa: F401
+        import flatpoly.smoothing  # noqa: F401
+        if fp.kernel_backend != "native":
+            raise RuntimeError(f"baseline/_ref: kernel backend {fp.kernel_backend!r}, "
+                               "expected the compiled 'native' one")
+        _FLATPOLY = fp
+    return _FLATPOLY
+
+
 def native():
-    """The reference's compiled _native module, or None."""
+    """The reference's compiled _native module from oracle/_ref, or None."""
     global _NATIVE
     if _NATIVE is None:
         so = os.path.join(_HERE, "_ref", "_native.so")
@@ -43,17 +70,55 @@ def native():
 
 
 def kind() -> str:
+    if flatpoly() is not None:
+        return "reference"
     return "reference" if native() is not None else "port"
 
 
-def front_end(opc, lap=(1.0, 3, 10), bil=(0.1, 0.15, 3, 5)):
-    """One frame through the reference's CPU implementation; returns stage timings (s)."""
-    nat = native()
-    t = {}
+def path_name() -> str:
+    if flatpoly() is not None:
+        return ("the stock reference (baseline/_ref flatpoly, native Cython backend): "
+                "smoothing.laplacian_filter_opc -> mesh.mesh_from_opc -> "
+                "smoothing.bilateral_filter_opc (pipeline.py:125-134)")
+    if native() is not None:
+        return ("the reference's compiled kernels (oracle/_ref) + NumPy restatement of "
+                "mesh.py / smoothing.py (baseline/_ref missing)")
+    return "the C restatement oracle/opc_oracle.c (reference not built)"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def front_end(opc, lap=(1.0, 3, 10), bil=(0.1, 0.15, 3, 5), want=False):
+    """One frame through the reference; returns (stage timings in s, T, outputs or None)."""
+    fp = flatpoly()
     t0 = time.perf_counter()
-    opc = np.ascontiguousarray(opc, dtype=np.float64)
-    if nat is not None:
-        sm = nat.laplacian_filter(opc, float(lap[0]), int(lap[1]), int(lap[2])) if lap else opc
+    opc = np.asarray(opc, dtype=np.float64)
+    if fp is not None:
+        from flatpoly.mesh import mesh_from_opc
+        from flatpoly.smoothing import (BilateralParams, LaplacianParams, bilateral_filter_opc,
+                                        laplacian_filter_opc)
+        sm = laplacian_filter_opc(opc, LaplacianParams(*lap)) if lap else opc
+        t1 = time.perf_counter()
+        mesh = mesh_from_opc(sm)
+        t2 = time.perf_counter()
+        if bil:
+            mesh.normals = bilateral_filter_opc(sm, BilateralParams(*bil), mesh.trimap)
+        tris, trimap, he, normals = mesh.triangles, mesh.trimap, mesh.halfedges, mesh.normals
+    elif native() is not None:
+        from . import flatpoly_oracle as fo
+        nat = native()
+        sm = nat.laplacian_filter(np.ascontiguousarray(opc), float(lap[0]), int(lap[1]),
+                                  int(lap[2])) if lap else opc
         t1 = time.perf_counter()
         tris, trimap = fo.extract_triangles_opc(sm)
         he = fo.extract_halfedges_opc(trimap, sm.shape[0], sm.shape[1])
@@ -77,8 +142,13 @@ def front_end(opc, lap=(1.0, 3, 10), bil=(0.1, 0.15, 3, 5)):
             cen, nrm = c_oracle.compute_fc_triangle_data(sm)
             normals = c_oracle.gather(c_oracle.bilateral_iterate(cen, nrm, *bil), trimap, len(tris))
     t3 = time.perf_counter()
-    t.update(laplacian=t1 - t0, front_end=t2 - t1, bilateral=t3 - t2, total=t3 - t0)
-    return t, len(tris)
+    t = dict(laplacian=t1 - t0, front_end=t2 - t1, bilateral=t3 - t2, total=t3 - t0)
+    out = None
+    if want:
+        out = dict(smoothed=np.asarray(sm), trimap=np.asarray(trimap),
+                   n_halfedges_linked=int((np.asarray(he) >= 0).sum()),
+                   normals=np.asarray(normals))
+    return t, len(tris), out
 
 
 # ---------------------------------------------------------------- pool worker
@@ -87,46 +157,42 @@ _POOL_FRAME = None
 
 def _init_worker(frame):
     global _POOL_FRAME
-    os.environ["OMP_NUM_THREADS"] = "1"
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
     _POOL_FRAME = frame
-    native()
+    kind()                                  # import the reference once per process
 
 
 def _work(args):
-    row0, rows, lap, bil = args
-    sub = _POOL_FRAME[row0:row0 + rows]
-    t, _ = front_end(sub, lap, bil)
-    return t["total"]
+    frames, lap, bil, want = args
+    total, outs = 0.0, None
+    for i in range(frames):
+        t, _, o = front_end(_POOL_FRAME, lap, bil, want=want and i == 0)
+        total += t["total"]
+        outs = outs or o
+    return total, outs
 
 
 class ReferencePool:
-    """Process pool running the reference front-end on row strips of one frame.
+    """One process per host core, each running the reference on WHOLE frames."""
 
-    The reference has no intra-frame parallelism (the _native.pyx loops are serial),
-    so its best multi-core mode is one independent task per process.  A task is a
-    horizontal strip of `rows` rows of the frame; a strip costs the same per pixel
-    as the full frame (+ a 1-row overlap per strip, negligible), so a step of
-    W strips of R rows credits W*R/M frames.
-    """
-
-    def __init__(self, frame, workers, rows, lap, bil):
+    def __init__(self, frame, workers, lap, bil, frames_per_task=1):
         import multiprocessing as mp
         self.frame = frame
         self.workers = workers
-        self.rows = rows
         self.lap, self.bil = lap, bil
+        self.per_task = frames_per_task
         ctx = mp.get_context("fork")
         self.pool = ctx.Pool(workers, initializer=_init_worker, initargs=(frame,))
 
-    def step(self):
-        M = self.frame.shape[0]
-        tasks = []
-        for w in range(self.workers):
-            row0 = (w * self.rows) % max(1, M - self.rows)
-            tasks.append((row0, self.rows, self.lap, self.bil))
+    def step(self, want_sample=False):
+        """All workers run `frames_per_task` whole frames; -> (seconds, frames, sample)."""
+        tasks = [(self.per_task, self.lap, self.bil, want_sample and w == 0)
+                 for w in range(self.workers)]
         t0 = time.perf_counter()
-        self.pool.map(_work, tasks, chunksize=1)
-        return time.perf_counter() - t0, self.workers * self.rows / M
+        res = self.pool.map(_work, tasks, chunksize=1)
+        dt = time.perf_counter() - t0
+        return dt, self.workers * self.per_task, res[0][1]
 
     def close(self):
         self.pool.close()
