@@ -377,6 +377,18 @@ def dropin_e2e(fe, wl, frame, dev, frames=3):
                     "float64 (pageable) arrays, one frame per call, host wall clock"}
 
 
+def gpu_index(local_rank, args):
+    """The rank's CUDA device: LOCAL_RANK, or LOCAL_RANK % device_count under --share-gpus."""
+    import torch
+    n = torch.cuda.device_count()
+    if args.share_gpus:
+        return local_rank % max(n, 1)
+    if local_rank >= n:
+        raise SystemExit(f"LOCAL_RANK {local_rank} but only {n} CUDA device(s); "
+                         "use --share-gpus for a dry run")
+    return local_rank
+
+
 def run_ours(args, rank, world, local_rank, wl):
     import torch
     import torch.distributed as dist
@@ -384,8 +396,9 @@ def run_ours(args, rank, world, local_rank, wl):
     import paper_2007_12065_b200 as fe
     from paper_2007_12065_b200 import distributed as D
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    gpu = gpu_index(local_rank, args)
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     M, N = wl.M, wl.N
     lap_p = fe.LaplacianParams(*wl.lap) if wl.lap else None
     bil_p = fe.BilateralParams(*wl.bil) if wl.bil else None
@@ -425,7 +438,7 @@ def run_ours(args, rank, world, local_rank, wl):
     barrier()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(gpu) as clk:
         barrier()
         t_start.record(stream)
         for k in range(args.steps):
@@ -450,6 +463,15 @@ def run_ours(args, rank, world, local_rank, wl):
     T = int(eng.n_tri[0].item())
     # max over ranks (device time)
     max_ms = D.max_over_ranks(elapsed_ms, dev)
+    dist_info = None
+    if world > 1:
+        dist_info = {"backend": dist.get_backend(), "world": world,
+                     "frames_this_rank": F, "frames_all_ranks": int(D.sum_over_ranks(F, dev)),
+                     "devices_visible": torch.cuda.device_count(),
+                     "shared_gpu": bool(args.share_gpus)}
+        if args.share_gpus:
+            dist_info["note"] = ("ranks share GPUs (--share-gpus): a plumbing check of the "
+                                 "multi-rank path, NOT a scaling measurement")
     value = (wl.total if wl.total else world * F) * args.steps / (max_ms / 1e3)
 
     # ---------------- e2e through the host API (pinned f64 host frames -> outputs on host)
@@ -551,8 +573,13 @@ def run_ours(args, rank, world, local_rank, wl):
     dom = max(share, key=share.get)
     bytes_pl, ms_pl, _ = per_kernel[dom]
     achieved = bytes_pl / (ms_pl / 1e3) / 1e9
-    tr = load_traffic().get(dom)  # ncu --set full DRAM bytes (profiles/traffic.json)
+    # ncu --set full DRAM bytes of this kernel (profiles/traffic.json), captured at the
+    # bench's own batch (16 C4 frames); other batch sizes scale the per-frame figure
+    tr = load_traffic().get(dom)
     traffic = None if tr is None else round(tr["dram_bytes_per_launch_per_frame"] * F)
+    traffic_src = None if tr is None else (
+        f"{tr['capture']}: ncu --set full at {tr['frames']} frames"
+        + ("" if tr["frames"] == F else f", scaled to {F} frames"))
     kernels = {k: {"bytes_per_launch": b, "ms_per_launch": round(ms, 4),
                    "GBps": round(b / (ms / 1e3) / 1e9, 1),
                    "frac": round(b / (ms / 1e3) / 1e9 / peak, 3), "launches_per_step": n}
@@ -589,7 +616,10 @@ def run_ours(args, rank, world, local_rank, wl):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(F, wl),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": traffic, "peak_source": peak_src,
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "traffic_over_algorithmic": (None if traffic is None
+                                                  else round(traffic / bytes_pl, 3)),
+                     "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_pl,
                      "note": "algorithmic bytes per SURVEY.md 8d (unfused); fusion can make "
                              "achieved exceed DRAM traffic",
@@ -600,7 +630,7 @@ def run_ours(args, rank, world, local_rank, wl):
                       "timed step runs the same launches on one stream (opcfe_front_end)",
         "frame_hbm_frac": round(ab["frame_total"] * F / (max_ms / args.steps / 1e3) / 1e9 / peak, 4),
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
-        "parity": parity, "strict": strict,
+        "parity": parity, "strict": strict, "distributed": dist_info,
         "clocks": clk.summary(), "n_tri_per_frame": T,
     }
     print(json.dumps(line), flush=True)
@@ -621,6 +651,10 @@ def main():
     ap.add_argument("--no-e2e-files", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e-dropin", action="store_true")
+    ap.add_argument("--share-gpus", action="store_true",
+                    help="dry run of the multi-rank path on fewer GPUs than ranks: rank r uses "
+                         "GPU LOCAL_RANK %% device_count, gloo for the timing collectives "
+                         "(plumbing check, NOT a scaling measurement)")
     ap.add_argument("--no-strict", action="store_true",
                     help="skip the strict (fp64 reference-chain) device throughput leg")
     args = ap.parse_args()
@@ -637,8 +671,15 @@ def main():
     if world > 1:
         import torch.distributed as dist
         import torch
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        gpu = gpu_index(local_rank, args)
+        torch.cuda.set_device(gpu)
+        # NCCL refuses two ranks on one device: the shared-GPU dry run uses gloo (the only
+        # collectives are the barrier and the max-over-ranks of a scalar)
+        backend = os.environ.get("OPCFE_DIST_BACKEND") or ("gloo" if args.share_gpus else "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
     try:
         return run_ours(args, rank, world, local_rank, wl)
     finally:

@@ -20,8 +20,15 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(os.path.dirname(HERE), "gpurun_out")
-FRAMES = 2  # collect.sh profiles bench.py --frames 2
+FRAMES = 16  # collect.sh profiles bench.py --frames 16 (the bench's own C4 batch)
+LAP_ITERS = 10  # C4
 BIL_ITERS = 5  # C4
+# capture -> (name, frames in the launch)
+CAPTURES = (("lap1", "laplacian_kernel_pass1", FRAMES), ("lap", "laplacian_kernel", FRAMES),
+            ("tri", "triangulate_kernel", FRAMES), ("bil", "bilateral_kernel", FRAMES),
+            ("bil1", "bilateral_kernel_iter1", FRAMES), ("qx", "quad_extras_kernel (C3)", 512),
+            ("lap64", "laplacian_f64_kernel (strict)", FRAMES),
+            ("bil64", "bilateral_f64_kernel (strict)", FRAMES))
 
 METRICS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -70,6 +77,8 @@ def launch_shares(path):
             name = r[ki].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
             if name == "bilateral_packed_kernel":
                 name = "bilateral_kernel"  # one bench stage: iteration 1 + packed 2..B
+            if name == "laplacian3p_kernel" or name == "laplacian3_kernel":
+                name = "laplacian_kernel"  # one bench stage: pass 1 + packed passes 2..L
             agg[name].append(float(r[vi].replace(",", "")))
     tot = sum(sum(v) for v in agg.values())
     return {k: (len(v), sum(v) / len(v), sum(v) / tot) for k, v in agg.items()}
@@ -78,7 +87,8 @@ def launch_shares(path):
 def main(tag):
     lines = [f"# ncu summary {tag}", "",
              "Command: `python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline "
-             f"--frames {FRAMES}` (1080x1920, lap 10 + bil 5).  Launch-list times are "
+             f"--no-strict --frames {FRAMES}` (1080x1920, lap 10 + bil 5; 16 frames = the "
+             "bench's own batch, inputs 398 MB > L2).  Launch-list times are "
              "cold-cache and serialised: compare SHARES with bench.py's stage times.", ""]
     lp = os.path.join(OUT, f"{tag}_launches.csv")
     if os.path.exists(lp):
@@ -89,13 +99,14 @@ def main(tag):
             lines.append(f"| {k} | {n} | {mean / 1e3:.1f} | {share:.3f} |")
         lines.append("")
     traffic = {}
-    for short, kname in (("lap", "laplacian_kernel"), ("tri", "triangulate_kernel"),
-                         ("bil", "bilateral_kernel"), ("bil1", "bilateral_kernel_iter1")):
+    for short, kname, frames in CAPTURES:
         rep = os.path.join(OUT, f"{tag}_{short}.ncu-rep")
         if not os.path.exists(rep):
             continue
         d = raw_metrics(rep)
-        lines += [f"## {kname} (`--set full`, one launch, {FRAMES} frames)", "",
+        if "dram__bytes_read.sum" not in d:
+            continue
+        lines += [f"## {kname} (`--set full`, one launch, {frames} frames)", "",
                   f"`{d.get('kernel', '?')[:140]}`", "", "| metric | value |", "|---|---|"]
         for m in METRICS:
             if m in d:
@@ -106,8 +117,8 @@ def main(tag):
         unit = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         rb = float(d["dram__bytes_read.sum"][0]) * unit[d["dram__bytes_read.sum"][1]]
         wb = float(d["dram__bytes_write.sum"][0]) * unit[d["dram__bytes_write.sum"][1]]
-        traffic[kname] = {"dram_bytes_per_launch_per_frame": (rb + wb) / FRAMES,
-                          "dram_read_bytes": rb, "dram_write_bytes": wb, "frames": FRAMES,
+        traffic[kname] = {"dram_bytes_per_launch_per_frame": (rb + wb) / frames,
+                          "dram_read_bytes": rb, "dram_write_bytes": wb, "frames": frames,
                           "capture": f"profiles/{tag}_summary.md"}
     if "bilateral_kernel_iter1" in traffic and "bilateral_kernel" in traffic:
         # the bench's bilateral "launch" is the stage / B: iteration 1 + (B-1) packed ones
@@ -117,6 +128,15 @@ def main(tag):
             b1["dram_bytes_per_launch_per_frame"] + (BIL_ITERS - 1) * bp["dram_bytes_per_launch_per_frame"]
         ) / BIL_ITERS
         bp["note"] = f"mean over the {BIL_ITERS} launches: iteration 1 + {BIL_ITERS - 1} packed"
+        bp["iteration1_bytes_per_frame"] = b1["dram_bytes_per_launch_per_frame"]
+    if "laplacian_kernel_pass1" in traffic and "laplacian_kernel" in traffic:
+        l1 = traffic.pop("laplacian_kernel_pass1")
+        lp = traffic["laplacian_kernel"]
+        lp["dram_bytes_per_launch_per_frame"] = (
+            l1["dram_bytes_per_launch_per_frame"] + (LAP_ITERS - 1) * lp["dram_bytes_per_launch_per_frame"]
+        ) / LAP_ITERS
+        lp["note"] = f"mean over the {LAP_ITERS} launches: pass 1 + {LAP_ITERS - 1} packed"
+        lp["pass1_bytes_per_frame"] = l1["dram_bytes_per_launch_per_frame"]
     with open(os.path.join(HERE, f"{tag}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(os.path.join(HERE, "traffic.json"), "w") as f:

@@ -56,7 +56,24 @@ def _worker(rank, world, port, q):
         start, stop, counts = D.run_sharded(frames, process, batch=3, info=info)
         t = D.max_over_ranks(1.0 + rank)
         total = D.sum_over_ranks(len(counts))
-        q.put((rank, start, stop, counts, t, total))
+        # real per-frame outputs: every rank meshes its shard of 7 small NaN-holed frames
+        # (the front end's CPU restatement stands in for the GPU, which is absent here),
+        # results gathered at their global frame offsets
+        from oracle import c_oracle
+        rng = np.random.default_rng(3)
+        opcs = rng.normal(size=(7, 9, 11, 3))
+        opcs[rng.random((7, 9, 11)) < 0.2] = np.nan
+
+        def mesh(chunk):
+            out = []
+            for o in chunk:
+                r = c_oracle.front_end(o, (1.0, 3, 2), (0.1, 0.15, 3, 1))
+                out.append((r["triangles"], r["halfedges"], r["normals"]))
+            return out
+
+        s2, e2, meshes = D.run_sharded(opcs, mesh, batch=2, info=info)
+        allm = D.gather_shards(s2, meshes)
+        q.put((rank, start, stop, counts, t, total, (s2, e2), allm))
     finally:
         dist.destroy_process_group()
 
@@ -69,12 +86,25 @@ def test_two_rank_gloo_sharding_and_timing():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = sorted(q.get(timeout=120) for _ in range(world))
+    out = sorted((q.get(timeout=180) for _ in range(world)), key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (r0, a0, b0, c0, t0, n0), (r1, a1, b1, c1, t1, n1) = out
+    (r0, a0, b0, c0, t0, n0, sh0, m0), (r1, a1, b1, c1, t1, n1, sh1, m1) = out
     assert (a0, b0, a1, b1) == (0, 5, 5, 10)
     assert c0 + c1 == [i * 60 for i in range(10)]      # every frame processed once, in order
     assert t0 == t1 == 2.0                               # max over ranks
     assert n0 == n1 == 10
+    assert (sh0, sh1) == ((0, 4), (4, 7))
+    # both ranks hold all 7 meshes at their global offsets, equal to one process's
+    from oracle import c_oracle
+    rng = np.random.default_rng(3)
+    opcs = rng.normal(size=(7, 9, 11, 3))
+    opcs[rng.random((7, 9, 11)) < 0.2] = np.nan
+    for f in range(7):
+        r = c_oracle.front_end(opcs[f], (1.0, 3, 2), (0.1, 0.15, 3, 1))
+        for m in (m0, m1):
+            tri, he, nrm = m[f]
+            assert np.array_equal(tri, r["triangles"]) and np.array_equal(he, r["halfedges"])
+            assert np.array_equal(np.isnan(nrm), np.isnan(r["normals"]))
+            assert np.array_equal(np.nan_to_num(nrm), np.nan_to_num(r["normals"]))
