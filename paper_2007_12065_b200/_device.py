@@ -6,6 +6,8 @@ buffers, move bytes between host and device, and supply the current CUDA stream.
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -36,6 +38,114 @@ def fc_pitch(N: int) -> int:
     return (6 * (N - 1) + 3) // 4 * 4
 
 
+class HostTransfer:
+    """Large host <-> device copies for the NumPy drop-in API, through a ring of pinned
+    staging chunks with the host-side memcpy spread over threads.
+
+    A D2H straight into a fresh NumPy array runs at ~2 GB/s on the B200 box (the driver's
+    pageable path page-faults the destination as it copies); pinned D2H runs at ~57 GB/s
+    and a host thread first-touches + copies at ~8 GB/s, so chunks are DMA'd into pinned
+    slots on a side stream while `THREADS` threads copy finished slots into the NumPy
+    array (numpy releases the GIL for the copy).  H2D is the mirror image.  Small arrays
+    take the plain path.
+    """
+
+    CHUNK = 8 << 20
+    SLOTS = 8
+    MIN_BYTES = 4 << 20
+    _inst = {}
+
+    def __init__(self, device):
+        from concurrent.futures import ThreadPoolExecutor
+        self.device = device
+        self.stage = [torch.empty(self.CHUNK, dtype=torch.uint8, pin_memory=True)
+                      for _ in range(self.SLOTS)]
+        self.stage_np = [t.numpy() for t in self.stage]
+        self.stream = torch.cuda.Stream(device=device)
+        self.events = [torch.cuda.Event() for _ in range(self.SLOTS)]
+        self.pool = ThreadPoolExecutor(self.SLOTS)
+        self.lock = threading.Lock()         # one transfer at a time per device (shared slots)
+
+    @classmethod
+    def get(cls, device) -> "HostTransfer":
+        key = torch.device(device).index or 0
+        if key not in cls._inst:
+            cls._inst[key] = cls(torch.device("cuda", key))
+        return cls._inst[key]
+
+    def to_numpy(self, t: torch.Tensor) -> np.ndarray:
+        """Device tensor -> a new NumPy array (synchronous, like t.cpu().numpy())."""
+        t = t.contiguous()
+        nbytes = t.numel() * t.element_size()
+        if nbytes < self.MIN_BYTES:
+            return t.cpu().numpy()
+        out = np.empty(tuple(t.shape), dtype=torch.empty((), dtype=t.dtype).numpy().dtype)
+        with self.lock:
+            self._d2h(t, out, nbytes)
+        return out
+
+    def _d2h(self, t, out, nbytes):
+        src = t.reshape(-1).view(torch.uint8)
+        dst = out.reshape(-1).view(np.uint8)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        futs = [None] * self.SLOTS
+        for i, a in enumerate(range(0, nbytes, self.CHUNK)):
+            b = min(nbytes, a + self.CHUNK)
+            k = i % self.SLOTS
+            if futs[k] is not None:
+                futs[k].result()                      # the slot's previous chunk is copied out
+            with torch.cuda.stream(self.stream):
+                self.stage[k][:b - a].copy_(src[a:b], non_blocking=True)
+                self.events[k].record(self.stream)
+            ev, stg = self.events[k], self.stage_np[k]
+            futs[k] = self.pool.submit(lambda ev=ev, stg=stg, a=a, b=b: (
+                ev.synchronize(), np.copyto(dst[a:b], stg[:b - a])))
+        for f in futs:
+            if f is not None:
+                f.result()
+
+    def to_device(self, arr: np.ndarray, dtype=None) -> torch.Tensor:
+        """A contiguous NumPy array -> a new device tensor (ordered before later work on
+        the current stream)."""
+        arr = np.ascontiguousarray(arr)
+        t_host = torch.from_numpy(arr)
+        if arr.nbytes < self.MIN_BYTES:
+            return t_host.to(self.device)
+        out = torch.empty(tuple(arr.shape), dtype=t_host.dtype, device=self.device)
+        with self.lock:
+            self._h2d(arr, out)
+        return out
+
+    def _h2d(self, arr, out):
+        src = arr.reshape(-1).view(np.uint8)
+        dst = out.reshape(-1).view(torch.uint8)
+        nbytes = arr.nbytes
+        chunks = list(range(0, nbytes, self.CHUNK))
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
+        fill = {}
+
+        def stage_in(i):
+            a = chunks[i]
+            b = min(nbytes, a + self.CHUNK)
+            k = i % self.SLOTS
+            np.copyto(self.stage_np[k][:b - a], src[a:b])
+            return a, b, k
+
+        for i in range(min(self.SLOTS, len(chunks))):
+            fill[i] = self.pool.submit(stage_in, i)
+        for i in range(len(chunks)):
+            a, b, k = fill.pop(i).result()
+            with torch.cuda.stream(self.stream):
+                dst[a:b].copy_(self.stage[k][:b - a], non_blocking=True)
+                self.events[k].record(self.stream)
+            if i + self.SLOTS < len(chunks):
+                ev = self.events[k]
+                fill[i + self.SLOTS] = self.pool.submit(
+                    lambda ev=ev, j=i + self.SLOTS: (ev.synchronize(), stage_in(j))[1])
+        torch.cuda.current_stream(self.device).wait_stream(self.stream)
+        self.stream.synchronize()                      # staging slots reusable by the caller
+
+
 class Staged:
     """An input array on the device plus how to hand results back to the caller."""
 
@@ -47,8 +157,7 @@ class Staged:
             if float_only and arr.dtype not in (np.float32, np.float64):
                 arr = arr.astype(np.float64)
             self.out_dtype = torch.float64 if float_only else None
-            t = torch.from_numpy(np.ascontiguousarray(arr))
-            self.dev = t.to("cuda", non_blocking=False)
+            self.dev = HostTransfer.get(torch.cuda.current_device()).to_device(arr)
         else:
             t = x
             if float_only and t.dtype not in (torch.float32, torch.float64):
@@ -64,7 +173,7 @@ class Staged:
         if self.numpy:
             if self.out_dtype is not None and t.is_floating_point():
                 t = t.to(self.out_dtype)
-            return t.cpu().numpy()
+            return HostTransfer.get(t.device).to_numpy(t)
         return t
 
 
