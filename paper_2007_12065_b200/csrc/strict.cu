@@ -7,9 +7,10 @@
 //                   setup.py:24-26), neighbours in the same du-outer / dv-inner order.
 //   bilateral_f64   _kernels.bilateral_iterate (_native.pyx:287-364; _fallback.py:120-166)
 //                   + the trimap gather of bilateral_filter_opc (smoothing.py:108-114):
-//                   same arithmetic and accumulation order; only exp() differs (CUDA's
-//                   vs libm's, both <= 1 ulp -- the reference's own two backends differ
-//                   by as much).
+//                   same accumulation order; fp64 throughout, FMA-contracted products and
+//                   an own exp (exp_neg, ~2 ulp), so each weight is within a few ulp of
+//                   the reference's -- its own two backends differ by ~1 ulp already
+//                   (SURVEY.md App. A.5); chained C4 result within 1.5e-14.
 //   batched helpers the strict front end needs: FC data, triangle normals and l_max
 //   flags over F frames with per-frame live counts.
 //
@@ -34,13 +35,68 @@ constexpr int kSNT = kSTW * kSTH;
 constexpr int kSmemMax = 200 * 1024;
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000LL); }
+constexpr double kSentinel = 1e200;
+  // centroid of a skipped neighbour: |dc|^2 = inf -> w = 0
+
+// exp(x) for the bilateral weights, x <= 0 (global-memory path: the exponent
+// -dc2/(2 sl^2) - dn2/(2 sa^2)).  Cody-Waite reduction x = n ln2 + r, |r| <= ln2/2,
+// degree-13 Taylor polynomial (truncation < 2e-16 relative): within ~2 ulp of the correctly
+// rounded value (the reference's libm exp is within 1 ulp; its two backends differ by as
+// much).  x < -708 returns 0 (a weight < 1e-307 is invisible: the reference's |acc| >
+// 1e-30 test leaves a triangle whose weights are all that small unchanged, and next to
+// any larger weight it is below the last ulp); NaN passes through (poisons the sum, as in
+// the reference).
+__constant__ double kExpC[14] = {
+    1.0, 1.0, 1.0 / 2, 1.0 / 6, 1.0 / 24, 1.0 / 120, 1.0 / 720, 1.0 / 5040, 1.0 / 40320,
+    1.0 / 362880, 1.0 / 3628800, 1.0 / 39916800, 1.0 / 479001600, 1.0 / 6227020800.0};
+__device__ __forceinline__ double exp_neg(double x) {
+  if (x < -708.0) return 0.0;
+  const double n = rint(x * 1.4426950408889634);
+  double r = fma(n, -6.93147180369123816490e-01, x);   // ln2 hi (Cody-Waite split)
+  r = fma(n, -1.90821492927058770002e-10, r);          // ln2 lo
+  double p = kExpC[13];
+#pragma unroll
+  for (int k = 12; k >= 0; --k) p = fma(p, r, kExpC[k]);
+  return p * __hiloint2double(((int)n + 1023) << 20, 0);
+}
+
+__device__ __forceinline__ void exp_table_init(double* T) {  // T[j] = 2^(j/32)
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;
+  if (t < 32) T[t] = exp2((double)t / 32.0);
+}
+
+// 2^(y/32) for y <= 0 (the shared-memory path, whose features are prescaled so that the
+// weight is 2^(-t/32), t = |dc'|^2 + |dn'|^2): y = 32 m + j + f with n = rint(y), f = y - n
+// EXACT (|f| <= 1/2, no Cody-Waite split), j = n & 31, m = n >> 5; the result is
+// T[j] * 2^m * e^(f ln2/32) with T[j] = 2^(j/32) from a 32-entry shared table (2^m folded
+// into T[j]'s exponent bits: one integer add) and a degree-6 polynomial in f (truncation
+// < 4e-18) by Estrin's scheme (dependency depth 4).  Branch-free: y below -32704 (weight
+// < 2^-1022) selects 0; NaN propagates.  ~2 ulp.
+__constant__ double kExp2C[7] = {  // (ln2/32)^k / k!
+    1.0, 0.02166084939249829, 0.00023459619820224677, 1.6938509724371819e-06,
+    9.172562701824643e-09, 3.9737099845494154e-11, 1.4345655584131932e-13};
+__device__ __forceinline__ double exp2_32(double y, const double* T) {
+  const double n = rint(y);
+  const double f = y - n;                                   // exact
+  const int ni = (int)n;
+  const double f2 = f * f;
+  const double a = fma(kExp2C[1], f, kExp2C[0]);
+  const double b = fma(kExp2C[3], f, kExp2C[2]);
+  const double c = fma(kExp2C[5], f, kExp2C[4]);
+  const double ab = fma(b, f2, a);
+  const double cd = fma(kExp2C[6], f2, c);
+  const double p = fma(cd, f2 * f2, ab);
+  const double t = T[ni & 31];
+  const double s = __hiloint2double(__double2hiint(t) + ((ni >> 5) << 20), __double2loint(t));
+  return y < -32704.0 ? 0.0 : p * s;
+}
 
 // ------------------------------------------------------------------ Laplacian
 // in/out: [F][M][N][3].  HC > 0: compile-time half width; HC == 0: runtime h.
 // SMEM: the tile + halo is staged in three planes of (kSTH+2h) x (kSTW+2h) doubles;
 // out-of-grid cells hold NaN (the reference skips them; a NaN distance is skipped too).
 template <int HC, bool SMEM>
-__global__ void __launch_bounds__(kSNT) laplacian_f64_kernel(const double* __restrict__ in,
+__global__ void __launch_bounds__(kSNT, 5) laplacian_f64_kernel(const double* __restrict__ in,
                                                              double* __restrict__ out, int M,
                                                              int N, int h_rt, double lam) {
   const int h = HC > 0 ? HC : h_rt;
@@ -52,18 +108,21 @@ __global__ void __launch_bounds__(kSNT) laplacian_f64_kernel(const double* __res
   const int u = blockIdx.y * kSTH + ty, v = blockIdx.x * kSTW + tx;
   extern __shared__ double sm[];
   const int bw = kSTW + 2 * h, bh = kSTH + 2 * h, plane = bw * bh;
-  if (SMEM) {
+  if (SMEM) {  // one box point per thread and step: 3 loads, 3 planar stores
     const int u0 = blockIdx.y * kSTH - h, v0 = blockIdx.x * kSTW - h;
-    const int tid = ty * kSTW + tx;
-    const int rowlen = 3 * bw;
-    for (int i = tid; i < rowlen * bh; i += kSNT) {
-      const int r = i / rowlen, c3 = i - r * rowlen;
-      const int c = c3 / 3, comp = c3 - 3 * c;
+    for (int q = threadIdx.y * kSTW + threadIdx.x; q < plane; q += kSNT) {
+      const int r = q / bw, c = q - r * bw;
       const int uu = u0 + r, vv = v0 + c;
-      const double x = (uu >= 0 && uu < M && vv >= 0 && vv < N)
-                           ? src[((long long)uu * N + vv) * 3 + comp]
-                           : qnan();
-      sm[comp * plane + r * bw + c] = x;
+      double x = qnan(), y = qnan(), z = qnan();
+      if (uu >= 0 && uu < M && vv >= 0 && vv < N) {
+        const double* g = src + ((long long)uu * N + vv) * 3;
+        x = __ldg(g);
+        y = __ldg(g + 1);
+        z = __ldg(g + 2);
+      }
+      sm[q] = x;
+      sm[plane + q] = y;
+      sm[2 * plane + q] = z;
     }
     __syncthreads();
   }
@@ -112,7 +171,7 @@ __global__ void __launch_bounds__(kSNT) laplacian_f64_kernel(const double* __res
       const double dx = dsub(qx, px), dy = dsub(qy, py), dz = dsub(qz, pz);
       const double dist = __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
       if (!(dist > 0.0)) continue;  // NaN or <= 0 (:265-266)
-      const double w = __ddiv_rn(1.0, dist);
+      const double w = __drcp_rn(dist);  // correctly rounded 1/dist == the reference's 1.0/dist
       ax = dadd(ax, dmul(dx, w));
       ay = dadd(ay, dmul(dy, w));
       az = dadd(az, dmul(dz, w));
@@ -143,100 +202,47 @@ struct Bil64Args {
   long long out_rows;
   int Mq, Nq, h;
   double inv2sc, inv2ss;
+  double sC, sN;          // sqrt(32 log2(e) inv2sc), sqrt(32 log2(e) inv2ss): prescaled path
 };
 
-template <int HC, bool SMEM, typename OUT>
+// Global-memory path (windows too large for shared memory): neighbours read through L1,
+// the reference's own operation order, exp_neg.
+template <typename OUT>
 __global__ void __launch_bounds__(kSNT) bilateral_f64_kernel(Bil64Args a) {
-  const int h = HC > 0 ? HC : a.h;
+  const int h = a.h;
   const int Mq = a.Mq, Nq = a.Nq;
   const int f = blockIdx.z;
   const long long fs = 6ll * Mq * Nq;
   const double* cen = a.cen + f * fs;
   const double* nrm = a.nin + f * fs;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int u = blockIdx.y * kSTH + ty, v = blockIdx.x * kSTW + tx;
-  extern __shared__ double sm[];
-  const int bw = kSTW + 2 * h, bh = kSTH + 2 * h, plane = bw * bh;
-  // plane index: (k * 2 + {0 centroid, 1 normal}) * 3 + comp
-  if (SMEM) {
-    const int u0 = blockIdx.y * kSTH - h, v0 = blockIdx.x * kSTW - h;
-    const int tid = ty * kSTW + tx;
-    const int rowlen = 6 * bw;  // doubles of one array per box row
-    for (int i = tid; i < 2 * rowlen * bh; i += kSNT) {
-      const int arr = i >= rowlen * bh;  // 0 centroids, 1 normals
-      const int j = i - arr * rowlen * bh;
-      const int r = j / rowlen, c6 = j - r * rowlen;
-      const int c = c6 / 6, kc = c6 - 6 * c, k = kc / 3, comp = kc - 3 * k;
-      const int uu = u0 + r, vv = v0 + c;
-      const double* base = arr ? nrm : cen;
-      const double x = (uu >= 0 && uu < Mq && vv >= 0 && vv < Nq)
-                           ? base[((long long)uu * Nq + vv) * 6 + kc]
-                           : qnan();
-      sm[((k * 2 + arr) * 3 + comp) * plane + r * bw + c] = x;
-    }
-    __syncthreads();
-  }
+  const int u = blockIdx.y * kSTH + threadIdx.y, v = blockIdx.x * kSTW + threadIdx.x;
   if (u >= Mq || v >= Nq) return;
   const long long qo = ((long long)u * Nq + v) * 6;
-#pragma unroll 1
   for (int k = 0; k < 2; ++k) {
-    double cx, cy, cz, nx, ny, nz;
-    if (SMEM) {
-      const int c = (ty + h) * bw + tx + h;
-      cx = sm[((k * 2) * 3 + 0) * plane + c];
-      cy = sm[((k * 2) * 3 + 1) * plane + c];
-      cz = sm[((k * 2) * 3 + 2) * plane + c];
-      nx = sm[((k * 2 + 1) * 3 + 0) * plane + c];
-      ny = sm[((k * 2 + 1) * 3 + 1) * plane + c];
-      nz = sm[((k * 2 + 1) * 3 + 2) * plane + c];
-    } else {
-      cx = cen[qo + 3 * k];
-      cy = cen[qo + 3 * k + 1];
-      cz = cen[qo + 3 * k + 2];
-      nx = nrm[qo + 3 * k];
-      ny = nrm[qo + 3 * k + 1];
-      nz = nrm[qo + 3 * k + 2];
-    }
+    const double cx = cen[qo + 3 * k], cy = cen[qo + 3 * k + 1], cz = cen[qo + 3 * k + 2];
+    const double nx = nrm[qo + 3 * k], ny = nrm[qo + 3 * k + 1], nz = nrm[qo + 3 * k + 2];
     double rx = nx, ry = ny, rz = nz;  // NaN centre: kept (:313-318)
     if (!(nx != nx || ny != ny || nz != nz)) {
       double wsum = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
-#pragma unroll
       for (int du = -h; du <= h; ++du) {
         const int uu = u + du;
-        if (!SMEM && (uu < 0 || uu >= Mq)) continue;
-#pragma unroll
+        if (uu < 0 || uu >= Mq) continue;
         for (int dv = -h; dv <= h; ++dv) {
           const int vv = v + dv;
-          if (!SMEM && (vv < 0 || vv >= Nq)) continue;
-#pragma unroll
+          if (vv < 0 || vv >= Nq) continue;
           for (int kk = 0; kk < 2; ++kk) {
             if (du == 0 && dv == 0 && kk == k) continue;
-            double mx, my, mz, qx, qy, qz;
-            if (SMEM) {
-              const int c = (ty + h + du) * bw + tx + h + dv;
-              mx = sm[((kk * 2 + 1) * 3 + 0) * plane + c];
-              my = sm[((kk * 2 + 1) * 3 + 1) * plane + c];
-              mz = sm[((kk * 2 + 1) * 3 + 2) * plane + c];
-              qx = sm[((kk * 2) * 3 + 0) * plane + c];
-              qy = sm[((kk * 2) * 3 + 1) * plane + c];
-              qz = sm[((kk * 2) * 3 + 2) * plane + c];
-            } else {
-              const long long o = ((long long)uu * Nq + vv) * 6 + 3 * kk;
-              mx = __ldg(nrm + o);
-              my = __ldg(nrm + o + 1);
-              mz = __ldg(nrm + o + 2);
-              qx = __ldg(cen + o);
-              qy = __ldg(cen + o + 1);
-              qz = __ldg(cen + o + 2);
-            }
+            const long long o = ((long long)uu * Nq + vv) * 6 + 3 * kk;
+            const double mx = __ldg(nrm + o), my = __ldg(nrm + o + 1), mz = __ldg(nrm + o + 2);
             if (mx != mx || my != my || mz != mz) continue;  // (:337-338)
-            double dx = dsub(qx, cx), dy = dsub(qy, cy), dz = dsub(qz, cz);
+            double dx = dsub(__ldg(cen + o), cx), dy = dsub(__ldg(cen + o + 1), cy),
+                   dz = dsub(__ldg(cen + o + 2), cz);
             const double dc2 = dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
             dx = dsub(mx, nx);
             dy = dsub(my, ny);
             dz = dsub(mz, nz);
             const double dn2 = dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
-            const double w = exp(dsub(dmul(-dc2, a.inv2sc), dmul(dn2, a.inv2ss)));
+            const double w = exp_neg(dsub(dmul(-dc2, a.inv2sc), dmul(dn2, a.inv2ss)));
             ax = dadd(ax, dmul(mx, w));
             ay = dadd(ay, dmul(my, w));
             az = dadd(az, dmul(mz, w));
@@ -265,6 +271,215 @@ __global__ void __launch_bounds__(kSNT) bilateral_f64_kernel(Bil64Args a) {
       o[0] = rx;
       o[1] = ry;
       o[2] = rz;
+    }
+  }
+}
+
+// Shared-memory path (any window that fits): the tile + halo is staged once, then every
+// box triangle is PRESCALED in place -- c' = (c - o) sC with o a centroid of the tile
+// (tile-relative: c - o is exact for nearby values, so the scaling's rounding scales with
+// the tile extent, not the distance from the coordinate origin), n' = n sN -- so that the
+// weight is 2^(-t/32) with t = |c'_j - c'_i|^2 + |n'_j - n'_i|^2: exp2_32 needs no
+// Cody-Waite reduction and the exponent no scaling products.  Neighbours the reference
+// skips (NaN normal, off the grid) become sentinels (n' = 0, c' = 1e200: t = inf, w = 0):
+// no per-pair test.  wsum is not accumulated: wsum > 0 is implied by |acc| > 1e-30
+// (a NaN weight makes both tests false), here |acc'| > 1e-30 sN.  Products are
+// FMA-contracted and sums reordered relative to the reference -- results within a few
+// ulp (the 1e-13 bar of the strict tests).
+template <int HC, bool VEC, typename OUT>
+__global__ void __launch_bounds__(kSNT, 4) bilateral_f64s_kernel(Bil64Args a) {
+  const int h = HC > 0 ? HC : a.h;
+  const int Mq = a.Mq, Nq = a.Nq;
+  const int f = blockIdx.z;
+  const long long fs = 6ll * Mq * Nq;
+  const double* cen = a.cen + f * fs;
+  const double* nrm = a.nin + f * fs;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * kSTW + tx;
+  const int u = blockIdx.y * kSTH + ty, v = blockIdx.x * kSTW + tx;
+  extern __shared__ double sm[];
+  __shared__ double expT[32];
+  __shared__ double s_o[3];
+  __shared__ int s_first;
+  exp_table_init(expT);
+  const int bw = kSTW + 2 * h, bh = kSTH + 2 * h, plane = bw * bh;
+  // plane index: (k * 2 + {0 centroid, 1 normal}) * 3 + comp
+  const int u0 = blockIdx.y * kSTH - h, v0 = blockIdx.x * kSTW - h;
+  const double sC = a.sC, sN = a.sN;
+  // tile origin o: the tile's centre quad's triangle-0 centroid (read by every thread;
+  // one L1 line), so staging can prescale on the fly; a non-finite centre (rare: a NaN
+  // there) stages raw values first and picks the first finite centroid of the box
+  const int cu = min(blockIdx.y * kSTH + kSTH / 2, Mq - 1), cv = min(blockIdx.x * kSTW + kSTW / 2, Nq - 1);
+  const double* co = cen + ((long long)cu * Nq + cv) * 6;
+  double o[3] = {co[0], co[1], co[2]};
+  const bool direct = isfinite(o[0]) && isfinite(o[1]) && isfinite(o[2]);
+  // one box quad per thread and step: its 12 doubles (centroids, normals of both
+  // triangles; 2 x 48 contiguous bytes, 16-B loads when aligned) -> 12 planar slots.
+  // Skipped neighbours (NaN normal, off the grid) become sentinels: n' = 0, c' = 1e200
+  // (t = inf -> w = 0): no per-pair test in the loop.
+  for (int q = tid; q < plane; q += kSNT) {
+    const int r = q / bw, c = q - r * bw;
+    const int uu = u0 + r, vv = v0 + c;
+    double cv6[6], nv6[6];
+    if (uu >= 0 && uu < Mq && vv >= 0 && vv < Nq) {
+      const long long off = ((long long)uu * Nq + vv) * 6;
+      if (VEC) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const double2 x = __ldg(reinterpret_cast<const double2*>(cen + off) + j);
+          const double2 y = __ldg(reinterpret_cast<const double2*>(nrm + off) + j);
+          cv6[2 * j] = x.x;
+          cv6[2 * j + 1] = x.y;
+          nv6[2 * j] = y.x;
+          nv6[2 * j + 1] = y.y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+          cv6[j] = __ldg(cen + off + j);
+          nv6[j] = __ldg(nrm + off + j);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 6; ++j) cv6[j] = nv6[j] = qnan();
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      double* cb = sm + (k * 2) * 3 * plane + q;
+      double* nb = cb + 3 * plane;
+      const double* cc = cv6 + 3 * k;
+      const double* nn = nv6 + 3 * k;
+      if (!direct) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          cb[d * plane] = cc[d];
+          nb[d * plane] = nn[d];
+        }
+      } else if (isnan(nn[0]) || isnan(nn[1]) || isnan(nn[2])) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          cb[d * plane] = kSentinel;
+          nb[d * plane] = 0.0;
+        }
+      } else {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          cb[d * plane] = (cc[d] - o[d]) * sC;
+          nb[d * plane] = nn[d] * sN;
+        }
+      }
+    }
+  }
+  if (!direct) {  // uniform over the CTA: the rare NaN-centre tile
+    if (tid == 0) s_first = 0x7fffffff;
+    __syncthreads();
+    auto finite_c = [&](int i) {  // box triangle i = k * plane + cell
+      const int k = i >= plane, cell = i - k * plane;
+      const double* cb = sm + (k * 2) * 3 * plane + cell;
+      return isfinite(cb[0]) && isfinite(cb[plane]) && isfinite(cb[2 * plane]);
+    };
+    for (int i = tid; i < 2 * plane; i += kSNT)
+      if (finite_c(i)) {
+        atomicMin(&s_first, i);
+        break;
+      }
+    __syncthreads();
+    if (tid == 0) {
+      const int i = s_first;
+      const int k = i >= plane, cell = i - k * plane;
+      for (int d = 0; d < 3; ++d)
+        s_o[d] = i == 0x7fffffff ? 0.0 : sm[((k * 2) * 3 + d) * plane + cell];
+    }
+    __syncthreads();
+    for (int i = tid; i < 2 * plane; i += kSNT) {
+      const int k = i >= plane, cell = i - k * plane;
+      double* cb = sm + (k * 2) * 3 * plane + cell;
+      double* nb = cb + 3 * plane;
+      if (isnan(nb[0]) || isnan(nb[plane]) || isnan(nb[2 * plane])) {
+        nb[0] = nb[plane] = nb[2 * plane] = 0.0;
+        cb[0] = cb[plane] = cb[2 * plane] = kSentinel;
+      } else {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          cb[d * plane] = (cb[d * plane] - s_o[d]) * sC;
+          nb[d * plane] *= sN;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (u >= Mq || v >= Nq) return;
+  const long long qo = ((long long)u * Nq + v) * 6;
+  const double thr = 1e-30 * sN;
+#pragma unroll 1
+  for (int k = 0; k < 2; ++k) {
+    const int c0 = (ty + h) * bw + tx + h;
+    const double cx = sm[((k * 2) * 3 + 0) * plane + c0];
+    const double cy = sm[((k * 2) * 3 + 1) * plane + c0];
+    const double cz = sm[((k * 2) * 3 + 2) * plane + c0];
+    const double nx = sm[((k * 2 + 1) * 3 + 0) * plane + c0];
+    const double ny = sm[((k * 2 + 1) * 3 + 1) * plane + c0];
+    const double nz = sm[((k * 2 + 1) * 3 + 2) * plane + c0];
+    double ax = 0.0, ay = 0.0, az = 0.0;
+    bool moved = false;
+    if (cx != kSentinel) {
+#pragma unroll
+      for (int du = -h; du <= h; ++du) {
+#pragma unroll
+        for (int dv = -h; dv <= h; ++dv) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            if (du == 0 && dv == 0 && kk == k) continue;
+            const int c = (ty + h + du) * bw + tx + h + dv;
+            const double mx = sm[((kk * 2 + 1) * 3 + 0) * plane + c];
+            const double my = sm[((kk * 2 + 1) * 3 + 1) * plane + c];
+            const double mz = sm[((kk * 2 + 1) * 3 + 2) * plane + c];
+            const double qx = sm[((kk * 2) * 3 + 0) * plane + c];
+            const double qy = sm[((kk * 2) * 3 + 1) * plane + c];
+            const double qz = sm[((kk * 2) * 3 + 2) * plane + c];
+            const double ex = qx - cx, ey = qy - cy, ez = qz - cz;
+            const double fx = mx - nx, fy = my - ny, fz = mz - nz;
+            double t = ex * ex;
+            t = fma(ey, ey, t);
+            t = fma(ez, ez, t);
+            t = fma(fx, fx, t);
+            t = fma(fy, fy, t);
+            t = fma(fz, fz, t);
+            const double w = exp2_32(-t, expT);
+            ax = fma(mx, w, ax);
+            ay = fma(my, w, ay);
+            az = fma(mz, w, az);
+          }
+        }
+      }
+      const double norm = sqrt(fma(az, az, fma(ay, ay, ax * ax)));
+      moved = norm > thr;  // (:352-360); NaN -> unchanged
+      if (moved) {
+        ax /= norm;
+        ay /= norm;
+        az /= norm;
+      }
+    }
+    if (!moved) {  // unchanged (NaN / isolated / |acc| <= 1e-30): the input normal exactly
+      ax = nrm[qo + 3 * k];
+      ay = nrm[qo + 3 * k + 1];
+      az = nrm[qo + 3 * k + 2];
+    }
+    if (a.trimap != nullptr) {
+      const long long G = 2ll * Mq * Nq;
+      const long long t = a.trimap[f * G + 2ll * ((long long)u * Nq + v) + k];
+      if (t >= 0 && t < a.out_rows) {
+        OUT* o = static_cast<OUT*>(a.out_mesh) + (f * a.out_rows + t) * 3;
+        o[0] = (OUT)ax;
+        o[1] = (OUT)ay;
+        o[2] = (OUT)az;
+      }
+    } else {
+      double* o = a.nout + f * fs + qo + 3 * k;
+      o[0] = ax;
+      o[1] = ay;
+      o[2] = az;
     }
   }
 }
@@ -352,12 +567,19 @@ int lap_launch(const double* in, double* out, int F, int M, int N, int h, double
 
 template <int HC, bool SMEM, typename OUT>
 int bil_launch(const Bil64Args& a, int F, cudaStream_t st) {
-  const int smem = SMEM ? bil_smem(a.h) : 0;
-  int rc;
-  if ((rc = set_smem(bilateral_f64_kernel<HC, SMEM, OUT>, smem))) return rc;
   dim3 grid((a.Nq + kSTW - 1) / kSTW, (a.Mq + kSTH - 1) / kSTH, F);
-  bilateral_f64_kernel<HC, SMEM, OUT><<<grid, dim3(kSTW, kSTH), smem, st>>>(a);
-  return check_launch("bilateral_f64_kernel");
+  int rc;
+  if constexpr (SMEM) {
+    const int smem = bil_smem(a.h);
+    const bool vec = (reinterpret_cast<uintptr_t>(a.cen) | reinterpret_cast<uintptr_t>(a.nin)) % 16 == 0;
+    auto kern = vec ? bilateral_f64s_kernel<HC, true, OUT> : bilateral_f64s_kernel<HC, false, OUT>;
+    if ((rc = set_smem(kern, smem))) return rc;
+    kern<<<grid, dim3(kSTW, kSTH), smem, st>>>(a);
+    return check_launch("bilateral_f64s_kernel");
+  } else {
+    bilateral_f64_kernel<OUT><<<grid, dim3(kSTW, kSTH), 0, st>>>(a);
+    return check_launch("bilateral_f64_kernel");
+  }
 }
 
 template <typename OUT>
@@ -417,6 +639,8 @@ int bilateral_f64(const double* centroids, const double* normals_in, int F, int 
   // the reference's constants, same operation order (_native.pyx:295-296)
   a.inv2sc = 1.0 / (2.0 * sigma_length * sigma_length);
   a.inv2ss = 1.0 / (2.0 * sigma_angle * sigma_angle);
+  a.sC = std::sqrt(32.0 * 1.4426950408889634 * a.inv2sc);
+  a.sN = std::sqrt(32.0 * 1.4426950408889634 * a.inv2ss);
   a.out_rows = out_rows;
   const double* src = normals_in;
   for (int it = 0; it < iters; ++it) {
