@@ -17,6 +17,7 @@ separate streams.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -328,8 +329,8 @@ class HostPipeline:
     Two FrontEnd slots (each a CUDA graph over `frames_per_slot` frames) and three
     streams: chunk i+1's H2D and front end run while chunk i's outputs stream back (D2H).
     A frame's D2H is sized by its own triangle count (one event wait per chunk on the
-    host), so only live rows travel.  Small frames go several to a slot (default: ~8 MB
-    of input per slot), so the per-chunk host wait and launch latency are amortised.
+    host), so only live rows travel.  Small frames go several to a slot (default: ~32 MB
+    of input per slot, at most 64 frames; OPCFE_SLOT_MB / OPCFE_SLOT_MAX), so the per-chunk host wait and launch latency are amortised.
 
     outputs      which results come back (default: the drop-in set mesh_from_opc +
                  bilateral_filter_opc return -- smoothed grid, trimap, triangles,
@@ -357,7 +358,9 @@ class HostPipeline:
             raise ValueError("the labels output needs dominant_normals")
         if frames_per_slot is None:
             esz = torch.empty((), dtype=src_dtype).element_size()
-            frames_per_slot = max(1, min(16, (8 << 20) // (M * N * 3 * esz)))
+            frames_per_slot = max(1, min(int(os.environ.get("OPCFE_SLOT_MAX", "64")),
+                                         (int(os.environ.get("OPCFE_SLOT_MB", "32")) << 20)
+                                         // (M * N * 3 * esz)))
         self.k = k = int(frames_per_slot)
         self.outputs = outputs
         self.slots = [FrontEnd(M, N, k, laplacian=laplacian, bilateral=bilateral, l_max=l_max,
