@@ -53,6 +53,34 @@ inline bool is_ws(unsigned char c) {
   return c == ' ' || (c >= '\t' && c <= '\r') || (c >= 0x1c && c <= 0x1f);
 }
 
+// Text files are read the way the reference's text-mode open() sees them (io.py:43, :55):
+// universal newlines (\n, \r\n and a lone \r each end a line) and str.split()'s Unicode
+// whitespace in the UTF-8 decoding (U+0085, U+00A0, U+1680, U+2000-U+200A, U+2028,
+// U+2029, U+202F, U+205F, U+3000).  Files without any \r / non-ASCII byte (the usual
+// case, checked once) take the plain byte paths.
+struct TextMode {
+  bool cr = false;    // a '\r' somewhere: universal newlines
+  bool utf8 = false;  // a byte >= 0x80 somewhere: multi-byte whitespace
+};
+TextMode g_text_plain;  // PLY bodies / headers: bytes, '\n' lines (binary-mode readline)
+
+// length of the Unicode whitespace sequence at p (0 if none)
+inline int ws_len(const char* p, const char* e, const TextMode& m) {
+  const unsigned char c = (unsigned char)*p;
+  if (c < 0x80) return is_ws(c) ? 1 : 0;
+  if (!m.utf8) return 0;
+  const unsigned char* u = reinterpret_cast<const unsigned char*>(p);
+  const ptrdiff_t n = e - p;
+  if (c == 0xC2 && n >= 2 && (u[1] == 0x85 || u[1] == 0xA0)) return 2;
+  if (c == 0xE1 && n >= 3 && u[1] == 0x9A && u[2] == 0x80) return 3;
+  if (c == 0xE2 && n >= 3 && u[1] == 0x80 &&
+      (u[2] <= 0x8A || u[2] == 0xA8 || u[2] == 0xA9 || u[2] == 0xAF))
+    return 3;
+  if (c == 0xE2 && n >= 3 && u[1] == 0x81 && u[2] == 0x9F) return 3;
+  if (c == 0xE3 && n >= 3 && u[1] == 0x80 && u[2] == 0x80) return 3;
+  return 0;
+}
+
 // ---------------------------------------------------------------- Python float()
 // Accepts exactly what CPython's float(str) accepts for an ASCII token: optional sign,
 // then inf / infinity / nan (any case) or a decimal literal whose digit groups may be
@@ -178,23 +206,56 @@ struct Tok {
   const char* e;
 };
 
-// split [b, e) (one line, no '\n') into up to `cap` tokens; returns the total count
-int split(const char* b, const char* e, Tok* t, int cap) {
+// split [b, e) (one line, no line terminator) into up to `cap` tokens; returns the count
+int split(const char* b, const char* e, Tok* t, int cap, const TextMode& m = g_text_plain) {
   int k = 0;
+  if (!m.utf8) {
+    while (b < e) {
+      while (b < e && is_ws((unsigned char)*b)) ++b;
+      if (b >= e) break;
+      const char* s = b;
+      while (b < e && !is_ws((unsigned char)*b)) ++b;
+      if (k < cap) t[k] = Tok{s, b};
+      ++k;
+    }
+    return k;
+  }
   while (b < e) {
-    while (b < e && is_ws((unsigned char)*b)) ++b;
+    int w;
+    while (b < e && (w = ws_len(b, e, m)) > 0) b += w;
     if (b >= e) break;
     const char* s = b;
-    while (b < e && !is_ws((unsigned char)*b)) ++b;
+    while (b < e && ws_len(b, e, m) == 0) ++b;
     if (k < cap) t[k] = Tok{s, b};
     ++k;
   }
   return k;
 }
 
-inline const char* line_end(const char* b, const char* e) {
-  const void* q = memchr(b, '\n', (size_t)(e - b));
-  return q ? static_cast<const char*>(q) : e;
+// end of the line starting at b: the first '\n' (or, universal newlines, '\r')
+inline const char* line_end(const char* b, const char* e, const TextMode& m = g_text_plain) {
+  if (!m.cr) {
+    const void* q = memchr(b, '\n', (size_t)(e - b));
+    return q ? static_cast<const char*>(q) : e;
+  }
+  while (b < e && *b != '\n' && *b != '\r') ++b;
+  return b;
+}
+// start of the next line after the terminator at le ("\r\n" is one terminator)
+inline const char* next_line(const char* le, const char* e, const TextMode& m = g_text_plain) {
+  if (le >= e) return e;
+  if (m.cr && *le == '\r' && le + 1 < e && le[1] == '\n') return le + 2;
+  return le + 1;
+}
+TextMode text_mode(const char* b, const char* e) {
+  TextMode m;
+  m.cr = memchr(b, '\r', (size_t)(e - b)) != nullptr;
+  for (const char* p = b; p < e; ++p)
+    if ((unsigned char)*p >= 0x80) {
+      m.utf8 = true;
+      break;
+    }
+  return m;
 }
 
 // A text body parsed in parallel.  Mode kRows: skip blank / '#' lines, every other line
@@ -232,16 +293,19 @@ void parallel(int T, F fn) {
   for (auto& t : th) t.join();
 }
 
-std::vector<ChunkStat> chunk(const char* b, const char* e, int T) {
+std::vector<ChunkStat> chunk(const char* b, const char* e, int T, const TextMode& m) {
   std::vector<ChunkStat> c(T);
   const size_t n = (size_t)(e - b);
   const char* s = b;
   for (int i = 0; i < T; ++i) {
     const char* x = (i == T - 1) ? e : b + n * (size_t)(i + 1) / (size_t)T;
     if (x < s) x = s;
-    if (x < e) {  // end the chunk after a newline
-      const char* nl = line_end(x, e);
-      x = nl < e ? nl + 1 : e;
+    if (x < e) {  // end the chunk after a line terminator (never inside "\r\n")
+      if (m.cr && x > b && x[-1] == '\r' && *x == '\n') ++x;
+      else {
+        const char* nl = line_end(x, e, m);
+        x = next_line(nl, e, m);
+      }
     }
     c[i].b = s;
     c[i].e = x;
@@ -253,19 +317,19 @@ std::vector<ChunkStat> chunk(const char* b, const char* e, int T) {
 inline bool skip_line(const Tok* t, int k) { return k == 0 || t[0].b[0] == '#'; }
 
 // count lines and data rows of each chunk (pass 1)
-void count_pass(std::vector<ChunkStat>& cs, Mode mode, int T) {
+void count_pass(std::vector<ChunkStat>& cs, Mode mode, int T, const TextMode& m) {
   parallel(T, [&](int i) {
     ChunkStat& c = cs[i];
     for (const char* p = c.b; p < c.e;) {
-      const char* le = line_end(p, c.e);
+      const char* le = line_end(p, c.e, m);
       ++c.lines;
       if (mode == kRows) {
         Tok t[1];
-        if (!skip_line(t, split(p, le, t, 1))) ++c.rows;
+        if (!skip_line(t, split(p, le, t, 1, m))) ++c.rows;
       } else {
         ++c.rows;
       }
-      p = le < c.e ? le + 1 : c.e;
+      p = next_line(le, c.e, m);
     }
   });
   int64_t l = 0, r = 0;
@@ -284,15 +348,15 @@ std::string not_float_msg(const Tok& t) {
 // parse rows (pass 2); dst == nullptr validates only.  Rows beyond `max_rows` are
 // validated but not stored.  line_base = line number of the body's first line.
 void parse_pass(std::vector<ChunkStat>& cs, Mode mode, int T, double* dst, int64_t max_rows,
-                int64_t line_base, const int* idx, int max_idx) {
+                int64_t line_base, const int* idx, int max_idx, const TextMode& m) {
   parallel(T, [&](int i) {
     ChunkStat& c = cs[i];
     int64_t line = line_base + c.line0, row = c.row0;
     for (const char* p = c.b; p < c.e; ++line) {
-      const char* le = line_end(p, c.e);
+      const char* le = line_end(p, c.e, m);
       Tok t[64];
-      const int k = split(p, le, t, 64);
-      p = le < c.e ? le + 1 : c.e;
+      const int k = split(p, le, t, 64, m);
+      p = next_line(le, c.e, m);
       if (mode == kRows && skip_line(t, k)) continue;
       double v[3];
       if (mode == kRows) {
@@ -392,6 +456,7 @@ int probe_ply(const Mapped& m, const std::string& path, opcfe_cloud_info* info) 
     int64_t count;
     std::vector<std::pair<std::string, std::string>> props;  // (name, type) or ("list", ...)
     bool has_list = false;
+    std::string list_count_t, list_item_t;  // the first list property's types (faces)
   };
   std::vector<Elem> els;
   int64_t gm = -1, gn = -1;
@@ -418,10 +483,14 @@ int probe_ply(const Mapped& m, const std::string& path, opcfe_cloud_info* info) 
       int64_t cnt = 0;
       if (k < 3 || !py_int(t[2].b, t[2].e, &cnt))
         return fail(OPCFE_IO_ERR_PARSE, path, line_no, "invalid element line");
-      els.push_back(Elem{std::string(t[1].b, t[1].e), cnt, {}, false});
+      els.push_back(Elem{std::string(t[1].b, t[1].e), cnt, {}, false, "", ""});
     } else if (w0 == "property") {
       if (els.empty()) return fail(OPCFE_IO_ERR_PARSE, path, line_no, "property before element");
       if (k >= 2 && std::string(t[1].b, t[1].e) == "list") {
+        if (!els.back().has_list && k >= 4) {
+          els.back().list_count_t = std::string(t[2].b, t[2].e);
+          els.back().list_item_t = std::string(t[3].b, t[3].e);
+        }
         els.back().has_list = true;
         els.back().props.emplace_back("list", k >= 5 ? std::string(t[4].b, t[4].e) : "");
       } else if (k >= 3) {
@@ -445,9 +514,45 @@ int probe_ply(const Mapped& m, const std::string& path, opcfe_cloud_info* info) 
       break;
     }
   if (vi < 0) return fail(OPCFE_IO_ERR_PARSE, path, line_no, "no vertex element");
-  if (vi != 0)
-    return fail(OPCFE_IO_ERR_PARSE, path, line_no,
-                "elements before the vertex element are not supported");
+  // elements before the vertex element are read past as the reference reads them
+  // (io.py:139-181): ascii -- `count` lines each, face rows must be triangles; binary --
+  // face records (count + 3 indices, triangles only), any other element is an error
+  for (int i = 0; i < vi; ++i) {
+    const Elem& el = els[i];
+    const bool face = el.name == "face";
+    if (!bin) {
+      const int64_t first = line_no + 1;
+      for (int64_t r = 0; r < el.count; ++r) {
+        ++line_no;
+        const char* le2 = line_end(p, e);
+        if (face) {
+          Tok t[2];
+          int64_t nv = 0;
+          if (split(p, le2, t, 2) < 1 || !py_int(t[0].b, t[0].e, &nv))
+            return fail(OPCFE_IO_ERR_PARSE, path, line_no, "invalid face row");
+          if (nv != 3) {  // the reference checks after reading the element's rows
+            line_no = first + el.count - 1;
+            return fail(OPCFE_IO_ERR_PARSE, path, line_no, "only triangular faces are supported");
+          }
+        }
+        p = le2 < e ? le2 + 1 : e;
+      }
+    } else {
+      if (!face)
+        return fail(OPCFE_IO_ERR_PARSE, path, line_no,
+                    "cannot skip binary element '" + el.name + "'");
+      char cc = 0, ic = 0;
+      const int cs = type_size(el.list_count_t, &cc), is = type_size(el.list_item_t, &ic);
+      if (cs == 0 || is == 0)
+        return fail(OPCFE_IO_ERR_PARSE, path, line_no, "face element without a list property");
+      for (int64_t r = 0; r < el.count; ++r) {
+        if (e - p < cs + 3 * is) return fail(OPCFE_IO_ERR_PARSE, path, 0, "face data truncated");
+        if (load_le(p, cc) != 3.0)
+          return fail(OPCFE_IO_ERR_PARSE, path, 0, "only triangular faces are supported");
+        p += cs + 3 * is;
+      }
+    }
+  }
   const Elem& v = els[vi];
   info->format = OPCFE_FMT_PLY;
   info->ply_binary = bin ? 1 : 0;
@@ -495,14 +600,15 @@ int probe_text(const Mapped& m, const std::string& path, int format, opcfe_cloud
   const char* p = m.p;
   const char* e = m.p + m.n;
   int64_t line_no = 0, M = -1, N = -1;
+  const TextMode tm = text_mode(p, e);
   if (format == OPCFE_FMT_GRID) {
     bool found = false;
     while (p < e) {
-      const char* le = line_end(p, e);
+      const char* le = line_end(p, e, tm);
       ++line_no;
       Tok t[3];
-      const int k = split(p, le, t, 3);
-      p = le < e ? le + 1 : e;
+      const int k = split(p, le, t, 3, tm);
+      p = next_line(le, e, tm);
       if (skip_line(t, k)) continue;
       if (k < 2 || !py_int(t[0].b, t[0].e, &M) || !py_int(t[1].b, t[1].e, &N))
         return fail(OPCFE_IO_ERR_PARSE, path, line_no, "grid header must be two integers 'M N'");
@@ -519,21 +625,21 @@ int probe_text(const Mapped& m, const std::string& path, int format, opcfe_cloud
   info->data_offset = (int64_t)(p - m.p);
   info->first_line = line_no + 1;
   const int T = nthreads(threads, (size_t)(e - p));
-  auto cs = chunk(p, e, T);
-  count_pass(cs, kRows, T);
+  auto cs = chunk(p, e, T, tm);
+  count_pass(cs, kRows, T, tm);
   info->count = cs.empty() ? 0 : cs.back().row0 + cs.back().rows;
   info->vertex_stride = 0;
   info->direct = 0;
   return OPCFE_IO_OK;
 }
 
-int64_t total_lines(const Mapped& m) {
-  // Python readlines(): a final line without '\n' still counts
+int64_t total_lines(const Mapped& m, const TextMode& tm) {
+  // Python readlines(): a final line without a terminator still counts
   int64_t n = 0;
   for (const char* p = m.p; p < m.p + m.n;) {
-    const char* le = line_end(p, m.p + m.n);
+    const char* le = line_end(p, m.p + m.n, tm);
     ++n;
-    p = le < m.p + m.n ? le + 1 : m.p + m.n;
+    p = next_line(le, m.p + m.n, tm);
   }
   return n;
 }
@@ -615,26 +721,27 @@ int opcfe_io_read(const char* path, const opcfe_cloud_info* info, double* dst, i
       return fail(OPCFE_IO_ERR_PARSE, P, info->first_line + got, "unexpected end of vertex data");
     const int idx[3] = {info->x_off, info->y_off, info->z_off};
     const int T = nthreads(threads, (size_t)(q - b));
-    auto cs = chunk(b, q, T);
-    count_pass(cs, kPly, T);
+    auto cs = chunk(b, q, T, g_text_plain);
+    count_pass(cs, kPly, T, g_text_plain);
     parse_pass(cs, kPly, T, dst, info->count, info->first_line, idx,
-               std::max(idx[0], std::max(idx[1], idx[2])));
+               std::max(idx[0], std::max(idx[1], idx[2])), g_text_plain);
     return first_error(cs, P);
   }
   // grid / xyz text: parse errors first (in line order), then the row count
+  const TextMode tm = text_mode(m.p, e);
   const int T = nthreads(threads, (size_t)(e - b));
-  auto cs = chunk(b, e, T);
-  count_pass(cs, kRows, T);
+  auto cs = chunk(b, e, T, tm);
+  count_pass(cs, kRows, T, tm);
   const int64_t rows = cs.empty() ? 0 : cs.back().row0 + cs.back().rows;
   const bool fits = rows == info->count;
-  parse_pass(cs, kRows, T, fits ? dst : nullptr, info->count, info->first_line, nullptr, 0);
+  parse_pass(cs, kRows, T, fits ? dst : nullptr, info->count, info->first_line, nullptr, 0, tm);
   if (int rc = first_error(cs, P)) return rc;
   if (info->format == OPCFE_FMT_GRID && rows != info->rows * info->cols)
-    return fail(OPCFE_IO_ERR_PARSE, P, total_lines(m),
+    return fail(OPCFE_IO_ERR_PARSE, P, total_lines(m, tm),
                 "expected " + std::to_string(info->rows * info->cols) + " rows, got " +
                     std::to_string(rows));
   if (!fits)
-    return fail(OPCFE_IO_ERR_PARSE, P, total_lines(m), "file changed while reading");
+    return fail(OPCFE_IO_ERR_PARSE, P, total_lines(m, tm), "file changed while reading");
   return OPCFE_IO_OK;
 }
 

@@ -93,6 +93,59 @@ def main():
         fh.write("0 0 0\n1.5 2 3\n# comment\nnan nan nan\n-1 -2 -3 4\n\n1e-3 2e3 inf\n")
     keep("pts.xyz")
 
+    # round 2: text-mode corner cases -- lone-CR line ends (universal newlines), Unicode
+    # whitespace between values (str.split()), and PLY files whose vertex element is not
+    # the first one (ascii: a face element first; binary: a face element first)
+    rows = rng.normal(size=(6, 3))
+    with open(os.path.join(OUT, "lone_cr.grid"), "w", newline="") as fh:
+        fh.write("# cr only\r2 3\r" + "\r".join(" ".join(repr(float(x)) for x in r)
+                                              for r in rows) + "\r")
+    keep("lone_cr.grid")
+    seps = ["\u00a0", "\u3000", "\u2009", " \u2028 ", "\t\u00a0"]
+    with open(os.path.join(OUT, "unicode_ws.grid"), "w", encoding="utf-8", newline="") as fh:
+        fh.write("2\u00a03\n")
+        for i, r in enumerate(rows):
+            sep = seps[i % len(seps)]
+            fh.write(sep.join(repr(float(x)) for x in r) + "\u3000\n")
+    keep("unicode_ws.grid")
+    with open(os.path.join(OUT, "unicode_ws.xyz"), "w", encoding="utf-8", newline="") as fh:
+        for i, r in enumerate(rows):
+            fh.write("\u0085".join(repr(float(x)) for x in r) + "\r\n")
+    keep("unicode_ws.xyz")
+    verts = rng.normal(size=(6, 3))
+    body = "\n".join(" ".join(repr(float(x)) for x in v) for v in verts) + "\n"
+    with open(os.path.join(OUT, "face_first_ascii.ply"), "w") as fh:
+        fh.write("ply\nformat ascii 1.0\ncomment grid 2 3\nelement face 2\n"
+                 "property list uchar int vertex_indices\nelement vertex 6\n"
+                 "property double x\nproperty double y\nproperty double z\nend_header\n"
+                 "3 0 1 2\n3 2 1 3\n" + body)
+    keep("face_first_ascii.ply")
+    with open(os.path.join(OUT, "quad_first_ascii.ply"), "w") as fh:
+        fh.write("ply\nformat ascii 1.0\nelement face 2\n"
+                 "property list uchar int vertex_indices\nelement vertex 6\n"
+                 "property double x\nproperty double y\nproperty double z\nend_header\n"
+                 "3 0 1 2\n4 0 1 2 3\n" + body)
+    keep("quad_first_ascii.ply")
+    import struct
+    with open(os.path.join(OUT, "face_first_bin.ply"), "wb") as fh:
+        fh.write(b"ply\nformat binary_little_endian 1.0\ncomment grid 3 2\nelement face 2\n"
+                 b"property list uchar int vertex_indices\nelement vertex 6\n"
+                 b"property double x\nproperty double y\nproperty double z\nend_header\n")
+        fh.write(struct.pack("<B3i", 3, 0, 1, 2) + struct.pack("<B3i", 3, 2, 1, 3))
+        fh.write(np.ascontiguousarray(verts, dtype="<f8").tobytes())
+    keep("face_first_bin.ply")
+    with open(os.path.join(OUT, "other_first_bin.ply"), "wb") as fh:
+        fh.write(b"ply\nformat binary_little_endian 1.0\nelement camera 1\n"
+                 b"property float fx\nelement vertex 6\n"
+                 b"property double x\nproperty double y\nproperty double z\nend_header\n")
+        fh.write(struct.pack("<f", 1.0) + np.ascontiguousarray(verts, dtype="<f8").tobytes())
+    keep("other_first_bin.ply")
+    with open(os.path.join(OUT, "other_first_ascii.ply"), "w") as fh:
+        fh.write("ply\nformat ascii 1.0\nelement camera 1\nproperty float fx\n"
+                 "element vertex 6\nproperty double x\nproperty double y\nproperty double z\n"
+                 "end_header\n1.0\n" + body)
+    keep("other_first_ascii.ply")
+
     # error cases (the reference's ParseError text and line)
     bad = {
         "bad_header.grid": "two two\n",

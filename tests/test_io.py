@@ -161,6 +161,39 @@ def test_parse_error_line_in_a_late_chunk(fio, tmp_path):
     assert "could not convert string to float: 'oops'" in str(ei.value)
 
 
+@pytest.mark.parametrize("eol", ["\r", "\r\n", "mixed"])
+@pytest.mark.parametrize("ws", [" ", "\u00a0", "\t\u3000"])
+def test_large_grid_universal_newlines_unicode_ws(fio, tmp_path, rng, eol, ws):
+    """Multi-threaded text parsing with lone-CR / CRLF / mixed line ends and Unicode
+    whitespace (the reference's text-mode open() + str.split(), io.py:55-78): every chunk
+    boundary lands on a line boundary, line numbers count each terminator once."""
+    M, N = 200, 300                                     # > 1 MiB of text: several threads
+    pts = rng.normal(scale=5.0, size=(M * N, 3))
+    pts[rng.random(M * N) < 0.05] = np.nan
+    lines = [ws.join(repr(float(x)) for x in r) for r in pts]
+    if eol == "mixed":
+        ends = np.array(["\n", "\r", "\r\n"])[rng.integers(0, 3, M * N)]
+        body = "".join(l + e for l, e in zip(lines, ends))
+        head = f"{M} {N}\r\n"
+    else:
+        body = eol.join(lines) + eol
+        head = f"{M} {N}{eol}"
+    p = tmp_path / "big.grid"
+    with open(p, "w", encoding="utf-8", newline="") as fh:
+        fh.write(head + body)
+    got = fio.load_cloud(p)
+    assert got.shape == (M, N, 3) and same(got, pts.reshape(M, N, 3))
+    # an error late in the file reports the reference's line number
+    bad = list(lines)
+    bad[M * N - 11] = bad[M * N - 11].replace(repr(float(pts[M * N - 11][1])), "oops", 1) \
+        if np.isfinite(pts[M * N - 11][1]) else "1 oops 2"
+    with open(p, "w", encoding="utf-8", newline="") as fh:
+        fh.write(f"{M} {N}\r" + "\r".join(bad) + "\r")
+    with pytest.raises(fio.ParseError) as ei:
+        fio.load_cloud(p)
+    assert ei.value.line_no == 1 + (M * N - 11) + 1
+
+
 def test_direct_binary_into_pinned_tensor(fio, tmp_path, rng):
     import torch
     M, N = 120, 160
