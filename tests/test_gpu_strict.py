@@ -416,3 +416,54 @@ def test_host_pipeline_output_options(fe, mode):
         assert pipe.d2h_bytes < full * 0.8
     if mode == "strict":
         assert res.points.dtype == torch.float64 and res.normals.dtype == torch.float64
+
+
+# --------------------------------------------------------------- randomised strict chains
+@pytest.mark.parametrize("seed", range(24))
+def test_strict_front_end_randomised(fe, seed):
+    """Randomised strict chains against the C oracle's fp64 chain (pinned to the
+    reference's): odd shapes (partial tiles), NaN fractions up to 40 %, duplicated
+    vertices, partial-NaN vertices, Laplacian 0..6 passes and bilateral 0..3 iterations at
+    kernel sizes 3..13, random sigmas and l_max, 1..3 frames per batch -- smoothed grid,
+    topology and l_max flags bit-exact, normals <= 1e-13."""
+    rng = np.random.default_rng(5000 + seed)
+    M, N = int(rng.integers(3, 150)), int(rng.integers(3, 150))
+    F = int(rng.integers(1, 4))
+    frames = []
+    for _ in range(F):
+        u, v = np.meshgrid(np.arange(M, dtype=float), np.arange(N, dtype=float), indexing="ij")
+        s = rng.uniform(0.002, 0.05)
+        opc = np.stack([v * s, -u * s, rng.normal(0, 0.01, (M, N)) +
+                        0.2 * np.sin(np.arange(N) / 9.0)[None, :]], axis=2)
+        opc += rng.normal(scale=rng.uniform(0, 0.004), size=opc.shape)
+        for a, b in rng.integers(0, [max(1, M - 1), max(1, N - 1)],
+                                 size=(int(rng.integers(0, 6)), 2)):
+            opc[a, min(b + 1, N - 1)] = opc[a, b]
+        opc[rng.random((M, N)) < rng.uniform(0, 0.4)] = np.nan
+        if rng.random() < 0.5:
+            opc[int(rng.integers(0, M)), int(rng.integers(0, N)), 1] = np.nan   # partial NaN
+        frames.append(opc)
+    k_lap = int(rng.choice([3, 3, 5, 7, 9, 11, 13]))
+    lap = (float(rng.uniform(0.3, 1.0)), k_lap, int(rng.integers(1, 7))) \
+        if rng.random() < 0.85 and min(M, N) >= k_lap else None
+    k_bil = int(rng.choice([3, 3, 3, 5, 7, 11, 13]))
+    bil = (float(rng.uniform(0.02, 0.3)), float(rng.uniform(0.05, 0.5)), k_bil,
+           int(rng.integers(1, 4))) if rng.random() < 0.75 else None
+    l_max = float(rng.uniform(0.001, 0.05)) if rng.random() < 0.5 else None
+    eng = fe.FrontEnd(M, N, F, laplacian=None if lap is None else fe.LaplacianParams(*lap),
+                      bilateral=None if bil is None else fe.BilateralParams(*bil), l_max=l_max,
+                      src_dtype=torch.float64, precision="strict")
+    res = eng.run(torch.from_numpy(np.stack(frames)).cuda())
+    torch.cuda.synchronize()
+    for f in range(F):
+        ref = c_oracle.front_end(frames[f], lap, bil, l_max)
+        T = res.n_tri[f]
+        assert same(res.points[f].cpu().numpy(), ref["smoothed"]), (seed, f)
+        assert np.array_equal(res.trimap[f].cpu().numpy(), ref["trimap"])
+        assert np.array_equal(res.triangles[f, :T].cpu().numpy(), ref["triangles"])
+        assert np.array_equal(res.halfedges[f, :3 * T].cpu().numpy(), ref["halfedges"])
+        err = normal_err(res.normals[f, :T].cpu().numpy(), ref["normals"])
+        assert err.max() <= STRICT_NORMAL_TOL, (seed, f, err.max())
+        if l_max is not None:
+            assert np.array_equal(res.lmax_mask[f, :T].cpu().numpy().astype(bool),
+                                  ref["lmax_mask"])
