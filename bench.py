@@ -337,7 +337,8 @@ def strict_throughput(fe, wl, eng_fast, args, dev):
            "steps": steps, "dtype": "f64", "gpu_launches_per_step": eng.kernel_launches,
            "stage_ms_per_step": {k: round(v, 4) for k, v in stage.items()},
            "what": "precision='strict': the reference's fp64 chain (bit-exact Laplacian, FC "
-                   "data and topology; bilateral to exp()'s last ulp), float64 outputs"}
+                   "data and topology; bilateral normals within a few ulp per iteration), "
+                   "float64 outputs"}
     del eng
     torch.cuda.empty_cache()
     return out

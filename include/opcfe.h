@@ -174,8 +174,9 @@ int opcfe_fc_data_f64(const double* opc, int F, int M, int N, double* centroids,
 /* Replaces _kernels.bilateral_iterate (_native.pyx:287-364, _fallback.py:120-166) on an
  * (M-1) x (N-1) FC grid, and with trimap != NULL also bilateral_filter_opc's gather
  * (smoothing.py:108-114: out_mesh[f][trimap[gid]] for trimap >= 0, out_rows rows per
- * frame); otherwise out_fc.  Same arithmetic and accumulation order as the reference; exp()
- * is CUDA's (<= 1 ulp, as the reference's two backends differ).  buf_a / buf_b: FC-sized
+ * frame); otherwise out_fc.  fp64 throughout; each iteration within a few ulp of the
+ * reference's (FMA-contracted products, a pair-symmetric sum at kernel size 3, an own exp2;
+ * the reference's two backends differ by ~1 ulp already).  buf_a / buf_b: FC-sized
  * ping-pong buffers (iterations > 1 / > 2). */
 int opcfe_bilateral_f64(const double* centroids, const double* normals, int F, int M, int N,
                         double sigma_length, double sigma_angle, int kernel_size, int iterations,
