@@ -19,7 +19,10 @@ ACTIVE = "cuda-sm100a"
 def laplacian_filter(points, lam, kernel_size, iterations):
     """Same contract as _kernels.laplacian_filter (_native.pyx:225 / _fallback.py:82)."""
     from .smoothing import _laplacian_staged
-    return _laplacian_staged(Staged(points), lam, kernel_size, iterations)
+    S = Staged(points)
+    if S.dev.numel() == 0:                # the reference's loops run zero times: a copy
+        return S.give(S.dev.clone())
+    return _laplacian_staged(S, lam, kernel_size, iterations)
 
 
 def bilateral_iterate(centroids, normals, sigma_length, sigma_angle, kernel_size, iterations):
@@ -32,6 +35,8 @@ def bilateral_iterate(centroids, normals, sigma_length, sigma_angle, kernel_size
     Nn = Staged(normals)
     n = Nn.dev
     Mq, Nq = n.shape[:2]
+    if n.numel() == 0:                    # the reference's loops run zero times: a copy
+        return Nn.give(n.clone())
     if resolve_precision(None, n.dtype) == "strict" or kernel_size > BILATERAL_MAX_K32:
         out = _ops.bilateral_f64(C.dev.to(torch.float64), n.to(torch.float64), sigma_length,
                                  sigma_angle, kernel_size, iterations)

@@ -469,3 +469,11 @@ def test_strict_front_end_randomised(fe, seed):
         if l_max is not None:
             assert np.array_equal(res.lmax_mask[f, :T].cpu().numpy().astype(bool),
                                   ref["lmax_mask"])
+
+
+def test_kernels_empty_inputs(fe):
+    """_kernels.* on empty grids return copies, as the reference's loops do."""
+    out = fe._kernels.laplacian_filter(np.zeros((0, 4, 3)), 1.0, 3, 2)
+    assert out.shape == (0, 4, 3) and out.dtype == np.float64
+    e = np.zeros((0, 3, 2, 3))
+    assert fe._kernels.bilateral_iterate(e, e, 0.1, 0.15, 3, 1).shape == (0, 3, 2, 3)
