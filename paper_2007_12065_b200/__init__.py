@@ -17,7 +17,9 @@ from .mesh import (HalfEdgeMesh, compute_normals, extract_halfedges_opc, extract
 from .segmentation import (MAX_GROUPS, UNASSIGNED, SegmentationParams, extract_planar_segment,
                            group_assignment, grow_segments, max_edge_mask)
 from .smoothing import (BilateralParams, LaplacianParams, bilateral_filter_opc, bilateral_opc,
-                        compute_fc_triangle_data, laplacian_filter_opc, laplacian_opc)
+                        compute_fc_triangle_data, get_precision, laplacian_filter_opc,
+                        laplacian_opc, set_precision)
+from .distributed import MultiDevicePipeline
 
 __version__ = "0.1.0"
 
@@ -29,5 +31,6 @@ __all__ = [
     "max_edge_mask", "SegmentationParams", "extract_planar_segment", "grow_segments",
     "BilateralParams",
     "LaplacianParams", "bilateral_filter_opc", "bilateral_opc", "compute_fc_triangle_data",
-    "laplacian_filter_opc", "laplacian_opc", "io",
+    "laplacian_filter_opc", "laplacian_opc", "io", "set_precision", "get_precision",
+    "MultiDevicePipeline",
 ]
