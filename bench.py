@@ -535,13 +535,18 @@ def run_ours(args, rank, world, local_rank, wl):
                 shutil.rmtree(tmp, ignore_errors=True)
         e2e["from_files"] = e2e_files
         del pipe
-        # ---- compact (NON-reference) output modes: int32 indices narrowed on the device,
-        # optionally only a subset of the outputs
-        for key, outs in (("compact", fe.HostPipeline.DROPIN),
-                          ("selected", ("points", "triangles", "normals"))):
+        # ---- strict precision end to end (the reference's fp64 chain, float64 points and
+        # normals back, int64 indices: exactly the reference's outputs), then the compact
+        # (NON-reference) output modes: int32 indices narrowed on the device, optionally
+        # only a subset of the outputs
+        for key, outs, kw in (("strict", fe.HostPipeline.DROPIN, dict(precision="strict")),
+                              ("compact", fe.HostPipeline.DROPIN, dict(index_dtype=torch.int32)),
+                              ("selected", ("points", "triangles", "normals"),
+                               dict(index_dtype=torch.int32))):
+            if key == "strict" and args.no_strict:
+                continue
             p2 = fe.HostPipeline(M, N, laplacian=lap_p, bilateral=bil_p, l_max=wl.l_max,
-                                 src_dtype=torch.float64, device=dev, outputs=outs,
-                                 index_dtype=torch.int32)
+                                 src_dtype=torch.float64, device=dev, outputs=outs, **kw)
             p2.run(host)
             barrier()
             e0.record(stream)
@@ -553,7 +558,9 @@ def run_ours(args, rank, world, local_rank, wl):
             e2e[key] = {"value": world * FE * e2e_steps / (tc / 1e3), "unit": "frames/s",
                         "h2d_bytes_per_step": int(p2.h2d_bytes),
                         "d2h_bytes_per_step": int(p2.d2h_bytes), "outputs": list(outs),
-                        "index_dtype": "int32 (non-reference)"}
+                        "precision": kw.get("precision", "fast"),
+                        "index_dtype": ("int64 (reference)" if "index_dtype" not in kw
+                                        else "int32 (non-reference)")}
             del p2
         # ---- the unchanged pipeline.py:125-134 sequence through the drop-in API: NumPy f64
         # in and out, one frame per call (default precision: strict for float64 input)
