@@ -349,9 +349,10 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
                               p->laplacian_kernel_size, p->laplacian_iterations, st)))
         return rc;
     } else if (src64 != points64) {
-      if (cudaMemcpyAsync(points64, src64, (size_t)F * M * N * 3 * sizeof(double),
-                          cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-        return check_launch("front_end: copy");
+      const cudaError_t e = cudaMemcpyAsync(points64, src64, (size_t)F * M * N * 3 * sizeof(double),
+                                            cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess)
+        return fail(ERR_CUDA, std::string("front_end: copy: ") + cudaGetErrorString(e));
     }
     // validity bits of the smoothed grid (the NaN mask is iteration-invariant)
     if ((rc = stage_in(points64, true, 3ll * N, 3ll * N * M, F, M, N, nullptr, pitch, vmask, st)))
