@@ -6,6 +6,7 @@ buffers, move bytes between host and device, and supply the current CUDA stream.
 
 from __future__ import annotations
 
+import os
 import threading
 
 import numpy as np
@@ -50,8 +51,8 @@ class HostTransfer:
     take the plain path.
     """
 
-    CHUNK = 8 << 20
-    SLOTS = 8
+    CHUNK = int(os.environ.get("OPCFE_XFER_CHUNK_MB", "8")) << 20
+    SLOTS = int(os.environ.get("OPCFE_XFER_SLOTS", "16"))
     MIN_BYTES = 4 << 20
     _inst = {}
 
