@@ -7,11 +7,13 @@ the maintainer's patch (integration/flatpoly_cuda.patch: the FLATPOLY_CUDA branc
 _kernels/__init__.py:9-30, mesh / FC functions routed to the backend).  With
 FLATPOLY_CUDA=1 the reference's own tests -- tests/test_kernels.py (compiled backend vs
 the NumPy fallback), test_smoothing.py, test_mesh.py, test_segmentation.py and
-test_acceptance.py -- then exercise the GPU kernels through the C ABI.
+test_acceptance.py, test_accumulator.py (find_cells through the backend) and
+test_stress.py (meshes of degenerate / noisy organized clouds) -- then exercise the GPU
+kernels through the C ABI.
 
-Deselected: acceptance #06 / #07 / #10 run the polygon stage, which needs the real
-Shapely (absent from this image; tests/golden/_stubs has an import stub only) -- they
-fail identically on the stock reference here.
+Deselected: acceptance #06 / #07 / #10 and one stress test run the polygon stage, which
+needs the real Shapely (absent from this image; tests/golden/_stubs has an import stub
+only) -- they fail identically on the stock reference here.
 """
 
 import os
@@ -32,10 +34,13 @@ pytestmark = [pytest.mark.gpu,
                                  reason="baseline/_ref missing (run baseline/install_ref.sh)")]
 
 FILES = ["tests/test_kernels.py", "tests/test_smoothing.py", "tests/test_mesh.py",
-         "tests/test_segmentation.py", "tests/test_acceptance.py"]
+         "tests/test_segmentation.py", "tests/test_acceptance.py", "tests/test_accumulator.py",
+         "tests/test_stress.py"]
 DESELECT = ["tests/test_acceptance.py::test_06_room_benchmark",
             "tests/test_acceptance.py::test_07_thread_determinism",
-            "tests/test_acceptance.py::test_10_buffer_geometry"]
+            "tests/test_acceptance.py::test_10_buffer_geometry",
+            "tests/test_stress.py::TestNoisyProjection::"
+            "test_crossed_projection_passes_through_and_buffer_repairs"]
 
 
 @pytest.fixture(scope="module")
