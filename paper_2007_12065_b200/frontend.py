@@ -18,6 +18,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -464,18 +465,19 @@ class HostPipeline:
                               grid_shape=(self.M, self.N), labels=get("labels"))
 
 
-_ENGINES: "OrderedDict[tuple, FrontEnd]" = None
 _ENGINES_MAX = 4
+_ENGINES_TLS = threading.local()
 
 
 def cached_engine(M, N, laplacian, bilateral, l_max, src_dtype, precision, frames=1,
                   dominant_normals=None, ang_min=0.95, device=None) -> FrontEnd:
     """A FrontEnd for these shapes / parameters, reused across calls (buffers, workspace
-    and TMA descriptors are built once; small LRU per process)."""
+    and TMA descriptors are built once; a small LRU per THREAD, so concurrent callers
+    never share an engine's buffers -- the reference's functions are reentrant)."""
     from collections import OrderedDict
-    global _ENGINES
+    _ENGINES = getattr(_ENGINES_TLS, "engines", None)
     if _ENGINES is None:
-        _ENGINES = OrderedDict()
+        _ENGINES = _ENGINES_TLS.engines = OrderedDict()
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     dn_key = None if dominant_normals is None else \
         np.asarray(dominant_normals, dtype=np.float64).tobytes()
