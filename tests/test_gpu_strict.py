@@ -477,3 +477,41 @@ def test_kernels_empty_inputs(fe):
     assert out.shape == (0, 4, 3) and out.dtype == np.float64
     e = np.zeros((0, 3, 2, 3))
     assert fe._kernels.bilateral_iterate(e, e, 0.1, 0.15, 3, 1).shape == (0, 3, 2, 3)
+
+
+def test_drop_in_concurrent_threads(fe):
+    """The reference's kernels are reentrant (GIL released, _native.pyx:239,306): drop-in
+    calls from several host threads at once give each thread its own exact result (shared
+    pinned staging is locked, front_end() engines are per thread)."""
+    import threading
+    frames = [fe.synthetic.room_scene(n=160 + 8 * i, noise=0.002, seed=i) for i in range(4)]
+    lp, bp = fe.LaplacianParams(1.0, 3, 3), fe.BilateralParams(0.1, 0.15, 3, 2)
+
+    def chain(opc):
+        sm = fe.laplacian_filter_opc(opc, lp)
+        mesh = fe.mesh_from_opc(sm)
+        mesh.normals = fe.bilateral_filter_opc(sm, bp, mesh.trimap)
+        sm2, mesh2, _ = fe.front_end(opc, lp, bp)
+        return sm, mesh, sm2, mesh2
+
+    ref = [chain(o) for o in frames]
+    out = [None] * len(frames)
+    errs = []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                out[i] = chain(frames[i])
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(frames))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for (a_sm, a_m, a_sm2, a_m2), (b_sm, b_m, b_sm2, b_m2) in zip(out, ref):
+        assert same(a_sm, b_sm) and same(a_sm2, b_sm2)
+        assert np.array_equal(a_m.triangles, b_m.triangles)
+        assert same(a_m.normals, b_m.normals) and same(a_m2.normals, b_m2.normals)
