@@ -40,20 +40,26 @@ def fc_pitch(N: int) -> int:
 
 
 class HostTransfer:
-    """Large host <-> device copies for the NumPy drop-in API, through a ring of pinned
-    staging chunks with the host-side memcpy spread over threads.
+    """Large host <-> device copies for the NumPy drop-in API.
 
-    A D2H straight into a fresh NumPy array runs at ~2 GB/s on the B200 box (the driver's
-    pageable path page-faults the destination as it copies); pinned D2H runs at ~57 GB/s
-    and a host thread first-touches + copies at ~8 GB/s, so chunks are DMA'd into pinned
-    slots on a side stream while `THREADS` threads copy finished slots into the NumPy
-    array (numpy releases the GIL for the copy).  H2D is the mirror image.  Small arrays
-    take the plain path.
+    D2H: a large result is returned as a NumPy view of a PINNED host block (torch's
+    caching host allocator: freed blocks are reused once the array is garbage), so the
+    DMA writes straight into the caller's array at the link rate (~54 GB/s on the B200
+    box) -- a D2H into a fresh pageable array runs at ~2 GB/s (the driver's pageable
+    path page-faults the destination as it copies) and even a staged copy is bound by
+    first-touch page faults (~7 GB/s per thread).  Past `PINNED_OUT_MB` of pinned host
+    memory in use (callers holding many results) it falls back to a ring of pinned
+    staging chunks DMA'd on a side stream while `SLOTS` threads copy finished chunks into
+    a fresh NumPy array (numpy releases the GIL for the copy).
+    H2D: an input that already lives in pinned memory (e.g. a previous call's result)
+    is DMA'd directly; a pageable one goes through the staging ring (threads fill the
+    slots).  Small arrays take the plain path.
     """
 
     CHUNK = int(os.environ.get("OPCFE_XFER_CHUNK_MB", "8")) << 20
     SLOTS = int(os.environ.get("OPCFE_XFER_SLOTS", "16"))
     MIN_BYTES = 4 << 20
+    PINNED_OUT_MB = int(os.environ.get("OPCFE_PINNED_OUT_MB", "16384"))
     _inst = {}
 
     def __init__(self, device):
@@ -80,10 +86,18 @@ class HostTransfer:
         nbytes = t.numel() * t.element_size()
         if nbytes < self.MIN_BYTES:
             return t.cpu().numpy()
+        if self._pinned_room(nbytes):
+            h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+            h.copy_(t)                  # one DMA into the returned array's own memory
+            return h.numpy()            # the array keeps the pinned block alive
         out = np.empty(tuple(t.shape), dtype=torch.empty((), dtype=t.dtype).numpy().dtype)
         with self.lock:
             self._d2h(t, out, nbytes)
         return out
+
+    def _pinned_room(self, nbytes: int) -> bool:
+        used = torch.cuda.host_memory_stats().get("active_bytes.current", 0)
+        return used + 2 * nbytes <= self.PINNED_OUT_MB << 20   # blocks round up to 2^k
 
     def _d2h(self, t, out, nbytes):
         src = t.reshape(-1).view(torch.uint8)
@@ -112,6 +126,10 @@ class HostTransfer:
         t_host = torch.from_numpy(arr)
         if arr.nbytes < self.MIN_BYTES:
             return t_host.to(self.device)
+        if t_host.is_pinned():          # e.g. a result of a previous call: DMA directly
+            out = t_host.to(self.device, non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize()   # caller may reuse arr
+            return out
         out = torch.empty(tuple(arr.shape), dtype=t_host.dtype, device=self.device)
         with self.lock:
             self._h2d(arr, out)
