@@ -9,7 +9,8 @@ There is no CPU fallback.
 
 from . import _kernels, accumulator, io, synthetic
 from ._kernels import ACTIVE as kernel_backend
-from .accumulator import find_cell_indices, integrate_normals
+from .accumulator import (GaussianAccumulator, build_accumulator, find_cell_index,
+                          find_cell_indices, integrate_normals)
 from .frontend import FrontEnd, FrontEndResult, HostPipeline, front_end
 from .geometry import DegenerateInputError, triangle_normals
 from .mesh import (HalfEdgeMesh, compute_normals, extract_halfedges_opc, extract_triangles_opc,
@@ -32,5 +33,6 @@ __all__ = [
     "BilateralParams",
     "LaplacianParams", "bilateral_filter_opc", "bilateral_opc", "compute_fc_triangle_data",
     "laplacian_filter_opc", "laplacian_opc", "io", "set_precision", "get_precision",
-    "MultiDevicePipeline",
+    "MultiDevicePipeline", "GaussianAccumulator", "build_accumulator", "find_cell_index",
+    "find_cell_indices", "integrate_normals",
 ]

@@ -1141,3 +1141,45 @@ def test_front_end_many_frames(fe):
     _, res = _engine_run(fe, np.stack(frames), lap, bil, 0.03, frames=F)
     for f in [0, F - 1] + [int(x) for x in rng.choice(np.arange(1, F - 1), 8, replace=False)]:
         _per_stage_check(fe, frames[f], lap, bil, 0.03, _frame_view(res, f))
+
+
+@pytest.mark.parametrize("level", [2, 4])
+def test_fastga_on_own_accumulator(fe, level):
+    """build_accumulator (host gauss_sphere, bit-identical structure) + the GPU search:
+    the same cells and votes as the reference-built structure, and the reference's own
+    accumulator tests (test_accumulator.py:92-172) on it."""
+    g = FASTGA[f"level{level}"]
+    ga = fe.build_accumulator(level)
+    slope, icpt, wlo, whi = g["model"]
+    ref = fe._kernels.find_cells(g["queries"], g["ids"], g["cell_normals"], g["neighbors"],
+                                 slope, icpt, int(wlo), int(whi))
+    assert np.array_equal(fe.find_cell_indices(ga, g["queries"]), ref)
+    counts = fe.integrate_normals(ga, g["mesh_normals"], sample_pct=0.12)
+    assert counts is ga.counts and counts.sum() == g["counts"].sum()
+    for idx in (0, 17, ga.num_cells // 2, ga.num_cells - 1):
+        assert fe.find_cell_index(ga, ga.normals[idx]) == idx
+        assert fe.find_cell_index(ga, 3.0 * ga.normals[idx]) == idx
+    with pytest.raises(ValueError):
+        fe.find_cell_index(ga, np.zeros(3))
+    rng = np.random.default_rng(level)
+    q = rng.normal(size=(5000, 3))
+    q /= np.linalg.norm(q, axis=1)[:, None]
+    got = fe.find_cell_indices(ga, q)
+    true = np.argmax(q @ ga.normals.T, axis=1)
+    agree = got == true
+    assert agree.mean() >= 0.999
+    for i in np.nonzero(~agree)[0]:
+        assert got[i] in ga.neighbors[true[i]]
+    ga2 = fe.build_accumulator(level)                 # fresh zero counts, shared structure
+    assert fe.integrate_normals(ga2, np.empty((0, 3))).sum() == 0
+    fe.integrate_normals(ga2, np.tile(ga2.normals[42], (9, 1)))
+    assert ga2.counts[42] == 9 and ga2.counts.sum() == 9
+    ga3 = fe.build_accumulator(level)
+    fe.integrate_normals(ga3, np.tile(ga3.normals[7], (10, 1)), sample_pct=0.25)
+    assert ga3.counts.sum() == 3                      # rows 0, 4, 8
+    ga4 = fe.build_accumulator(level)
+    n = np.tile(ga4.normals[3], (5, 1))
+    n[1] = np.nan
+    n[3, 2] = np.inf
+    fe.integrate_normals(ga4, n)
+    assert ga4.counts.sum() == 3
