@@ -78,6 +78,8 @@ class DeviceAccumulator:
         q = queries.reshape(-1, 3).contiguous().to(torch.float64)
         n = (q.shape[0] + stride - 1) // stride
         cells = torch.empty((n,), dtype=torch.int64, device=q.device) if want_cells else None
+        if n == 0:
+            return cells
         _lib.check(_lib.lib().opcfe_find_cells(q.data_ptr(), n, stride, self.ids.data_ptr(),
                                                self.normals.data_ptr(), self.neighbors.data_ptr(),
                                                self.n_cells, self.slope, self.intercept,

@@ -1172,6 +1172,7 @@ def test_fastga_on_own_accumulator(fe, level):
         assert got[i] in ga.neighbors[true[i]]
     ga2 = fe.build_accumulator(level)                 # fresh zero counts, shared structure
     assert fe.integrate_normals(ga2, np.empty((0, 3))).sum() == 0
+    assert fe.find_cell_indices(ga2, np.empty((0, 3))).shape == (0,)
     fe.integrate_normals(ga2, np.tile(ga2.normals[42], (9, 1)))
     assert ga2.counts[42] == 9 and ga2.counts.sum() == 9
     ga3 = fe.build_accumulator(level)
