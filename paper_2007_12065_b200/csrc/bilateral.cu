@@ -90,6 +90,11 @@ struct BilTile {
   static constexpr int PH = QH + 1;
   static constexpr int PSHIFT = LP - LQ;  // point column of pack column 0
   static constexpr int NQ = QW * QH;      // quads in the pack
+  // pack columns any weighing reads: [CB, CB + CW); the rest (16-B alignment padding of
+  // the FC / packed boxes) are never packed
+  static constexpr int CB = LQ - H;
+  static constexpr int CW = kBilTQW + 2 * H;
+  static_assert(CB >= 0 && CB + CW <= QW, "weighing window inside the pack");
   static constexpr int PTS_F = ((PW * 3 * PH) + 31) / 32 * 32;
   static constexpr int FC_F = ((QW * 6 * QH) + 31) / 32 * 32;
   // 4 pack planes (pack_quad), each 128-B aligned so TMA can fill them directly:
@@ -512,9 +517,17 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     if (!finite3f(o.x, o.y, o.z)) o = tile_origin<kBilNT>(pts_s, T::PW * T::PH, 3, &s_first);
   }
 
-  // ---- pack every halo quad into the planes (scaled + sentinel-encoded)
-  for (int q = threadIdx.x; q < T::NQ; q += kBilNT) {
-    const int r = q / T::QW, c = q % T::QW;
+  // ---- pack every quad the weighing reads into the planes (scaled + sentinel-encoded)
+  if (PACKOUT && T::CW < T::QW) {  // unread padding columns of the stored window: zeros
+    constexpr int PADW = T::QW - T::CW;
+    for (int i = threadIdx.x; i < T::QH * PADW; i += kBilNT) {
+      const int r = i / PADW, j = i % PADW, q = r * T::QW + (j < T::CB ? j : T::CW + j);
+      P.c0[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      P.c1[q] = make_float2(0.f, 0.f);
+    }
+  }
+  for (int i = threadIdx.x; i < T::QH * T::CW; i += kBilNT) {
+    const int r = i / T::CW, c = T::CB + i % T::CW, q = r * T::QW + c;
     float n[6], cc[6];  // cc: scaled centroids c' = c * sqrt(A)
     if (MODE == kNormalsCentBuf) {
 #pragma unroll
