@@ -64,10 +64,12 @@ class DeviceAccumulator:
 
     def __init__(self, ga, device=None):
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-        self.ids = torch.from_numpy(np.ascontiguousarray(ga.s2ids, dtype=np.uint64)
-                                    .view(np.int64)).to(dev)
-        self.normals = torch.from_numpy(np.ascontiguousarray(ga.normals, dtype=np.float64)).to(dev)
-        self.neighbors = torch.from_numpy(np.ascontiguousarray(ga.neighbors, dtype=np.int64)).to(dev)
+
+        def up(a, dtype):   # a host copy first: the shared structures are read-only
+            return torch.from_numpy(np.array(a, dtype=dtype, order="C", copy=True)).to(dev)
+        self.ids = up(np.ascontiguousarray(ga.s2ids, dtype=np.uint64).view(np.int64), np.int64)
+        self.normals = up(ga.normals, np.float64)
+        self.neighbors = up(ga.neighbors, np.int64)
         self.slope = float(ga.model_slope)
         self.intercept = float(ga.model_intercept)
         self.window = (int(ga.window_lo), int(ga.window_hi))
