@@ -69,19 +69,7 @@ constexpr int kBilNT = kBilTQW * kBilTQH / kQPT;  // threads per CTA
 #ifndef OPCFE_BIL_BLOCKS3
 #define OPCFE_BIL_BLOCKS3 7
 #endif
-// k = 3 weighs every unordered triangle pair once (bil_weigh_sym1, shared-memory weight
-// exchange); OPCFE_BIL_SYM=0 builds the one-sided form (bil_weigh) for A/B
-#ifndef OPCFE_BIL_SYM
-#define OPCFE_BIL_SYM 1
-#endif
-#ifndef OPCFE_BIL_BLOCKS3S
-#define OPCFE_BIL_BLOCKS3S 6
-#endif
-template <int H>
-__host__ __device__ constexpr bool bil_sym() { return OPCFE_BIL_SYM != 0 && H == 1; }
-constexpr int bil_min_blocks(int h) {
-  return h == 1 ? (OPCFE_BIL_SYM ? OPCFE_BIL_BLOCKS3S : OPCFE_BIL_BLOCKS3) : (h == 2 ? 5 : 4);
-}
+constexpr int bil_min_blocks(int h) { return h == 1 ? OPCFE_BIL_BLOCKS3 : (h == 2 ? 5 : 4); }
 
 enum BilMode : int {
   kFromPoints = 0,     // iteration 1: normals + centroids from the point grid
@@ -122,27 +110,11 @@ struct BilTile {
   static_assert(FC_F >= OUT_F, "out tile aliases the FC normal tile");
 };
 
-// Shared-memory weight exchange of the pair-symmetric k = 3 weighing (bil_weigh_sym1), in
-// f2 (two-lane) entries: 14 slots per thread (its quads' forward blocks, two rows each),
-// then the halo quads' forward blocks into the tile: top row [3 dirs][2 rows][QW], left
-// column [2 dirs][2 rows][QH], right column [2 rows][QH].
-template <int H>
-struct SymW {
-  static constexpr int QW = BilTile<H>::QW, QH = BilTile<H>::QH;
-  static constexpr int TOP = 14 * kBilNT;
-  static constexpr int LEFT = TOP + 3 * 2 * QW;
-  static constexpr int RIGHT = LEFT + 2 * 2 * QH;
-  static constexpr int FLOATS = bil_sym<H>() ? ((RIGHT + 2 * QH) * 2 + 31) / 32 * 32 : 0;
-};
-
-// out tile: its own region in mode 0; aliases the (dead after packing) FC tile otherwise.
-// The weight exchange overlays the point tile (dead after packing) where there is one.
+// out tile: its own region in mode 0; aliases the (dead after packing) FC tile otherwise
 template <int H, int MODE>
 constexpr int bil_smem_bytes() {
   using T = BilTile<H>;
-  constexpr int WF = SymW<H>::FLOATS;
-  constexpr int front = (MODE != kNormalsCentBuf) ? (T::PTS_F > WF ? T::PTS_F : WF) : WF;
-  return (front + ((MODE != kFromPoints) ? T::FC_F : 0) +
+  return (((MODE != kNormalsCentBuf) ? T::PTS_F : 0) + ((MODE != kFromPoints) ? T::FC_F : 0) +
           ((MODE == kNormalsCentBuf) ? 2 * T::FC_F : 0) + T::PACK_F +  // f64 centroid tile
           ((MODE == kFromPoints) ? T::OUT_F : 0)) *
              4 +
@@ -437,220 +409,6 @@ __device__ __forceinline__ void bil_weigh(const Planes& P, int R0, int C, float 
   }
 }
 
-// k = 3, pair-symmetric: every unordered triangle pair inside the window is weighed ONCE.
-// A quad's 8 neighbour quads split into 4 forward ones, (0,+1) (+1,-1) (+1,0) (+1,+1), and
-// their mirrors.  Phase A: each thread weighs its quads' forward blocks (2 own triangles x
-// the neighbour's 2 triangle lanes), accumulates them into its own triangles at once and
-// stores the two weight rows (w(own_j, nb_0), w(own_j, nb_1)) in shared memory; threads
-// also weigh, one block each, the halo quads' forward blocks that reach into the tile.
-// Phase B (after one barrier): each quad takes its 4 backward blocks from the producers'
-// rows: w(o_j, q0..1) x n_{o_j} accumulates with the quad's two triangles as the packed
-// lanes (accT), so no transposition is needed.  Forward work per quad: 4 blocks instead
-// of 8 -- the distance + MUFU half of the pair cost; the accumulation is unchanged.
-// Thread slots (f2 rows, [slot][thread]): a(0,+1) 0-1, a(+1,-1) 2-3, a(+1,+1) 4-5,
-// b(0,+1) 6-7, b(+1,-1) 8-9, b(+1,0) 10-11, b(+1,+1) 12-13 (a(+1,0) = b: in-thread).
-__device__ __forceinline__ f2_t weight2(const OwnTri& t, const Quad2& nb) {
-  const f2_t sd = dist2(t, nb);
-  return f2(ex2_approx(-f2lo(sd)), ex2_approx(-f2hi(sd)));
-}
-
-__device__ __forceinline__ void bil_weigh_sym1(const Planes& P, f2_t* W, int R0, int C, float sB,
-                                               Quad2& qa, Quad2& qb, float res[2][6],
-                                               bool upd[2][2]) {
-  using T = BilTile<1>;
-  using S = SymW<1>;
-  constexpr int QW = T::QW, QH = T::QH, NT = kBilNT;
-  constexpr int RT = 0, CL = T::LQ - 1, CR = T::LQ + kBilTQW;  // halo row / columns
-  constexpr int RI0 = 1, RI1 = kBilTQH, CI0 = T::LQ, CI1 = T::LQ + kBilTQW - 1;  // interior
-  static_assert(3 * (CR - CL + 1) + 3 * kBilTQH <= NT, "one halo block per thread");
-  static_assert(RT == 1 - 1 && CI0 - CL == 1 && CR - CI1 == 1, "k = 3 layout");
-  const int tid = threadIdx.x, tx = tid % kBilTQW, ty = tid / kBilTQW;
-  qa = load_quad2(P, R0 * QW + C);
-  qb = load_quad2(P, (R0 + 1) * QW + C);
-  f2_t acc[2][2][3];
-#pragma unroll
-  for (int o = 0; o < 2; ++o)
-#pragma unroll
-    for (int k = 0; k < 2; ++k) acc[o][k][0] = acc[o][k][1] = acc[o][k][2] = 0ull;
-
-  {  // in-thread pairs: intra-quad and a-b, as bil_weigh
-    const OwnTri own[2][2] = {{own_tri(qa, 0), own_tri(qa, 1)}, {own_tri(qb, 0), own_tri(qb, 1)}};
-#pragma unroll
-    for (int o = 0; o < 2; ++o) {
-      const Quad2& q = o == 0 ? qa : qb;
-      const OwnTri& t0 = own[o][0];
-      const OwnTri& t1 = own[o][1];
-      const float dx = t1.cx - t0.cx, dy = t1.cy - t0.cy, dz = t1.cz - t0.cz;
-      const float ex = t1.nx - t0.nx, ey = t1.ny - t0.ny, ez = t1.nz - t0.nz;
-      float e = dx * dx;
-      e = fmaf(dy, dy, e);
-      e = fmaf(dz, dz, e);
-      e = fmaf(ex, ex, e);
-      e = fmaf(ey, ey, e);
-      e = fmaf(ez, ez, e);
-      const float w = ex2_approx(-e);
-      const f2_t w_to1 = f2(w, 0.f), w_to0 = f2(0.f, w);
-      acc[o][1][0] = fma2(q.nx, w_to1, acc[o][1][0]);
-      acc[o][1][1] = fma2(q.ny, w_to1, acc[o][1][1]);
-      acc[o][1][2] = fma2(q.nz, w_to1, acc[o][1][2]);
-      acc[o][0][0] = fma2(q.nx, w_to0, acc[o][0][0]);
-      acc[o][0][1] = fma2(q.ny, w_to0, acc[o][0][1]);
-      acc[o][0][2] = fma2(q.nz, w_to0, acc[o][0][2]);
-    }
-    f2_t wv[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      wv[k] = weight2(own[0][k], qb);
-      acc[0][k][0] = fma2(qb.nx, wv[k], acc[0][k][0]);
-      acc[0][k][1] = fma2(qb.ny, wv[k], acc[0][k][1]);
-      acc[0][k][2] = fma2(qb.nz, wv[k], acc[0][k][2]);
-    }
-#pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
-      const f2_t w = kk == 0 ? f2(f2lo(wv[0]), f2lo(wv[1])) : f2(f2hi(wv[0]), f2hi(wv[1]));
-      acc[1][kk][0] = fma2(qa.nx, w, acc[1][kk][0]);
-      acc[1][kk][1] = fma2(qa.ny, w, acc[1][kk][1]);
-      acc[1][kk][2] = fma2(qa.nz, w, acc[1][kk][2]);
-    }
-  }
-
-  // phase A: forward blocks of the thread's quads
-  auto fwd = [&](int o, const Quad2& q, int slot, const Quad2& nb) {
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const f2_t w = weight2(own_tri(q, k), nb);
-      acc[o][k][0] = fma2(nb.nx, w, acc[o][k][0]);
-      acc[o][k][1] = fma2(nb.ny, w, acc[o][k][1]);
-      acc[o][k][2] = fma2(nb.nz, w, acc[o][k][2]);
-      W[(slot + k) * NT + tid] = w;
-    }
-  };
-  {
-    const Quad2 n = load_quad2(P, R0 * QW + C + 1);
-    fwd(0, qa, 0, n);
-  }
-  {
-    const Quad2 n = load_quad2(P, (R0 + 1) * QW + C - 1);
-    fwd(0, qa, 2, n);
-  }
-  {
-    const Quad2 n = load_quad2(P, (R0 + 1) * QW + C + 1);  // a(+1,+1) == b(0,+1)
-    fwd(0, qa, 4, n);
-    fwd(1, qb, 6, n);
-  }
-#pragma unroll
-  for (int dc = -1; dc <= 1; ++dc) {
-    const Quad2 n = load_quad2(P, (R0 + 2) * QW + C + dc);
-    fwd(1, qb, 10 + 2 * dc, n);
-  }
-  // halo quads' forward blocks into the tile, one per thread: top row x (+1, -1 / 0 / +1),
-  // left column x (0,+1) / (+1,+1), right column x (+1,-1); rows stored per (dir, row j)
-  {
-    int orow = -1, ocol = 0, trow = 0, tcol = 0, js = 0;
-    f2_t* dst = nullptr;
-    if (tid < 3 * (CR - CL + 1)) {
-      const int d = tid % 3;
-      orow = RT;
-      ocol = CL + tid / 3;
-      trow = RT + 1;
-      tcol = ocol + d - 1;
-      dst = W + S::TOP + 2 * d * QW + ocol;
-      js = QW;
-      if (tcol < CI0 || tcol > CI1) orow = -1;
-    } else if (tid < 3 * (CR - CL + 1) + 2 * kBilTQH) {
-      const int i = tid - 3 * (CR - CL + 1), d = i % 2;
-      orow = RI0 + i / 2;
-      ocol = CL;
-      trow = orow + d;
-      tcol = CI0;
-      dst = W + S::LEFT + 2 * d * QH + orow;
-      js = QH;
-      if (trow > RI1) orow = -1;
-    } else if (tid < 3 * (CR - CL + 1) + 3 * kBilTQH) {
-      orow = RI0 + (tid - 3 * (CR - CL + 1) - 2 * kBilTQH);
-      ocol = CR;
-      trow = orow + 1;
-      tcol = CI1;
-      dst = W + S::RIGHT + orow;
-      js = QH;
-      if (trow > RI1) orow = -1;
-    }
-    if (orow >= 0) {
-      const Quad2 qo = load_quad2(P, orow * QW + ocol);
-      const Quad2 qt = load_quad2(P, trow * QW + tcol);
-      dst[0] = weight2(own_tri(qo, 0), qt);
-      dst[js] = weight2(own_tri(qo, 1), qt);
-    }
-  }
-  __syncthreads();
-
-  // phase B: backward blocks -- producer rows w(o_j, q_0..1) x n_{o_j}, lanes = q's triangles
-  f2_t accT[2][3];
-#pragma unroll
-  for (int o = 0; o < 2; ++o) accT[o][0] = accT[o][1] = accT[o][2] = 0ull;
-  auto back = [&](int o, const f2_t* w, int js, int opos) {
-    const float4 n0 = P.n0[opos];  // (n'x0, n'x1, n'y0, n'y1)
-    const float2 n1 = P.n1[opos];  // (n'z0, n'z1)
-    const f2_t w0 = w[0], w1 = w[js];
-    accT[o][0] = fma2(w0, bc2(n0.x), accT[o][0]);
-    accT[o][1] = fma2(w0, bc2(n0.z), accT[o][1]);
-    accT[o][2] = fma2(w0, bc2(n1.x), accT[o][2]);
-    accT[o][0] = fma2(w1, bc2(n0.y), accT[o][0]);
-    accT[o][1] = fma2(w1, bc2(n0.w), accT[o][1]);
-    accT[o][2] = fma2(w1, bc2(n1.y), accT[o][2]);
-  };
-  const bool top = ty == 0, left = tx == 0, right = tx == kBilTQW - 1;
-  // quad a = (R0, C)
-  back(0, left ? W + S::LEFT + R0 : W + 0 * NT + tid - 1, left ? QH : NT, R0 * QW + C - 1);
-  back(0, top ? W + S::TOP + 0 * QW + C + 1 : (right ? W + S::RIGHT + R0 - 1 : W + 8 * NT + tid - kBilTQW + 1),
-       top ? QW : (right ? QH : NT), (R0 - 1) * QW + C + 1);
-  back(0, top ? W + S::TOP + 2 * QW + C : W + 10 * NT + tid - kBilTQW, top ? QW : NT,
-       (R0 - 1) * QW + C);
-  back(0, top ? W + S::TOP + 4 * QW + C - 1
-              : (left ? W + S::LEFT + 2 * QH + R0 - 1 : W + 12 * NT + tid - kBilTQW - 1),
-       top ? QW : (left ? QH : NT), (R0 - 1) * QW + C - 1);
-  // quad b = (R0 + 1, C); its (-1, 0) neighbour is a (in-thread, above)
-  back(1, left ? W + S::LEFT + R0 + 1 : W + 6 * NT + tid - 1, left ? QH : NT,
-       (R0 + 1) * QW + C - 1);
-  back(1, right ? W + S::RIGHT + R0 : W + 2 * NT + tid + 1, right ? QH : NT, R0 * QW + C + 1);
-  back(1, left ? W + S::LEFT + 2 * QH + R0 : W + 4 * NT + tid - 1, left ? QH : NT,
-       R0 * QW + C - 1);
-
-  // underflow-safe normalisation (as bil_weigh); own sentinel tests on the reloaded quads
-  qa = load_quad2(P, R0 * QW + C);
-  qb = load_quad2(P, (R0 + 1) * QW + C);
-  const float thr = 1e-30f * sB;
-#pragma unroll
-  for (int o = 0; o < 2; ++o) {
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      float* r = &res[o][3 * k];
-      const Quad2& q = o == 0 ? qa : qb;
-      const bool valid = (k == 0 ? f2lo(q.cx) : f2hi(q.cx)) != 1e18f;  // not the pack sentinel
-      auto lane = [&](f2_t v) { return k == 0 ? f2lo(v) : f2hi(v); };
-      const float ax = (f2lo(acc[o][k][0]) + f2hi(acc[o][k][0])) + lane(accT[o][0]);
-      const float ay = (f2lo(acc[o][k][1]) + f2hi(acc[o][k][1])) + lane(accT[o][1]);
-      const float az = (f2lo(acc[o][k][2]) + f2hi(acc[o][k][2])) + lane(accT[o][2]);
-      const float sc = fmaxf(fabsf(ax), fmaxf(fabsf(ay), fabsf(az)));
-      upd[o][k] = false;
-      r[0] = r[1] = r[2] = 0.f;
-      if (valid && sc > 0.f) {
-        const float is = rcp_approx(sc);
-        const float mx = ax * is, my = ay * is, mz = az * is;
-        const float l2 = mx * mx + my * my + mz * mz;
-        float il = rsqrt_approx(l2);
-        il = il * fmaf(-0.5f * l2, il * il, 1.5f);
-        if (l2 * il * sc > thr) {
-          r[0] = mx * il;
-          r[1] = my * il;
-          r[2] = mz * il;
-          upd[o][k] = true;
-        }
-      }
-    }
-  }
-}
-
 // the fused pipeline's packed FC arrays in global memory (per frame, row-major quads):
 // C0 / N0 float4 [Mq][Nq], C1 / N1 float2 [Mq][Nq2] (Nq2 = Nq rounded up to even)
 struct PackedG {  // the packed normal planes N0 / N1 of the fused pipeline
@@ -713,10 +471,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
   float* pts_s = nullptr;
   float* nrm_s = nullptr;
   float* cen_s = nullptr;
-  constexpr int WF = SymW<H>::FLOATS;
-  f2_t* wx = reinterpret_cast<f2_t*>(p);  // weight exchange (overlays the point tile)
-  if (MODE != kNormalsCentBuf) { pts_s = p; p += (T::PTS_F > WF ? T::PTS_F : WF); }
-  else { p += WF; }
+  if (MODE != kNormalsCentBuf) { pts_s = p; p += T::PTS_F; }
   if (MODE != kFromPoints) { nrm_s = p; p += T::FC_F; }
   if (MODE == kNormalsCentBuf) { cen_s = p; p += 2 * T::FC_F; }  // float64 centroid tile
   const double* cen_d = reinterpret_cast<const double*>(cen_s);
@@ -823,10 +578,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
   Quad2 qa, qb;
   float res[2][6];
   bool upd[2][2];
-  if constexpr (bil_sym<H>())
-    bil_weigh_sym1(P, wx, R0, C, sB, qa, qb, res, upd);
-  else
-    bil_weigh<H>(P, R0, C, sB, qa, qb, res, upd);
+  bil_weigh<H>(P, R0, C, sB, qa, qb, res, upd);
 
   if constexpr (PACKOUT) {
 #pragma unroll
@@ -896,7 +648,6 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
   uint64_t* barp;
   float* p = reinterpret_cast<float*>(smem_aligned_base(smem_raw, &barp));
   const Planes P = planes_at<H>(p);
-  f2_t* wx = reinterpret_cast<f2_t*>(p + T::PACK_F);  // weight exchange (k = 3)
   uint64_t& bar = *barp;
   const int Mq = a.M - 1, Nq = a.N - 1;
   const int q0 = blockIdx.x * kBilTQW;
@@ -922,10 +673,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
   Quad2 qa, qb;
   float res[2][6];
   bool upd[2][2];
-  if constexpr (bil_sym<H>())
-    bil_weigh_sym1(P, wx, R0, C, sB, qa, qb, res, upd);
-  else
-    bil_weigh<H>(P, R0, C, sB, qa, qb, res, upd);
+  bil_weigh<H>(P, R0, C, sB, qa, qb, res, upd);
 
 #pragma unroll
   for (int o = 0; o < 2; ++o) {
@@ -994,7 +742,7 @@ template <int H, bool SCATTER>
 int launch_packed(const CUtensorMap* maps, const BilArgs& a, int F, const PackedG& out,
                   cudaStream_t st) {
   using T = BilTile<H>;
-  constexpr int smem = (T::PACK_F + SymW<H>::FLOATS) * 4 + kSmemSlack;
+  constexpr int smem = T::PACK_F * 4 + kSmemSlack;
   static std::atomic<unsigned long long> attr_mask{0};
   if (const int rc = ensure_smem_attr(bilateral_packed_kernel<H, SCATTER>, smem, attr_mask))
     return rc;
