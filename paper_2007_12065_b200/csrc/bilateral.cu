@@ -322,13 +322,16 @@ __device__ __forceinline__ void bil_weigh(const Planes& P, int R0, int C, float 
     e = fmaf(ey, ey, e);
     e = fmaf(ez, ez, e);
     const float w = ex2_approx(-e);
-    const f2_t w_to1 = f2(w, 0.f), w_to0 = f2(0.f, w);  // tri 1 <- tri 0 (lane kk = 0), ...
-    acc[o][1][0] = fma2(q.nx, w_to1, acc[o][1][0]);
-    acc[o][1][1] = fma2(q.ny, w_to1, acc[o][1][1]);
-    acc[o][1][2] = fma2(q.nz, w_to1, acc[o][1][2]);
-    acc[o][0][0] = fma2(q.nx, w_to0, acc[o][0][0]);
-    acc[o][0][1] = fma2(q.ny, w_to0, acc[o][0][1]);
-    acc[o][0][2] = fma2(q.nz, w_to0, acc[o][0][2]);
+    // tri 1 <- tri 0 into lane kk = 0, tri 0 <- tri 1 into lane kk = 1: one scalar FMA per
+    // component (the other lane is untouched)
+    auto lo_fma = [&](f2_t n, f2_t& a) { a = f2(fmaf(f2lo(n), w, f2lo(a)), f2hi(a)); };
+    auto hi_fma = [&](f2_t n, f2_t& a) { a = f2(f2lo(a), fmaf(f2hi(n), w, f2hi(a))); };
+    lo_fma(q.nx, acc[o][1][0]);
+    lo_fma(q.ny, acc[o][1][1]);
+    lo_fma(q.nz, acc[o][1][2]);
+    hi_fma(q.nx, acc[o][0][0]);
+    hi_fma(q.ny, acc[o][0][1]);
+    hi_fma(q.nz, acc[o][0][2]);
   }
   //   vertical a-b: a's triangle k against b's pair (lanes kk), shared with b
   {
@@ -387,22 +390,34 @@ __device__ __forceinline__ void bil_weigh(const Planes& P, int R0, int C, float 
       const float ax = f2lo(acc[o][k][0]) + f2hi(acc[o][k][0]);
       const float ay = f2lo(acc[o][k][1]) + f2hi(acc[o][k][1]);
       const float az = f2lo(acc[o][k][2]) + f2hi(acc[o][k][2]);
-      const float sc = fmaxf(fabsf(ax), fmaxf(fabsf(ay), fabsf(az)));
       upd[o][k] = false;
       r[0] = r[1] = r[2] = 0.f;
-      if (valid && sc > 0.f) {
-        const float is = rcp_approx(sc);  // a common scale: cancels in the normalisation
-        const float mx = ax * is, my = ay * is, mz = az * is;
-        // |m|^2 in [1, 3]: MUFU rsqrt + one Newton step (~1 ulp, like IEEE sqrt + divide,
-        // whose slow-path checks cost ~8 % of the kernel's instructions)
-        const float l2 = mx * mx + my * my + mz * mz;
-        float il = rsqrt_approx(l2);
-        il = il * fmaf(-0.5f * l2, il * il, 1.5f);
-        if (l2 * il * sc > thr) {
-          r[0] = mx * il;
-          r[1] = my * il;
-          r[2] = mz * il;
-          upd[o][k] = true;
+      // |acc'|^2 inside [2^-120, 2^120] (the usual case): normalise directly, and |acc'| >=
+      // 2^-60 > thr, so the triangle moves.  Outside (rare): rescale by max |acc'_i| first.
+      // MUFU rsqrt + one Newton step (~1 ulp, like IEEE sqrt + divide, whose slow-path
+      // checks cost ~8 % of the kernel's instructions).
+      const float d2 = fmaf(az, az, fmaf(ay, ay, ax * ax));
+      if (valid && d2 >= 7.5231638e-37f && d2 <= 1.329228e36f) {
+        float il = rsqrt_approx(d2);
+        il = il * fmaf(-0.5f * d2, il * il, 1.5f);
+        r[0] = ax * il;
+        r[1] = ay * il;
+        r[2] = az * il;
+        upd[o][k] = true;
+      } else {
+        const float sc = fmaxf(fabsf(ax), fmaxf(fabsf(ay), fabsf(az)));
+        if (valid && sc > 0.f) {
+          const float is = rcp_approx(sc);  // a common scale: cancels in the normalisation
+          const float mx = ax * is, my = ay * is, mz = az * is;
+          const float l2 = mx * mx + my * my + mz * mz;  // in [1, 3]
+          float il = rsqrt_approx(l2);
+          il = il * fmaf(-0.5f * l2, il * il, 1.5f);
+          if (l2 * il * sc > thr) {
+            r[0] = mx * il;
+            r[1] = my * il;
+            r[2] = mz * il;
+            upd[o][k] = true;
+          }
         }
       }
     }
