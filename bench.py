@@ -105,6 +105,7 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.start = self.stop = 0
 
     def __enter__(self):
         try:
@@ -114,8 +115,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()                    # nvidia-smi takes ~0.1-0.3 s to start:
+            while not self.rows and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)                # sample only once it is streaming
         except OSError:
             self.proc = None
+        self.start = len(self.rows)
         return self
 
     def _read(self):
@@ -123,12 +128,19 @@ class ClockSampler:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        self.stop = len(self.rows)
         if self.proc is not None:
+            if self.stop == self.start:         # region shorter than one interval: take
+                t0 = time.time()                # the sample that closes it
+                while len(self.rows) == self.stop and time.time() - t0 < 0.2:
+                    time.sleep(0.005)
+                self.stop = len(self.rows)
             self.proc.terminate()
             self.proc.wait()
 
     def summary(self):
-        load = [r for r in self.rows if len(r) >= 8 and r[0].replace(".", "").isdigit()]
+        load = [r for r in self.rows[self.start:self.stop]
+                if len(r) >= 8 and r[0].replace(".", "").isdigit()]
         if not load:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         mhz = [float(r[0]) for r in load]
