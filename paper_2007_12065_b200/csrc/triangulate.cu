@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kTriNT, 1024 / kTriNT) triangulate_kernel(TriA
         const long long gid = 2ll * ((long long)u * Nq + v);
         const long long t0 = t_first + l0;
         const long long t1 = t0 + bf;
-        *reinterpret_cast<longlong2*>(trimap + gid) = make_longlong2(bf ? t0 : -1ll, bs ? t1 : -1ll);
+        __stcs(reinterpret_cast<longlong2*>(trimap + gid), make_longlong2(bf ? t0 : -1ll, bs ? t1 : -1ll));
         const int64_t i1 = (int64_t)u * N + v, i2 = i1 + 1, i4 = i1 + N, i3 = i4 + 1;
         if (bf) {
           st_t[3 * l0] = i3;
@@ -316,10 +316,10 @@ __global__ void __launch_bounds__(kTriNT, 1024 / kTriNT) triangulate_kernel(TriA
       // contiguous, coalesced copy-out of this group's triangles [t_first, + n)
       const int n3 = 3 * (__popc(qc.f) + __popc(qc.s));
       int64_t* tdst = tris + 3 * t_first;
-      for (int i = lane; i < n3; i += 32) tdst[i] = st_t[i];
+      for (int i = lane; i < n3; i += 32) __stcs(reinterpret_cast<long long*>(tdst) + i, st_t[i]);
       if (he) {
         int64_t* hdst = he + 3 * t_first;
-        for (int i = lane; i < n3; i += 32) hdst[i] = st_h[i];
+        for (int i = lane; i < n3; i += 32) __stcs(reinterpret_cast<long long*>(hdst) + i, st_h[i]);
       }
       __syncwarp();  // staging reused by the warp's next group
     }
