@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import os
 import threading
+import warnings
 
 import numpy as np
 import torch
@@ -37,6 +38,14 @@ def points_pitch(N: int) -> int:
 
 def fc_pitch(N: int) -> int:
     return (6 * (N - 1) + 3) // 4 * 4
+
+
+def host_view(arr: np.ndarray) -> torch.Tensor:
+    """torch view of a NumPy array that is only ever READ (a read-only caller array is
+    fine: torch's non-writable warning does not apply)."""
+    with warnings.catch_warnings():
+        warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+        return torch.from_numpy(arr)
 
 
 class HostTransfer:
@@ -123,7 +132,7 @@ class HostTransfer:
         """A contiguous NumPy array -> a new device tensor (ordered before later work on
         the current stream)."""
         arr = np.ascontiguousarray(arr)
-        t_host = torch.from_numpy(arr)
+        t_host = host_view(arr)
         if arr.nbytes < self.MIN_BYTES:
             return t_host.to(self.device)
         if t_host.is_pinned():          # e.g. a result of a previous call: DMA directly

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._device import points_pitch, require_cuda
+from ._device import host_view, points_pitch, require_cuda
 from .mesh import HalfEdgeMesh
 from .smoothing import BilateralParams, LaplacianParams
 
@@ -510,7 +510,7 @@ def front_end(opc, laplacian: LaplacianParams | None = None,
     """
     from .smoothing import resolve_precision
     is_np = not isinstance(opc, torch.Tensor)
-    src = torch.from_numpy(np.ascontiguousarray(opc, dtype=np.float64)) if is_np else opc
+    src = host_view(np.ascontiguousarray(opc, dtype=np.float64)) if is_np else opc
     if src.dtype not in (torch.float32, torch.float64):
         src = src.to(torch.float64)
     src = src.to("cuda").contiguous()

@@ -22,7 +22,7 @@ import numpy as np
 import torch
 
 from . import _ops
-from ._device import Staged
+from ._device import Staged, host_view
 
 UNASSIGNED = np.uint8(255)
 MAX_GROUPS = 254
@@ -46,7 +46,7 @@ def group_assignment(mesh, dominant_normals, l_max: float, ang_min: float):
     tri = Staged(mesh.triangles, float_only=False).dev.to(torch.int64).reshape(-1, 3).contiguous()
     nrm = Staged(mesh.normals).dev.reshape(-1, 3).contiguous()
     lflag = _ops.max_edge_mask(pts, tri, l_max).to(torch.uint8)
-    labels = _ops.group_assignment(nrm, torch.from_numpy(dn), ang_min, lflag=lflag)
+    labels = _ops.group_assignment(nrm, host_view(dn), ang_min, lflag=lflag)
     return P.give(labels)
 
 
