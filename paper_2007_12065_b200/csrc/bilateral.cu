@@ -541,8 +541,8 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
       P.c1[q] = make_float2(0.f, 0.f);
     }
   }
-  for (int i = threadIdx.x; i < T::QH * T::CW; i += kBilNT) {
-    const int r = i / T::CW, c = T::CB + i % T::CW, q = r * T::QW + c;
+  auto pack_at = [&](int r, int c) {
+    const int q = r * T::QW + c;
     float n[6], cc[6];  // cc: scaled centroids c' = c * sqrt(A)
     if (MODE == kNormalsCentBuf) {
 #pragma unroll
@@ -579,7 +579,14 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
       }
     }
     pack_quad(P, q, n, cc, sB);
-  }
+  };
+  // a warp packs 32 consecutive quads of one row (no row wrap inside a warp: conflict-free
+  // point loads and plane stores), then the last warps the 2H leftover columns of each row
+  static_assert(T::CW >= kBilTQW && kBilTQW == 32, "row segments of one warp");
+  for (int r = threadIdx.x / 32; r < T::QH; r += kBilNT / 32) pack_at(r, T::CB + threadIdx.x % 32);
+  constexpr int LW = T::CW - kBilTQW;
+  for (int j = kBilNT - 1 - threadIdx.x; j < T::QH * LW; j += kBilNT)
+    pack_at(j / LW, T::CB + kBilTQW + j % LW);
   __syncthreads();
   if (PACKOUT && threadIdx.x == 0) {  // the tile's centroid window, for iterations 2..B
     char* win = a.cwin + (((long long)f * a.gy + blockIdx.y) * a.gx + blockIdx.x) * a.wstride;
