@@ -356,7 +356,7 @@ def strict_throughput(fe, wl, eng_fast, args, dev):
     return out
 
 
-def dropin_e2e(fe, wl, frame, dev, frames=3):
+def dropin_e2e(fe, wl, frame, dev, frames=5):
     """pipeline.py:125-134 unchanged, through the drop-in API (NumPy float64 in, NumPy
     out, one frame per call), host wall clock around each whole frame."""
     import numpy as np
@@ -372,7 +372,10 @@ def dropin_e2e(fe, wl, frame, dev, frames=3):
             mesh.normals = fe.bilateral_filter_opc(sm, bp, mesh.trimap)
         return sm, mesh
 
-    one()
+    # warm-up as the timed loop runs (the previous frame's results alive while the next
+    # is computed), so the pinned result blocks of both are cached before timing
+    sm, mesh = one()
+    sm, mesh = one()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for _ in range(frames):

@@ -1,0 +1,8 @@
+# the driver's default bench invocation once, summarised
+cd $GRAFT_REPO_ROOT
+( time timeout 900 python bench.py ) > gpurun_out/b1.json 2> gpurun_out/b1.err; echo "rc=$?"; tail -3 gpurun_out/b1.err
+python - <<'PY'
+import json
+d = json.load(open("gpurun_out/b1.json"))
+print(round(d["value"],1), "e2e", round(d["e2e"]["value"],1), {k: round(v["value"],1) for k, v in d["e2e"].items() if isinstance(v, dict) and "value" in v}, "strict", round(d["strict"]["value"],1), d["roofline"]["frac"], d["clocks"], d["stage_ms_per_step"])
+PY
