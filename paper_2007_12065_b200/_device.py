@@ -68,7 +68,7 @@ class HostTransfer:
     CHUNK = int(os.environ.get("OPCFE_XFER_CHUNK_MB", "8")) << 20
     SLOTS = int(os.environ.get("OPCFE_XFER_SLOTS", "16"))
     MIN_BYTES = 4 << 20
-    PINNED_OUT_MB = int(os.environ.get("OPCFE_PINNED_OUT_MB", "16384"))
+    PINNED_OUT_MB = int(os.environ.get("OPCFE_PINNED_OUT_MB", "4096"))
     _inst = {}
 
     def __init__(self, device):
