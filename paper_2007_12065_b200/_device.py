@@ -9,6 +9,7 @@ from __future__ import annotations
 import os
 import threading
 import warnings
+import weakref
 
 import numpy as np
 import torch
@@ -56,8 +57,8 @@ class HostTransfer:
     DMA writes straight into the caller's array at the link rate (~54 GB/s on the B200
     box) -- a D2H into a fresh pageable array runs at ~2 GB/s (the driver's pageable
     path page-faults the destination as it copies) and even a staged copy is bound by
-    first-touch page faults (~7 GB/s per thread).  Past `PINNED_OUT_MB` of pinned host
-    memory in use (callers holding many results) it falls back to a ring of pinned
+    first-touch page faults (~7 GB/s per thread).  Past `PINNED_OUT_MB` of such results
+    still alive in callers' hands it falls back to a ring of pinned
     staging chunks DMA'd on a side stream while `SLOTS` threads copy finished chunks into
     a fresh NumPy array (numpy releases the GIL for the copy).
     H2D: an input that already lives in pinned memory (e.g. a previous call's result)
@@ -81,6 +82,8 @@ class HostTransfer:
         self.events = [torch.cuda.Event() for _ in range(self.SLOTS)]
         self.pool = ThreadPoolExecutor(self.SLOTS)
         self.lock = threading.Lock()         # one transfer at a time per device (shared slots)
+        self.out_lock = threading.Lock()
+        self.out_bytes = 0                   # pinned result blocks alive in callers' arrays
 
     @classmethod
     def get(cls, device) -> "HostTransfer":
@@ -98,15 +101,25 @@ class HostTransfer:
         if self._pinned_room(nbytes):
             h = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
             h.copy_(t)                  # one DMA into the returned array's own memory
-            return h.numpy()            # the array keeps the pinned block alive
+            arr = h.numpy()             # the array (its base) keeps the pinned block alive
+            blk = 1 << (nbytes - 1).bit_length()        # the allocator's power-of-2 block
+            with self.out_lock:
+                self.out_bytes += blk
+            weakref.finalize(arr.base, self._released, blk)
+            return arr
         out = np.empty(tuple(t.shape), dtype=torch.empty((), dtype=t.dtype).numpy().dtype)
         with self.lock:
             self._d2h(t, out, nbytes)
         return out
 
     def _pinned_room(self, nbytes: int) -> bool:
-        used = torch.cuda.host_memory_stats().get("active_bytes.current", 0)
-        return used + 2 * nbytes <= self.PINNED_OUT_MB << 20   # blocks round up to 2^k
+        """Results handed out in pinned blocks and still alive stay under the budget."""
+        with self.out_lock:
+            return self.out_bytes + 2 * nbytes <= self.PINNED_OUT_MB << 20
+
+    def _released(self, blk: int) -> None:
+        with self.out_lock:
+            self.out_bytes -= blk
 
     def _d2h(self, t, out, nbytes):
         src = t.reshape(-1).view(torch.uint8)

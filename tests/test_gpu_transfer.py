@@ -56,6 +56,16 @@ def test_pinned_blocks_are_reused(xfer):
         del a
     after = torch.cuda.host_memory_stats().get("allocated_bytes.current", 0)
     assert after == before                          # no new pinned blocks per call
+    held = xfer.out_bytes
+    keep = [xfer.to_numpy(t) for _ in range(3)]     # results alive count against the budget
+    assert xfer.out_bytes == held + 3 * (4 << 23)
+    view = keep[0][5:]
+    del keep
+    gc.collect()
+    assert xfer.out_bytes == held + (4 << 23)       # a view keeps its block
+    del view
+    gc.collect()
+    assert xfer.out_bytes == held
 
 
 def test_pinned_input_round_trip(xfer):
