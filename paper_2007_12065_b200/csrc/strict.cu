@@ -189,170 +189,6 @@ __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_kernel(const double* __
   dst[o + 2] = pz;
 }
 
-// k = 3, pair-symmetric: the weight of a pair and its d * w are the same numbers from
-// either end (|q - p|^2 == |p - q|^2 exactly, dmul(-dx, w) == -dmul(dx, w)), so every
-// unordered pair's IEEE sqrt + divide -- the bulk of the kernel -- is evaluated once.
-// Phase A: each point computes its 4 forward pairs E (0,+1), SW (+1,-1), S (+1,0),
-// SE (+1,+1) into shared memory as (dx w, dy w, dz w, w) -- zeros for a pair the
-// reference skips (NaN or zero distance: adding +0 leaves the sums bit-identical, none of
-// them can be -0) -- and threads also evaluate, one each, the halo points' forward pairs
-// into the tile (row above: SW / S / SE; left column: E / SE; right column: SW).  Phase B
-// (after one barrier): each point sums its 8 pairs in the reference's du-outer / dv-inner
-// order, the 4 backward ones negated from their computers' records: bit-identical to
-// laplacian_f64_kernel.
-struct LapSymS {
-  static constexpr int BW = kSTW + 2, BH = kSTH + 2, PLANE = BW * BH;
-  static constexpr int TILE = 3 * PLANE;                  // doubles: pair records follow
-  static constexpr int TOP = TILE + 4 * 4 * kSNT;         // [4 dirs][kSNT][4]
-  static constexpr int LEFT = TOP + 3 * 4 * BW;           // top row [3 dirs][BW][4]
-  static constexpr int RIGHT = LEFT + 2 * 4 * kSTH;       // left column [2 dirs][kSTH][4]
-  static constexpr int DOUBLES = RIGHT + 4 * kSTH;        // right column [kSTH][4]
-};
-
-// one pair p -> q: (dx w, dy w, dz w, w), zeros where the reference skips it
-__device__ __forceinline__ void lap_pair_f64(const double* sm, int pc, int qc, double* rec) {
-  constexpr int PL = LapSymS::PLANE;
-  const double dx = dsub(sm[qc], sm[pc]), dy = dsub(sm[PL + qc], sm[PL + pc]),
-               dz = dsub(sm[2 * PL + qc], sm[2 * PL + pc]);
-  const double dist = __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
-  double w = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
-  if (dist > 0.0) {  // NaN or <= 0: skipped (_native.pyx:265-266)
-    w = __drcp_rn(dist);
-    ax = dmul(dx, w);
-    ay = dmul(dy, w);
-    az = dmul(dz, w);
-  }
-  reinterpret_cast<double2*>(rec)[0] = make_double2(ax, ay);
-  reinterpret_cast<double2*>(rec)[1] = make_double2(az, w);
-}
-
-__global__ void __launch_bounds__(kSNT, 4) laplacian_f64_sym_kernel(const double* __restrict__ in,
-                                                                    double* __restrict__ out,
-                                                                    int M, int N, double lam) {
-  using S = LapSymS;
-  constexpr int BW = S::BW, PL = S::PLANE;
-  const int f = blockIdx.z;
-  const long long fs = 3ll * M * N;
-  const double* src = in + f * fs;
-  double* dst = out + f * fs;
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kSTW + tx;
-  const int u = blockIdx.y * kSTH + ty, v = blockIdx.x * kSTW + tx;
-  extern __shared__ double sm[];
-  {
-    const int u0 = blockIdx.y * kSTH - 1, v0 = blockIdx.x * kSTW - 1;
-    for (int q = tid; q < PL; q += kSNT) {
-      const int r = q / BW, c = q - r * BW;
-      const int uu = u0 + r, vv = v0 + c;
-      double x = qnan(), y = qnan(), z = qnan();
-      if (uu >= 0 && uu < M && vv >= 0 && vv < N) {
-        const double* g = src + ((long long)uu * N + vv) * 3;
-        x = __ldg(g);
-        y = __ldg(g + 1);
-        z = __ldg(g + 2);
-      }
-      sm[q] = x;
-      sm[PL + q] = y;
-      sm[2 * PL + q] = z;
-    }
-    __syncthreads();
-  }
-  // box coordinates: tile point (ty, tx) is box (ty + 1, tx + 1)
-  const int pc = (ty + 1) * BW + tx + 1;
-  double* const T = sm + S::TOP - 4 * 4 * kSNT;  // == sm + S::TILE: per-thread records
-  // phase A: the thread's forward pairs E, SW, S, SE
-  lap_pair_f64(sm, pc, pc + 1, T + (0 * kSNT + tid) * 4);
-  lap_pair_f64(sm, pc, pc + BW - 1, T + (1 * kSNT + tid) * 4);
-  lap_pair_f64(sm, pc, pc + BW, T + (2 * kSNT + tid) * 4);
-  lap_pair_f64(sm, pc, pc + BW + 1, T + (3 * kSNT + tid) * 4);
-  //         halo points' forward pairs into the tile, one per thread: row above (box
-  //         row 0) SW / S / SE, left column (box column 0) E / SE, right column SW
-  {
-    int hp = -1, hq = 0;
-    double* rec = nullptr;
-    if (tid < 3 * BW) {
-      const int c = tid / 3, d = tid % 3, tc = c + d - 1;
-      if (tc >= 1 && tc <= kSTW) {
-        hp = c;
-        hq = BW + tc;
-        rec = sm + S::TOP + (d * BW + c) * 4;
-      }
-    } else if (tid < 3 * BW + 2 * kSTH) {
-      const int i = tid - 3 * BW, r = i / 2, d = i % 2;
-      if (r + d < kSTH) {
-        hp = (r + 1) * BW;
-        hq = (r + 1 + d) * BW + 1;
-        rec = sm + S::LEFT + (d * kSTH + r) * 4;
-      }
-    } else if (tid < 3 * BW + 3 * kSTH) {
-      const int r = tid - 3 * BW - 2 * kSTH;
-      if (r + 1 < kSTH) {
-        hp = (r + 1) * BW + BW - 1;
-        hq = (r + 2) * BW + BW - 2;
-        rec = sm + S::RIGHT + r * 4;
-      }
-    }
-    if (hp >= 0) lap_pair_f64(sm, hp, hq, rec);
-  }
-  __syncthreads();
-  if (u >= M || v >= N) return;
-  const long long o = ((long long)u * N + v) * 3;
-  double px = sm[pc], py = sm[PL + pc], pz = sm[2 * PL + pc];
-  // outer ring copied (_native.pyx:240-241); NaN centre kept (:245-249)
-  if (u == 0 || u == M - 1 || v == 0 || v == N - 1 || px != px || py != py || pz != pz) {
-    dst[o] = px;
-    dst[o + 1] = py;
-    dst[o + 2] = pz;
-    return;
-  }
-  double ax = 0.0, ay = 0.0, az = 0.0, wsum = 0.0;
-  auto add = [&](const double* rec, bool neg) {
-    const double2 a = reinterpret_cast<const double2*>(rec)[0];
-    const double2 b = reinterpret_cast<const double2*>(rec)[1];
-    ax = dadd(ax, neg ? -a.x : a.x);
-    ay = dadd(ay, neg ? -a.y : a.y);
-    az = dadd(az, neg ? -b.x : b.x);
-    wsum = dadd(wsum, b.y);
-  };
-  const bool top = ty == 0, left = tx == 0, right = tx == kSTW - 1;
-  // (-1,-1): the SE pair of (ty-1, tx-1)
-  add(top ? sm + S::TOP + (2 * BW + tx) * 4
-          : (left ? sm + S::LEFT + (1 * kSTH + ty - 1) * 4 : T + (3 * kSNT + tid - kSTW - 1) * 4),
-      true);
-  // (-1, 0): the S pair of (ty-1, tx)
-  add(top ? sm + S::TOP + (1 * BW + tx + 1) * 4 : T + (2 * kSNT + tid - kSTW) * 4, true);
-  // (-1,+1): the SW pair of (ty-1, tx+1)
-#ifdef OPCFE_LAPSYM_DEBUG
-  if (right && !top) {
-    double chk[4];
-    lap_pair_f64(sm, pc - BW + 1, pc, chk);
-    const double* rr = sm + S::RIGHT + (ty - 1) * 4;
-    if (chk[0] != rr[0] || chk[1] != rr[1] || chk[2] != rr[2] || chk[3] != rr[3]) {
-      dst[o] = qnan(); dst[o + 1] = rr[3]; dst[o + 2] = chk[3];
-      return;
-    }
-  }
-#endif
-  add(top ? sm + S::TOP + (0 * BW + tx + 2) * 4
-          : (right ? sm + S::RIGHT + (ty - 1) * 4 : T + (1 * kSNT + tid - kSTW + 1) * 4),
-      true);
-  // ( 0,-1): the E pair of (ty, tx-1)
-  add(left ? sm + S::LEFT + (0 * kSTH + ty) * 4 : T + (0 * kSNT + tid - 1) * 4, true);
-  // ( 0,+1), (+1,-1), (+1,0), (+1,+1): the thread's own records
-  add(T + (0 * kSNT + tid) * 4, false);
-  add(T + (1 * kSNT + tid) * 4, false);
-  add(T + (2 * kSNT + tid) * 4, false);
-  add(T + (3 * kSNT + tid) * 4, false);
-  if (wsum > 0.0) {
-    const double s = __ddiv_rn(lam, wsum);
-    px = dadd(px, dmul(s, ax));
-    py = dadd(py, dmul(s, ay));
-    pz = dadd(pz, dmul(s, az));
-  }
-  dst[o] = px;
-  dst[o + 1] = py;
-  dst[o + 2] = pz;
-}
-
 // ------------------------------------------------------------------ bilateral
 // centroids, normals: [F][Mq][Nq][2][3].  Output: FC layout (out_fc) or, with trimap,
 // mesh order out_mesh[f][trimap[gid]] (OUT = double or float).  Shared planes (SMEM):
@@ -808,16 +644,6 @@ int lap_launch(const double* in, double* out, int F, int M, int N, int h, double
   return check_launch("laplacian_f64_kernel");
 }
 
-int lap_sym_launch(const double* in, double* out, int F, int M, int N, double lam,
-                   cudaStream_t st) {
-  constexpr int smem = LapSymS::DOUBLES * (int)sizeof(double);
-  int rc;
-  if ((rc = set_smem(laplacian_f64_sym_kernel, smem))) return rc;
-  dim3 grid((N + kSTW - 1) / kSTW, (M + kSTH - 1) / kSTH, F);
-  laplacian_f64_sym_kernel<<<grid, dim3(kSTW, kSTH), smem, st>>>(in, out, M, N, lam);
-  return check_launch("laplacian_f64_sym_kernel");
-}
-
 template <int HC, bool SMEM, typename OUT>
 int bil_launch(const Bil64Args& a, int F, cudaStream_t st) {
   dim3 grid((a.Nq + kSTW - 1) / kSTW, (a.Mq + kSTH - 1) / kSTH, F);
@@ -862,7 +688,7 @@ int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int 
   for (int it = 0; it < iters; ++it) {
     double* dst = to_out ? out : tmp;
     int rc;
-    if (h == 1) rc = lap_sym_launch(src, dst, F, M, N, lam, st);
+    if (h == 1) rc = lap_launch<1, true>(src, dst, F, M, N, h, lam, st);
     else if (h == 2) rc = lap_launch<2, true>(src, dst, F, M, N, h, lam, st);
     else if (lap_smem(h) <= kSmemMax) rc = lap_launch<0, true>(src, dst, F, M, N, h, lam, st);
     else rc = lap_launch<0, false>(src, dst, F, M, N, h, lam, st);
