@@ -177,12 +177,14 @@ __device__ __forceinline__ auto tile_origin(const S* v, int count, int stride, i
 // cost of the correctly rounded fp64 divide/sqrt used where bit-exact normals are
 // returned (gridops.cu).  Tiny triangles (|cross| below the fp32 normal range, i.e.
 // vertices closer than ~1e-19 m) are out of contract.
+// Degenerate (zero cross product), non-finite or out-of-range crosses give NaN normals: the
+// test runs on the fp32-rounded components (a NaN component makes the Newton step NaN).
 __device__ __forceinline__ void normalise_fast(double x, double y, double z, float* n) {
-  const double s = x * x + y * y + z * z;
-  if (s > 0.0 && s < 1e300) {
-    const float fx = (float)x, fy = (float)y, fz = (float)z;
+  const float fx = (float)x, fy = (float)y, fz = (float)z;
+  const float m = fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz)));
+  if (m > 0.f && m <= 3.402823466e38f) {
     // rescale into [1, 3] before squaring (tiny triangles: |x| ~ 1e-20); the scale cancels
-    const float is = rcp_approx(fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz))));
+    const float is = rcp_approx(m);
     const float gx = fx * is, gy = fy * is, gz = fz * is;
     const float l2 = gx * gx + gy * gy + gz * gz;
     float r = rsqrt_approx(l2);
@@ -237,14 +239,18 @@ __device__ __forceinline__ Planes planes_at(float* base) {
 // pack one quad: n' = n*sqrt(B); `cs` are the centroids already scaled (c' = c*sqrt(A));
 // a triangle with a NaN normal or centroid is encoded as n' = 0, c' = 1e18 (its weight
 // to / from any valid triangle underflows to exactly 0).  One NaN test per triangle: on
-// the sum of its six values (an infinite value either yields NaN or a zero weight).
+// the sum of its six values (an infinite value either yields NaN or a zero weight) -- or,
+// for normals computed here from the points (FC), on one component: such a normal is NaN
+// in all three or in none, and a NaN vertex (NaN centroid) makes it NaN.
+template <bool FC>
 __device__ __forceinline__ void pack_quad(const Planes& P, int q, const float* n,
                                           const float* cs, float sB) {
   float c2[2][3], n2[2][3];
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
-    const float t = ((n[3 * k] + n[3 * k + 1]) + (n[3 * k + 2] + cs[3 * k])) +
-                    (cs[3 * k + 1] + cs[3 * k + 2]);
+    const float t = FC ? n[3 * k]
+                       : ((n[3 * k] + n[3 * k + 1]) + (n[3 * k + 2] + cs[3 * k])) +
+                             (cs[3 * k + 1] + cs[3 * k + 2]);
     const bool ok = !isnan(t);
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
@@ -578,7 +584,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
         }
       }
     }
-    pack_quad(P, q, n, cc, sB);
+    pack_quad<MODE == kFromPoints>(P, q, n, cc, sB);
   };
   // a warp packs 32 consecutive quads of one row (no row wrap inside a warp: conflict-free
   // point loads and plane stores), then the last warps the 2H leftover columns of each row
