@@ -393,6 +393,75 @@ def dropin_e2e(fe, wl, frame, dev, frames=5):
                     "float64 (pageable) arrays, one frame per call, host wall clock"}
 
 
+PLUGIN_CHILD = r"""
+import json, sys, time
+import numpy as np
+from flatpoly import _kernels, mesh, smoothing
+assert _kernels.ACTIVE == "cuda", _kernels.ACTIVE
+opc = np.load(sys.argv[1])
+cfg = json.loads(sys.argv[2])
+lp = smoothing.LaplacianParams(*cfg["lap"]) if cfg["lap"] else None
+bp = smoothing.BilateralParams(*cfg["bil"]) if cfg["bil"] else None
+def one():
+    sm = smoothing.laplacian_filter_opc(opc, lp) if lp else opc
+    m = mesh.mesh_from_opc(sm)
+    if bp:
+        m.normals = smoothing.bilateral_filter_opc(sm, bp, m.trimap)
+    return sm, m
+sm, m = one()
+sm, m = one()
+n = cfg["frames"]
+t = time.perf_counter()
+for _ in range(n):
+    sm, m = one()
+dt = (time.perf_counter() - t) / n
+print(json.dumps({"dt": dt, "T": int(m.num_triangles), "sm": int(sm.nbytes),
+                  "tm": int(m.trimap.nbytes)}))
+"""
+
+
+def plugin_e2e(wl, frame, frames=5):
+    """pipeline.py:125-134 run by the STOCK reference package with libopcfe plugged into
+    its own kernel switch (integration/: FLATPOLY_CUDA=1 -- the maintainer's binding over
+    the C ABI, strict precision), NumPy f64 in and out, one frame per call, host wall
+    clock.  Needs the reference install in baseline/_ref."""
+    import subprocess
+    import tempfile
+    import numpy as np
+    ref = os.path.join(REPO, "baseline", "_ref", "flatpoly")
+    if not os.path.isdir(ref):
+        return {"unavailable": "baseline/_ref missing (baseline/install_ref.sh)"}
+    with tempfile.TemporaryDirectory(prefix="flatpoly_cuda_") as dest:
+        subprocess.run([sys.executable, os.path.join(REPO, "integration", "install.py"), dest],
+                       check=True, stdout=subprocess.DEVNULL)
+        fpath = os.path.join(dest, "frame.npy")
+        np.save(fpath, np.ascontiguousarray(frame, dtype=np.float64))
+        cfg = {"lap": list(wl.lap) if wl.lap else None, "bil": list(wl.bil) if wl.bil else None,
+               "frames": frames}
+        env = dict(os.environ, FLATPOLY_CUDA="1",
+                   OPCFE_LIB=os.path.join(REPO, "paper_2007_12065_b200", "lib", "libopcfe.so"),
+                   PYTHONPATH=os.pathsep.join([dest, os.path.join(REPO, "tests", "golden",
+                                                                  "_stubs")]))
+        r = subprocess.run([sys.executable, "-c", PLUGIN_CHILD, fpath, json.dumps(cfg)], env=env,
+                           cwd=dest, capture_output=True, text=True, timeout=600)
+    if r.returncode != 0:
+        return {"unavailable": "plugin run failed: " + r.stderr.strip().splitlines()[-1][:200]}
+    o = json.loads(r.stdout.strip().splitlines()[-1])
+    T, fb = o["T"], frame.size * 8
+    # uploads: the cloud to the Laplacian, the smoothed cloud to mesh_from_opc and (+ the
+    # trimap) to bilateral_filter_opc; downloads: the smoothed cloud, triangles, trimap,
+    # twins and normals of the mesh, the filtered normals
+    h2d = (fb if wl.lap else 0) + fb + ((fb + o["tm"]) if wl.bil else 0)
+    d2h = (o["sm"] if wl.lap else 0) + 3 * 24 * T + o["tm"] + (24 * T if wl.bil else 0)
+    return {"value": 1.0 / o["dt"], "unit": "frames/s", "frames": frames,
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "path": "the stock reference package (baseline/_ref) with the shipped binding "
+                    "(integration/_opcfe.py + flatpoly_cuda.patch, FLATPOLY_CUDA=1): its own "
+                    "laplacian_filter_opc -> mesh_from_opc -> bilateral_filter_opc calling "
+                    "libopcfe through ctypes, strict precision, NumPy float64 in and out, one "
+                    "frame per call, host wall clock"}
+
+
 def gpu_index(local_rank, args):
     """The rank's CUDA device: LOCAL_RANK, or LOCAL_RANK % device_count under --share-gpus."""
     import torch
@@ -581,6 +650,8 @@ def run_ours(args, rank, world, local_rank, wl):
         # in and out, one frame per call (default precision: strict for float64 input)
         if not args.no_e2e_dropin:
             e2e["dropin"] = dropin_e2e(fe, wl, host[0].numpy(), dev)
+            if world == 1:
+                e2e["plugin"] = plugin_e2e(wl, host[0].numpy())
 
     if rank != 0:
         return 0

@@ -4,5 +4,5 @@ cd $GRAFT_REPO_ROOT
 python - <<'PY'
 import json
 d = json.load(open("gpurun_out/b1.json"))
-print(round(d["value"],1), "e2e", round(d["e2e"]["value"],1), {k: round(v["value"],1) for k, v in d["e2e"].items() if isinstance(v, dict) and "value" in v}, "strict", round(d["strict"]["value"],1), d["roofline"]["frac"], d["clocks"], d["stage_ms_per_step"])
+print(round(d["value"],1), "e2e", round(d["e2e"]["value"],1), {k: (round(v["value"],1) if "value" in v else v) for k, v in d["e2e"].items() if isinstance(v, dict)}, "strict", round(d["strict"]["value"],1), d["roofline"]["frac"], d["clocks"], d["stage_ms_per_step"])
 PY

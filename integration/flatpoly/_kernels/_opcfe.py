@@ -21,6 +21,14 @@ plus the mesh / FC functions the patch routes here from mesh.py and smoothing.py
     extract_halfedges_opc   (mesh.py:99-135)      -> opcfe_halfedges_from_trimap
     triangle_normals        (geometry.py:134-147) -> opcfe_triangle_normals (bit-exact)
     compute_fc_triangle_data (smoothing.py:61-88) -> opcfe_fc_data (bit-exact)
+    mesh_opc                (mesh.py:165-178)     -> one upload: triangles, trimap, twins and
+                                                     normals of mesh_from_opc
+    bilateral_filter_opc    (smoothing.py:91-114) -> FC data + filter + trimap gather on the
+                                                     device (opcfe_bilateral_f64 scatter form)
+
+Large results come back in pinned host blocks (a pool recycled as arrays are dropped):
+a D2H into a fresh pageable NumPy array runs at ~2 GB/s, into pinned memory at the link
+rate.  Device buffers come from a size-bucketed pool (no cudaFree per call).
 
 Precision: the reference computes in float64, and so does this backend (the strict
 kernels); ``FLATPOLY_CUDA=fast`` selects the fp32 Laplacian / bilateral kernels instead
@@ -31,6 +39,8 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
+import weakref
 
 import numpy as np
 
@@ -53,6 +63,8 @@ def _load_cudart():
 _rt = _load_cudart()
 _rt.cudaMalloc.argtypes = [ctypes.POINTER(_vp), _sz]
 _rt.cudaFree.argtypes = [_vp]
+_rt.cudaHostAlloc.argtypes = [ctypes.POINTER(_vp), _sz, ctypes.c_uint]
+_rt.cudaFreeHost.argtypes = [_vp]
 _rt.cudaMemcpy.argtypes = [_vp, _vp, _sz, _i]
 _rt.cudaMemset.argtypes = [_vp, _i, _sz]
 _rt.cudaDeviceSynchronize.argtypes = []
@@ -99,15 +111,73 @@ def _check(rc, what):
         raise RuntimeError(f"libopcfe error {rc}: {msg}")
 
 
+class _Pool:
+    """Size-bucketed (powers of two) cache of CUDA allocations: device buffers, or pinned
+    host blocks.  Every call here ends with a synchronous copy on the legacy stream, so a
+    released buffer is idle; cudaFree would synchronise the device on every call."""
+
+    def __init__(self, name, alloc, free, cache_cap):
+        self.name, self._alloc, self._free, self.cap = name, alloc, free, cache_cap
+        self.free, self.cached, self.in_use = {}, 0, 0
+        self.lock = threading.Lock()
+
+    def get(self, nbytes):
+        blk = 1 << max(int(nbytes) - 1, 15).bit_length()
+        with self.lock:
+            lst = self.free.get(blk)
+            if lst:
+                self.cached -= blk
+                self.in_use += blk
+                return lst.pop(), blk
+        ptr = _vp()
+        e = self._alloc(ctypes.byref(ptr), blk)
+        if e != 0:
+            raise MemoryError(f"{self.name}({blk}): {_rt.cudaGetErrorString(e).decode()}")
+        with self.lock:
+            self.in_use += blk
+        return ptr, blk
+
+    def put(self, ptr, blk):
+        with self.lock:
+            self.in_use -= blk
+            if self.cached + blk <= self.cap:
+                self.free.setdefault(blk, []).append(ptr)
+                self.cached += blk
+                return
+        self._free(ptr)
+
+
+_DEV = _Pool("cudaMalloc", _rt.cudaMalloc, _rt.cudaFree, 8 << 30)
+_HOST = _Pool("cudaHostAlloc", lambda p, n: _rt.cudaHostAlloc(p, n, 0), _rt.cudaFreeHost, 4 << 30)
+_PIN_MIN, _PIN_CAP = 4 << 20, int(os.environ.get("OPCFE_PINNED_OUT_MB", "4096")) << 20
+
+
+def _host_empty(shape, dtype=np.float64):
+    """A new host array for a large result: a view of a PINNED block (the D2H runs at the
+    link rate instead of ~2 GB/s into fresh pageable memory), recycled once the array is
+    garbage; plain np.empty below 4 MB or past OPCFE_PINNED_OUT_MB of results alive."""
+    dtype = np.dtype(dtype)
+    n = int(np.prod(shape))
+    nbytes = n * dtype.itemsize
+    if nbytes < _PIN_MIN or _HOST.in_use + 2 * nbytes > _PIN_CAP:
+        return np.empty(shape, dtype)
+    try:
+        ptr, blk = _HOST.get(nbytes)
+    except MemoryError:
+        return np.empty(shape, dtype)
+    raw = (ctypes.c_char * blk).from_address(ptr.value)
+    arr = np.frombuffer(raw, dtype=dtype, count=n).reshape(shape)
+    fin = weakref.finalize(raw, _HOST.put, ptr, blk)     # the array's base is `raw`
+    fin.atexit = False
+    return arr
+
+
 class _Dev:
-    """One device allocation (freed with the object)."""
+    """One device allocation (returned to the pool with the object)."""
 
     def __init__(self, nbytes):
         self.nbytes = max(int(nbytes), 16)
-        self.ptr = _vp()
-        e = _rt.cudaMalloc(ctypes.byref(self.ptr), self.nbytes)
-        if e != 0:
-            raise MemoryError(f"cudaMalloc({self.nbytes}): {_rt.cudaGetErrorString(e).decode()}")
+        self.ptr, self.blk = _DEV.get(self.nbytes)
 
     @classmethod
     def of(cls, arr):
@@ -124,7 +194,10 @@ class _Dev:
 
     def __del__(self):
         if getattr(self, "ptr", None) is not None and self.ptr.value:
-            _rt.cudaFree(self.ptr)
+            try:
+                _DEV.put(self.ptr, self.blk)
+            except Exception:           # interpreter shutdown
+                pass
 
 
 def _sync_check(e):
@@ -143,7 +216,7 @@ def laplacian_filter(points, lam, kernel_size, iterations):
     if src.ndim != 3 or src.shape[2] != 3:
         raise ValueError("points must be an (M, N, 3) array")
     M, N = src.shape[:2]
-    out = np.empty_like(src)
+    out = _host_empty(src.shape)
     if src.size == 0:
         return out
     d_in = _Dev.of(src)
@@ -170,7 +243,7 @@ def bilateral_iterate(centroids, normals, sigma_length, sigma_angle, kernel_size
     """_native.pyx:287-364 / _fallback.py:120-166."""
     c, n = _f64(centroids), _f64(normals)
     Mq, Nq = n.shape[:2]
-    out = np.empty_like(n)
+    out = _host_empty(n.shape)
     if n.size == 0:
         return out
     d_c, d_n, d_out = _Dev.of(c), _Dev.of(n), _Dev(n.nbytes)
@@ -257,16 +330,16 @@ def extract_triangles_opc(opc):
                                  None, -1.0, None, d_ws.ptr, ws_bytes, None),
            "extract_triangles_opc")
     T = int(d_nt.get(np.empty(1, dtype=np.int64))[0])
-    return d_tri.get(np.empty((T, 3), dtype=np.int64)), d_tm.get(np.empty(G, dtype=np.int64))
+    return d_tri.get(_host_empty((T, 3), np.int64)), d_tm.get(_host_empty(G, np.int64))
 
 
 def extract_halfedges_opc(trimap, M, N):
     """mesh.py:99-135 (the caller has validated the trimap's shape)."""
     tm = np.ascontiguousarray(trimap, dtype=np.int64).reshape(-1)
     n_tri = int(tm.max()) + 1 if tm.size else 0
-    he = np.full(3 * max(n_tri, 0), -1, dtype=np.int64)
     if n_tri <= 0:
-        return he
+        return np.full(0, -1, dtype=np.int64)
+    he = _host_empty(3 * n_tri, np.int64)               # every entry written below
     d_tm, d_he = _Dev.of(tm), _Dev(he.nbytes)
     _sync_check(_rt.cudaMemset(d_he.ptr, 0xFF, he.nbytes))          # -1 in every int64
     _check(_op.opcfe_halfedges_from_trimap(d_tm.ptr, int(M), int(N), n_tri, d_he.ptr, None),
@@ -278,7 +351,7 @@ def triangle_normals(points, triangles):
     """geometry.py:134-147: unit normals, NaN for degenerate triangles (bit-exact)."""
     p = _f64(points).reshape(-1, 3)
     t = np.ascontiguousarray(triangles, dtype=np.int64).reshape(-1, 3)
-    out = np.empty((len(t), 3))
+    out = _host_empty((len(t), 3))
     if len(t) == 0:
         return out
     d_p, d_t, d_o = _Dev.of(p), _Dev.of(t), _Dev(out.nbytes)
@@ -287,12 +360,72 @@ def triangle_normals(points, triangles):
     return d_o.get(out)
 
 
+def mesh_opc(opc):
+    """mesh.py:165-178 in one upload (the caller has validated the shape): (triangles,
+    trimap, halfedges, normals) -- extract_triangles_opc, extract_halfedges_opc and
+    compute_normals of the reference, bit-identical."""
+    src = _f64(opc)
+    M, N = src.shape[:2]
+    G = 2 * (M - 1) * (N - 1)
+    d_src = _Dev.of(src)
+    d_vm = _Dev(4 * _op.opcfe_vmask_words(1, M, N))
+    _check(_op.opcfe_stage_in(d_src.ptr, 1, 3 * N, 3 * M * N, 1, M, N, None, 0, d_vm.ptr, None),
+           "mesh_from_opc")
+    d_tm, d_tri, d_he, d_nt = _Dev(8 * G), _Dev(24 * G), _Dev(24 * G), _Dev(8)
+    ws_bytes = int(_op.opcfe_triangulate_workspace(1, M, N))
+    d_ws = _Dev(ws_bytes)
+    _check(_op.opcfe_triangulate(d_vm.ptr, 1, M, N, d_tm.ptr, d_tri.ptr, d_he.ptr, d_nt.ptr, None,
+                                 0, None, -1.0, None, d_ws.ptr, ws_bytes, None), "mesh_from_opc")
+    T = int(d_nt.get(np.empty(1, dtype=np.int64))[0])
+    d_nrm = _Dev(24 * max(T, 1))
+    if T:
+        _check(_op.opcfe_triangle_normals(d_src.ptr, 1, d_tri.ptr, T, d_nrm.ptr, None),
+               "mesh_from_opc")
+    return (d_tri.get(_host_empty((T, 3), np.int64)), d_tm.get(_host_empty(G, np.int64)),
+            d_he.get(_host_empty(3 * T, np.int64)), d_nrm.get(_host_empty((T, 3))))
+
+
+def bilateral_filter_opc(opc, sigma_length, sigma_angle, kernel_size, iterations, trimap=None):
+    """smoothing.py:91-114 (the caller has validated the shape and parameters): FC data,
+    the bilateral iterations and the trimap gather on the device -- the fp64 kernels
+    (strict); FLATPOLY_CUDA=fast keeps the reference's host gather over bilateral_iterate."""
+    src = _f64(opc)
+    M, N = src.shape[:2]
+    if trimap is None:
+        _, trimap = extract_triangles_opc(src)
+    tm = np.ascontiguousarray(trimap, dtype=np.int64).reshape(-1)
+    if FAST:
+        cen, nrm = compute_fc_triangle_data(src)
+        flat = bilateral_iterate(cen, nrm, sigma_length, sigma_angle, kernel_size,
+                                 iterations).reshape(-1, 3)
+        valid = tm >= 0
+        out = np.empty((int(valid.sum()), 3))
+        out[tm[valid]] = flat[valid]
+        return out
+    T = int(np.count_nonzero(tm >= 0))
+    out = _host_empty((T, 3))
+    if T == 0:
+        return out
+    Mq, Nq = M - 1, N - 1
+    fc = Mq * Nq * 6 * 8
+    d_src, d_tm = _Dev.of(src), _Dev.of(tm)
+    d_c, d_n, d_out = _Dev(fc), _Dev(fc), _Dev(out.nbytes)
+    _check(_op.opcfe_fc_data(d_src.ptr, 1, M, N, d_c.ptr, d_n.ptr, None), "bilateral_filter_opc")
+    bufs = [_Dev(fc) if iterations > j else None for j in (1, 2)]
+    _check(_op.opcfe_bilateral_f64(d_c.ptr, d_n.ptr, 1, M, N, float(sigma_length),
+                                   float(sigma_angle), int(kernel_size), int(iterations),
+                                   bufs[0].ptr if bufs[0] else None,
+                                   bufs[1].ptr if bufs[1] else None, None, d_tm.ptr, d_out.ptr,
+                                   T, None), "bilateral_filter_opc")
+    return d_out.get(out)
+
+
 def compute_fc_triangle_data(opc):
     """smoothing.py:61-88 (the caller has validated the shape): (centroids, normals)."""
     src = _f64(opc)
     M, N = src.shape[:2]
-    cen = np.empty((M - 1, N - 1, 2, 3))
-    nrm = np.empty_like(cen)
+    cen = _host_empty((M - 1, N - 1, 2, 3))
+    nrm = _host_empty((M - 1, N - 1, 2, 3))
     d_src, d_c, d_n = _Dev.of(src), _Dev(cen.nbytes), _Dev(nrm.nbytes)
     _check(_op.opcfe_fc_data(d_src.ptr, 1, M, N, d_c.ptr, d_n.ptr, None),
            "compute_fc_triangle_data")
