@@ -82,3 +82,44 @@ def test_reference_suite_through_libopcfe(installed):
     print(tail)
     assert r.returncode == 0, tail + r.stderr[-2000:]
     assert " passed" in tail and "failed" not in tail
+
+
+CHAIN = r"""
+import sys
+import numpy as np
+from flatpoly import _kernels, mesh, smoothing
+from flatpoly.synthetic import room_scene
+rng = np.random.default_rng(7)
+opc = room_scene(n=96, noise=0.002, seed=3).opc
+opc[rng.random(opc.shape[:2]) < 0.05] = np.nan
+sm = smoothing.laplacian_filter_opc(opc, smoothing.LaplacianParams(0.8, 3, 4))
+m = mesh.mesh_from_opc(sm)
+n = smoothing.bilateral_filter_opc(sm, smoothing.BilateralParams(0.1, 0.2, 5, 3), m.trimap)
+n2 = smoothing.bilateral_filter_opc(sm, smoothing.BilateralParams(0.1, 0.2, 3, 2))
+np.savez(sys.argv[1], active=_kernels.ACTIVE, sm=sm, tri=m.triangles, he=m.halfedges,
+         tm=m.trimap, mn=m.normals, n=n, n2=n2)
+"""
+
+
+def test_fused_binding_chain_equals_stock_native(installed, tmp_path):
+    """The patch's fused mesh_from_opc / bilateral_filter_opc (one upload; gather on the
+    device) against the same stock code on the reference's compiled CPU backend."""
+    import numpy as np
+    out = {}
+    for mode in ("cuda", "native"):
+        env = _env(installed)
+        if mode == "native":
+            env.pop("FLATPOLY_CUDA")
+        path = str(tmp_path / f"{mode}.npz")
+        r = subprocess.run([sys.executable, "-c", CHAIN, path], cwd=installed, env=env,
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[mode] = np.load(path)
+        assert str(out[mode]["active"]) == mode
+    g, r = out["cuda"], out["native"]
+    for k in ("sm", "tri", "he", "tm", "mn"):
+        assert g[k].shape == r[k].shape and np.array_equal(g[k], r[k], equal_nan=(k in ("sm", "mn"))), k
+    for k in ("n", "n2"):
+        bad = np.isnan(r[k]).any(1)
+        assert np.array_equal(np.isnan(g[k]).any(1), bad), k
+        assert np.abs(g[k][~bad] - r[k][~bad]).max() <= 1e-12, k
