@@ -135,3 +135,37 @@ def test_error_types_match_stock_reference(fe, ref):
         assert isinstance(g_exc.value, ValueError) == isinstance(r_exc.value, ValueError)
         assert type(g_exc.value).__name__ == type(r_exc.value).__name__, \
             (type(g_exc.value), type(r_exc.value))
+
+
+@pytest.mark.parametrize("case", ["lidar_k3", "lidar_k5_13", "room_k11", "lidar_big"])
+def test_structured_scenes_equal_stock_reference(fe, ref, case):
+    """Range images (the C3 scanner: NaN rows / sky, 80 m ranges) and a room at large
+    kernel sizes through the drop-in chain and the stock reference, incl. l_max group
+    labels -- same bars as the random clouds."""
+    if case.startswith("lidar"):
+        rows, cols = (64, 1024) if case == "lidar_big" else (32, 256)
+        opc = fe.synthetic.lidar_scan(rows=rows, cols=cols, seed=11)
+        lap = {"lidar_k3": (1.0, 3, 5), "lidar_k5_13": (0.6, 5, 3), "lidar_big": (1.0, 3, 5)}[case]
+        bil = {"lidar_k3": (0.3, 0.2, 3, 3), "lidar_k5_13": (0.3, 0.2, 13, 2),
+               "lidar_big": (0.3, 0.2, 3, 5)}[case]
+        l_max = 0.5
+    else:
+        opc = fe.synthetic.room_scene(n=120, noise=0.002, seed=9)
+        lap, bil, l_max = (0.9, 11, 2), (0.1, 0.15, 11, 2), 0.05
+    dn = np.array([[0, 0, 1.0], [1.0, 0, 0], [0, 1.0, 0], [-1.0, 0, 0], [0, -1.0, 0]])
+
+    r_sm = ref.smoothing.laplacian_filter_opc(opc, ref.smoothing.LaplacianParams(*lap))
+    g_sm = fe.laplacian_filter_opc(opc, fe.LaplacianParams(*lap))
+    assert same(g_sm, r_sm)
+    r_mesh, g_mesh = ref.mesh.mesh_from_opc(r_sm), fe.mesh_from_opc(g_sm)
+    for name in ("triangles", "halfedges", "trimap", "normals"):
+        assert same(getattr(g_mesh, name), getattr(r_mesh, name)), name
+    r_n = ref.smoothing.bilateral_filter_opc(r_sm, ref.smoothing.BilateralParams(*bil),
+                                             r_mesh.trimap)
+    g_n = fe.bilateral_filter_opc(g_sm, fe.BilateralParams(*bil), g_mesh.trimap)
+    bad = np.isnan(r_n).any(1)
+    assert np.array_equal(np.isnan(g_n).any(1), bad)
+    assert np.linalg.norm(g_n[~bad] - r_n[~bad], axis=1).max() <= 1e-12
+    r_mesh.normals, g_mesh.normals = r_n, g_n
+    assert same(fe.group_assignment(g_mesh, dn, l_max, 0.9),
+                ref.segmentation.group_assignment(r_mesh, dn, l_max, 0.9))
