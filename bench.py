@@ -226,7 +226,7 @@ def run_reference(args, rank, world, wl):
 
 def chained_parity(sample, wl, dev):
     """GPU chain vs the reference's OWN chain on the same whole frame (worker 0's output of
-    the cpu_baseline leg): fast (fp32) and strict (fp64) precision."""
+    the cpu_baseline leg): fast (fp32), mixed and strict (fp64) precision."""
     import numpy as np
     import torch
 
@@ -236,7 +236,7 @@ def chained_parity(sample, wl, dev):
     ref_sm, ref_n, ref_tm = sample["smoothed"], sample["normals"], sample["trimap"]
     ok = np.isfinite(ref_sm).all(2)
     out = {"frame": f"{wl.name} base frame {M}x{N} (the cpu_baseline leg's worker 0)"}
-    for prec in ("fast", "strict"):
+    for prec in ("fast", "mixed", "strict"):
         eng = fe.FrontEnd(M, N, 1, laplacian=fe.LaplacianParams(*wl.lap) if wl.lap else None,
                           bilateral=fe.BilateralParams(*wl.bil) if wl.bil else None,
                           l_max=wl.l_max, src_dtype=torch.float64, device=dev, graph=False,
@@ -317,14 +317,24 @@ def load_traffic():
     return {}
 
 
-def strict_throughput(fe, wl, eng_fast, args, dev):
-    """Device-resident frames/s of the STRICT chain (the reference's fp64 arithmetic) on
-    the same frames as the fast line (eng_fast.src), CUDA events on the launching stream."""
+PRECISION_WHAT = {
+    "strict": "precision='strict': the reference's fp64 chain (bit-exact Laplacian, FC data "
+              "and topology; bilateral normals within a few ulp per iteration), float64 outputs",
+    "mixed": "precision='mixed': the strict Laplacian, topology and FC data (bit-exact), then "
+             "the fp32 bilateral on the exact FC arrays -- normals within 1e-5 of the "
+             "reference's chain end to end (parity.chained.mixed), float64 outputs",
+}
+
+
+def precision_throughput(fe, wl, eng_fast, args, dev, precision="strict"):
+    """Device-resident frames/s of the STRICT (the reference's fp64 arithmetic) or MIXED
+    chain on the same frames as the fast line (eng_fast.src), CUDA events on the launching
+    stream."""
     import torch
     F = eng_fast.F
     eng = fe.FrontEnd(wl.M, wl.N, F, laplacian=fe.LaplacianParams(*wl.lap) if wl.lap else None,
                       bilateral=fe.BilateralParams(*wl.bil) if wl.bil else None, l_max=wl.l_max,
-                      src_dtype=eng_fast.src.dtype, device=dev, graph=False, precision="strict")
+                      src_dtype=eng_fast.src.dtype, device=dev, graph=False, precision=precision)
     eng.src.copy_(eng_fast.src)
     stream = torch.cuda.current_stream(dev)
     for _ in range(2):
@@ -348,9 +358,7 @@ def strict_throughput(fe, wl, eng_fast, args, dev):
     out = {"value": F / (ms / 1e3), "unit": "frames/s", "ms_per_step": ms, "frames_per_step": F,
            "steps": steps, "dtype": "f64", "gpu_launches_per_step": eng.kernel_launches,
            "stage_ms_per_step": {k: round(v, 4) for k, v in stage.items()},
-           "what": "precision='strict': the reference's fp64 chain (bit-exact Laplacian, FC "
-                   "data and topology; bilateral normals within a few ulp per iteration), "
-                   "float64 outputs"}
+           "what": PRECISION_WHAT[precision]}
     del eng
     torch.cuda.empty_cache()
     return out
@@ -624,10 +632,11 @@ def run_ours(args, rank, world, local_rank, wl):
         # (NON-reference) output modes: int32 indices narrowed on the device, optionally
         # only a subset of the outputs
         for key, outs, kw in (("strict", fe.HostPipeline.DROPIN, dict(precision="strict")),
+                              ("mixed", fe.HostPipeline.DROPIN, dict(precision="mixed")),
                               ("compact", fe.HostPipeline.DROPIN, dict(index_dtype=torch.int32)),
                               ("selected", ("points", "triangles", "normals"),
                                dict(index_dtype=torch.int32))):
-            if key == "strict" and args.no_strict:
+            if key in ("strict", "mixed") and args.no_strict:
                 continue
             p2 = fe.HostPipeline(M, N, laplacian=lap_p, bilateral=bil_p, l_max=wl.l_max,
                                  src_dtype=torch.float64, device=dev, outputs=outs, **kw)
@@ -695,9 +704,10 @@ def run_ours(args, rank, world, local_rank, wl):
                    "ops_per_launch": fp32_ops, "peak_source": fp32_src,
                    "note": f"{pairs_per_quad} directed pairs per quad x 15 FP32 lane-ops "
                            "(6 differences, 6 squared-distance, 3 accumulate) + 1 MUFU ex2"}
-    strict = None
+    strict = mixed = None
     if not args.no_strict:
-        strict = strict_throughput(fe, wl, eng, args, dev)
+        strict = precision_throughput(fe, wl, eng, args, dev, "strict")
+        mixed = precision_throughput(fe, wl, eng, args, dev, "mixed")
     cpu = parity = None
     if world == 1 and not args.no_cpu_baseline:
         cb, sample = cpu_reference(steps=1, warmup=0, budget_s=25.0, wl=wl, want_sample=True)
@@ -726,7 +736,7 @@ def run_ours(args, rank, world, local_rank, wl):
                       "timed step runs the same launches on one stream (opcfe_front_end)",
         "frame_hbm_frac": round(ab["frame_total"] * F / (max_ms / args.steps / 1e3) / 1e9 / peak, 4),
         "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
-        "parity": parity, "strict": strict, "distributed": dist_info,
+        "parity": parity, "strict": strict, "mixed": mixed, "distributed": dist_info,
         "clocks": clk.summary(), "n_tri_per_frame": T,
     }
     print(json.dumps(line), flush=True)

@@ -222,7 +222,10 @@ typedef struct {
   double ang_min;
   /* OPCFE_PRECISION_FAST: fp32 kernels (+ the fp64 steps the 1e-5 contract needs);
    * OPCFE_PRECISION_STRICT: the reference's fp64 chain (points / normals outputs are
-   * double: bit-exact Laplacian, FC data, topology; bilateral to <= a few ulp).
+   * double: bit-exact Laplacian, FC data, topology; bilateral to <= a few ulp);
+   * OPCFE_PRECISION_MIXED: the strict Laplacian, topology and FC data (bit-exact, double
+   * points), then the fp32 bilateral on the exact FC arrays (normals double, within 1e-5
+   * of the reference's chain end to end -- the fast chain's drift is fp32 vertex storage).
    * Fast-precision stages whose kernel size exceeds the fp32 kernels (Laplacian > 17,
    * bilateral > 9) run on the fp64 generic-window kernels, results rounded to fp32. */
   int precision;
@@ -230,6 +233,7 @@ typedef struct {
 
 #define OPCFE_PRECISION_FAST 0
 #define OPCFE_PRECISION_STRICT 1
+#define OPCFE_PRECISION_MIXED 2
 
 typedef struct {
   /* input: src_kind 0 = padded fp32 grid (src_pitch floats/row, frame stride M*src_pitch),

@@ -36,6 +36,7 @@ EXPORTS = (
 
 PRECISION_FAST = 0      # OPCFE_PRECISION_FAST
 PRECISION_STRICT = 1    # OPCFE_PRECISION_STRICT
+PRECISION_MIXED = 2     # OPCFE_PRECISION_MIXED
 
 
 class FrontEndParams(ctypes.Structure):

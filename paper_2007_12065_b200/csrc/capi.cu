@@ -78,9 +78,11 @@ struct FeLayout {
   size_t vmask = 0, status = 0, staged = 0, lap_tmp = 0, bil_a = 0, bil_b = 0, bil_c = 0,
          total = 0;
   size_t vmask_b = 0, status_b = 0, staged_b = 0, lap_b = 0, bil_b_bytes = 0;
-  // fp64 stages (strict precision, or kernel sizes beyond the fp32 kernels)
-  bool strict = false, lap64 = false, bil64 = false;
+  // fp64 stages (strict precision, or kernel sizes beyond the fp32 kernels); mixed: the
+  // strict stages up to the FC data, then the fp32 bilateral on the FC arrays
+  bool strict = false, mixed = false, lap64 = false, bil64 = false, bil_mixed = false;
   size_t g64_in = 0, g64_tmp = 0, g64_out = 0, fc_c = 0, fc_n = 0, fc_a = 0, fc_b = 0;
+  size_t fc32 = 0, nrm32 = 0;
 };
 
 FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src_kind,
@@ -94,8 +96,11 @@ FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src
   const bool lap = p->laplacian_iterations > 0;
   const bool bil = p->bilateral_iterations > 0;
   L.strict = p->precision == OPCFE_PRECISION_STRICT;
-  L.lap64 = lap && (L.strict || p->laplacian_kernel_size > kLapMaxK32);
+  L.mixed = p->precision == OPCFE_PRECISION_MIXED;
+  const bool f64_grid = L.strict || L.mixed;  // the smoothed grid (points output) is double
+  L.lap64 = lap && (f64_grid || p->laplacian_kernel_size > kLapMaxK32);
   L.bil64 = bil && (L.strict || p->bilateral_kernel_size > kBilMaxK32);
+  L.bil_mixed = bil && L.mixed && !L.bil64;
   L.vmask_b = (size_t)F * M * ((N + 31) / 32) * sizeof(uint32_t);
   L.status_b = triangulate_workspace_bytes(F, M);
   const bool need_stage = lap && !L.lap64 && !(src_kind == 0 && src_pitch == pitch);
@@ -103,6 +108,7 @@ FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src
   L.lap_b = (lap && !L.lap64 && p->laplacian_iterations > 1) ? grid_bytes : 0;
   L.bil_b_bytes = fc_bytes;
   const bool bil32 = bil && !L.bil64;
+  const bool packed_bil = bil32 && !L.bil_mixed;  // the fused pipeline's packed windows
   size_t off = 0;
   auto take = [&](size_t& at, size_t bytes) {
     at = off;
@@ -115,16 +121,18 @@ FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src
   take(L.bil_a, (bil32 && p->bilateral_iterations > 1) ? fc_bytes : 0);
   take(L.bil_b, (bil32 && p->bilateral_iterations > 2) ? fc_bytes : 0);
   // packed centroid planes + tile origins of the fused bilateral (>= 2 it.)
-  take(L.bil_c, (bil32 && p->bilateral_iterations > 1)
+  take(L.bil_c, (packed_bil && p->bilateral_iterations > 1)
                     ? bilateral_buf_c_bytes(F, M, N, p->bilateral_kernel_size)
                     : 0);
   // fp64 grids: the source as f64 (unless it is f64 already), the Laplacian ping-pong,
   // and (fast precision) the f64 smoothed grid the fp64 stages read
-  take(L.g64_in, ((L.strict || L.lap64) && src_kind != 2) ? g64 : 0);
+  take(L.g64_in, ((f64_grid || L.lap64) && src_kind != 2) ? g64 : 0);
   take(L.g64_tmp, (L.lap64 && p->laplacian_iterations > 1) ? g64 : 0);
-  take(L.g64_out, (!L.strict && (L.lap64 || L.bil64)) ? g64 : 0);
-  take(L.fc_c, L.bil64 ? fc64 : 0);
-  take(L.fc_n, L.bil64 ? fc64 : 0);
+  take(L.g64_out, (!f64_grid && (L.lap64 || L.bil64)) ? g64 : 0);
+  take(L.fc_c, (L.bil64 || L.bil_mixed) ? fc64 : 0);
+  take(L.fc_n, (L.bil64 || L.bil_mixed) ? fc64 : 0);
+  take(L.fc32, L.bil_mixed ? fc_bytes : 0);
+  take(L.nrm32, L.bil_mixed ? (size_t)F * 3 * 2 * (M - 1) * (N - 1) * sizeof(float) : 0);
   take(L.fc_a, (L.bil64 && p->bilateral_iterations > 1) ? fc64 : 0);
   take(L.fc_b, (L.bil64 && p->bilateral_iterations > 2) ? fc64 : 0);
   L.total = off + 256;
@@ -307,7 +315,8 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   if (io->src_kind == 0 && (io->src_pitch < 3 * N || io->src_pitch % 4))
     return fail(ERR_INVALID, "front_end: src_pitch must be >= 3N and a multiple of 4");
   if (io->lmax_flag && p->l_max < 0) return fail(ERR_INVALID, "front_end: lmax_flag needs l_max");
-  if (p->precision != OPCFE_PRECISION_FAST && p->precision != OPCFE_PRECISION_STRICT)
+  if (p->precision != OPCFE_PRECISION_FAST && p->precision != OPCFE_PRECISION_STRICT &&
+      p->precision != OPCFE_PRECISION_MIXED)
     return fail(ERR_INVALID, "front_end: bad precision");
   const int pitch = points_pitch(N);
   const FeLayout L = fe_layout(F, M, N, p, io->src_kind, io->src_pitch);
@@ -331,9 +340,10 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   const bool lap = p->laplacian_iterations > 0;
   int rc;
   mark(ev, 0, st);
+  const bool f64_grid = L.strict || L.mixed;  // points output (and the stages on it) double
   // the source as contiguous f64 (fp64 Laplacian input / strict points)
   const double* src64 = f64 ? static_cast<const double*>(io->src) : nullptr;
-  if (!f64 && (L.strict || L.lap64)) {
+  if (!f64 && (f64_grid || L.lap64)) {
     if ((rc = unstage(static_cast<const float*>(io->src), (int)rs, F, M, N, g64_in, true, nullptr,
                       st)))
       return rc;
@@ -341,8 +351,8 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   }
   // 1. Laplacian (smoothing.laplacian_filter_opc, pipeline.py:127-129)
   // points64: the smoothed grid as f64 for the fp64 stages (strict: the output itself)
-  double* points64 = L.strict ? static_cast<double*>(io->points) : nullptr;
-  if (L.strict) {
+  double* points64 = f64_grid ? static_cast<double*>(io->points) : nullptr;
+  if (f64_grid) {
     mark(ev, 1, st);
     if (lap) {
       if ((rc = laplacian_f64(src64, points64, g64_tmp, F, M, N, p->laplacian_lambda,
@@ -390,13 +400,13 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   mark(ev, 2, st);
   // 2. mesh_from_opc (pipeline.py:130-131): triangles + trimap + twins [+ normals, flags]
   const bool bil = p->bilateral_iterations > 0 && io->normals != nullptr;
-  const bool extras32 = !L.strict;  // fp32 grid: normals / flags fused with the triangulation
+  const bool extras32 = !f64_grid;  // fp32 grid: normals / flags fused with the triangulation
   rc = triangulate(vmask, F, M, N, io->trimap, io->triangles, io->halfedges, io->n_tri,
                    extras32 ? static_cast<const float*>(io->points) : nullptr, pitch,
                    (extras32 && !bil) ? static_cast<float*>(io->normals) : nullptr, p->l_max,
                    extras32 ? io->lmax_flag : nullptr, status, L.status_b, st);
   if (rc) return rc;
-  if (L.strict && (io->lmax_flag || (!bil && io->normals))) {
+  if (f64_grid && (io->lmax_flag || (!bil && io->normals))) {
     rc = tri_extras_f64(points64, F, M, N, io->triangles, io->n_tri, bil ? nullptr : io->normals,
                         false, p->l_max, io->lmax_flag, st);
     if (rc) return rc;
@@ -417,8 +427,28 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
                        p->sigma_angle, p->bilateral_kernel_size, p->bilateral_iterations,
                        reinterpret_cast<double*>(base + L.fc_a),
                        reinterpret_cast<double*>(base + L.fc_b), nullptr, io->trimap, io->normals,
-                       !L.strict, G, st);
+                       !f64_grid, G, st);
     if (rc) return rc;
+  } else if (bil && L.bil_mixed) {
+    // mixed: the exact f64 FC arrays of the exact smoothed grid, the fp32 filter on them
+    // (FC-array form), the mesh-order normals widened to double
+    double* fc_c = reinterpret_cast<double*>(base + L.fc_c);
+    double* fc_n = reinterpret_cast<double*>(base + L.fc_n);
+    float* fc32 = reinterpret_cast<float*>(base + L.fc32);
+    float* nrm32 = reinterpret_cast<float*>(base + L.nrm32);
+    if ((rc = fc_data_f64(points64, F, M, N, fc_c, fc_n, st))) return rc;
+    if ((rc = stage_in(fc_n, true, 6ll * (N - 1), 6ll * (N - 1) * (M - 1), F, M - 1,
+                       2 * (N - 1), fc32, fc_pitch(N), nullptr, st)))
+      return rc;
+    rc = bilateral(nullptr, F, M, N, 0, fc32, fc_c, (float)p->sigma_length,
+                   (float)p->sigma_angle, p->bilateral_kernel_size, p->bilateral_iterations,
+                   p->bilateral_iterations > 1 ? bil_a : nullptr,
+                   p->bilateral_iterations > 2 ? bil_b : nullptr, nullptr, io->trimap, nrm32, G,
+                   st);
+    if (rc) return rc;
+    if ((rc = widen_rows(nrm32, static_cast<double*>(io->normals), F, G, 3, io->n_tri, 3 * G,
+                         3 * G, st)))
+      return rc;
   } else if (bil) {
     rc = bilateral(static_cast<const float*>(io->points), F, M, N, pitch, nullptr, nullptr,
                    (float)p->sigma_length, (float)p->sigma_angle, p->bilateral_kernel_size,
@@ -431,7 +461,7 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   // 4. group labels (segmentation.group_assignment) on the final normals
   if (p->dominant_normals && io->labels) {
     if (!io->normals) return fail(ERR_INVALID, "front_end: labels need normals");
-    rc = group_assignment(io->normals, L.strict, G, F, io->n_tri, p->dominant_normals,
+    rc = group_assignment(io->normals, f64_grid, G, F, io->n_tri, p->dominant_normals,
                           p->n_dominant, p->ang_min, p->l_max >= 0 ? io->lmax_flag : nullptr,
                           io->labels, st);
     if (rc) return rc;

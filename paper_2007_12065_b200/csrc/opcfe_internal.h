@@ -36,6 +36,8 @@ int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaS
 
 int narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int width,
                    const int64_t* n_rows, long long src_fs, long long dst_fs, cudaStream_t st);
+int widen_rows(const float* src, double* dst, int F, long long rows, int width,
+               const int64_t* n_rows, long long src_fs, long long dst_fs, cudaStream_t st);
 
 // strict (fp64, reference operation order) kernels: strict.cu
 int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N, double lam,

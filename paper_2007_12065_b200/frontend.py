@@ -33,7 +33,7 @@ from .smoothing import BilateralParams, LaplacianParams
 @dataclass
 class FrontEndResult:
     """Device (or pinned host) outputs of one batch; rows beyond n_tri[f] are unused.
-    Float outputs are fp32 (precision "fast") or float64 (precision "strict")."""
+    Float outputs are fp32 (precision "fast") or float64 ("strict", "mixed")."""
     points: torch.Tensor        # (F, M, N, 3) smoothed grid (fast: view of the padded buffer)
     triangles: torch.Tensor     # (F, G, 3) int64, GID order
     trimap: torch.Tensor        # (F, G) int64
@@ -63,7 +63,10 @@ class FrontEnd:
     precision "fast" (default): fp32 kernels (+ the fp64 steps of the 1e-5 contract);
     "strict": the reference's own fp64 chain (opcfe_front_end with
     OPCFE_PRECISION_STRICT) -- float64 points and normals, bit-exact Laplacian and
-    topology, bilateral normals within a few ulp of the reference chain.
+    topology, bilateral normals within a few ulp of the reference chain;
+    "mixed": the strict Laplacian, topology and FC data, then the fp32 bilateral on the
+    exact FC arrays (OPCFE_PRECISION_MIXED) -- float64 outputs, bit-exact smoothed grid
+    and topology, normals within 1e-5 of the reference chain end to end.
     """
 
     def __init__(self, M: int, N: int, frames: int = 1,
@@ -76,10 +79,11 @@ class FrontEnd:
         require_cuda()
         if index_dtype not in (torch.int64, torch.int32):
             raise ValueError("index_dtype must be torch.int64 (reference) or torch.int32")
-        if precision not in ("fast", "strict"):
-            raise ValueError(f"precision must be 'fast' or 'strict', got {precision!r}")
+        if precision not in ("fast", "strict", "mixed"):
+            raise ValueError(f"precision must be 'fast', 'strict' or 'mixed', got {precision!r}")
         self.precision = precision
-        self.strict = strict = precision == "strict"
+        self.strict = precision == "strict"
+        self.f64 = f64 = precision in ("strict", "mixed")   # float64 grid / normals outputs
         if M < 2 or N < 2:
             from .geometry import DegenerateInputError
             raise DegenerateInputError("organized cloud must be at least 2 x 2")
@@ -103,7 +107,8 @@ class FrontEnd:
             bilateral.iterations if bilateral else 0, bilateral.kernel_size if bilateral else 3,
             bilateral.sigma_length if bilateral else 0.1, bilateral.sigma_angle if bilateral else 0.15,
             float(l_max) if l_max is not None else -1.0)
-        self.p.precision = _lib.PRECISION_STRICT if strict else _lib.PRECISION_FAST
+        self.p.precision = {"fast": _lib.PRECISION_FAST, "strict": _lib.PRECISION_STRICT,
+                            "mixed": _lib.PRECISION_MIXED}[precision]
         self.dn = None
         if dominant_normals is not None:   # fused group_assignment (segmentation.py:52-74)
             dn = torch.as_tensor(np.atleast_2d(np.asarray(dominant_normals, dtype=np.float64)))
@@ -113,8 +118,8 @@ class FrontEnd:
             self.p.dominant_normals = self.dn.data_ptr()
             self.p.n_dominant = self.dn.shape[0]
             self.p.ang_min = float(ang_min)
-        fdt = torch.float64 if strict else torch.float32
-        self.grid = torch.empty((frames, M, N, 3) if strict else (frames, M, self.pitch),
+        fdt = torch.float64 if f64 else torch.float32
+        self.grid = torch.empty((frames, M, N, 3) if f64 else (frames, M, self.pitch),
                                 dtype=fdt, device=dev)
         self.trimap = torch.empty((frames, G), dtype=torch.int64, device=dev)
         self.triangles = torch.empty((frames, G, 3), dtype=torch.int64, device=dev)
@@ -151,31 +156,34 @@ class FrontEnd:
         self._use_graph = graph
         extras = (normals and bilateral is None) or l_max is not None
         self.kernel_launches = self._count_launches(laplacian, bilateral if normals else None,
-                                                    src_kind, extras, strict) + \
+                                                    src_kind, extras, precision) + \
             (1 if self.labels is not None else 0) + \
             (0 if self.trimap32 is None else (3 if halfedges else 2))
 
     @staticmethod
-    def _count_launches(lap, bil, src_kind, extras=False, strict=False):
+    def _count_launches(lap, bil, src_kind, extras=False, precision="fast"):
         """Kernels one batch launches (mirrors front_end_impl in csrc/capi.cu)."""
         from .smoothing import BILATERAL_MAX_K32, LAPLACIAN_MAX_K32
-        lap64 = lap is not None and (strict or lap.kernel_size > LAPLACIAN_MAX_K32)
+        strict, f64 = precision == "strict", precision in ("strict", "mixed")
+        lap64 = lap is not None and (f64 or lap.kernel_size > LAPLACIAN_MAX_K32)
         bil64 = bil is not None and (strict or bil.kernel_size > BILATERAL_MAX_K32)
         n = 3                                                   # triangulate: count, scan, emit
-        if strict or lap64:
+        if f64 or lap64:
             n += 1 if src_kind != 2 else 0                      # source -> f64 (unstage)
             n += lap.iterations if lap else 0                   # laplacian_f64
-            n += 1 if (lap or strict) else 0                    # validity bits (+ fp32 grid)
-            n += 1 if (strict and extras) else 0                # tri_extras_f64
+            n += 1 if (lap or f64) else 0                       # validity bits (+ fp32 grid)
+            n += 1 if (f64 and extras) else 0                   # tri_extras_f64
         else:
             n += lap.iterations if lap else 0
             if not lap or src_kind != 0:
                 n += 1                                          # stage-in
-        if not strict:
+        if not f64:
             n += 1 if extras else 0                             # quad_extras: normals / l_max
         if bil64:
-            n += 0 if (strict or lap64) else 1                  # fp32 grid -> f64 (unstage)
+            n += 0 if (f64 or lap64) else 1                     # fp32 grid -> f64 (unstage)
             n += 1 + bil.iterations                             # fc_data_f64 + bilateral_f64
+        elif bil and f64:                                       # mixed: fc_data_f64, stage,
+            n += 3 + bil.iterations                             # fp32 iterations, widen
         elif bil:
             n += bil.iterations
         return n
@@ -256,7 +264,7 @@ class FrontEnd:
 
     def points_view(self) -> torch.Tensor:
         """The smoothed grid as (F, M, N, 3) (fast: a view of the padded fp32 rows)."""
-        if self.strict:
+        if self.f64:
             return self.grid
         return self.grid[..., :3 * self.N].unflatten(-1, (self.N, 3))
 
@@ -339,7 +347,8 @@ class HostPipeline:
                  dominant_normals)).  Unrequested outputs are not copied.
     index_dtype  torch.int64 (the reference's dtype) or torch.int32 -- compact,
                  NON-reference indices narrowed on the device (half the index bytes).
-    precision    "fast" (fp32 outputs) or "strict" (float64, the reference's chain).
+    precision    "fast" (fp32 outputs), "strict" (float64, the reference's chain) or
+                 "mixed" (float64; strict up to the FC data, fp32 bilateral).
     """
 
     DROPIN = ("points", "trimap", "triangles", "halfedges", "normals")

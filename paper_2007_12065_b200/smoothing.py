@@ -17,6 +17,10 @@ Precision (``precision=`` argument, or the process default from
   normals the filters leave unchanged come back bit-identical, moved ones are
   within 1e-5 per stage.  Kernel sizes beyond the fp32 kernels' compiled set
   (Laplacian > 17, bilateral > 9) run on the fp64 kernels.
+* ``"mixed"`` -- the strict Laplacian (bit-identical vertices) and fp64 FC data, then
+  the fp32 bilateral on those exact arrays: the chained normals stay within 1e-5 of the
+  reference's chain (the fast chain's drift comes from fp32 vertex storage), at about
+  twice the strict speed.  Opt-in.
 * ``"auto"`` (default) -- strict for float64 input (what the reference computes
   in), fast for float32.
 
@@ -68,7 +72,7 @@ class BilateralParams:
             raise ValueError("iterations must be >= 1")
 
 
-PRECISIONS = ("auto", "fast", "strict")
+PRECISIONS = ("auto", "fast", "strict", "mixed")
 LAPLACIAN_MAX_K32 = 17   # fp32 kernels' compiled kernel sizes (kLapMaxK32 / kBilMaxK32)
 BILATERAL_MAX_K32 = 9
 _precision = os.environ.get("OPCFE_PRECISION", "auto")
@@ -77,7 +81,8 @@ if _precision not in PRECISIONS:
 
 
 def set_precision(precision: str) -> None:
-    """Process-wide default precision of the drop-in functions ("auto" | "fast" | "strict")."""
+    """Process-wide default precision of the drop-in functions ("auto" | "fast" | "strict"
+    | "mixed")."""
     global _precision
     if precision not in PRECISIONS:
         raise ValueError(f"precision must be one of {PRECISIONS}, got {precision!r}")
@@ -89,7 +94,7 @@ def get_precision() -> str:
 
 
 def resolve_precision(precision, dtype) -> str:
-    """"fast" or "strict" for an input of `dtype` (None = the process default)."""
+    """"fast", "strict" or "mixed" for an input of `dtype` (None = the process default)."""
     p = _precision if precision is None else precision
     if p not in PRECISIONS:
         raise ValueError(f"precision must be one of {PRECISIONS}, got {p!r}")
@@ -101,7 +106,8 @@ def resolve_precision(precision, dtype) -> str:
 def _laplacian_staged(S: Staged, lam, kernel_size, iterations, precision=None):
     x = S.dev
     M, N = x.shape[:2]
-    if resolve_precision(precision, x.dtype) == "strict" or kernel_size > LAPLACIAN_MAX_K32:
+    if resolve_precision(precision, x.dtype) in ("strict", "mixed") or \
+            kernel_size > LAPLACIAN_MAX_K32:
         res = _ops.laplacian_f64(x.to(torch.float64), lam, kernel_size, iterations)
         return S.give(res.to(x.dtype))
     grid, _ = _ops.stage_in(x, want_points=True, want_mask=False)

@@ -349,7 +349,8 @@ def graph_kernel_names(eng):
 
 
 @pytest.mark.parametrize("prec,dt", [("strict", torch.float64), ("strict", torch.float32),
-                                     ("fast", torch.float32), ("fast", torch.float64)])
+                                     ("fast", torch.float32), ("fast", torch.float64),
+                                     ("mixed", torch.float64), ("mixed", torch.float32)])
 @pytest.mark.parametrize("big", [False, True])
 @pytest.mark.parametrize("index32", [False, True])
 def test_strict_kernel_launch_count_matches_graph(fe, prec, dt, big, index32):
@@ -362,6 +363,70 @@ def test_strict_kernel_launch_count_matches_graph(fe, prec, dt, big, index32):
     names = graph_kernel_names(eng)
     assert len(names) == eng.kernel_launches, names
     assert all("opcfe" in nm for nm in names), names
+
+
+# --------------------------------------------------------------- mixed precision
+MIXED_NORMAL_TOL = 1e-5     # the north-star contract, END TO END against the reference chain
+
+
+@pytest.mark.parametrize("case", sorted(CHAIN))
+def test_mixed_chain_vs_reference_chain(fe, case):
+    """FrontEnd(precision="mixed"): strict Laplacian / topology / FC data, fp32 bilateral
+    on the exact FC arrays -- smoothed grid and topology bit-exact, normals within 1e-5 of
+    the reference's own fp64 chain, labels equal except at exact ang_min / argmax ties."""
+    g = CHAIN[case]
+    M, N = g["opc"].shape[:2]
+    eng, res, T = run_engine(fe, g, "mixed")
+    assert res.points.dtype == torch.float64 and res.normals.dtype == torch.float64
+    assert same(res.points[0].cpu().numpy(), g["smoothed"])
+    trimap = g["trimap"].astype(np.int64)
+    assert np.array_equal(res.trimap[0].cpu().numpy(), trimap)
+    assert np.array_equal(res.triangles[0, :T].cpu().numpy(), triangles_from_trimap(trimap, M, N))
+    err = normal_err(res.normals[0, :T].cpu().numpy(), g["normals"])
+    print(f"{case}: mixed chain normals max {err.max():.3e} p99.9 {np.quantile(err, 0.999):.3e}")
+    assert err.max() <= MIXED_NORMAL_TOL, f"{case}: mixed chain normal error {err.max():.3e}"
+    lab = res.labels[0, :T].cpu().numpy()
+    assert (lab != g["labels"]).sum() <= max(1, T // 100000)
+    if "lmax_flag" in g:
+        assert np.array_equal(res.lmax_mask[0, :T].cpu().numpy().astype(bool), g["lmax_flag"])
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C4"])
+def test_mixed_chain_full_size(fe, cfg):
+    """Full-size frames: mixed vs strict (itself within ~4e-14 of the reference chain)."""
+    from paper_2007_12065_b200 import synthetic
+    base = {"C2": synthetic.config_c2, "C4": synthetic.config_c4}[cfg]()
+    lap = {"C2": (1.0, 3, 3), "C4": (1.0, 3, 10)}[cfg]
+    bil = {"C2": (0.1, 0.15, 3, 2), "C4": (0.1, 0.15, 3, 5)}[cfg]
+    M, N = base.shape[:2]
+    out = {}
+    for prec in ("strict", "mixed"):
+        eng = fe.FrontEnd(M, N, 1, laplacian=fe.LaplacianParams(*lap),
+                          bilateral=fe.BilateralParams(*bil), src_dtype=torch.float64,
+                          precision=prec)
+        res = eng.run(torch.from_numpy(base).cuda().unsqueeze(0))
+        T = res.n_tri[0]
+        out[prec] = (res.points[0].cpu().numpy(), res.triangles[0, :T].cpu().numpy(),
+                     res.normals[0, :T].cpu().numpy())
+        del eng
+    assert same(out["mixed"][0], out["strict"][0])
+    assert np.array_equal(out["mixed"][1], out["strict"][1])
+    err = normal_err(out["mixed"][2], out["strict"][2])
+    assert err.max() <= MIXED_NORMAL_TOL, f"{cfg}: {err.max():.3e}"
+
+
+@pytest.mark.parametrize("case", ["room72", "lidar_bil", "k11"])
+def test_mixed_drop_in_chain(fe, case):
+    """precision="mixed" through the drop-in functions: the same bars."""
+    g = CHAIN[case]
+    lp, bp, l_max, ang = chain_params(fe, g)
+    sm = fe.laplacian_filter_opc(g["opc"], lp, precision="mixed")
+    assert same(sm, g["smoothed"])
+    mesh = fe.mesh_from_opc(sm)
+    if bp is not None:
+        n = fe.bilateral_filter_opc(sm, bp, mesh.trimap, precision="mixed")
+        assert n.dtype == np.float64
+        assert normal_err(n, g["normals"]).max() <= MIXED_NORMAL_TOL
 
 
 # --------------------------------------------------------------- host pipeline options
