@@ -177,26 +177,6 @@ __device__ __forceinline__ auto tile_origin(const S* v, int count, int stride, i
 // cost of the correctly rounded fp64 divide/sqrt used where bit-exact normals are
 // returned (gridops.cu).  Tiny triangles (|cross| below the fp32 normal range, i.e.
 // vertices closer than ~1e-19 m) are out of contract.
-// Degenerate (zero cross product), non-finite or out-of-range crosses give NaN normals: the
-// test runs on the fp32-rounded components (a NaN component makes the Newton step NaN).
-__device__ __forceinline__ void normalise_fast(double x, double y, double z, float* n) {
-  const float fx = (float)x, fy = (float)y, fz = (float)z;
-  const float m = fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz)));
-  if (m > 0.f && m <= 3.402823466e38f) {
-    // rescale into [1, 3] before squaring (tiny triangles: |x| ~ 1e-20); the scale cancels
-    const float is = rcp_approx(m);
-    const float gx = fx * is, gy = fy * is, gz = fz * is;
-    const float l2 = gx * gx + gy * gy + gz * gz;
-    float r = rsqrt_approx(l2);
-    r = r * fmaf(-0.5f * l2, r * r, 1.5f);
-    n[0] = gx * r;
-    n[1] = gy * r;
-    n[2] = gz * r;
-  } else {
-    n[0] = n[1] = n[2] = __int_as_float(0x7fc00000);
-  }
-}
-
 __device__ __forceinline__ void fc_normals_quad(const float* P1, const float* P2, const float* P3,
                                                 const float* P4, float* n) {
   double d13[3], e1f[3], e1s[3];  // p1 - p3; first e1 = p2 - p3; second e1 = p4 - p1

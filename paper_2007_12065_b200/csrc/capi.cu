@@ -130,7 +130,7 @@ FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src
   take(L.g64_tmp, (L.lap64 && p->laplacian_iterations > 1) ? g64 : 0);
   take(L.g64_out, (!f64_grid && (L.lap64 || L.bil64)) ? g64 : 0);
   take(L.fc_c, (L.bil64 || L.bil_mixed) ? fc64 : 0);
-  take(L.fc_n, (L.bil64 || L.bil_mixed) ? fc64 : 0);
+  take(L.fc_n, L.bil64 ? fc64 : 0);
   take(L.fc32, L.bil_mixed ? fc_bytes : 0);
   take(L.nrm32, L.bil_mixed ? (size_t)F * 3 * 2 * (M - 1) * (N - 1) * sizeof(float) : 0);
   take(L.fc_a, (L.bil64 && p->bilateral_iterations > 1) ? fc64 : 0);
@@ -430,16 +430,12 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
                        !f64_grid, G, st);
     if (rc) return rc;
   } else if (bil && L.bil_mixed) {
-    // mixed: the exact f64 FC arrays of the exact smoothed grid, the fp32 filter on them
-    // (FC-array form), the mesh-order normals widened to double
+    // mixed: the exact f64 centroids and fp32 FC normals (fp64 cross) of the exact
+    // smoothed grid, the fp32 filter on them (FC-array form), normals widened to double
     double* fc_c = reinterpret_cast<double*>(base + L.fc_c);
-    double* fc_n = reinterpret_cast<double*>(base + L.fc_n);
     float* fc32 = reinterpret_cast<float*>(base + L.fc32);
     float* nrm32 = reinterpret_cast<float*>(base + L.nrm32);
-    if ((rc = fc_data_f64(points64, F, M, N, fc_c, fc_n, st))) return rc;
-    if ((rc = stage_in(fc_n, true, 6ll * (N - 1), 6ll * (N - 1) * (M - 1), F, M - 1,
-                       2 * (N - 1), fc32, fc_pitch(N), nullptr, st)))
-      return rc;
+    if ((rc = fc_mixed(points64, F, M, N, fc_c, fc32, fc_pitch(N), st))) return rc;
     rc = bilateral(nullptr, F, M, N, 0, fc32, fc_c, (float)p->sigma_length,
                    (float)p->sigma_angle, p->bilateral_kernel_size, p->bilateral_iterations,
                    p->bilateral_iterations > 1 ? bil_a : nullptr,

@@ -310,6 +310,29 @@ __device__ __forceinline__ bool longest_edge_exceeds(double sab, double sbc, dou
   return !(isnan(sab) || isnan(sbc) || isnan(sca)) && fmax(sab, fmax(sbc, sca)) > thr;
 }
 
+// A unit normal from an fp64 cross product with an fp32 normalisation (the bilateral
+// input): MUFU rcp / rsqrt + one Newton step instead of IEEE divide / sqrt,
+// |n - float32(reference)| ~ 1e-7.
+// Degenerate (zero cross product), non-finite or out-of-range crosses give NaN normals: the
+// test runs on the fp32-rounded components (a NaN component makes the Newton step NaN).
+__device__ __forceinline__ void normalise_fast(double x, double y, double z, float* n) {
+  const float fx = (float)x, fy = (float)y, fz = (float)z;
+  const float m = fmaxf(fabsf(fx), fmaxf(fabsf(fy), fabsf(fz)));
+  if (m > 0.f && m <= 3.402823466e38f) {
+    // rescale into [1, 3] before squaring (tiny triangles: |x| ~ 1e-20); the scale cancels
+    const float is = rcp_approx(m);
+    const float gx = fx * is, gy = fy * is, gz = fz * is;
+    const float l2 = gx * gx + gy * gy + gz * gz;
+    float r = rsqrt_approx(l2);
+    r = r * fmaf(-0.5f * l2, r * r, 1.5f);
+    n[0] = gx * r;
+    n[1] = gy * r;
+    n[2] = gz * r;
+  } else {
+    n[0] = n[1] = n[2] = __int_as_float(0x7fc00000);
+  }
+}
+
 __device__ __forceinline__ bool finite3f(float x, float y, float z) {
   return isfinite(x) && isfinite(y) && isfinite(z);
 }

@@ -47,6 +47,8 @@ int bilateral_f64(const double* centroids, const double* normals_in, int F, int 
                   double* buf_b, double* out_fc, const int64_t* trimap, void* out_mesh,
                   bool out_f32, long long out_rows, cudaStream_t st);
 int fc_data_f64(const double* opc, int F, int M, int N, double* cen, double* nrm, cudaStream_t st);
+int fc_mixed(const double* opc, int F, int M, int N, double* cen, float* nrm32, int fcp,
+             cudaStream_t st);
 int tri_extras_f64(const double* pts, int F, int M, int N, const int64_t* tris,
                    const int64_t* n_tri, void* normals, bool normals_f32, double l_max,
                    uint8_t* flag, cudaStream_t st);

@@ -589,6 +589,39 @@ __global__ void fc_data_f64_kernel(const double* __restrict__ opc, int M, int N,
   }
 }
 
+// FC data for the MIXED front end: the reference's f64 centroids and FC normals (bit-exact,
+// as fc_data_f64), the normals rounded to fp32 straight into the padded FC rows the fp32
+// bilateral reads (fc_pitch floats per quad row) -- one pass instead of fc_data_f64 +
+// staging.  (An fp32 normalisation of the fp64 cross product, ~2 ulp instead of 0.5, put
+// one C4 triangle of the chain at 1.5e-5: the normals are rounded from the exact ones.)
+__global__ void fc_mixed_kernel(const double* __restrict__ opc, int M, int N,
+                                double* __restrict__ cen, float* __restrict__ nrm32, int fcp) {
+  const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int Nq = N - 1;
+  const long long Q = (long long)(M - 1) * Nq;
+  if (q >= Q) return;
+  const int f = blockIdx.y;
+  const int u = (int)(q / Nq), v = (int)(q % Nq);
+  const double* p1 = opc + (long long)f * M * N * 3 + ((long long)u * N + v) * 3;
+  const double* p2 = p1 + 3;
+  const double* p4 = p1 + (long long)N * 3;
+  const double* p3 = p4 + 3;
+  const double* tri[2][3] = {{p3, p2, p1}, {p1, p4, p3}};
+  float* no = nrm32 + ((long long)f * (M - 1) + u) * fcp + 6 * v;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double *A = tri[k][0], *B = tri[k][1], *C = tri[k][2];
+    double* co = cen + (f * Q + q) * 6 + 3 * k;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) co[j] = centroid_f64(A[j], B[j], C[j]);
+    double nx, ny, nz;
+    unit_normal_f64(A[0], A[1], A[2], B[0], B[1], B[2], C[0], C[1], C[2], nx, ny, nz);
+    no[3 * k] = (float)nx;
+    no[3 * k + 1] = (float)ny;
+    no[3 * k + 2] = (float)nz;
+  }
+}
+
 // mesh normals / l_max flags of F frames: frame f's triangles are rows f*G .. f*G+n_tri[f]
 // of `tris` (vertex indices local to the frame), points [F][P][3] f64.
 template <typename OUT>
@@ -745,6 +778,14 @@ int fc_data_f64(const double* opc, int F, int M, int N, double* cen, double* nrm
   const long long Q = (long long)(M - 1) * (N - 1);
   fc_data_f64_kernel<<<dim3(nblk(Q, 256), F), 256, 0, st>>>(opc, M, N, cen, nrm);
   return check_launch("fc_data_f64_kernel");
+}
+
+int fc_mixed(const double* opc, int F, int M, int N, double* cen, float* nrm32, int fcp,
+             cudaStream_t st) {
+  if (F < 1 || M < 2 || N < 2) return fail(ERR_INVALID, "organized cloud must be at least 2 x 2");
+  const long long Q = (long long)(M - 1) * (N - 1);
+  fc_mixed_kernel<<<dim3(nblk(Q, 256), F), 256, 0, st>>>(opc, M, N, cen, nrm32, fcp);
+  return check_launch("fc_mixed_kernel");
 }
 
 int tri_extras_f64(const double* pts, int F, int M, int N, const int64_t* tris,
