@@ -430,7 +430,7 @@ def test_mixed_drop_in_chain(fe, case):
 
 
 # --------------------------------------------------------------- host pipeline options
-@pytest.mark.parametrize("mode", ["dropin", "compact", "strict", "subset", "labels"])
+@pytest.mark.parametrize("mode", ["dropin", "compact", "strict", "mixed", "subset", "labels"])
 def test_host_pipeline_output_options(fe, mode):
     """HostPipeline: selected outputs only, int32 (non-reference) indices, strict float64;
     every returned array equals the device engine's, and run() returns with all host
@@ -442,8 +442,8 @@ def test_host_pipeline_output_options(fe, mode):
     kw, ekw = {}, {}
     if mode == "compact":
         kw = dict(index_dtype=torch.int32)
-    elif mode == "strict":
-        kw = ekw = dict(precision="strict")
+    elif mode in ("strict", "mixed"):
+        kw = ekw = dict(precision=mode)
     elif mode == "subset":
         kw = dict(outputs=("points", "triangles", "normals"))
     elif mode == "labels":
@@ -481,7 +481,7 @@ def test_host_pipeline_output_options(fe, mode):
             assert torch.equal(tm.to(torch.int64), ref.trimap[f].cpu())
     if mode == "compact":
         assert pipe.d2h_bytes < full * 0.8
-    if mode == "strict":
+    if mode in ("strict", "mixed"):
         assert res.points.dtype == torch.float64 and res.normals.dtype == torch.float64
 
 
