@@ -13,7 +13,7 @@ print("C4", round(d["value"],1), "e2e", round(d["e2e"]["value"],1), {k: round(v[
 for w in ["C1","C2","C3","C5"]:
     try:
         d = json.load(open(f"gpurun_out/r2_wl_{w}.json")); r = json.load(open(f"gpurun_out/r2_wl_{w}_ref.json"))
-        print(w, round(d["value"],1), "e2e", round(d["e2e"]["value"],1), "strict", d["strict"] and round(d["strict"]["value"],1), "ref", round(r["value"],2), d["stage_ms_per_step"], d["roofline"]["kernel"], d["roofline"]["frac"], d["clocks"]["sm_mhz"])
+        print(w, round(d["value"],1), "e2e", round(d["e2e"]["value"],1), "strict", d["strict"] and round(d["strict"]["value"],1), "mixed", d.get("mixed") and round(d["mixed"]["value"],1), "ref", round(r["value"],2), d["stage_ms_per_step"], d["roofline"]["kernel"], d["roofline"]["frac"], d["clocks"]["sm_mhz"])
         print("   parity", json.dumps(d["parity"]["chained"]["fast"]["normals_abs"] if d.get("parity") else None), json.dumps(d["parity"]["chained"]["strict"]["normals_abs"] if d.get("parity") else None))
     except Exception as e:
         print(w, "ERR", e)
