@@ -169,3 +169,32 @@ def test_structured_scenes_equal_stock_reference(fe, ref, case):
     r_mesh.normals, g_mesh.normals = r_n, g_n
     assert same(fe.group_assignment(g_mesh, dn, l_max, 0.9),
                 ref.segmentation.group_assignment(r_mesh, dn, l_max, 0.9))
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_mixed_front_end_vs_stock_reference(fe, ref, seed):
+    """FrontEnd(precision="mixed") on random clouds against the stock reference's chain:
+    smoothed grid and topology bit-identical, normals within the 1e-5 contract."""
+    rng = np.random.default_rng(9300 + seed)
+    opc = random_cloud(rng)
+    M, N = opc.shape[:2]
+    lap = (float(rng.uniform(0.2, 1.0)), 3, int(rng.integers(1, 6)))
+    bil = (float(rng.uniform(0.02, 0.3)), float(rng.uniform(0.05, 0.5)),
+           int(rng.choice([3, 5, 7])), int(rng.integers(1, 4)))
+    r_sm = ref.smoothing.laplacian_filter_opc(opc, ref.smoothing.LaplacianParams(*lap))
+    r_mesh = ref.mesh.mesh_from_opc(r_sm)
+    r_n = ref.smoothing.bilateral_filter_opc(r_sm, ref.smoothing.BilateralParams(*bil),
+                                             r_mesh.trimap)
+    eng = fe.FrontEnd(M, N, 1, laplacian=fe.LaplacianParams(*lap),
+                      bilateral=fe.BilateralParams(*bil), src_dtype=torch.float64,
+                      precision="mixed")
+    res = eng.run(torch.from_numpy(opc).cuda().unsqueeze(0))
+    T = res.n_tri[0]
+    assert same(res.points[0].cpu().numpy(), r_sm)
+    assert np.array_equal(res.trimap[0].cpu().numpy(), r_mesh.trimap)
+    assert np.array_equal(res.triangles[0, :T].cpu().numpy(), r_mesh.triangles)
+    g_n = res.normals[0, :T].cpu().numpy()
+    bad = np.isnan(r_n).any(1)
+    assert np.array_equal(np.isnan(g_n).any(1), bad)
+    if (~bad).any():
+        assert np.linalg.norm(g_n[~bad] - r_n[~bad], axis=1).max() <= 1e-5
