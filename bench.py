@@ -572,9 +572,10 @@ def run_ours(args, rank, world, local_rank, wl):
     if not args.no_e2e:
         pipe = fe.HostPipeline(M, N, laplacian=lap_p, bilateral=bil_p, l_max=wl.l_max,
                                src_dtype=torch.float64, device=dev)
-        # e2e batch: ~400 MB of f64 input per run() (C4: 8 frames, ~2.8 GB of pinned in/out
-        # buffers; small frames: up to the step's frames, so per-run latency amortises)
-        FE = min(F, max(8, int(400e6 // (M * N * 24))))
+        # e2e batch: >= 16 frames (OPCFE_E2E_FRAMES) or ~400 MB of f64 input per run(), at
+        # most the step's frames (C4: 16 frames, ~5.7 GB of pinned in/out buffers; the
+        # pipeline's fill / drain amortises over the batch: 16 vs 8 frames +2-3 %)
+        FE = min(F, max(int(os.environ.get("OPCFE_E2E_FRAMES", "16")), int(400e6 // (M * N * 24))))
         host = torch.empty((FE, M, N, 3), dtype=torch.float64, pin_memory=True)
         host.copy_(eng.src[:FE].double().cpu())
         pipe.run(host)                              # warm-up (pinned outputs allocated)
