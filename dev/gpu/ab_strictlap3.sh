@@ -1,0 +1,6 @@
+# strict Laplacian staging A/B (TMA vs per-thread, env switch) + strict suites
+cd $GRAFT_REPO_ROOT
+timeout 1200 python -m pytest tests/test_gpu_strict.py tests/test_gpu_vs_reference.py -q -x -p no:cacheprovider 2>&1 | tail -1
+for E in 0 1 0 1; do
+  echo "tma=$E: $(OPCFE_LAP64_TMA=$E timeout 300 python profiles/strict_driver.py --frames 16 --steps 6 2>&1 | tail -1)"
+done

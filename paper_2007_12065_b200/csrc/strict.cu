@@ -24,6 +24,8 @@
 #include "opcfe_internal.h"
 
 #include <algorithm>
+#include <atomic>
+#include <cstdlib>
 
 namespace opcfe {
 
@@ -172,6 +174,82 @@ __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_kernel(const double* __
       const double dist = __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
       if (!(dist > 0.0)) continue;  // NaN or <= 0 (:265-266)
       const double w = __drcp_rn(dist);  // correctly rounded 1/dist == the reference's 1.0/dist
+      ax = dadd(ax, dmul(dx, w));
+      ay = dadd(ay, dmul(dy, w));
+      az = dadd(az, dmul(dz, w));
+      wsum = dadd(wsum, w);
+    }
+  }
+  if (wsum > 0.0) {
+    const double s = __ddiv_rn(lam, wsum);
+    px = dadd(px, dmul(s, ax));
+    py = dadd(py, dmul(s, ay));
+    pz = dadd(pz, dmul(s, az));
+  }
+  dst[o] = px;
+  dst[o + 1] = py;
+  dst[o + 2] = pz;
+}
+
+// k = 3, even N (16-B row stride of the f64 grid): the same arithmetic as
+// laplacian_f64_kernel<1, true>, with the tile + halo arriving by ONE TMA 3-D box load
+// (NaN out-of-bounds fill) instead of per-thread global loads, then transposed in shared
+// memory into the conflict-free planar layout.  The box starts 2 points left of the tile
+// (a 16-B aligned start: 2 x 24 B) and is 36 points wide.
+constexpr int kLapTmaBW = kSTW + 4;   // box width (points)
+constexpr int kLapTmaBH = kSTH + 2;
+constexpr int kLapTmaRawF = (kLapTmaBW * 3 * kLapTmaBH * 8 + 127) / 128 * 128 / 8;  // doubles
+
+__global__ void __launch_bounds__(kSNT, 5) laplacian_f64_tma_kernel(
+    const __grid_constant__ CUtensorMap tin, double* __restrict__ out, int M, int N, double lam) {
+  constexpr int BW = kSTW + 2, BH = kSTH + 2, PL = BW * BH;
+  extern __shared__ __align__(16) char smem_raw[];
+  uint64_t* barp;
+  double* raw = reinterpret_cast<double*>(smem_aligned_base(smem_raw, &barp));
+  double* sm = raw + kLapTmaRawF;
+  uint64_t& bar = *barp;
+  const int f = blockIdx.z;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kSTW + tx;
+  const int u0 = blockIdx.y * kSTH, v0 = blockIdx.x * kSTW;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, kLapTmaBW * 3 * kLapTmaBH * 8);
+    tma_load_3d(raw, &tin, &bar, (v0 - 2) * 3, u0 - 1, f);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  for (int q = tid; q < PL; q += kSNT) {  // AoS box (r, c + 1) -> planes (r, c)
+    const int r = q / BW, c = q - r * BW;
+    const double* p = raw + (r * kLapTmaBW + c + 1) * 3;
+    sm[q] = p[0];
+    sm[PL + q] = p[1];
+    sm[2 * PL + q] = p[2];
+  }
+  __syncthreads();
+  const int u = u0 + ty, v = v0 + tx;
+  if (u >= M || v >= N) return;
+  double* dst = out + (long long)f * 3 * M * N;
+  const long long o = ((long long)u * N + v) * 3;
+  const int c0 = (ty + 1) * BW + tx + 1;
+  double px = sm[c0], py = sm[PL + c0], pz = sm[2 * PL + c0];
+  if (u == 0 || u == M - 1 || v == 0 || v == N - 1 || px != px || py != py || pz != pz) {
+    dst[o] = px;
+    dst[o + 1] = py;
+    dst[o + 2] = pz;
+    return;
+  }
+  double wsum = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll
+  for (int du = -1; du <= 1; ++du) {
+#pragma unroll
+    for (int dv = -1; dv <= 1; ++dv) {
+      if (du == 0 && dv == 0) continue;
+      const int c = c0 + du * BW + dv;
+      const double dx = dsub(sm[c], px), dy = dsub(sm[PL + c], py), dz = dsub(sm[2 * PL + c], pz);
+      const double dist = __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
+      if (!(dist > 0.0)) continue;  // NaN or <= 0 (:265-266)
+      const double w = __drcp_rn(dist);
       ax = dadd(ax, dmul(dx, w));
       ay = dadd(ay, dmul(dy, w));
       az = dadd(az, dmul(dz, w));
@@ -677,6 +755,22 @@ int lap_launch(const double* in, double* out, int F, int M, int N, int h, double
   return check_launch("laplacian_f64_kernel");
 }
 
+int lap_tma_launch(const double* in, double* out, int F, int M, int N, double lam,
+                   cudaStream_t st) {
+  CUtensorMap m;
+  int rc;
+  if ((rc = make_tmap_3d(&m, in, true, 3ull * N, M, F, 3ull * N, 3ull * N * M, kLapTmaBW * 3,
+                         kLapTmaBH)))
+    return rc;
+  constexpr int smem = (kLapTmaRawF + 3 * (kSTW + 2) * (kSTH + 2)) * (int)sizeof(double) +
+                       kSmemSlack;
+  static std::atomic<unsigned long long> attr_mask{0};
+  if ((rc = ensure_smem_attr(laplacian_f64_tma_kernel, smem, attr_mask))) return rc;
+  dim3 grid((N + kSTW - 1) / kSTW, (M + kSTH - 1) / kSTH, F);
+  laplacian_f64_tma_kernel<<<grid, dim3(kSTW, kSTH), smem, st>>>(m, out, M, N, lam);
+  return check_launch("laplacian_f64_tma_kernel");
+}
+
 template <int HC, bool SMEM, typename OUT>
 int bil_launch(const Bil64Args& a, int F, cudaStream_t st) {
   dim3 grid((a.Nq + kSTW - 1) / kSTW, (a.Mq + kSTH - 1) / kSTH, F);
@@ -707,6 +801,12 @@ int bil_dispatch(const Bil64Args& a, int F, cudaStream_t st) {
 
 }  // namespace
 
+// OPCFE_LAP64_TMA=0 keeps the per-thread staging for every N (A/B)
+static const bool g_lap_tma = [] {
+  const char* v = std::getenv("OPCFE_LAP64_TMA");
+  return v == nullptr || v[0] != '0';
+}();
+
 int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
                   int ksize, int iters, cudaStream_t st) {
   if (F < 1 || M < 1 || N < 1 || iters < 1 || ksize < 3 || (ksize % 2) == 0 || !in || !out)
@@ -721,7 +821,9 @@ int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int 
   for (int it = 0; it < iters; ++it) {
     double* dst = to_out ? out : tmp;
     int rc;
-    if (h == 1) rc = lap_launch<1, true>(src, dst, F, M, N, h, lam, st);
+    // k = 3 with a 16-B f64 row stride (N even): TMA-staged; otherwise per-thread loads
+    if (h == 1 && N % 2 == 0 && g_lap_tma) rc = lap_tma_launch(src, dst, F, M, N, lam, st);
+    else if (h == 1) rc = lap_launch<1, true>(src, dst, F, M, N, h, lam, st);
     else if (h == 2) rc = lap_launch<2, true>(src, dst, F, M, N, h, lam, st);
     else if (lap_smem(h) <= kSmemMax) rc = lap_launch<0, true>(src, dst, F, M, N, h, lam, st);
     else rc = lap_launch<0, false>(src, dst, F, M, N, h, lam, st);
