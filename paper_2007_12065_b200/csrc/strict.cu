@@ -371,9 +371,15 @@ __global__ void __launch_bounds__(kSNT) bilateral_f64_kernel(Bil64Args a) {
 // receiving thread through shared memory (16 weights per quad); pairs whose forward quad
 // lies in the halo are weighed by the receiver itself.  41 % fewer fp64 operations per
 // output triangle for 32 KB more shared memory.
-template <int HC, bool VEC, bool SYM, typename OUT>
-__global__ void __launch_bounds__(kSNT, SYM ? 3 : 4) bilateral_f64s_kernel(Bil64Args a) {
+// TMA (with SYM): the centroid and normal boxes arrive by two TMA loads (NaN out-of-bounds
+// fill == off-grid) into the weight-exchange region (free until after staging), and the
+// staging pass transforms them from shared memory instead of global loads.
+template <int HC, bool VEC, bool SYM, typename OUT, bool TMA = false>
+__global__ void __launch_bounds__(kSNT, SYM ? 3 : 4)
+    bilateral_f64s_kernel(Bil64Args a, const __grid_constant__ CUtensorMap tc,
+                          const __grid_constant__ CUtensorMap tn) {
   static_assert(!SYM || HC == 1, "the symmetric schedule is written for kernel size 3");
+  static_assert(!TMA || SYM, "TMA staging is written for the kernel-size-3 layout");
   const int h = HC > 0 ? HC : a.h;
   const int Mq = a.Mq, Nq = a.Nq;
   const int f = blockIdx.z;
@@ -383,7 +389,10 @@ __global__ void __launch_bounds__(kSNT, SYM ? 3 : 4) bilateral_f64s_kernel(Bil64
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int tid = ty * kSTW + tx;
   const int u = blockIdx.y * kSTH + ty, v = blockIdx.x * kSTW + tx;
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) char smem_raw[];
+  uint64_t* barp = nullptr;
+  double* const sm = TMA ? reinterpret_cast<double*>(smem_aligned_base(smem_raw, &barp))
+                         : reinterpret_cast<double*>(smem_raw);
   __shared__ double expT[32];
   __shared__ double s_o[3];
   __shared__ int s_first;
@@ -403,11 +412,34 @@ __global__ void __launch_bounds__(kSNT, SYM ? 3 : 4) bilateral_f64s_kernel(Bil64
   // triangles; 2 x 48 contiguous bytes, 16-B loads when aligned) -> 12 planar slots.
   // Skipped neighbours (NaN normal, off the grid) become sentinels: n' = 0, c' = 1e200
   // (t = inf -> w = 0): no per-pair test in the loop.
+  double* const rawc = sm + 12 * plane;  // TMA boxes [bh][bw * 6] (the W region)
+  double* const rawn = rawc + 2048;
+  if constexpr (TMA) {
+    if (tid == 0) {
+      mbar_init(barp, 1);
+      fence_mbar_init();
+      mbar_expect_tx(barp, 2 * bw * 6 * bh * 8);
+      tma_load_3d(rawc, &tc, barp, v0 * 6, u0, f);
+      tma_load_3d(rawn, &tn, barp, v0 * 6, u0, f);
+    }
+    __syncthreads();
+    mbar_wait(barp, 0);
+  }
   for (int q = tid; q < plane; q += kSNT) {
     const int r = q / bw, c = q - r * bw;
     const int uu = u0 + r, vv = v0 + c;
     double cv6[6], nv6[6];
-    if (uu >= 0 && uu < Mq && vv >= 0 && vv < Nq) {
+    if constexpr (TMA) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const double2 x = reinterpret_cast<const double2*>(rawc + q * 6)[j];
+        const double2 y = reinterpret_cast<const double2*>(rawn + q * 6)[j];
+        cv6[2 * j] = x.x;
+        cv6[2 * j + 1] = x.y;
+        nv6[2 * j] = y.x;
+        nv6[2 * j + 1] = y.y;
+      }
+    } else if (uu >= 0 && uu < Mq && vv >= 0 && vv < Nq) {
       const long long off = ((long long)uu * Nq + vv) * 6;
       if (VEC) {
 #pragma unroll
@@ -771,6 +803,12 @@ int lap_tma_launch(const double* in, double* out, int F, int M, int N, double la
   return check_launch("laplacian_f64_tma_kernel");
 }
 
+// OPCFE_BIL64_TMA=0 keeps the per-thread staging of the strict k = 3 bilateral (A/B)
+static const bool g_bil64_tma = [] {
+  const char* v = std::getenv("OPCFE_BIL64_TMA");
+  return v == nullptr || v[0] != '0';
+}();
+
 template <int HC, bool SMEM, typename OUT>
 int bil_launch(const Bil64Args& a, int F, cudaStream_t st) {
   dim3 grid((a.Nq + kSTW - 1) / kSTW, (a.Mq + kSTH - 1) / kSTH, F);
@@ -779,11 +817,27 @@ int bil_launch(const Bil64Args& a, int F, cudaStream_t st) {
     int smem = bil_smem(a.h);
     const bool vec = (reinterpret_cast<uintptr_t>(a.cen) | reinterpret_cast<uintptr_t>(a.nin)) % 16 == 0;
     constexpr bool kSym = HC == 1;
+    CUtensorMap tc{}, tn{};
+    if constexpr (kSym) {
+      if (vec && g_bil64_tma) {  // 48-B quads: the FC rows are 16-B multiples for any Nq
+        const int bw = kSTW + 2, bh = kSTH + 2;
+        if ((rc = make_tmap_3d(&tc, a.cen, true, 6ull * a.Nq, a.Mq, F, 6ull * a.Nq,
+                               6ull * a.Nq * a.Mq, bw * 6, bh)) ||
+            (rc = make_tmap_3d(&tn, a.nin, true, 6ull * a.Nq, a.Mq, F, 6ull * a.Nq,
+                               6ull * a.Nq * a.Mq, bw * 6, bh)))
+          return rc;
+        smem += 16 * kSNT * (int)sizeof(double) + kSmemSlack;
+        auto kern = bilateral_f64s_kernel<HC, true, true, OUT, true>;
+        if ((rc = set_smem(kern, smem))) return rc;
+        kern<<<grid, dim3(kSTW, kSTH), smem, st>>>(a, tc, tn);
+        return check_launch("bilateral_f64s_kernel");
+      }
+    }
     auto kern = vec ? bilateral_f64s_kernel<HC, true, kSym, OUT>
                     : bilateral_f64s_kernel<HC, false, kSym, OUT>;
     if (kSym) smem += 16 * kSNT * (int)sizeof(double);
     if ((rc = set_smem(kern, smem))) return rc;
-    kern<<<grid, dim3(kSTW, kSTH), smem, st>>>(a);
+    kern<<<grid, dim3(kSTW, kSTH), smem, st>>>(a, tc, tn);
     return check_launch("bilateral_f64s_kernel");
   } else {
     bilateral_f64_kernel<OUT><<<grid, dim3(kSTW, kSTH), 0, st>>>(a);
