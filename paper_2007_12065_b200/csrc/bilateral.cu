@@ -128,6 +128,7 @@ struct BilArgs {
   const int64_t* trimap;  // scatter mode: per frame [G]
   long long tm_fs;
   float* out_mesh;   // scatter destination: per frame [cap][3]
+  double* out_mesh64;  // ... or float64 (the mixed-precision front end), when non-null
   long long out_fs;  // floats per frame
   long long n_out;   // rows per frame available in out_mesh (bounds check)
   const float* pts;  // point grid (packed scatter: exact rebuild of unchanged normals)
@@ -443,17 +444,22 @@ __device__ __forceinline__ void scatter_mesh(const BilArgs& a, int f, int u, int
   const int Nq = a.N - 1;
   const long long g = 2ll * ((long long)u * Nq + v);
   const longlong2 tm = *reinterpret_cast<const longlong2*>(a.trimap + f * a.tm_fs + g);
-  float* dst = a.out_mesh + f * a.out_fs;
-  if (tm.x >= 0 && tm.x < a.n_out) {
-    dst[3 * tm.x] = r[0];
-    dst[3 * tm.x + 1] = r[1];
-    dst[3 * tm.x + 2] = r[2];
-  }
-  if (tm.y >= 0 && tm.y < a.n_out) {
-    dst[3 * tm.y] = r[3];
-    dst[3 * tm.y + 1] = r[4];
-    dst[3 * tm.y + 2] = r[5];
-  }
+  auto put = [&](auto* dst) {
+    if (tm.x >= 0 && tm.x < a.n_out) {
+      dst[3 * tm.x] = r[0];
+      dst[3 * tm.x + 1] = r[1];
+      dst[3 * tm.x + 2] = r[2];
+    }
+    if (tm.y >= 0 && tm.y < a.n_out) {
+      dst[3 * tm.y] = r[3];
+      dst[3 * tm.y + 1] = r[4];
+      dst[3 * tm.y + 2] = r[5];
+    }
+  };
+  if (a.out_mesh64)  // uniform: the mixed front end's float64 normals
+    put(a.out_mesh64 + f * a.out_fs);
+  else
+    put(a.out_mesh + f * a.out_fs);
 }
 
 // PACKOUT (mode 0, fused pipeline with >= 2 iterations): besides filtering, write the
@@ -840,7 +846,8 @@ size_t bilateral_buf_c_bytes(int F, int M, int N, int ksize) {
 int bilateral(const float* pts, int F, int M, int N, int pitch, const float* normals_in,
               const double* centroids_in, float sigma_length, float sigma_angle, int ksize,
               int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
-              float* out_mesh, long long out_rows, cudaStream_t st, float* buf_c) {
+              float* out_mesh, long long out_rows, cudaStream_t st, float* buf_c,
+              double* out_mesh64) {
   if (F < 1 || M < 2 || N < 2 || iters < 1 || ksize < 3 || (ksize % 2) == 0)
     return fail(ERR_INVALID, "bilateral: bad shape or parameters");
   if (!(sigma_length > 0.f) || !(sigma_angle > 0.f))
@@ -853,7 +860,7 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   const bool resume = normals_in != nullptr && centroids_in == nullptr;
   if (!from_arrays && (pts == nullptr || pitch < 3 * N || pitch % 4))
     return fail(ERR_INVALID, "bilateral: point grid (pitch multiple of 4 floats) required");
-  const bool scatter = out_mesh != nullptr;
+  const bool scatter = out_mesh != nullptr || out_mesh64 != nullptr;
   if (scatter && trimap == nullptr) return fail(ERR_INVALID, "bilateral: scatter needs trimap");
   if (!scatter && out_fc == nullptr) return fail(ERR_INVALID, "bilateral: no output given");
   if ((iters > 1 && !buf_a) || (iters > 2 && !buf_b))
@@ -905,6 +912,7 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   a.trimap = trimap;
   a.tm_fs = 2ll * Mq * Nq;
   a.out_mesh = out_mesh;
+  a.out_mesh64 = out_mesh64;
   a.out_fs = 3ll * out_rows;
   a.n_out = out_rows;
   a.pts = pts;

@@ -82,7 +82,7 @@ struct FeLayout {
   // strict stages up to the FC data, then the fp32 bilateral on the FC arrays
   bool strict = false, mixed = false, lap64 = false, bil64 = false, bil_mixed = false;
   size_t g64_in = 0, g64_tmp = 0, g64_out = 0, fc_c = 0, fc_n = 0, fc_a = 0, fc_b = 0;
-  size_t fc32 = 0, nrm32 = 0;
+  size_t fc32 = 0;
 };
 
 FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src_kind,
@@ -132,7 +132,7 @@ FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src
   take(L.fc_c, (L.bil64 || L.bil_mixed) ? fc64 : 0);
   take(L.fc_n, L.bil64 ? fc64 : 0);
   take(L.fc32, L.bil_mixed ? fc_bytes : 0);
-  take(L.nrm32, L.bil_mixed ? (size_t)F * 3 * 2 * (M - 1) * (N - 1) * sizeof(float) : 0);
+
   take(L.fc_a, (L.bil64 && p->bilateral_iterations > 1) ? fc64 : 0);
   take(L.fc_b, (L.bil64 && p->bilateral_iterations > 2) ? fc64 : 0);
   L.total = off + 256;
@@ -430,21 +430,17 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
                        !f64_grid, G, st);
     if (rc) return rc;
   } else if (bil && L.bil_mixed) {
-    // mixed: the exact f64 centroids and fp32 FC normals (fp64 cross) of the exact
-    // smoothed grid, the fp32 filter on them (FC-array form), normals widened to double
+    // mixed: the exact f64 centroids and fp32 FC normals of the exact smoothed grid, the
+    // fp32 filter on them (FC-array form), the last iteration scattering float64 normals
     double* fc_c = reinterpret_cast<double*>(base + L.fc_c);
     float* fc32 = reinterpret_cast<float*>(base + L.fc32);
-    float* nrm32 = reinterpret_cast<float*>(base + L.nrm32);
     if ((rc = fc_mixed(points64, F, M, N, fc_c, fc32, fc_pitch(N), st))) return rc;
     rc = bilateral(nullptr, F, M, N, 0, fc32, fc_c, (float)p->sigma_length,
                    (float)p->sigma_angle, p->bilateral_kernel_size, p->bilateral_iterations,
                    p->bilateral_iterations > 1 ? bil_a : nullptr,
-                   p->bilateral_iterations > 2 ? bil_b : nullptr, nullptr, io->trimap, nrm32, G,
-                   st);
+                   p->bilateral_iterations > 2 ? bil_b : nullptr, nullptr, io->trimap, nullptr,
+                   G, st, nullptr, static_cast<double*>(io->normals));
     if (rc) return rc;
-    if ((rc = widen_rows(nrm32, static_cast<double*>(io->normals), F, G, 3, io->n_tri, 3 * G,
-                         3 * G, st)))
-      return rc;
   } else if (bil) {
     rc = bilateral(static_cast<const float*>(io->points), F, M, N, pitch, nullptr, nullptr,
                    (float)p->sigma_length, (float)p->sigma_angle, p->bilateral_kernel_size,

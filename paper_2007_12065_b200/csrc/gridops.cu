@@ -188,33 +188,9 @@ __global__ void narrow_indices_kernel(const int64_t* __restrict__ src, int32_t* 
   }
 }
 
-// fp32 rows -> f64 (the mixed-precision front end's mesh normals): frame f's first
-// n_rows[f] rows of `width` values
-__global__ void widen_rows_kernel(const float* __restrict__ src, double* __restrict__ dst,
-                                  long long rows, int width, const int64_t* __restrict__ n_rows,
-                                  long long src_fs, long long dst_fs) {
-  const int f = blockIdx.y;
-  const long long n = (n_rows ? n_rows[f] : rows) * width;
-  const float* s = src + f * src_fs;
-  double* d = dst + f * dst_fs;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    d[i] = (double)s[i];
-}
-
 inline unsigned blocks_for(long long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
 }  // namespace
-
-int widen_rows(const float* src, double* dst, int F, long long rows, int width,
-               const int64_t* n_rows, long long src_fs, long long dst_fs, cudaStream_t st) {
-  if (F < 1 || rows < 0 || width < 1 || !src || !dst)
-    return fail(ERR_INVALID, "widen_rows: bad arguments");
-  if (rows == 0) return OK;
-  dim3 grid((unsigned)std::min<long long>(blocks_for(rows * width, 256), 148 * 8), F);
-  widen_rows_kernel<<<grid, 256, 0, st>>>(src, dst, rows, width, n_rows, src_fs, dst_fs);
-  return check_launch("widen_rows_kernel");
-}
 
 int narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int width,
                    const int64_t* n_rows, long long src_fs, long long dst_fs, cudaStream_t st) {

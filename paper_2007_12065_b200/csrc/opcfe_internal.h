@@ -30,14 +30,13 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
               const double* centroids_in, float sigma_length, float sigma_angle, int ksize,
               int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
               float* out_mesh, long long out_rows, cudaStream_t st,
-              float* buf_c = nullptr);  // fused pipeline: centroid windows (bilateral_buf_c_bytes)
+              float* buf_c = nullptr,  // fused pipeline: centroid windows (bilateral_buf_c_bytes)
+              double* out_mesh64 = nullptr);  // float64 scatter destination instead
 
 int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st);
 
 int narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int width,
                    const int64_t* n_rows, long long src_fs, long long dst_fs, cudaStream_t st);
-int widen_rows(const float* src, double* dst, int F, long long rows, int width,
-               const int64_t* n_rows, long long src_fs, long long dst_fs, cudaStream_t st);
 
 // strict (fp64, reference operation order) kernels: strict.cu
 int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N, double lam,

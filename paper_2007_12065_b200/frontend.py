@@ -182,8 +182,8 @@ class FrontEnd:
         if bil64:
             n += 0 if (f64 or lap64) else 1                     # fp32 grid -> f64 (unstage)
             n += 1 + bil.iterations                             # fc_data_f64 + bilateral_f64
-        elif bil and f64:                                       # mixed: fc_mixed, fp32
-            n += 2 + bil.iterations                             # iterations, widen
+        elif bil and f64:                                       # mixed: fc_mixed + fp32
+            n += 1 + bil.iterations                             # iterations (f64 scatter)
         elif bil:
             n += bil.iterations
         return n
