@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
                      const __grid_constant__ CUtensorMap tcen, const __grid_constant__ CUtensorMap tout,
                      BilArgs a, PackedG pg) {
   using T = BilTile<H>;
-  static_assert(!PACKOUT || (MODE == kFromPoints && !SCATTER), "PACKOUT: mode 0, no scatter");
+  static_assert(!PACKOUT || (MODE != kNormalsBuf && !SCATTER), "PACKOUT: mode 0 / 2, no scatter");
   extern __shared__ __align__(16) char smem_raw[];
   uint64_t* barp;
   float* p = reinterpret_cast<float*>(smem_aligned_base(smem_raw, &barp));
@@ -713,7 +713,8 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
           rebuild |= valid;
         }
       }
-      if (rebuild) {  // rare: a valid triangle left unchanged
+      if (rebuild && a.pts != nullptr) {  // rare: a valid triangle left unchanged (FC-array
+                                          // input: no points, n' / sqrt(B) stays)
         const float* P1 = a.pts + f * a.pts_fs + (long long)u * a.pitch + 3 * v;
         float raw[6];
         fc_normals_quad(P1, P1 + 3, P1 + a.pitch + 3, P1 + a.pitch, raw);
@@ -803,6 +804,19 @@ int launch_packout_h(int h, const CUtensorMap& tp, const BilArgs& a, int F, cons
     case 2: return launch_bil<2, kFromPoints, false, true>(tp, tp, tp, tp, a, F, st, pg);
     case 3: return launch_bil<3, kFromPoints, false, true>(tp, tp, tp, tp, a, F, st, pg);
     case 4: return launch_bil<4, kFromPoints, false, true>(tp, tp, tp, tp, a, F, st, pg);
+    default: return fail(ERR_UNSUPPORTED, "bilateral: kernel_size > 9 is not compiled in");
+  }
+}
+
+// iteration 1 of the fused pipeline from FC arrays (fp32 normals + f64 centroids: the
+// mixed-precision front end)
+int launch_packout_arrays_h(int h, const CUtensorMap& tn, const CUtensorMap& tc,
+                            const BilArgs& a, int F, const PackedG& pg, cudaStream_t st) {
+  switch (h) {
+    case 1: return launch_bil<1, kNormalsCentBuf, false, true>(tn, tn, tc, tn, a, F, st, pg);
+    case 2: return launch_bil<2, kNormalsCentBuf, false, true>(tn, tn, tc, tn, a, F, st, pg);
+    case 3: return launch_bil<3, kNormalsCentBuf, false, true>(tn, tn, tc, tn, a, F, st, pg);
+    case 4: return launch_bil<4, kNormalsCentBuf, false, true>(tn, tn, tc, tn, a, F, st, pg);
     default: return fail(ERR_UNSUPPORTED, "bilateral: kernel_size > 9 is not compiled in");
   }
 }
@@ -926,7 +940,7 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   // Fused pipeline with >= 2 iterations and a third buffer: iteration 1 writes the packed
   // planes (centroids once into C, normals into A); iterations 2..B read them by TMA with
   // no pack phase (bilateral_packed_kernel), ping-ponging A / B; the last one scatters.
-  if (buf_c != nullptr && g_bil_packed && !from_arrays && !resume && scatter && iters >= 2) {
+  if (buf_c != nullptr && g_bil_packed && !resume && scatter && iters >= 2) {
     const long long Nq2 = (Nq + 1) & ~1ll;
     auto planes_of = [&](float* b) {
       PackedG g;
@@ -950,7 +964,9 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
     CUtensorMap mna[2], mnb[2];
     if ((rc = maps_of(ga, &mna[0], &mna[1])) || (rc = maps_of(gb, &mnb[0], &mnb[1]))) return rc;
     // iteration 1: centroid windows -> buf_c, normals -> A
-    if ((rc = launch_packout_h(h, m_pts, a, F, ga, st))) return rc;
+    if ((rc = from_arrays ? launch_packout_arrays_h(h, m_nin, m_cin, a, F, ga, st)
+                          : launch_packout_h(h, m_pts, a, F, ga, st)))
+      return rc;
     for (int it = 1; it < iters; ++it) {
       const bool last = it == iters - 1;
       const bool from_a = (it % 2) == 1;

@@ -108,7 +108,7 @@ FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src
   L.lap_b = (lap && !L.lap64 && p->laplacian_iterations > 1) ? grid_bytes : 0;
   L.bil_b_bytes = fc_bytes;
   const bool bil32 = bil && !L.bil64;
-  const bool packed_bil = bil32 && !L.bil_mixed;  // the fused pipeline's packed windows
+  const bool packed_bil = bil32;  // the fused pipeline's packed windows (fast and mixed)
   size_t off = 0;
   auto take = [&](size_t& at, size_t bytes) {
     at = off;
@@ -439,7 +439,8 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
                    (float)p->sigma_angle, p->bilateral_kernel_size, p->bilateral_iterations,
                    p->bilateral_iterations > 1 ? bil_a : nullptr,
                    p->bilateral_iterations > 2 ? bil_b : nullptr, nullptr, io->trimap, nullptr,
-                   G, st, nullptr, static_cast<double*>(io->normals));
+                   G, st, p->bilateral_iterations > 1 ? bil_c : nullptr,
+                   static_cast<double*>(io->normals));
     if (rc) return rc;
   } else if (bil) {
     rc = bilateral(static_cast<const float*>(io->points), F, M, N, pitch, nullptr, nullptr,
