@@ -763,7 +763,8 @@ def main():
                          "GPU LOCAL_RANK %% device_count, gloo for the timing collectives "
                          "(plumbing check, NOT a scaling measurement)")
     ap.add_argument("--no-strict", action="store_true",
-                    help="skip the strict (fp64 reference-chain) device throughput leg")
+                    help="skip the strict (fp64 reference chain) and mixed-precision device "
+                         "and e2e legs")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
