@@ -225,7 +225,9 @@ typedef struct {
    * double: bit-exact Laplacian, FC data, topology; bilateral to <= a few ulp);
    * OPCFE_PRECISION_MIXED: the strict Laplacian, topology and FC data (bit-exact, double
    * points), then the fp32 bilateral on the exact FC arrays (normals double, within 1e-5
-   * of the reference's chain end to end -- the fast chain's drift is fp32 vertex storage).
+   * of the reference's chain end to end on well-conditioned frames -- the fast chain's
+   * drift is fp32 vertex storage; at small sigma_angle fp32 normals alone can move the
+   * reference's answer past 1e-5).
    * Fast-precision stages whose kernel size exceeds the fp32 kernels (Laplacian > 17,
    * bilateral > 9) run on the fp64 generic-window kernels, results rounded to fp32. */
   int precision;

@@ -19,8 +19,10 @@ Precision (``precision=`` argument, or the process default from
   (Laplacian > 17, bilateral > 9) run on the fp64 kernels.
 * ``"mixed"`` -- the strict Laplacian (bit-identical vertices) and fp64 FC data, then
   the fp32 bilateral on those exact arrays: the chained normals stay within 1e-5 of the
-  reference's chain (the fast chain's drift comes from fp32 vertex storage), at about
-  twice the strict speed.  Opt-in.
+  reference's chain on the benchmark frames (the fast chain's drift comes from fp32
+  vertex storage), at about twice the strict speed; ill-conditioned clouds (small
+  sigma_angle) can exceed it, since fp32 normals alone move the reference's answer
+  there.  Opt-in.
 * ``"auto"`` (default) -- strict for float64 input (what the reference computes
   in), fast for float32.
 
