@@ -156,6 +156,14 @@ int opcfe_narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows
                          const int64_t* n_rows, long long src_frame_stride,
                          long long dst_frame_stride, opcfe_stream_t stream);
 
+/* Row count and bound of a GID map, on the device: stats (device, 2 x int64) = {number of
+ * entries >= 0, max(-1, largest entry)} of trimap[0..n).  Replaces the host pass
+ * `valid = trimap >= 0; out = np.empty((int(valid.sum()), 3))` of bilateral_filter_opc
+ * (smoothing.py:110-112); stats[1] >= stats[0] is the reference's IndexError
+ * (`out[trimap[valid]] = ...` out of bounds).  Asynchronous on `stream`. */
+int opcfe_trimap_stats(const int64_t* trimap, long long n, long long* stats,
+                       opcfe_stream_t stream);
+
 /* ---- strict precision: the reference's own fp64 arithmetic on its own layouts ----
  * Grids (F, M, N, 3) and FC arrays (F, M-1, N-1, 2, 3) are contiguous float64; any odd
  * kernel_size >= 3 (generic-window kernels).

@@ -90,6 +90,7 @@ _SIG = {
     "opcfe_bilateral_f64": (_i, [_vp, _vp, _i, _i, _i, _d, _d, _i, _i, _vp, _vp, _vp, _vp, _vp,
                                  _ll, _vp]),
     "opcfe_triangle_normals": (_i, [_vp, _i, _vp, _ll, _vp, _vp]),
+    "opcfe_trimap_stats": (_i, [_vp, _ll, _vp, _vp]),
     "opcfe_find_cells": (_i, [_vp, _ll, _ll, _vp, _vp, _vp, _ll, _d, _d, _ll, _ll, _vp, _vp,
                               _vp]),
     "opcfe_segments_workspace": (_sz, [_ll]),
@@ -336,11 +337,15 @@ def extract_triangles_opc(opc):
 def extract_halfedges_opc(trimap, M, N):
     """mesh.py:99-135 (the caller has validated the trimap's shape)."""
     tm = np.ascontiguousarray(trimap, dtype=np.int64).reshape(-1)
-    n_tri = int(tm.max()) + 1 if tm.size else 0
+    if tm.size == 0:
+        return np.full(0, -1, dtype=np.int64)
+    d_tm, d_st = _Dev.of(tm), _Dev(16)
+    _check(_op.opcfe_trimap_stats(d_tm.ptr, tm.size, d_st.ptr, None), "extract_halfedges_opc")
+    n_tri = int(d_st.get(np.empty(2, dtype=np.int64))[1]) + 1        # trimap.max() + 1
     if n_tri <= 0:
         return np.full(0, -1, dtype=np.int64)
     he = _host_empty(3 * n_tri, np.int64)               # every entry written below
-    d_tm, d_he = _Dev.of(tm), _Dev(he.nbytes)
+    d_he = _Dev(he.nbytes)
     _sync_check(_rt.cudaMemset(d_he.ptr, 0xFF, he.nbytes))          # -1 in every int64
     _check(_op.opcfe_halfedges_from_trimap(d_tm.ptr, int(M), int(N), n_tri, d_he.ptr, None),
            "extract_halfedges_opc")
@@ -402,13 +407,17 @@ def bilateral_filter_opc(opc, sigma_length, sigma_angle, kernel_size, iterations
         out = np.empty((int(valid.sum()), 3))
         out[tm[valid]] = flat[valid]
         return out
-    T = int(np.count_nonzero(tm >= 0))
+    d_tm, d_st = _Dev.of(tm), _Dev(16)
+    _check(_op.opcfe_trimap_stats(d_tm.ptr, tm.size, d_st.ptr, None), "bilateral_filter_opc")
+    T, top = (int(x) for x in d_st.get(np.empty(2, dtype=np.int64)))   # valid.sum(), max
+    if top >= T:                            # out[trimap[valid]] out of bounds (numpy's error)
+        raise IndexError(f"index {top} is out of bounds for axis 0 with size {T}")
     out = _host_empty((T, 3))
     if T == 0:
         return out
     Mq, Nq = M - 1, N - 1
     fc = Mq * Nq * 6 * 8
-    d_src, d_tm = _Dev.of(src), _Dev.of(tm)
+    d_src = _Dev.of(src)
     d_c, d_n, d_out = _Dev(fc), _Dev(fc), _Dev(out.nbytes)
     _check(_op.opcfe_fc_data(d_src.ptr, 1, M, N, d_c.ptr, d_n.ptr, None), "bilateral_filter_opc")
     bufs = [_Dev(fc) if iterations > j else None for j in (1, 2)]

@@ -93,6 +93,15 @@ def halfedges_from_trimap(trimap: torch.Tensor, M: int, N: int, n_tri: int):
     return he
 
 
+def trimap_stats(trimap: torch.Tensor):
+    """(valid-entry count, largest entry) of an int64 GID map (opcfe_trimap_stats)."""
+    st = torch.empty(2, dtype=torch.int64, device=trimap.device)
+    _lib.check(_lib.lib().opcfe_trimap_stats(trimap.data_ptr(), trimap.numel(), st.data_ptr(),
+                                             stream()), "trimap_stats")
+    cnt, mx = st.tolist()
+    return cnt, mx
+
+
 def fc_data(opc: torch.Tensor):
     """(M,N,3) f32/f64 contiguous -> centroids, normals (M-1,N-1,2,3) same dtype."""
     M, N = opc.shape[:2]

@@ -262,6 +262,11 @@ int opcfe_narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows
                         S(stream));
 }
 
+int opcfe_trimap_stats(const int64_t* trimap, long long n, long long* stats,
+                       opcfe_stream_t stream) {
+  return trimap_stats(trimap, n, stats, S(stream));
+}
+
 int opcfe_laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N,
                         double lam, int kernel_size, int iterations, opcfe_stream_t stream) {
   return laplacian_f64(in, out, tmp, F, M, N, lam, kernel_size, iterations, S(stream));

@@ -188,6 +188,42 @@ __global__ void narrow_indices_kernel(const int64_t* __restrict__ src, int32_t* 
   }
 }
 
+// Count of the valid (>= 0) entries of a GID map and its largest entry: the row count of
+// bilateral_filter_opc's output (smoothing.py:110-112: `valid.sum()`) and the bound its
+// `out[trimap[valid]]` scatter checks.  stats[0] += count, stats[1] = max(stats[1], max);
+// the caller pre-sets stats to {0, -1}.
+__global__ void trimap_stats_kernel(const int64_t* __restrict__ tm, long long n,
+                                    long long* __restrict__ stats) {
+  long long cnt = 0, mx = -1;
+  const long long stride = 2ll * gridDim.x * blockDim.x;
+  long long i = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x);
+  if (reinterpret_cast<uintptr_t>(tm) % 16 == 0) {
+    for (; i + 1 < n; i += stride) {
+      const longlong2 x = __ldcs(reinterpret_cast<const longlong2*>(tm + i));
+      cnt += (x.x >= 0) + (x.y >= 0);
+      mx = max(mx, max(x.x, x.y));
+    }
+  } else {
+    for (; i + 1 < n; i += stride) {
+      const long long a = tm[i], b = tm[i + 1];
+      cnt += (a >= 0) + (b >= 0);
+      mx = max(mx, max(a, b));
+    }
+  }
+  if (i < n) {  // the odd tail element
+    cnt += tm[i] >= 0;
+    mx = max(mx, (long long)tm[i]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0 && (cnt || mx >= 0)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(stats), (unsigned long long)cnt);
+    atomicMax(stats + 1, mx);
+  }
+}
+
 inline unsigned blocks_for(long long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
 }  // namespace
@@ -201,6 +237,17 @@ int narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int 
   dim3 grid((unsigned)std::min<long long>(blocks_for((n + 1) / 2, 256), 148 * 8), F);
   narrow_indices_kernel<<<grid, 256, 0, st>>>(src, dst, rows, width, n_rows, src_fs, dst_fs);
   return check_launch("narrow_indices_kernel");
+}
+
+int trimap_stats(const int64_t* trimap, long long n, long long* stats, cudaStream_t st) {
+  if (n < 0 || !stats || (n > 0 && !trimap)) return fail(ERR_INVALID, "trimap_stats: bad arguments");
+  if (cudaMemsetAsync(stats, 0, sizeof(long long), st) != cudaSuccess ||
+      cudaMemsetAsync(stats + 1, 0xFF, sizeof(long long), st) != cudaSuccess)  // {0, -1}
+    return check_launch("trimap_stats (init)");
+  if (n == 0) return OK;
+  const unsigned blocks = (unsigned)std::min<long long>(blocks_for((n + 1) / 2, 256), 148 * 4);
+  trimap_stats_kernel<<<blocks, 256, 0, st>>>(trimap, n, stats);
+  return check_launch("trimap_stats_kernel");
 }
 
 int stage_in(const void* src, bool f64, long long rs, long long fs, int F, int M, int N,

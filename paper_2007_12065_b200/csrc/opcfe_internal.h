@@ -35,6 +35,8 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
 
 int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st);
 
+int trimap_stats(const int64_t* trimap, long long n, long long* stats, cudaStream_t st);
+
 int narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int width,
                    const int64_t* n_rows, long long src_fs, long long dst_fs, cudaStream_t st);
 

@@ -169,7 +169,9 @@ def bilateral_filter_opc(opc, params: BilateralParams, trimap=None, precision: s
         raise DegenerateInputError("organized cloud must be at least 2 x 2")
     M, N = x.shape[:2]
     tm = _trimap_of(S, trimap, M, N)
-    n_out = int((tm >= 0).sum().item())
+    n_out, top = _ops.trimap_stats(tm)
+    if top >= n_out:   # the reference's out[trimap[valid]] scatter (smoothing.py:112)
+        raise IndexError(f"index {top} is out of bounds for axis 0 with size {n_out}")
     strict = resolve_precision(precision, x.dtype) == "strict"
     if strict or params.kernel_size > BILATERAL_MAX_K32:
         cen, nrm = _ops.fc_data_f64(x.to(torch.float64))

@@ -1184,3 +1184,18 @@ def test_fastga_on_own_accumulator(fe, level):
     n[3, 2] = np.inf
     fe.integrate_normals(ga4, n)
     assert ga4.counts.sum() == 3
+
+
+@pytest.mark.parametrize("n,offset", [(0, 0), (1, 0), (7, 1), (4_141_202, 0), (4_141_203, 1),
+                                      (1000, 0)])
+def test_trimap_stats(n, offset):
+    """opcfe_trimap_stats (count of entries >= 0, max(-1, largest)) against NumPy: odd
+    lengths, a 8-B (not 16-B) aligned start, all-invalid maps."""
+    from paper_2007_12065_b200 import _ops
+    rng = np.random.default_rng(n)
+    tm = np.where(rng.random(n + offset) < 0.7, rng.integers(0, 1 << 40, n + offset), -1)
+    if n == 1000:
+        tm[:] = -1
+    d = torch.from_numpy(tm).cuda()[offset:]
+    assert _ops.trimap_stats(d) == (int((tm[offset:] >= 0).sum()),
+                                    int(max(-1, tm[offset:].max())) if n else -1)

@@ -96,14 +96,23 @@ sm = smoothing.laplacian_filter_opc(opc, smoothing.LaplacianParams(0.8, 3, 4))
 m = mesh.mesh_from_opc(sm)
 n = smoothing.bilateral_filter_opc(sm, smoothing.BilateralParams(0.1, 0.2, 5, 3), m.trimap)
 n2 = smoothing.bilateral_filter_opc(sm, smoothing.BilateralParams(0.1, 0.2, 3, 2))
+he2 = mesh.extract_halfedges_opc(m.trimap, *sm.shape[:2])
+bad = m.trimap.copy()
+bad[np.flatnonzero(bad >= 0)[-1]] = 10 ** 9            # an out-of-range GID entry
+try:
+    smoothing.bilateral_filter_opc(sm, smoothing.BilateralParams(0.1, 0.2, 3, 1), bad)
+    err = "none"
+except Exception as e:
+    err = type(e).__name__
 np.savez(sys.argv[1], active=_kernels.ACTIVE, sm=sm, tri=m.triangles, he=m.halfedges,
-         tm=m.trimap, mn=m.normals, n=n, n2=n2)
+         tm=m.trimap, mn=m.normals, n=n, n2=n2, he2=he2, err=err)
 """
 
 
 def test_fused_binding_chain_equals_stock_native(installed, tmp_path):
     """The patch's fused mesh_from_opc / bilateral_filter_opc (one upload; gather on the
-    device) against the same stock code on the reference's compiled CPU backend."""
+    device) against the same stock code on the reference's compiled CPU backend, incl. the
+    IndexError of an out-of-range GID map (checked on the device: opcfe_trimap_stats)."""
     import numpy as np
     out = {}
     for mode in ("cuda", "native"):
@@ -117,7 +126,8 @@ def test_fused_binding_chain_equals_stock_native(installed, tmp_path):
         out[mode] = np.load(path)
         assert str(out[mode]["active"]) == mode
     g, r = out["cuda"], out["native"]
-    for k in ("sm", "tri", "he", "tm", "mn"):
+    assert str(g["err"]) == str(r["err"]) == "IndexError"
+    for k in ("sm", "tri", "he", "tm", "mn", "he2"):
         assert g[k].shape == r[k].shape and np.array_equal(g[k], r[k], equal_nan=(k in ("sm", "mn"))), k
     for k in ("n", "n2"):
         bad = np.isnan(r[k]).any(1)

@@ -127,6 +127,12 @@ def test_error_types_match_stock_reference(fe, ref):
         (lambda m: m.smoothing.BilateralParams(0.1, 0.15, 4, 1),
          lambda: fe.BilateralParams(0.1, 0.15, 4, 1)),
     ]
+    opc = np.random.default_rng(1).normal(size=(6, 7, 3))
+    bad = np.arange(2 * 5 * 6, dtype=np.int64)
+    bad[-1] = 10 ** 9                                       # out-of-range GID entry
+    cases.append((lambda m: m.smoothing.bilateral_filter_opc(
+        opc, m.smoothing.BilateralParams(0.1, 0.15, 3, 1), bad),
+        lambda: fe.bilateral_filter_opc(opc, fe.BilateralParams(0.1, 0.15, 3, 1), bad)))
     for r_call, g_call in cases:
         with pytest.raises(Exception) as r_exc:
             r_call(ref)
