@@ -267,123 +267,6 @@ __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_tma_kernel(
   dst[o + 2] = pz;
 }
 
-// k = 3, column walk: each unordered neighbour pair's IEEE sqrt + reciprocal once.  A warp
-// owns 32 adjacent columns (v0 - 1 .. v0 + 30; lanes 1..30 write columns v0..v0 + 29, the
-// edge lanes only supply pairs) and walks rows u0..u0 + kWalkRows - 1 top to bottom.  At
-// row u every lane weighs its point's four FORWARD pairs -- right (0,+1), down-left
-// (+1,-1), down (+1,0), down-right (+1,+1) -- and receives the other four by warp
-// shuffles: left = lane - 1's right pair (this row); up-left / up / up-right = lane - 1's
-// down-right / its own down / lane + 1's down-left pair (previous row).  The pair weight
-// 1/dist is the same bit pattern from either end (squares of negated differences), so the
-// centre accumulates the reference's sums in the reference's order (du outer, dv inner;
-// IEEE mul / add / sqrt / div, no contraction) from 4 weighings instead of 8: bit-identical
-// to laplacian_f64_kernel.  Points arrive one row per step (three coalesced loads per lane,
-// prefetched a row ahead); the neighbours' coordinates come by shuffles, and no shared
-// memory or barrier is used.  A weight of 0 marks a skipped pair (NaN / non-positive
-// distance, off-grid: the loads return NaN); acc is never -0.0, so skipping == adding 0.
-constexpr int kWalkRows = 32;
-constexpr int kWalkCols = 30;
-constexpr int kWalkWarps = 4;
-
-__global__ void __launch_bounds__(32 * kWalkWarps) laplacian_f64_walk_kernel(
-    const double* __restrict__ in, double* __restrict__ out, int M, int N, double lam) {
-  const int lane = threadIdx.x & 31;
-  const int strip = blockIdx.x * kWalkWarps + (threadIdx.x >> 5);
-  if (strip * kWalkCols >= N) return;  // warp-uniform
-  const int v = strip * kWalkCols - 1 + lane;
-  const int u0 = blockIdx.y * kWalkRows;
-  const int u1 = min(u0 + kWalkRows, M);
-  const long long fs = 3ll * M * N;
-  const double* src = in + blockIdx.z * fs;
-  double* dst = out + blockIdx.z * fs;
-  const bool col_ok = v >= 0 && v < N;
-  const bool writer = lane >= 1 && lane <= kWalkCols && col_ok;
-  auto load = [&](int u, double& x, double& y, double& z) {
-    if (col_ok && u >= 0 && u < M) {
-      const double* g = src + ((long long)u * N + v) * 3;
-      x = __ldg(g);
-      y = __ldg(g + 1);
-      z = __ldg(g + 2);
-    } else {
-      x = y = z = qnan();
-    }
-  };
-  // 1/dist of the pair (p, q) -- the reference's weight -- or 0 for a skipped pair
-  auto pairw = [](double px, double py, double pz, double qx, double qy, double qz) {
-    const double dx = dsub(qx, px), dy = dsub(qy, py), dz = dsub(qz, pz);
-    const double dist = __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
-    return dist > 0.0 ? __drcp_rn(dist) : 0.0;
-  };
-  auto up = [](double x) { return __shfl_up_sync(0xffffffffu, x, 1); };    // from lane - 1
-  auto dn = [](double x) { return __shfl_down_sync(0xffffffffu, x, 1); };  // from lane + 1
-  // rows u - 1 (a), u (c), u + 1 (n): own column, left (l) and right (r) neighbours
-  double ax, ay, az, cx, cy, cz;
-  load(u0 - 1, ax, ay, az);
-  load(u0, cx, cy, cz);
-  double alx = up(ax), aly = up(ay), alz = up(az), arx = dn(ax), ary = dn(ay), arz = dn(az);
-  double clx = up(cx), cly = up(cy), clz = up(cz), crx = dn(cx), cry = dn(cy), crz = dn(cz);
-  // weights of row u0's up pairs (the down pairs of row u0 - 1)
-  double w_ul = up(pairw(ax, ay, az, crx, cry, crz));
-  double w_u = pairw(ax, ay, az, cx, cy, cz);
-  double w_ur = dn(pairw(ax, ay, az, clx, cly, clz));
-  double fx, fy, fz;  // prefetched row u + 1
-  load(u0 + 1, fx, fy, fz);
-  for (int u = u0; u < u1; ++u) {
-    const double nx = fx, ny = fy, nz = fz;
-    load(u + 2, fx, fy, fz);
-    const double nlx = up(nx), nly = up(ny), nlz = up(nz);
-    const double nrx = dn(nx), nry = dn(ny), nrz = dn(nz);
-    const double w_r = pairw(cx, cy, cz, crx, cry, crz);
-    const double w_l = up(w_r);
-    const double w_dl = pairw(cx, cy, cz, nlx, nly, nlz);
-    const double w_d = pairw(cx, cy, cz, nx, ny, nz);
-    const double w_dr = pairw(cx, cy, cz, nrx, nry, nrz);
-    if (writer) {
-      double px = cx, py = cy, pz = cz;
-      // outer ring copied (_native.pyx:240-241); NaN centre kept (:245-249)
-      if (u != 0 && u != M - 1 && v != 0 && v != N - 1 && px == px && py == py && pz == pz) {
-        double wsum = 0.0, sx = 0.0, sy = 0.0, sz = 0.0;
-        auto acc = [&](double qx, double qy, double qz, double w) {
-          if (w != 0.0) {
-            sx = dadd(sx, dmul(dsub(qx, px), w));
-            sy = dadd(sy, dmul(dsub(qy, py), w));
-            sz = dadd(sz, dmul(dsub(qz, pz), w));
-            wsum = dadd(wsum, w);
-          }
-        };
-        acc(alx, aly, alz, w_ul);  // (-1,-1)
-        acc(ax, ay, az, w_u);      // (-1, 0)
-        acc(arx, ary, arz, w_ur);  // (-1,+1)
-        acc(clx, cly, clz, w_l);   // ( 0,-1)
-        acc(crx, cry, crz, w_r);   // ( 0,+1)
-        acc(nlx, nly, nlz, w_dl);  // (+1,-1)
-        acc(nx, ny, nz, w_d);      // (+1, 0)
-        acc(nrx, nry, nrz, w_dr);  // (+1,+1)
-        if (wsum > 0.0) {
-          const double s = __ddiv_rn(lam, wsum);
-          px = dadd(px, dmul(s, sx));
-          py = dadd(py, dmul(s, sy));
-          pz = dadd(pz, dmul(s, sz));
-        }
-      }
-      double* o = dst + ((long long)u * N + v) * 3;
-      o[0] = px;
-      o[1] = py;
-      o[2] = pz;
-    }
-    // step down one row
-    w_ul = up(w_dr);
-    w_u = w_d;
-    w_ur = dn(w_dl);
-    ax = cx; ay = cy; az = cz;
-    alx = clx; aly = cly; alz = clz;
-    arx = crx; ary = cry; arz = crz;
-    cx = nx; cy = ny; cz = nz;
-    clx = nlx; cly = nly; clz = nlz;
-    crx = nrx; cry = nry; crz = nrz;
-  }
-}
-
 // ------------------------------------------------------------------ bilateral
 // centroids, normals: [F][Mq][Nq][2][3].  Output: FC layout (out_fc) or, with trimap,
 // mesh order out_mesh[f][trimap[gid]] (OUT = double or float).  Shared planes (SMEM):
@@ -920,14 +803,6 @@ int lap_tma_launch(const double* in, double* out, int F, int M, int N, double la
   return check_launch("laplacian_f64_tma_kernel");
 }
 
-int lap_walk_launch(const double* in, double* out, int F, int M, int N, double lam,
-                    cudaStream_t st) {
-  const int strips = (N + kWalkCols - 1) / kWalkCols;
-  dim3 grid((strips + kWalkWarps - 1) / kWalkWarps, (M + kWalkRows - 1) / kWalkRows, F);
-  laplacian_f64_walk_kernel<<<grid, 32 * kWalkWarps, 0, st>>>(in, out, M, N, lam);
-  return check_launch("laplacian_f64_walk_kernel");
-}
-
 // OPCFE_BIL64_TMA=0 keeps the per-thread staging of the strict k = 3 bilateral (A/B)
 static const bool g_bil64_tma = [] {
   const char* v = std::getenv("OPCFE_BIL64_TMA");
@@ -985,11 +860,6 @@ static const bool g_lap_tma = [] {
   const char* v = std::getenv("OPCFE_LAP64_TMA");
   return v == nullptr || v[0] != '0';
 }();
-// OPCFE_LAP64_WALK=0 keeps the tile kernels for k = 3 (A/B)
-static const bool g_lap_walk = [] {
-  const char* v = std::getenv("OPCFE_LAP64_WALK");
-  return v == nullptr || v[0] != '0';
-}();
 
 int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
                   int ksize, int iters, cudaStream_t st) {
@@ -1006,8 +876,7 @@ int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int 
     double* dst = to_out ? out : tmp;
     int rc;
     // k = 3 with a 16-B f64 row stride (N even): TMA-staged; otherwise per-thread loads
-    if (h == 1 && g_lap_walk) rc = lap_walk_launch(src, dst, F, M, N, lam, st);
-    else if (h == 1 && N % 2 == 0 && g_lap_tma) rc = lap_tma_launch(src, dst, F, M, N, lam, st);
+    if (h == 1 && N % 2 == 0 && g_lap_tma) rc = lap_tma_launch(src, dst, F, M, N, lam, st);
     else if (h == 1) rc = lap_launch<1, true>(src, dst, F, M, N, h, lam, st);
     else if (h == 2) rc = lap_launch<2, true>(src, dst, F, M, N, h, lam, st);
     else if (lap_smem(h) <= kSmemMax) rc = lap_launch<0, true>(src, dst, F, M, N, h, lam, st);
