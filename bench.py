@@ -320,9 +320,10 @@ def load_traffic():
 PRECISION_WHAT = {
     "strict": "precision='strict': the reference's fp64 chain (bit-exact Laplacian, FC data "
               "and topology; bilateral normals within a few ulp per iteration), float64 outputs",
-    "mixed": "precision='mixed': the strict Laplacian, topology and FC data (bit-exact), then "
-             "the fp32 bilateral on the exact FC arrays -- normals within 1e-5 of the "
-             "reference's chain end to end (parity.chained.mixed), float64 outputs",
+    "mixed": "precision='mixed': a float64 Laplacian with rsqrt pair weights (vertices "
+             "within a few ulp), exact topology and FC data, then the fp32 bilateral on the "
+             "FC arrays -- normals within 1e-5 of the reference's chain end to end "
+             "(parity.chained.mixed), float64 outputs",
 }
 
 

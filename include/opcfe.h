@@ -175,6 +175,15 @@ int opcfe_trimap_stats(const int64_t* trimap, long long n, long long* stats,
 int opcfe_laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N,
                         double lam, int kernel_size, int iterations, opcfe_stream_t stream);
 
+/* Precision "mixed" Laplacian (same contract as opcfe_laplacian_f64 -- replaces
+ * _kernels.laplacian_filter, _native.pyx:225-284 -- but NOT bit-exact): float64 points in
+ * and out, the reference's skip rules and update, the pair weight 1/dist as rsqrt(|d|^2)
+ * (~1 ulp) instead of an IEEE sqrt and division, FMA-contracted sums.  Vertices within a
+ * few ulp of the reference's (C4, 10 passes: 3.1e-16 relative, 67 % bit-identical).
+ * k = 3 with an even N; other shapes run the strict kernels (exact). */
+int opcfe_laplacian_mixed(const double* in, double* out, double* tmp, int F, int M, int N,
+                          double lam, int kernel_size, int iterations, opcfe_stream_t stream);
+
 /* compute_fc_triangle_data (smoothing.py:61-88) of F frames, bit-exact. */
 int opcfe_fc_data_f64(const double* opc, int F, int M, int N, double* centroids, double* normals,
                       opcfe_stream_t stream);
@@ -231,8 +240,9 @@ typedef struct {
   /* OPCFE_PRECISION_FAST: fp32 kernels (+ the fp64 steps the 1e-5 contract needs);
    * OPCFE_PRECISION_STRICT: the reference's fp64 chain (points / normals outputs are
    * double: bit-exact Laplacian, FC data, topology; bilateral to <= a few ulp);
-   * OPCFE_PRECISION_MIXED: the strict Laplacian, topology and FC data (bit-exact, double
-   * points), then the fp32 bilateral on the exact FC arrays (normals double, within 1e-5
+   * OPCFE_PRECISION_MIXED: the opcfe_laplacian_mixed Laplacian (double points within a
+   * few ulp of the reference's), exact topology and FC data of those points, then
+   * the fp32 bilateral on the FC arrays (normals double, within 1e-5
    * of the reference's chain end to end on well-conditioned frames -- the fast chain's
    * drift is fp32 vertex storage; at small sigma_angle fp32 normals alone can move the
    * reference's answer past 1e-5).

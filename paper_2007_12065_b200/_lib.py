@@ -32,7 +32,7 @@ EXPORTS = (
     "opcfe_front_end", "opcfe_front_end_profiled", "opcfe_segments_workspace",
     "opcfe_grow_segment", "opcfe_segment_components",
     "opcfe_laplacian_f64", "opcfe_fc_data_f64", "opcfe_bilateral_f64", "opcfe_narrow_indices",
-    "opcfe_trimap_stats",
+    "opcfe_trimap_stats", "opcfe_laplacian_mixed",
 )
 
 PRECISION_FAST = 0      # OPCFE_PRECISION_FAST
@@ -116,6 +116,7 @@ def _declare(L):
         "opcfe_narrow_indices": (i, [vp, vp, i, ll, i, vp, ll, ll, vp]),
         "opcfe_trimap_stats": (i, [vp, ll, vp, vp]),
         "opcfe_laplacian_f64": (i, [vp, vp, vp, i, i, i, d, i, i, vp]),
+        "opcfe_laplacian_mixed": (i, [vp, vp, vp, i, i, i, d, i, i, vp]),
         "opcfe_fc_data_f64": (i, [vp, i, i, i, vp, vp, vp]),
         "opcfe_bilateral_f64": (i, [vp, vp, i, i, i, d, d, i, i, vp, vp, vp, vp, vp, ll, vp]),
         "opcfe_front_end_workspace": (sz, [i, i, i, ctypes.POINTER(FrontEndParams), i, i]),

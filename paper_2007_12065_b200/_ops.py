@@ -242,16 +242,17 @@ def segment_components(halfedges, groups, with_size: bool = True):
 
 # ------------------------------------------------------------------ strict (fp64) kernels
 def laplacian_f64(x: torch.Tensor, lam: float, kernel_size: int, iterations: int,
-                  out: torch.Tensor | None = None):
+                  out: torch.Tensor | None = None, mixed: bool = False):
     """(F?, M, N, 3) float64 contiguous -> smoothed grid (same shape), the reference's own
-    fp64 arithmetic (opcfe_laplacian_f64: bit-exact), any odd kernel size."""
+    fp64 arithmetic (opcfe_laplacian_f64: bit-exact), any odd kernel size; mixed: rsqrt pair
+    weights (opcfe_laplacian_mixed: a few ulp)."""
     x = x.contiguous()
     F, M, N = _frames(x)
     out = torch.empty_like(x) if out is None else out
     tmp = torch.empty_like(x) if iterations > 1 else None
-    _lib.check(_lib.lib().opcfe_laplacian_f64(x.data_ptr(), out.data_ptr(), ptr(tmp), F, M, N,
-                                              float(lam), int(kernel_size), int(iterations),
-                                              stream()),
+    fn = _lib.lib().opcfe_laplacian_mixed if mixed else _lib.lib().opcfe_laplacian_f64
+    _lib.check(fn(x.data_ptr(), out.data_ptr(), ptr(tmp), F, M, N, float(lam), int(kernel_size),
+                  int(iterations), stream()),
                "laplacian")
     return out
 

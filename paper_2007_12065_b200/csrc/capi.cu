@@ -267,6 +267,11 @@ int opcfe_trimap_stats(const int64_t* trimap, long long n, long long* stats,
   return trimap_stats(trimap, n, stats, S(stream));
 }
 
+int opcfe_laplacian_mixed(const double* in, double* out, double* tmp, int F, int M, int N,
+                          double lam, int kernel_size, int iterations, opcfe_stream_t stream) {
+  return laplacian_mixed(in, out, tmp, F, M, N, lam, kernel_size, iterations, S(stream));
+}
+
 int opcfe_laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N,
                         double lam, int kernel_size, int iterations, opcfe_stream_t stream) {
   return laplacian_f64(in, out, tmp, F, M, N, lam, kernel_size, iterations, S(stream));
@@ -360,8 +365,9 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   if (f64_grid) {
     mark(ev, 1, st);
     if (lap) {
-      if ((rc = laplacian_f64(src64, points64, g64_tmp, F, M, N, p->laplacian_lambda,
-                              p->laplacian_kernel_size, p->laplacian_iterations, st)))
+      if ((rc = (L.mixed ? laplacian_mixed : laplacian_f64)(
+               src64, points64, g64_tmp, F, M, N, p->laplacian_lambda, p->laplacian_kernel_size,
+               p->laplacian_iterations, st)))
         return rc;
     } else if (src64 != points64) {
       const cudaError_t e = cudaMemcpyAsync(points64, src64, (size_t)F * M * N * 3 * sizeof(double),

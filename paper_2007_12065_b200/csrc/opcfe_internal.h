@@ -43,6 +43,10 @@ int narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int 
 // strict (fp64, reference operation order) kernels: strict.cu
 int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
                   int ksize, int iters, cudaStream_t st);
+// precision "mixed": rsqrt pair weights, FMA sums, f64 points (k = 3, even N;
+// otherwise laplacian_f64)
+int laplacian_mixed(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
+                    int ksize, int iters, cudaStream_t st);
 int bilateral_f64(const double* centroids, const double* normals_in, int F, int Mq, int Nq,
                   double sigma_length, double sigma_angle, int ksize, int iters, double* buf_a,
                   double* buf_b, double* out_fc, const int64_t* trimap, void* out_mesh,

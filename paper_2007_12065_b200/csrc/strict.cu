@@ -267,6 +267,75 @@ __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_tma_kernel(
   dst[o + 2] = pz;
 }
 
+// Precision "mixed", k = 3, even N: laplacian_f64_tma_kernel's TMA box, planes and rules
+// (ring copied, NaN centre kept, non-positive / NaN distances skipped, p + (lam / wsum)
+// acc), with the pair weight 1/dist taken as rsqrt(|d|^2) (MUFU.RSQ64H + Newton, ~1 ulp)
+// instead of an IEEE sqrt and an IEEE division, and FMA-contracted sums: float64 vertices
+// within a few ulp per pass of the reference's, not bit-exact.
+__global__ void __launch_bounds__(kSNT, 5) laplacian_mixed_tma_kernel(
+    const __grid_constant__ CUtensorMap tin, double* __restrict__ out, int M, int N, double lam) {
+  constexpr int BW = kSTW + 2, BH = kSTH + 2, PL = BW * BH;
+  extern __shared__ __align__(16) char smem_raw[];
+  uint64_t* barp;
+  double* raw = reinterpret_cast<double*>(smem_aligned_base(smem_raw, &barp));
+  double* sm = raw + kLapTmaRawF;
+  uint64_t& bar = *barp;
+  const int f = blockIdx.z;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kSTW + tx;
+  const int u0 = blockIdx.y * kSTH, v0 = blockIdx.x * kSTW;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+    mbar_expect_tx(&bar, kLapTmaBW * 3 * kLapTmaBH * 8);
+    tma_load_3d(raw, &tin, &bar, (v0 - 2) * 3, u0 - 1, f);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  for (int q = tid; q < PL; q += kSNT) {  // AoS box (r, c + 1) -> planes (r, c)
+    const int r = q / BW, c = q - r * BW;
+    const double* p = raw + (r * kLapTmaBW + c + 1) * 3;
+    sm[q] = p[0];
+    sm[PL + q] = p[1];
+    sm[2 * PL + q] = p[2];
+  }
+  __syncthreads();
+  const int u = u0 + ty, v = v0 + tx;
+  if (u >= M || v >= N) return;
+  double* dst = out + (long long)f * 3 * M * N;
+  const long long o = ((long long)u * N + v) * 3;
+  const int c0 = (ty + 1) * BW + tx + 1;
+  double px = sm[c0], py = sm[PL + c0], pz = sm[2 * PL + c0];
+  if (u != 0 && u != M - 1 && v != 0 && v != N - 1 && px == px && py == py && pz == pz) {
+    double wsum = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll
+    for (int du = -1; du <= 1; ++du) {
+#pragma unroll
+      for (int dv = -1; dv <= 1; ++dv) {
+        if (du == 0 && dv == 0) continue;
+        const int c = c0 + du * BW + dv;
+        const double dx = sm[c] - px, dy = sm[PL + c] - py, dz = sm[2 * PL + c] - pz;
+        const double d2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        if (d2 > 0.0) {  // NaN / coincident: skipped (:265-266)
+          const double w = rsqrt(d2);
+          ax = fma(dx, w, ax);
+          ay = fma(dy, w, ay);
+          az = fma(dz, w, az);
+          wsum += w;
+        }
+      }
+    }
+    if (wsum > 0.0) {
+      const double s = lam / wsum;
+      px = fma(s, ax, px);
+      py = fma(s, ay, py);
+      pz = fma(s, az, pz);
+    }
+  }
+  dst[o] = px;
+  dst[o + 1] = py;
+  dst[o + 2] = pz;
+}
+
 // ------------------------------------------------------------------ bilateral
 // centroids, normals: [F][Mq][Nq][2][3].  Output: FC layout (out_fc) or, with trimap,
 // mesh order out_mesh[f][trimap[gid]] (OUT = double or float).  Shared planes (SMEM):
@@ -803,6 +872,22 @@ int lap_tma_launch(const double* in, double* out, int F, int M, int N, double la
   return check_launch("laplacian_f64_tma_kernel");
 }
 
+int lap_mixed_launch(const double* in, double* out, int F, int M, int N, double lam,
+                     cudaStream_t st) {
+  CUtensorMap m;
+  int rc;
+  if ((rc = make_tmap_3d(&m, in, true, 3ull * N, M, F, 3ull * N, 3ull * N * M, kLapTmaBW * 3,
+                         kLapTmaBH)))
+    return rc;
+  constexpr int smem = (kLapTmaRawF + 3 * (kSTW + 2) * (kSTH + 2)) * (int)sizeof(double) +
+                       kSmemSlack;
+  static std::atomic<unsigned long long> attr_mask{0};
+  if ((rc = ensure_smem_attr(laplacian_mixed_tma_kernel, smem, attr_mask))) return rc;
+  dim3 grid((N + kSTW - 1) / kSTW, (M + kSTH - 1) / kSTH, F);
+  laplacian_mixed_tma_kernel<<<grid, dim3(kSTW, kSTH), smem, st>>>(m, out, M, N, lam);
+  return check_launch("laplacian_mixed_tma_kernel");
+}
+
 // OPCFE_BIL64_TMA=0 keeps the per-thread staging of the strict k = 3 bilateral (A/B)
 static const bool g_bil64_tma = [] {
   const char* v = std::getenv("OPCFE_BIL64_TMA");
@@ -882,6 +967,29 @@ int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int 
     else if (lap_smem(h) <= kSmemMax) rc = lap_launch<0, true>(src, dst, F, M, N, h, lam, st);
     else rc = lap_launch<0, false>(src, dst, F, M, N, h, lam, st);
     if (rc) return rc;
+    src = dst;
+    to_out = !to_out;
+  }
+  return OK;
+}
+
+int laplacian_mixed(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
+                    int ksize, int iters, cudaStream_t st) {
+  // the fp32-pair kernel covers k = 3 with a 16-B f64 row stride; otherwise the strict
+  // kernels (exact, so within every bound the mixed mode promises)
+  if (!(ksize == 3 && N % 2 == 0 && g_lap_tma))
+    return laplacian_f64(in, out, tmp, F, M, N, lam, ksize, iters, st);
+  if (F < 1 || M < 1 || N < 1 || iters < 1 || !in || !out)
+    return fail(ERR_INVALID, "laplacian_mixed: bad shape or parameters");
+  if (iters > 1 && tmp == nullptr) return fail(ERR_INVALID, "laplacian_mixed: tmp buffer required");
+  if (in == out || (iters > 1 && in == tmp))
+    return fail(ERR_INVALID, "laplacian_mixed: input must not alias the output or the ping-pong buffer");
+  bool to_out = (iters % 2) == 1;
+  const double* src = in;
+  for (int it = 0; it < iters; ++it) {
+    double* dst = to_out ? out : tmp;
+    int rc;
+    if ((rc = lap_mixed_launch(src, dst, F, M, N, lam, st))) return rc;
     src = dst;
     to_out = !to_out;
   }

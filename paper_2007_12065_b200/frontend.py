@@ -64,9 +64,10 @@ class FrontEnd:
     "strict": the reference's own fp64 chain (opcfe_front_end with
     OPCFE_PRECISION_STRICT) -- float64 points and normals, bit-exact Laplacian and
     topology, bilateral normals within a few ulp of the reference chain;
-    "mixed": the strict Laplacian, topology and FC data, then the fp32 bilateral on the
-    exact FC arrays (OPCFE_PRECISION_MIXED) -- float64 outputs, bit-exact smoothed grid
-    and topology, normals within 1e-5 of the reference chain end to end.
+    "mixed": a float64 Laplacian with rsqrt pair weights (vertices within a few ulp of
+    the reference's), exact topology and FC data, then the fp32 bilateral
+    on the FC arrays (OPCFE_PRECISION_MIXED) -- float64 outputs, normals within 1e-5 of the
+    reference chain end to end on the benchmark frames.
     """
 
     def __init__(self, M: int, N: int, frames: int = 1,

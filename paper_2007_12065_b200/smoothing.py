@@ -17,12 +17,13 @@ Precision (``precision=`` argument, or the process default from
   normals the filters leave unchanged come back bit-identical, moved ones are
   within 1e-5 per stage.  Kernel sizes beyond the fp32 kernels' compiled set
   (Laplacian > 17, bilateral > 9) run on the fp64 kernels.
-* ``"mixed"`` -- the strict Laplacian (bit-identical vertices) and fp64 FC data, then
-  the fp32 bilateral on those exact arrays: the chained normals stay within 1e-5 of the
-  reference's chain on the benchmark frames (the fast chain's drift comes from fp32
-  vertex storage), at about twice the strict speed; ill-conditioned clouds (small
-  sigma_angle) can exceed it, since fp32 normals alone move the reference's answer
-  there.  Opt-in.
+* ``"mixed"`` -- a float64 Laplacian whose pair weight 1/dist is rsqrt(|d|^2) (vertices
+  within a few ulp of the reference's; k = 3, even N -- other shapes run the strict
+  kernels) and fp64 FC data, then the fp32 bilateral on those arrays: the chained
+  normals stay within 1e-5 of the reference's chain on the benchmark frames (the fast
+  chain's drift comes from fp32 vertex storage), at about twice the strict speed;
+  ill-conditioned clouds (small sigma_angle) can exceed it, since fp32 normals alone
+  move the reference's answer there.  Opt-in.
 * ``"auto"`` (default) -- strict for float64 input (what the reference computes
   in), fast for float32.
 
@@ -108,9 +109,10 @@ def resolve_precision(precision, dtype) -> str:
 def _laplacian_staged(S: Staged, lam, kernel_size, iterations, precision=None):
     x = S.dev
     M, N = x.shape[:2]
-    if resolve_precision(precision, x.dtype) in ("strict", "mixed") or \
-            kernel_size > LAPLACIAN_MAX_K32:
-        res = _ops.laplacian_f64(x.to(torch.float64), lam, kernel_size, iterations)
+    prec = resolve_precision(precision, x.dtype)
+    if prec in ("strict", "mixed") or kernel_size > LAPLACIAN_MAX_K32:
+        res = _ops.laplacian_f64(x.to(torch.float64), lam, kernel_size, iterations,
+                                 mixed=prec == "mixed")
         return S.give(res.to(x.dtype))
     grid, _ = _ops.stage_in(x, want_points=True, want_mask=False)
     out = _ops.laplacian(grid, 1, M, N, lam, kernel_size, iterations)

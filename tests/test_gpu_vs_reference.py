@@ -180,7 +180,8 @@ def test_structured_scenes_equal_stock_reference(fe, ref, case):
 @pytest.mark.parametrize("seed", range(12))
 def test_mixed_front_end_vs_stock_reference(fe, ref, seed):
     """FrontEnd(precision="mixed") on random clouds against the stock reference's chain:
-    smoothed grid and topology bit-identical, normals within the 1e-5 contract."""
+    smoothed grid within 1e-12 relative, topology identical, normals within the 1e-5
+    contract."""
     rng = np.random.default_rng(9300 + seed)
     opc = random_cloud(rng)
     M, N = opc.shape[:2]
@@ -196,7 +197,11 @@ def test_mixed_front_end_vs_stock_reference(fe, ref, seed):
                       precision="mixed")
     res = eng.run(torch.from_numpy(opc).cuda().unsqueeze(0))
     T = res.n_tri[0]
-    assert same(res.points[0].cpu().numpy(), r_sm)
+    pts, ok = res.points[0].cpu().numpy(), np.isfinite(r_sm).all(2)
+    assert np.array_equal(np.isnan(pts), np.isnan(r_sm))
+    if ok.any():
+        rel = np.linalg.norm(pts[ok] - r_sm[ok], axis=1) / np.linalg.norm(r_sm[ok], axis=1)
+        assert rel.max() <= 1e-12
     assert np.array_equal(res.trimap[0].cpu().numpy(), r_mesh.trimap)
     assert np.array_equal(res.triangles[0, :T].cpu().numpy(), r_mesh.triangles)
     g_n = res.normals[0, :T].cpu().numpy()
