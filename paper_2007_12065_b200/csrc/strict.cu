@@ -816,6 +816,89 @@ __global__ void fc_mixed_kernel(const double* __restrict__ opc, int M, int N,
   }
 }
 
+// FC data, row-segment form (fc_data_f64 / fc_mixed for every shape): a warp owns 32
+// consecutive quads of one row.  Each lane loads its two points (u, v), (u + 1, v); the
+// right-hand pair comes from the next lane by shuffles (lane 31 loads its own).  The
+// arithmetic is fc_data_f64_kernel's (bit-identical); the outputs -- 6 f64 centroids and
+// 6 normals per quad, f64 or fp32 (MIXED: padded FC rows) -- are staged in shared memory
+// and written as contiguous 16-B / 8-B runs instead of 48-B-strided scalar stores (4x the
+// DRAM sectors through L2 in the per-quad kernel).
+template <bool MIXED>
+__global__ void __launch_bounds__(256) fc_rows_kernel(const double* __restrict__ opc, int M, int N,
+                                                     double* __restrict__ cen, void* __restrict__ nrm,
+                                                     int fcp) {
+  __shared__ __align__(16) double s_cen[8][32 * 6];
+  __shared__ __align__(16) double s_nrm[8][32 * 6];  // MIXED: floats in the first half
+  const int lane = threadIdx.x, w = threadIdx.y;
+  const int Nq = N - 1, Mq = M - 1;
+  const int u = blockIdx.y * 8 + w;
+  const int v0 = blockIdx.x * 32, v = v0 + lane;
+  const int f = blockIdx.z;
+  if (u >= Mq) return;  // warp-uniform
+  const int nseg = min(32, Nq - v0);
+  const double* row0 = opc + ((long long)f * M + u) * N * 3;
+  const double* row1 = row0 + (long long)N * 3;
+  double a[3], b[3];  // (u, v), (u + 1, v)
+  if (v < N) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      a[j] = __ldg(row0 + 3ll * v + j);
+      b[j] = __ldg(row1 + 3ll * v + j);
+    }
+  }
+  double a2[3], b2[3];  // (u, v + 1), (u + 1, v + 1)
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    a2[j] = __shfl_down_sync(0xffffffffu, a[j], 1);
+    b2[j] = __shfl_down_sync(0xffffffffu, b[j], 1);
+  }
+  if (lane == 31 && v + 1 < N) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      a2[j] = __ldg(row0 + 3ll * (v + 1) + j);
+      b2[j] = __ldg(row1 + 3ll * (v + 1) + j);
+    }
+  }
+  if (lane < nseg) {
+    // p1 = (u, v), p2 = (u, v + 1), p3 = (u + 1, v + 1), p4 = (u + 1, v): (p3, p2, p1), (p1, p4, p3)
+    const double* tri[2][3] = {{b2, a2, a}, {a, b, b2}};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const double *A = tri[k][0], *B = tri[k][1], *C = tri[k][2];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) s_cen[w][lane * 6 + 3 * k + j] = centroid_f64(A[j], B[j], C[j]);
+      double nx, ny, nz;
+      unit_normal_f64(A[0], A[1], A[2], B[0], B[1], B[2], C[0], C[1], C[2], nx, ny, nz);
+      if (MIXED) {
+        float* sn = reinterpret_cast<float*>(s_nrm[w]) + lane * 6 + 3 * k;
+        sn[0] = (float)nx;
+        sn[1] = (float)ny;
+        sn[2] = (float)nz;
+      } else {
+        double* sn = s_nrm[w] + lane * 6 + 3 * k;
+        sn[0] = nx;
+        sn[1] = ny;
+        sn[2] = nz;
+      }
+    }
+  }
+  __syncwarp();
+  const long long qb = (long long)f * Mq * Nq + (long long)u * Nq + v0;  // first quad of the run
+  double2* gc = reinterpret_cast<double2*>(cen + qb * 6);
+  const double2* sc = reinterpret_cast<const double2*>(s_cen[w]);
+  for (int i = lane; i < nseg * 3; i += 32) gc[i] = sc[i];
+  if (MIXED) {
+    float2* gn = reinterpret_cast<float2*>(static_cast<float*>(nrm) +
+                                           ((long long)f * Mq + u) * fcp + 6ll * v0);
+    const float2* sn = reinterpret_cast<const float2*>(s_nrm[w]);
+    for (int i = lane; i < nseg * 3; i += 32) gn[i] = sn[i];
+  } else {
+    double2* gn = reinterpret_cast<double2*>(static_cast<double*>(nrm) + qb * 6);
+    const double2* sn = reinterpret_cast<const double2*>(s_nrm[w]);
+    for (int i = lane; i < nseg * 3; i += 32) gn[i] = sn[i];
+  }
+}
+
 // mesh normals / l_max flags of F frames: frame f's triangles are rows f*G .. f*G+n_tri[f]
 // of `tris` (vertex indices local to the frame), points [F][P][3] f64.
 template <typename OUT>
@@ -1069,9 +1152,21 @@ int bilateral_f64(const double* centroids, const double* normals_in, int F, int 
   return OK;
 }
 
+// OPCFE_FC_ROWS=0 keeps the per-quad FC-data kernels (A/B)
+static const bool g_fc_rows = [] {
+  const char* v = std::getenv("OPCFE_FC_ROWS");
+  return v == nullptr || v[0] != '0';
+}();
+
 int fc_data_f64(const double* opc, int F, int M, int N, double* cen, double* nrm,
                 cudaStream_t st) {
   if (F < 1 || M < 2 || N < 2) return fail(ERR_INVALID, "organized cloud must be at least 2 x 2");
+  if (g_fc_rows && reinterpret_cast<uintptr_t>(cen) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(nrm) % 16 == 0) {
+    dim3 grid((N - 1 + 31) / 32, (M - 1 + 7) / 8, F);
+    fc_rows_kernel<false><<<grid, dim3(32, 8), 0, st>>>(opc, M, N, cen, nrm, 0);
+    return check_launch("fc_rows_kernel");
+  }
   const long long Q = (long long)(M - 1) * (N - 1);
   fc_data_f64_kernel<<<dim3(nblk(Q, 256), F), 256, 0, st>>>(opc, M, N, cen, nrm);
   return check_launch("fc_data_f64_kernel");
@@ -1080,6 +1175,12 @@ int fc_data_f64(const double* opc, int F, int M, int N, double* cen, double* nrm
 int fc_mixed(const double* opc, int F, int M, int N, double* cen, float* nrm32, int fcp,
              cudaStream_t st) {
   if (F < 1 || M < 2 || N < 2) return fail(ERR_INVALID, "organized cloud must be at least 2 x 2");
+  if (g_fc_rows && reinterpret_cast<uintptr_t>(cen) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(nrm32) % 16 == 0 && fcp % 4 == 0) {
+    dim3 grid((N - 1 + 31) / 32, (M - 1 + 7) / 8, F);
+    fc_rows_kernel<true><<<grid, dim3(32, 8), 0, st>>>(opc, M, N, cen, nrm32, fcp);
+    return check_launch("fc_rows_kernel");
+  }
   const long long Q = (long long)(M - 1) * (N - 1);
   fc_mixed_kernel<<<dim3(nblk(Q, 256), F), 256, 0, st>>>(opc, M, N, cen, nrm32, fcp);
   return check_launch("fc_mixed_kernel");
