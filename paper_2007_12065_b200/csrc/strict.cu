@@ -198,14 +198,20 @@ __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_kernel(const double* __
 // (a 16-B aligned start: 2 x 24 B) and is 36 points wide.
 // RPT rows per thread: the tile is 32 x (8 RPT) points, thread (tx, ty) computes rows ty,
 // ty + 8, ... (independent chains; the halo and the staging amortised over RPT times the
-// points).
-template <int RPT>
+// points).  The smoothed tile is staged in the (then dead) raw box and leaves by one TMA
+// store (the grid edge clipped by the tensor map) instead of 24-B-strided scalar stores.
+// MIXED (precision "mixed"): the pair weight 1/dist is rsqrt(|d|^2) (MUFU.RSQ64H + Newton,
+// ~1 ulp) instead of an IEEE sqrt and an IEEE division, and the sums are FMA-contracted:
+// float64 vertices within a few ulp per pass of the reference's, not bit-exact.
+template <int RPT, bool MIXED>
 __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_tma_kernel(
-    const __grid_constant__ CUtensorMap tin, double* __restrict__ out, int M, int N, double lam) {
+    const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, int M,
+    int N, double lam) {
   constexpr int TH = kSTH * RPT;
   constexpr int BXW = kSTW + 4, BXH = TH + 2;  // TMA box (points)
   constexpr int RAWF = (BXW * 3 * BXH * 8 + 127) / 128 * 128 / 8;
   constexpr int BW = kSTW + 2, PL = BW * BXH;
+  static_assert(kSTW * 3 * TH <= RAWF, "the output tile reuses the raw box");
   extern __shared__ __align__(16) char smem_raw[];
   uint64_t* barp;
   double* raw = reinterpret_cast<double*>(smem_aligned_base(smem_raw, &barp));
@@ -229,18 +235,14 @@ __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_tma_kernel(
     sm[PL + q] = p[1];
     sm[2 * PL + q] = p[2];
   }
-  __syncthreads();
+  __syncthreads();  // raw is dead from here: the output tile [TH][32][3]
   const int v = v0 + tx;
-  if (v >= N) return;
-  double* dst = out + (long long)f * 3 * M * N;
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
     const int ty_k = ty + k * kSTH, u = u0 + ty_k;
-    if (u >= M) break;
-    const long long o = ((long long)u * N + v) * 3;
     const int c0 = (ty_k + 1) * BW + tx + 1;
     double px = sm[c0], py = sm[PL + c0], pz = sm[2 * PL + c0];
-    if (u != 0 && u != M - 1 && v != 0 && v != N - 1 && px == px && py == py && pz == pz) {
+    if (u > 0 && u < M - 1 && v > 0 && v < N - 1 && px == px && py == py && pz == pz) {
       double wsum = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
 #pragma unroll
       for (int du = -1; du <= 1; ++du) {
@@ -248,106 +250,53 @@ __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_tma_kernel(
         for (int dv = -1; dv <= 1; ++dv) {
           if (du == 0 && dv == 0) continue;
           const int c = c0 + du * BW + dv;
-          const double dx = dsub(sm[c], px), dy = dsub(sm[PL + c], py), dz = dsub(sm[2 * PL + c], pz);
-          const double dist = __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
-          if (!(dist > 0.0)) continue;  // NaN or <= 0 (:265-266)
-          const double w = __drcp_rn(dist);
-          ax = dadd(ax, dmul(dx, w));
-          ay = dadd(ay, dmul(dy, w));
-          az = dadd(az, dmul(dz, w));
-          wsum = dadd(wsum, w);
-        }
-      }
-      if (wsum > 0.0) {
-        const double s = __ddiv_rn(lam, wsum);
-        px = dadd(px, dmul(s, ax));
-        py = dadd(py, dmul(s, ay));
-        pz = dadd(pz, dmul(s, az));
-      }
-    }
-    dst[o] = px;
-    dst[o + 1] = py;
-    dst[o + 2] = pz;
-  }
-}
-
-// Precision "mixed", k = 3, even N: laplacian_f64_tma_kernel's TMA box, planes and rules
-// (ring copied, NaN centre kept, non-positive / NaN distances skipped, p + (lam / wsum)
-// acc), with the pair weight 1/dist taken as rsqrt(|d|^2) (MUFU.RSQ64H + Newton, ~1 ulp)
-// instead of an IEEE sqrt and an IEEE division, and FMA-contracted sums: float64 vertices
-// within a few ulp per pass of the reference's, not bit-exact.
-// RPT rows per thread: the tile is 32 x (8 RPT) points, thread (tx, ty) computes rows ty,
-// ty + 8, ... (independent chains; the halo amortised over RPT times the points).
-template <int RPT>
-__global__ void __launch_bounds__(kSNT, 5) laplacian_mixed_tma_kernel(
-    const __grid_constant__ CUtensorMap tin, double* __restrict__ out, int M, int N, double lam) {
-  constexpr int TH = kSTH * RPT;
-  constexpr int BXW = kSTW + 4, BXH = TH + 2;  // TMA box (points)
-  constexpr int RAWF = (BXW * 3 * BXH * 8 + 127) / 128 * 128 / 8;
-  constexpr int BW = kSTW + 2, PL = BW * BXH;
-  extern __shared__ __align__(16) char smem_raw[];
-  uint64_t* barp;
-  double* raw = reinterpret_cast<double*>(smem_aligned_base(smem_raw, &barp));
-  double* sm = raw + RAWF;
-  uint64_t& bar = *barp;
-  const int f = blockIdx.z;
-  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kSTW + tx;
-  const int u0 = blockIdx.y * TH, v0 = blockIdx.x * kSTW;
-  if (tid == 0) {
-    mbar_init(&bar, 1);
-    fence_mbar_init();
-    mbar_expect_tx(&bar, BXW * 3 * BXH * 8);
-    tma_load_3d(raw, &tin, &bar, (v0 - 2) * 3, u0 - 1, f);
-  }
-  __syncthreads();
-  mbar_wait(&bar, 0);
-  for (int q = tid; q < PL; q += kSNT) {  // AoS box (r, c + 1) -> planes (r, c)
-    const int r = q / BW, c = q - r * BW;
-    const double* p = raw + (r * BXW + c + 1) * 3;
-    sm[q] = p[0];
-    sm[PL + q] = p[1];
-    sm[2 * PL + q] = p[2];
-  }
-  __syncthreads();
-  const int v = v0 + tx;
-  if (v >= N) return;
-  double* dst = out + (long long)f * 3 * M * N;
-#pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int ty_k = ty + k * kSTH, u = u0 + ty_k;
-    if (u >= M) break;
-    const long long o = ((long long)u * N + v) * 3;
-    const int c0 = (ty_k + 1) * BW + tx + 1;
-    double px = sm[c0], py = sm[PL + c0], pz = sm[2 * PL + c0];
-    if (u != 0 && u != M - 1 && v != 0 && v != N - 1 && px == px && py == py && pz == pz) {
-      double wsum = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
-#pragma unroll
-      for (int du = -1; du <= 1; ++du) {
-#pragma unroll
-        for (int dv = -1; dv <= 1; ++dv) {
-          if (du == 0 && dv == 0) continue;
-          const int c = c0 + du * BW + dv;
-          const double dx = sm[c] - px, dy = sm[PL + c] - py, dz = sm[2 * PL + c] - pz;
-          const double d2 = fma(dz, dz, fma(dy, dy, dx * dx));
-          if (d2 > 0.0) {  // NaN / coincident: skipped (:265-266)
-            const double w = rsqrt(d2);
-            ax = fma(dx, w, ax);
-            ay = fma(dy, w, ay);
-            az = fma(dz, w, az);
-            wsum += w;
+          if constexpr (MIXED) {
+            const double dx = sm[c] - px, dy = sm[PL + c] - py, dz = sm[2 * PL + c] - pz;
+            const double d2 = fma(dz, dz, fma(dy, dy, dx * dx));
+            if (d2 > 0.0) {  // NaN / coincident: skipped (:265-266)
+              const double w = rsqrt(d2);
+              ax = fma(dx, w, ax);
+              ay = fma(dy, w, ay);
+              az = fma(dz, w, az);
+              wsum += w;
+            }
+          } else {
+            const double dx = dsub(sm[c], px), dy = dsub(sm[PL + c], py),
+                         dz = dsub(sm[2 * PL + c], pz);
+            const double dist = __dsqrt_rn(dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)));
+            if (!(dist > 0.0)) continue;  // NaN or <= 0 (:265-266)
+            const double w = __drcp_rn(dist);
+            ax = dadd(ax, dmul(dx, w));
+            ay = dadd(ay, dmul(dy, w));
+            az = dadd(az, dmul(dz, w));
+            wsum = dadd(wsum, w);
           }
         }
       }
       if (wsum > 0.0) {
-        const double s = lam / wsum;
-        px = fma(s, ax, px);
-        py = fma(s, ay, py);
-        pz = fma(s, az, pz);
+        if constexpr (MIXED) {
+          const double s = lam / wsum;
+          px = fma(s, ax, px);
+          py = fma(s, ay, py);
+          pz = fma(s, az, pz);
+        } else {
+          const double s = __ddiv_rn(lam, wsum);
+          px = dadd(px, dmul(s, ax));
+          py = dadd(py, dmul(s, ay));
+          pz = dadd(pz, dmul(s, az));
+        }
       }
     }
-    dst[o] = px;
-    dst[o + 1] = py;
-    dst[o + 2] = pz;
+    double* o = raw + (ty_k * kSTW + tx) * 3;  // ring / NaN / off-grid cells: the input value
+    o[0] = px;
+    o[1] = py;
+    o[2] = pz;
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (tid == 0) {
+    tma_store_3d(&tout, raw, v0 * 3, u0, f);
+    tma_store_commit_and_wait();
   }
 }
 
@@ -954,54 +903,37 @@ int lap_launch(const double* in, double* out, int F, int M, int N, int h, double
   return check_launch("laplacian_f64_kernel");
 }
 
-template <int RPT>
+template <int RPT, bool MIXED>
 int lap_tma_launch_t(const double* in, double* out, int F, int M, int N, double lam,
                      cudaStream_t st) {
   constexpr int TH = kSTH * RPT, BXH = TH + 2;
   constexpr int RAWF = ((kSTW + 4) * 3 * BXH * 8 + 127) / 128 * 128 / 8;
-  CUtensorMap m;
+  CUtensorMap mi, mo;
   int rc;
-  if ((rc = make_tmap_3d(&m, in, true, 3ull * N, M, F, 3ull * N, 3ull * N * M, (kSTW + 4) * 3,
-                         BXH)))
+  if ((rc = make_tmap_3d(&mi, in, true, 3ull * N, M, F, 3ull * N, 3ull * N * M, (kSTW + 4) * 3,
+                         BXH)) ||
+      (rc = make_tmap_3d(&mo, out, true, 3ull * N, M, F, 3ull * N, 3ull * N * M, kSTW * 3, TH)))
     return rc;
   constexpr int smem = (RAWF + 3 * (kSTW + 2) * BXH) * (int)sizeof(double) + kSmemSlack;
   static std::atomic<unsigned long long> attr_mask{0};
-  if ((rc = ensure_smem_attr(laplacian_f64_tma_kernel<RPT>, smem, attr_mask))) return rc;
+  auto kern = laplacian_f64_tma_kernel<RPT, MIXED>;
+  if ((rc = ensure_smem_attr(kern, smem, attr_mask))) return rc;
   dim3 grid((N + kSTW - 1) / kSTW, (M + TH - 1) / TH, F);
-  laplacian_f64_tma_kernel<RPT><<<grid, dim3(kSTW, kSTH), smem, st>>>(m, out, M, N, lam);
+  kern<<<grid, dim3(kSTW, kSTH), smem, st>>>(mi, mo, M, N, lam);
   return check_launch("laplacian_f64_tma_kernel");
 }
 
-// three rows per thread (32 x 24-point tiles): 6.74 ms per 10 strict C4 passes x 16 frames
-// against 6.79 (two rows) and 7.07 (one)
+// three rows per thread (32 x 24-point tiles): strict 6.74 ms per 10 C4 passes x 16 frames
+// against 6.79 (two rows) and 7.07 (one); mixed 4.49 against 4.56 / 4.85 (four rows, 3
+// CTAs / SM: 5.26)
 int lap_tma_launch(const double* in, double* out, int F, int M, int N, double lam,
                    cudaStream_t st) {
-  return lap_tma_launch_t<3>(in, out, F, M, N, lam, st);
+  return lap_tma_launch_t<3, false>(in, out, F, M, N, lam, st);
 }
 
-template <int RPT>
-int lap_mixed_launch_t(const double* in, double* out, int F, int M, int N, double lam,
-                       cudaStream_t st) {
-  constexpr int TH = kSTH * RPT, BXH = TH + 2;
-  constexpr int RAWF = ((kSTW + 4) * 3 * BXH * 8 + 127) / 128 * 128 / 8;
-  CUtensorMap m;
-  int rc;
-  if ((rc = make_tmap_3d(&m, in, true, 3ull * N, M, F, 3ull * N, 3ull * N * M, (kSTW + 4) * 3,
-                         BXH)))
-    return rc;
-  constexpr int smem = (RAWF + 3 * (kSTW + 2) * BXH) * (int)sizeof(double) + kSmemSlack;
-  static std::atomic<unsigned long long> attr_mask{0};
-  if ((rc = ensure_smem_attr(laplacian_mixed_tma_kernel<RPT>, smem, attr_mask))) return rc;
-  dim3 grid((N + kSTW - 1) / kSTW, (M + TH - 1) / TH, F);
-  laplacian_mixed_tma_kernel<RPT><<<grid, dim3(kSTW, kSTH), smem, st>>>(m, out, M, N, lam);
-  return check_launch("laplacian_mixed_tma_kernel");
-}
-
-// three rows per thread (32 x 24-point tiles, 5 CTAs / SM): 4.49 ms per 10 C4 passes x 16
-// frames against 4.56 (two rows), 4.85 (one) and 5.26 (four: 3 CTAs / SM)
 int lap_mixed_launch(const double* in, double* out, int F, int M, int N, double lam,
                      cudaStream_t st) {
-  return lap_mixed_launch_t<3>(in, out, F, M, N, lam, st);
+  return lap_tma_launch_t<3, true>(in, out, F, M, N, lam, st);
 }
 
 // OPCFE_BIL64_TMA=0 keeps the per-thread staging of the strict k = 3 bilateral (A/B)
