@@ -269,6 +269,9 @@ int stage_in(const void* src, bool f64, long long rs, long long fs, int F, int M
 int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st) {
   if (M < 2 || N < 2) return fail(ERR_INVALID, "organized cloud must be at least 2 x 2");
   const long long Q = (long long)(M - 1) * (N - 1);
+  if (f64 && reinterpret_cast<uintptr_t>(cen) % 16 == 0 && reinterpret_cast<uintptr_t>(nrm) % 16 == 0)
+    return fc_data_f64(static_cast<const double*>(opc), 1, M, N, static_cast<double*>(cen),
+                       static_cast<double*>(nrm), st);  // the row-segment kernel, same bits
   if (f64)
     fc_data_kernel<double><<<blocks_for(Q, 256), 256, 0, st>>>(
         static_cast<const double*>(opc), M, N, static_cast<double*>(cen), static_cast<double*>(nrm));
