@@ -39,6 +39,7 @@ METRICS = [
     "sm__warps_active.avg.per_cycle_active", "launch__registers_per_thread",
     "launch__occupancy_limit_shared_mem", "smsp__inst_executed.sum",
     "lts__t_bytes.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 
 
