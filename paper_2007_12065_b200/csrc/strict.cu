@@ -765,6 +765,34 @@ __global__ void fc_mixed_kernel(const double* __restrict__ opc, int M, int N,
   }
 }
 
+// OPCFE_FC_FAST=0 keeps the IEEE-exact FC arithmetic in the mixed FC data (A/B)
+static const bool g_fc_fast_host = [] {
+  const char* v = std::getenv("OPCFE_FC_FAST");
+  return v == nullptr || v[0] != '0';
+}();
+
+// cross(b - a, c - a) * rsqrt(|.|^2) (~1.5 ulp), NaN unless |.|^2 > 0.  The cross
+// product and its squared norm keep the reference's uncontracted operations, so the
+// degenerate (NaN) set is exactly the reference's; only sqrt + 3 divisions become rsqrt.
+__device__ __forceinline__ void fast_unit_normal_f64(const double* a, const double* b,
+                                                     const double* c, double& nx, double& ny,
+                                                     double& nz) {
+  const double e1x = dsub(b[0], a[0]), e1y = dsub(b[1], a[1]), e1z = dsub(b[2], a[2]);
+  const double e2x = dsub(c[0], a[0]), e2y = dsub(c[1], a[1]), e2z = dsub(c[2], a[2]);
+  const double x = dsub(dmul(e1y, e2z), dmul(e1z, e2y));
+  const double y = dsub(dmul(e1z, e2x), dmul(e1x, e2z));
+  const double z = dsub(dmul(e1x, e2y), dmul(e1y, e2x));
+  const double r2 = dadd(dadd(dmul(x, x), dmul(y, y)), dmul(z, z));
+  if (r2 > 0.0) {
+    const double r = rsqrt(r2);
+    nx = x * r;
+    ny = y * r;
+    nz = z * r;
+  } else {
+    nx = ny = nz = __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
 // FC data, row-segment form (fc_data_f64 / fc_mixed for every shape): a warp owns 32
 // consecutive quads of one row.  Each lane loads its two points (u, v), (u + 1, v); the
 // right-hand pair comes from the next lane by shuffles (lane 31 loads its own).  The
@@ -775,7 +803,7 @@ __global__ void fc_mixed_kernel(const double* __restrict__ opc, int M, int N,
 template <bool MIXED>
 __global__ void __launch_bounds__(256) fc_rows_kernel(const double* __restrict__ opc, int M, int N,
                                                      double* __restrict__ cen, void* __restrict__ nrm,
-                                                     int fcp) {
+                                                     int fcp, bool fast) {
   __shared__ __align__(16) double s_cen[8][32 * 6];
   __shared__ __align__(16) double s_nrm[8][32 * 6];  // MIXED: floats in the first half
   const int lane = threadIdx.x, w = threadIdx.y;
@@ -814,10 +842,20 @@ __global__ void __launch_bounds__(256) fc_rows_kernel(const double* __restrict__
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
       const double *A = tri[k][0], *B = tri[k][1], *C = tri[k][2];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) s_cen[w][lane * 6 + 3 * k + j] = centroid_f64(A[j], B[j], C[j]);
       double nx, ny, nz;
-      unit_normal_f64(A[0], A[1], A[2], B[0], B[1], B[2], C[0], C[1], C[2], nx, ny, nz);
+      if (MIXED && fast) {
+        // the fp32 bilateral reads these through fp32 (normals) / tile-relative fp32
+        // (centroids): a 1-ulp fp64 rsqrt and a product by 1/3 change nothing there but
+        // the rare double rounding, at a fraction of the IEEE divisions' cost
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          s_cen[w][lane * 6 + 3 * k + j] = (A[j] + B[j] + C[j]) * (1.0 / 3.0);
+        fast_unit_normal_f64(A, B, C, nx, ny, nz);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) s_cen[w][lane * 6 + 3 * k + j] = centroid_f64(A[j], B[j], C[j]);
+        unit_normal_f64(A[0], A[1], A[2], B[0], B[1], B[2], C[0], C[1], C[2], nx, ny, nz);
+      }
       if (MIXED) {
         float* sn = reinterpret_cast<float*>(s_nrm[w]) + lane * 6 + 3 * k;
         sn[0] = (float)nx;
@@ -1096,7 +1134,7 @@ int fc_data_f64(const double* opc, int F, int M, int N, double* cen, double* nrm
   if (g_fc_rows && reinterpret_cast<uintptr_t>(cen) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(nrm) % 16 == 0) {
     dim3 grid((N - 1 + 31) / 32, (M - 1 + 7) / 8, F);
-    fc_rows_kernel<false><<<grid, dim3(32, 8), 0, st>>>(opc, M, N, cen, nrm, 0);
+    fc_rows_kernel<false><<<grid, dim3(32, 8), 0, st>>>(opc, M, N, cen, nrm, 0, false);
     return check_launch("fc_rows_kernel");
   }
   const long long Q = (long long)(M - 1) * (N - 1);
@@ -1110,7 +1148,8 @@ int fc_mixed(const double* opc, int F, int M, int N, double* cen, float* nrm32, 
   if (g_fc_rows && reinterpret_cast<uintptr_t>(cen) % 16 == 0 &&
       reinterpret_cast<uintptr_t>(nrm32) % 16 == 0 && fcp % 4 == 0) {
     dim3 grid((N - 1 + 31) / 32, (M - 1 + 7) / 8, F);
-    fc_rows_kernel<true><<<grid, dim3(32, 8), 0, st>>>(opc, M, N, cen, nrm32, fcp);
+    fc_rows_kernel<true><<<grid, dim3(32, 8), 0, st>>>(opc, M, N, cen, nrm32, fcp,
+                                                          g_fc_fast_host);
     return check_launch("fc_rows_kernel");
   }
   const long long Q = (long long)(M - 1) * (N - 1);
