@@ -74,7 +74,8 @@ constexpr int bil_min_blocks(int h) { return h == 1 ? OPCFE_BIL_BLOCKS3 : (h == 
 enum BilMode : int {
   kFromPoints = 0,     // iteration 1: normals + centroids from the point grid
   kNormalsBuf = 1,     // normals from the previous iteration, centroids from points
-  kNormalsCentBuf = 2  // normals and centroids from FC arrays (drop-in bilateral_iterate)
+  kNormalsCentBuf = 2,  // normals and centroids from FC arrays (drop-in bilateral_iterate)
+  kFromPoints64 = 3     // fused iteration 1 of the mixed front end: FC data from the f64 grid
 };
 
 template <int H>
@@ -114,6 +115,7 @@ struct BilTile {
 template <int H, int MODE>
 constexpr int bil_smem_bytes() {
   using T = BilTile<H>;
+  if constexpr (MODE == kFromPoints64) return (2 * T::PTS_F + T::PACK_F) * 4 + kSmemSlack;
   return (((MODE != kNormalsCentBuf) ? T::PTS_F : 0) + ((MODE != kFromPoints) ? T::FC_F : 0) +
           ((MODE == kNormalsCentBuf) ? 2 * T::FC_F : 0) + T::PACK_F +  // f64 centroid tile
           ((MODE == kFromPoints) ? T::OUT_F : 0)) *
@@ -166,6 +168,22 @@ __device__ __forceinline__ auto tile_origin(const S* v, int count, int stride, i
   else
     return i == 0x7fffffff ? make_float3(0.f, 0.f, 0.f)
                            : make_float3(v[i * stride], v[i * stride + 1], v[i * stride + 2]);
+}
+
+// centroid of triangle k of pack quad (r, c) from the f64 point box (mode 3): the mixed FC
+// data's ((a + b) + c) * (1/3), triangles (p3, p2, p1) and (p1, p4, p3)
+template <int H>
+__device__ __forceinline__ void fc64_centroid_t(const double* pts, int r, int c, int k, double* out) {
+  using T = BilTile<H>;
+  const double* P1 = pts + (r * T::PW + c + T::PSHIFT) * 3;
+  const double* P2 = P1 + 3;
+  const double* P4 = P1 + T::PW * 3;
+  const double* P3 = P4 + 3;
+  const double* A = k == 0 ? P3 : P1;
+  const double* B = k == 0 ? P2 : P4;
+  const double* C = k == 0 ? P1 : P3;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) out[j] = mixed_centroid(A[j], B[j], C[j]);
 }
 
 // FC normals of a quad's two triangles (p3, p2, p1) and (p1, p4, p3) for the bilateral
@@ -471,15 +489,18 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
                      const __grid_constant__ CUtensorMap tcen, const __grid_constant__ CUtensorMap tout,
                      BilArgs a, PackedG pg) {
   using T = BilTile<H>;
-  static_assert(!PACKOUT || (MODE != kNormalsBuf && !SCATTER), "PACKOUT: mode 0 / 2, no scatter");
+  static_assert(!PACKOUT || (MODE != kNormalsBuf && !SCATTER), "PACKOUT: mode 0 / 2 / 3, no scatter");
+  static_assert(MODE != kFromPoints64 || PACKOUT, "mode 3 is the fused pipeline's iteration 1");
+  constexpr bool P64 = MODE == kFromPoints64;
   extern __shared__ __align__(16) char smem_raw[];
   uint64_t* barp;
   float* p = reinterpret_cast<float*>(smem_aligned_base(smem_raw, &barp));
   float* pts_s = nullptr;
   float* nrm_s = nullptr;
   float* cen_s = nullptr;
-  if (MODE != kNormalsCentBuf) { pts_s = p; p += T::PTS_F; }
-  if (MODE != kFromPoints) { nrm_s = p; p += T::FC_F; }
+  if (MODE != kNormalsCentBuf) { pts_s = p; p += (P64 ? 2 : 1) * T::PTS_F; }
+  if (MODE != kFromPoints && !P64) { nrm_s = p; p += T::FC_F; }
+  const double* pts_d = reinterpret_cast<const double*>(pts_s);  // mode 3: the f64 point box
   if (MODE == kNormalsCentBuf) { cen_s = p; p += 2 * T::FC_F; }  // float64 centroid tile
   const double* cen_d = reinterpret_cast<const double*>(cen_s);
   const Planes P = planes_at<H>(p);
@@ -495,12 +516,12 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     mbar_init(&bar, 1);
     fence_mbar_init();
     uint32_t bytes = 0;
-    if (MODE != kNormalsCentBuf) bytes += T::PW * 3 * T::PH * 4;
-    if (MODE != kFromPoints) bytes += T::QW * 6 * T::QH * 4;
+    if (MODE != kNormalsCentBuf) bytes += T::PW * 3 * T::PH * (P64 ? 8 : 4);
+    if (MODE != kFromPoints && !P64) bytes += T::QW * 6 * T::QH * 4;
     if (MODE == kNormalsCentBuf) bytes += T::QW * 6 * T::QH * 8;
     mbar_expect_tx(&bar, bytes);
     if (MODE != kNormalsCentBuf) tma_load_3d(pts_s, &tpts, &bar, (q0 - T::LP) * 3, u0 - H, f);
-    if (MODE != kFromPoints) tma_load_3d(nrm_s, &tnrm, &bar, (q0 - T::LQ) * 6, u0 - H, f);
+    if (MODE != kFromPoints && !P64) tma_load_3d(nrm_s, &tnrm, &bar, (q0 - T::LQ) * 6, u0 - H, f);
     if (MODE == kNormalsCentBuf) tma_load_3d(cen_s, &tcen, &bar, (q0 - T::LQ) * 6, u0 - H, f);
   }
   __syncthreads();  // barrier initialised (and its loads issued) before anyone waits
@@ -518,6 +539,31 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
     od = make_double3(cp[0], cp[1], cp[2]);
     if (!(isfinite(od.x) && isfinite(od.y) && isfinite(od.z)))
       od = tile_origin<kBilNT>(cen_d, T::QW * T::QH * 2, 3, &s_first);
+  } else if constexpr (P64) {
+    // the same origin mode 2 takes from the FC arrays: the centroid of the box's centre
+    // quad's triangle 0, else the first finite box centroid in (quad, triangle) order
+    double c[3];
+    fc64_centroid_t<H>(pts_d, T::QH / 2, T::QW / 2, 0, c);
+    od = make_double3(c[0], c[1], c[2]);
+    if (!(isfinite(od.x) && isfinite(od.y) && isfinite(od.z))) {
+      if (threadIdx.x == 0) s_first = 0x7fffffff;
+      __syncthreads();
+      for (int i = threadIdx.x; i < T::QW * T::QH * 2; i += kBilNT) {
+        fc64_centroid_t<H>(pts_d, (i / 2) / T::QW, (i / 2) % T::QW, i % 2, c);
+        if (isfinite(c[0]) && isfinite(c[1]) && isfinite(c[2])) {
+          atomicMin(&s_first, i);
+          break;
+        }
+      }
+      __syncthreads();
+      const int i = s_first;
+      if (i == 0x7fffffff) {
+        od = make_double3(0.0, 0.0, 0.0);
+      } else {
+        fc64_centroid_t<H>(pts_d, (i / 2) / T::QW, (i / 2) % T::QW, i % 2, c);
+        od = make_double3(c[0], c[1], c[2]);
+      }
+    }
   } else {
     const float* cp = pts_s + ((T::PH / 2) * T::PW + T::PW / 2) * 3;
     o = make_float3(cp[0], cp[1], cp[2]);
@@ -542,6 +588,28 @@ __global__ void __launch_bounds__(kBilNT, bil_min_blocks(H))
         n[j] = nrm_s[q * 6 + j];
         const double oj = j % 3 == 0 ? od.x : (j % 3 == 1 ? od.y : od.z);
         cc[j] = (float)((cen_d[q * 6 + j] - oj) * (double)sA);
+      }
+    } else if constexpr (P64) {
+      // fc_rows_kernel<true>'s arithmetic (mixed FC data), bit for bit, from the box
+      const double* P1 = pts_d + (r * T::PW + c + T::PSHIFT) * 3;
+      const double* P2 = P1 + 3;
+      const double* P4 = P1 + T::PW * 3;
+      const double* P3 = P4 + 3;
+      const double* tri[2][3] = {{P3, P2, P1}, {P1, P4, P3}};
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double *A = tri[k][0], *B = tri[k][1], *Cc = tri[k][2];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const double oj = j == 0 ? od.x : (j == 1 ? od.y : od.z);
+          const double cen = mixed_centroid(A[j], B[j], Cc[j]);
+          cc[3 * k + j] = (float)((cen - oj) * (double)sA);
+        }
+        double nx, ny, nz;
+        fast_unit_normal_f64(A, B, Cc, nx, ny, nz);
+        n[3 * k] = (float)nx;
+        n[3 * k + 1] = (float)ny;
+        n[3 * k + 2] = (float)nz;
       }
     } else {
       const float* P1 = pts_s + (r * T::PW + c + T::PSHIFT) * 3;
@@ -821,6 +889,18 @@ int launch_packout_arrays_h(int h, const CUtensorMap& tn, const CUtensorMap& tc,
   }
 }
 
+// iteration 1 of the fused pipeline from the f64 point grid (the mixed front end, even N)
+int launch_packout_pts64_h(int h, const CUtensorMap& tp, const BilArgs& a, int F,
+                           const PackedG& pg, cudaStream_t st) {
+  switch (h) {
+    case 1: return launch_bil<1, kFromPoints64, false, true>(tp, tp, tp, tp, a, F, st, pg);
+    case 2: return launch_bil<2, kFromPoints64, false, true>(tp, tp, tp, tp, a, F, st, pg);
+    case 3: return launch_bil<3, kFromPoints64, false, true>(tp, tp, tp, tp, a, F, st, pg);
+    case 4: return launch_bil<4, kFromPoints64, false, true>(tp, tp, tp, tp, a, F, st, pg);
+    default: return fail(ERR_UNSUPPORTED, "bilateral: kernel_size > 9 is not compiled in");
+  }
+}
+
 int launch_packed_h(int h, bool scatter, const CUtensorMap* maps, const BilArgs& a, int F,
                     const PackedG& out, cudaStream_t st) {
   switch (h) {
@@ -842,10 +922,20 @@ static const bool g_bil_packed = [] {
   return v == nullptr || v[0] != '0';
 }();
 
+// OPCFE_MIXED_FUSED_FC=0 keeps the separate FC-data pass of the mixed front end (A/B)
+static const bool g_mixed_fused_fc = [] {
+  const char* v = std::getenv("OPCFE_MIXED_FUSED_FC");
+  return v == nullptr || v[0] != '0';
+}();
+
 int box_q(int h) { return ((((h + 1) / 2 * 2) + kBilTQW + h + 1) / 2) * 2; }
 int box_p(int h) { return ((((h + 3) / 4 * 4) + kBilTQW + h + 1 + 3) / 4) * 4; }
 
 }  // namespace
+
+bool bilateral_fc_in_iteration1(int N, int iters) {
+  return g_mixed_fused_fc && g_bil_packed && N % 2 == 0 && iters >= 2;
+}
 
 // bytes of one tile's packed centroid window (C0 float4 + C1 float2 per box quad), 128-B rounded
 size_t centroid_window_bytes(int h) {
@@ -861,7 +951,7 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
               const double* centroids_in, float sigma_length, float sigma_angle, int ksize,
               int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
               float* out_mesh, long long out_rows, cudaStream_t st, float* buf_c,
-              double* out_mesh64) {
+              double* out_mesh64, const double* pts64) {
   if (F < 1 || M < 2 || N < 2 || iters < 1 || ksize < 3 || (ksize % 2) == 0)
     return fail(ERR_INVALID, "bilateral: bad shape or parameters");
   if (!(sigma_length > 0.f) || !(sigma_angle > 0.f))
@@ -872,7 +962,13 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   // to continue from (centroids from the grid: the fused pipeline's iterations 2..B)
   const bool from_arrays = normals_in != nullptr && centroids_in != nullptr;
   const bool resume = normals_in != nullptr && centroids_in == nullptr;
-  if (!from_arrays && (pts == nullptr || pitch < 3 * N || pitch % 4))
+  // pts64: the mixed front end's FC data computed inside the fused iteration 1 from the
+  // f64 grid (even N: 16-B rows; >= 2 iterations with the packed-window buffer)
+  const bool from_p64 = pts64 != nullptr;
+  if (from_p64 && (from_arrays || resume || N % 2 || iters < 2 || buf_c == nullptr ||
+                   !g_bil_packed || (out_mesh == nullptr && out_mesh64 == nullptr)))
+    return fail(ERR_INVALID, "bilateral: f64-grid input needs even N and the fused pipeline");
+  if (!from_arrays && !from_p64 && (pts == nullptr || pitch < 3 * N || pitch % 4))
     return fail(ERR_INVALID, "bilateral: point grid (pitch multiple of 4 floats) required");
   const bool scatter = out_mesh != nullptr || out_mesh64 != nullptr;
   if (scatter && trimap == nullptr) return fail(ERR_INVALID, "bilateral: scatter needs trimap");
@@ -895,7 +991,12 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
   auto fc_store = [&](CUtensorMap* m, const float* b) {
     return make_tmap_3d(m, b, false, 6ull * Nq, Mq, F, fcp, fc_fs, SW * 6, SH);
   };
-  if (from_arrays) {
+  if (from_p64) {
+    if ((rc = make_tmap_3d(&m_pts, pts64, true, 3ull * N, M, F, 3ull * N, 3ull * N * M, PW * 3,
+                           PH)))
+      return rc;
+    m_nin = m_cin = m_pts;
+  } else if (from_arrays) {
     if ((rc = fc_load(&m_nin, normals_in))) return rc;
     // float64 centroids, contiguous [F][Mq][Nq][2][3] (rows of 6 Nq doubles: 16-B multiples)
     if ((rc = make_tmap_3d(&m_cin, centroids_in, true, 6ull * Nq, Mq, F, 6ull * Nq,
@@ -964,8 +1065,9 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
     CUtensorMap mna[2], mnb[2];
     if ((rc = maps_of(ga, &mna[0], &mna[1])) || (rc = maps_of(gb, &mnb[0], &mnb[1]))) return rc;
     // iteration 1: centroid windows -> buf_c, normals -> A
-    if ((rc = from_arrays ? launch_packout_arrays_h(h, m_nin, m_cin, a, F, ga, st)
-                          : launch_packout_h(h, m_pts, a, F, ga, st)))
+    if ((rc = from_p64      ? launch_packout_pts64_h(h, m_pts, a, F, ga, st)
+              : from_arrays ? launch_packout_arrays_h(h, m_nin, m_cin, a, F, ga, st)
+                            : launch_packout_h(h, m_pts, a, F, ga, st)))
       return rc;
     for (int it = 1; it < iters; ++it) {
       const bool last = it == iters - 1;

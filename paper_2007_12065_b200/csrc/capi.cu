@@ -440,9 +440,17 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
                        reinterpret_cast<double*>(base + L.fc_b), nullptr, io->trimap, io->normals,
                        !f64_grid, G, st);
     if (rc) return rc;
+  } else if (bil && L.bil_mixed && bilateral_fc_in_iteration1(N, p->bilateral_iterations)) {
+    // mixed, fused: the FC data computed inside iteration 1 from the f64 grid (the same
+    // bits as fc_mixed + the FC-array iteration 1, without the FC arrays' round trip)
+    rc = bilateral(nullptr, F, M, N, 0, nullptr, nullptr, (float)p->sigma_length,
+                   (float)p->sigma_angle, p->bilateral_kernel_size, p->bilateral_iterations,
+                   bil_a, p->bilateral_iterations > 2 ? bil_b : nullptr, nullptr, io->trimap,
+                   nullptr, G, st, bil_c, static_cast<double*>(io->normals), points64);
+    if (rc) return rc;
   } else if (bil && L.bil_mixed) {
-    // mixed: the exact f64 centroids and fp32 FC normals of the exact smoothed grid, the
-    // fp32 filter on them (FC-array form), the last iteration scattering float64 normals
+    // mixed: the f64 centroids and fp32 FC normals of the smoothed grid, the fp32 filter on
+    // them (FC-array form), the last iteration scattering float64 normals
     double* fc_c = reinterpret_cast<double*>(base + L.fc_c);
     float* fc32 = reinterpret_cast<float*>(base + L.fc32);
     if ((rc = fc_mixed(points64, F, M, N, fc_c, fc32, fc_pitch(N), st))) return rc;

@@ -290,6 +290,34 @@ __device__ __forceinline__ void unit_normal_f64(double ax, double ay, double az,
   }
 }
 
+// cross(b - a, c - a) * rsqrt(|.|^2) (~1.5 ulp), NaN unless |.|^2 > 0.  The cross
+// product and its squared norm keep the reference's uncontracted operations, so the
+// degenerate (NaN) set is exactly the reference's; only sqrt + 3 divisions become rsqrt.
+__device__ __forceinline__ void fast_unit_normal_f64(const double* a, const double* b,
+                                                     const double* c, double& nx, double& ny,
+                                                     double& nz) {
+  const double e1x = dsub(b[0], a[0]), e1y = dsub(b[1], a[1]), e1z = dsub(b[2], a[2]);
+  const double e2x = dsub(c[0], a[0]), e2y = dsub(c[1], a[1]), e2z = dsub(c[2], a[2]);
+  const double x = dsub(dmul(e1y, e2z), dmul(e1z, e2y));
+  const double y = dsub(dmul(e1z, e2x), dmul(e1x, e2z));
+  const double z = dsub(dmul(e1x, e2y), dmul(e1y, e2x));
+  const double r2 = dadd(dadd(dmul(x, x), dmul(y, y)), dmul(z, z));
+  if (r2 > 0.0) {
+    const double r = rsqrt(r2);
+    nx = x * r;
+    ny = y * r;
+    nz = z * r;
+  } else {
+    nx = ny = nz = __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
+// the mixed FC data's centroid: ((a + b) + c) * (1/3) with an uncontracted product (the
+// fused bilateral's mode 3 recomputes it bit for bit)
+__device__ __forceinline__ double mixed_centroid(double a, double b, double c) {
+  return __dmul_rn(dadd(dadd(a, b), c), 1.0 / 3.0);
+}
+
 // ((a+b)+c)/3.0 (smoothing.py:79)
 __device__ __forceinline__ double centroid_f64(double a, double b, double c) {
   return __ddiv_rn(dadd(dadd(a, b), c), 3.0);

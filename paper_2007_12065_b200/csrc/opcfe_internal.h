@@ -31,7 +31,12 @@ int bilateral(const float* pts, int F, int M, int N, int pitch, const float* nor
               int iters, float* buf_a, float* buf_b, float* out_fc, const int64_t* trimap,
               float* out_mesh, long long out_rows, cudaStream_t st,
               float* buf_c = nullptr,  // fused pipeline: centroid windows (bilateral_buf_c_bytes)
-              double* out_mesh64 = nullptr);  // float64 scatter destination instead
+              double* out_mesh64 = nullptr,  // float64 scatter destination instead
+              const double* pts64 = nullptr);  // mixed: FC data from the f64 grid in iteration 1
+
+// the mixed front end computes its FC data inside the fused iteration 1 (bilateral(...,
+// pts64)): even N (16-B f64 rows) and >= 2 iterations
+bool bilateral_fc_in_iteration1(int N, int iters);
 
 int fc_data(const void* opc, bool f64, int M, int N, void* cen, void* nrm, cudaStream_t st);
 

@@ -771,28 +771,6 @@ static const bool g_fc_fast_host = [] {
   return v == nullptr || v[0] != '0';
 }();
 
-// cross(b - a, c - a) * rsqrt(|.|^2) (~1.5 ulp), NaN unless |.|^2 > 0.  The cross
-// product and its squared norm keep the reference's uncontracted operations, so the
-// degenerate (NaN) set is exactly the reference's; only sqrt + 3 divisions become rsqrt.
-__device__ __forceinline__ void fast_unit_normal_f64(const double* a, const double* b,
-                                                     const double* c, double& nx, double& ny,
-                                                     double& nz) {
-  const double e1x = dsub(b[0], a[0]), e1y = dsub(b[1], a[1]), e1z = dsub(b[2], a[2]);
-  const double e2x = dsub(c[0], a[0]), e2y = dsub(c[1], a[1]), e2z = dsub(c[2], a[2]);
-  const double x = dsub(dmul(e1y, e2z), dmul(e1z, e2y));
-  const double y = dsub(dmul(e1z, e2x), dmul(e1x, e2z));
-  const double z = dsub(dmul(e1x, e2y), dmul(e1y, e2x));
-  const double r2 = dadd(dadd(dmul(x, x), dmul(y, y)), dmul(z, z));
-  if (r2 > 0.0) {
-    const double r = rsqrt(r2);
-    nx = x * r;
-    ny = y * r;
-    nz = z * r;
-  } else {
-    nx = ny = nz = __longlong_as_double(0x7ff8000000000000LL);
-  }
-}
-
 // FC data, row-segment form (fc_data_f64 / fc_mixed for every shape): a warp owns 32
 // consecutive quads of one row.  Each lane loads its two points (u, v), (u + 1, v); the
 // right-hand pair comes from the next lane by shuffles (lane 31 loads its own).  The
@@ -849,7 +827,7 @@ __global__ void __launch_bounds__(256) fc_rows_kernel(const double* __restrict__
         // the rare double rounding, at a fraction of the IEEE divisions' cost
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-          s_cen[w][lane * 6 + 3 * k + j] = (A[j] + B[j] + C[j]) * (1.0 / 3.0);
+          s_cen[w][lane * 6 + 3 * k + j] = mixed_centroid(A[j], B[j], C[j]);
         fast_unit_normal_f64(A, B, C, nx, ny, nz);
       } else {
 #pragma unroll

@@ -30,6 +30,14 @@ from .mesh import HalfEdgeMesh
 from .smoothing import BilateralParams, LaplacianParams
 
 
+def _mixed_fc_fused(N: int, iterations: int) -> bool:
+    """Whether the mixed front end computes its FC data inside the fused bilateral
+    iteration 1 (csrc/bilateral.cu bilateral_fc_in_iteration1): even N, >= 2 iterations."""
+    on = os.environ.get("OPCFE_MIXED_FUSED_FC", "1")[:1] != "0" and \
+        os.environ.get("OPCFE_BILATERAL_PACKED", "1")[:1] != "0"
+    return on and N % 2 == 0 and iterations >= 2
+
+
 @dataclass
 class FrontEndResult:
     """Device (or pinned host) outputs of one batch; rows beyond n_tri[f] are unused.
@@ -157,12 +165,12 @@ class FrontEnd:
         self._use_graph = graph
         extras = (normals and bilateral is None) or l_max is not None
         self.kernel_launches = self._count_launches(laplacian, bilateral if normals else None,
-                                                    src_kind, extras, precision) + \
+                                                    src_kind, extras, precision, N) + \
             (1 if self.labels is not None else 0) + \
             (0 if self.trimap32 is None else (3 if halfedges else 2))
 
     @staticmethod
-    def _count_launches(lap, bil, src_kind, extras=False, precision="fast"):
+    def _count_launches(lap, bil, src_kind, extras=False, precision="fast", N=0):
         """Kernels one batch launches (mirrors front_end_impl in csrc/capi.cu)."""
         from .smoothing import BILATERAL_MAX_K32, LAPLACIAN_MAX_K32
         strict, f64 = precision == "strict", precision in ("strict", "mixed")
@@ -184,7 +192,8 @@ class FrontEnd:
             n += 0 if (f64 or lap64) else 1                     # fp32 grid -> f64 (unstage)
             n += 1 + bil.iterations                             # fc_data_f64 + bilateral_f64
         elif bil and f64:                                       # mixed: fc_mixed + fp32
-            n += 1 + bil.iterations                             # iterations (f64 scatter)
+            n += bil.iterations                                 # iterations (f64 scatter);
+            n += 0 if _mixed_fc_fused(N, bil.iterations) else 1  # FC data in iteration 1
         elif bil:
             n += bil.iterations
         return n

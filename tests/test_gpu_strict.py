@@ -13,6 +13,8 @@ Bars:
   * kernel sizes beyond the fp32 kernels' compiled set run (generic-window fp64 kernels).
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -625,3 +627,43 @@ def test_drop_in_concurrent_threads(fe):
         assert same(a_sm, b_sm) and same(a_sm2, b_sm2)
         assert np.array_equal(a_m.triangles, b_m.triangles)
         assert same(a_m.normals, b_m.normals) and same(a_m2.normals, b_m2.normals)
+
+
+MIXED_FUSED_CHILD = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2007_12065_b200 as fe
+rng = np.random.default_rng(3)
+hole = fe.synthetic.room_scene(n=181, noise=0.002, seed=5)[:, :180].copy()
+hole[rng.random(hole.shape[:2]) < 0.1] = np.nan
+hole[40:60, 50:90] = np.nan                                   # a tile-sized NaN block
+out = {}
+for name, opc, bil in [("C2", fe.synthetic.config_c2(), (0.1, 0.15, 5, 2)),
+                       ("hole", hole, (0.05, 0.2, 3, 3)), ("hole7", hole, (0.05, 0.2, 7, 2))]:
+    M, N = opc.shape[:2]
+    eng = fe.FrontEnd(M, N, 1, laplacian=fe.LaplacianParams(1.0, 3, 3),
+                      bilateral=fe.BilateralParams(*bil), src_dtype=torch.float64,
+                      precision="mixed")
+    res = eng.run(torch.from_numpy(opc).cuda().unsqueeze(0))
+    out[name] = res.normals[0, :res.n_tri[0]].cpu().numpy()
+np.savez(sys.argv[2], **out)
+'''
+
+
+def test_mixed_fused_fc_data_bit_identical(tmp_path):
+    """The mixed front end's FC data computed inside the fused bilateral iteration 1 from
+    the f64 grid (OPCFE_MIXED_FUSED_FC=1, the default for even N) equals the separate
+    FC pass + FC-array iteration 1 (=0) bit for bit: NaN holes, a NaN tile, k = 3 / 5 / 7."""
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for v in ("0", "1"):
+        path = str(tmp_path / f"m{v}.npz")
+        r = subprocess.run([sys.executable, "-c", MIXED_FUSED_CHILD, repo, path],
+                           env=dict(os.environ, OPCFE_MIXED_FUSED_FC=v), capture_output=True,
+                           text=True)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res[v] = np.load(path)
+    for k in ("C2", "hole", "hole7"):
+        assert same(res["0"][k], res["1"][k]), k
