@@ -129,9 +129,11 @@ FeLayout fe_layout(int F, int M, int N, const opcfe_front_end_params* p, int src
   take(L.g64_in, ((f64_grid || L.lap64) && src_kind != 2) ? g64 : 0);
   take(L.g64_tmp, (L.lap64 && p->laplacian_iterations > 1) ? g64 : 0);
   take(L.g64_out, (!f64_grid && (L.lap64 || L.bil64)) ? g64 : 0);
-  take(L.fc_c, (L.bil64 || L.bil_mixed) ? fc64 : 0);
+  // mixed FC arrays: only when iteration 1 cannot compute the FC data itself (odd N, B = 1)
+  const bool fc_arrays = L.bil_mixed && !bilateral_fc_in_iteration1(N, p->bilateral_iterations);
+  take(L.fc_c, (L.bil64 || fc_arrays) ? fc64 : 0);
   take(L.fc_n, L.bil64 ? fc64 : 0);
-  take(L.fc32, L.bil_mixed ? fc_bytes : 0);
+  take(L.fc32, fc_arrays ? fc_bytes : 0);
 
   take(L.fc_a, (L.bil64 && p->bilateral_iterations > 1) ? fc64 : 0);
   take(L.fc_b, (L.bil64 && p->bilateral_iterations > 2) ? fc64 : 0);
