@@ -639,7 +639,8 @@ hole[rng.random(hole.shape[:2]) < 0.1] = np.nan
 hole[40:60, 50:90] = np.nan                                   # a tile-sized NaN block
 out = {}
 for name, opc, bil in [("C2", fe.synthetic.config_c2(), (0.1, 0.15, 5, 2)),
-                       ("hole", hole, (0.05, 0.2, 3, 3)), ("hole7", hole, (0.05, 0.2, 7, 2))]:
+                       ("hole", hole, (0.05, 0.2, 3, 3)), ("hole7", hole, (0.05, 0.2, 7, 2)),
+                       ("hole9", hole, (0.05, 0.2, 9, 2)), ("tiny", hole[:5, :6], (0.1, 0.2, 3, 2))]:
     M, N = opc.shape[:2]
     eng = fe.FrontEnd(M, N, 1, laplacian=fe.LaplacianParams(1.0, 3, 3),
                       bilateral=fe.BilateralParams(*bil), src_dtype=torch.float64,
@@ -653,7 +654,8 @@ np.savez(sys.argv[2], **out)
 def test_mixed_fused_fc_data_bit_identical(tmp_path):
     """The mixed front end's FC data computed inside the fused bilateral iteration 1 from
     the f64 grid (OPCFE_MIXED_FUSED_FC=1, the default for even N) equals the separate
-    FC pass + FC-array iteration 1 (=0) bit for bit: NaN holes, a NaN tile, k = 3 / 5 / 7."""
+    FC pass + FC-array iteration 1 (=0) bit for bit: NaN holes, a NaN tile, k = 3 / 5 / 7 /
+    9, a grid smaller than one tile."""
     import subprocess
     import sys
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -665,5 +667,5 @@ def test_mixed_fused_fc_data_bit_identical(tmp_path):
                            text=True)
         assert r.returncode == 0, r.stderr[-3000:]
         res[v] = np.load(path)
-    for k in ("C2", "hole", "hole7"):
+    for k in ("C2", "hole", "hole7", "hole9", "tiny"):
         assert same(res["0"][k], res["1"][k]), k
