@@ -5,8 +5,8 @@ VAR=$1; shift
 for rep in 1 2; do for val in "$@"; do
 env $VAR=$val PREC=${PREC:-mixed} timeout 300 python - <<'PY'
 import os, torch, paper_2007_12065_b200 as fe
-eng = fe.FrontEnd(1080, 1920, 16, laplacian=fe.LaplacianParams(1.0, 3, 10), bilateral=fe.BilateralParams(0.1, 0.15, 3, 5), src_dtype=torch.float64, graph=False, precision=os.environ["PREC"])
-eng.src.copy_(torch.from_numpy(fe.synthetic.config_c4()).cuda().expand_as(eng.src))
+eng = fe.FrontEnd(1080, 1920, 16, laplacian=fe.LaplacianParams(1.0, 3, 10), bilateral=fe.BilateralParams(0.1, 0.15, 3, 5), src_dtype=torch.float32 if os.environ.get("SRC") == "f32" else torch.float64, graph=False, precision=os.environ["PREC"])
+eng.src.copy_(torch.from_numpy(fe.synthetic.config_c4()).cuda().to(eng.src.dtype).expand_as(eng.src))
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
 for e in ev: e.record()
 best = [1e9] * 4

@@ -355,7 +355,11 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   const bool f64_grid = L.strict || L.mixed;  // points output (and the stages on it) double
   // the source as contiguous f64 (fp64 Laplacian input / strict points)
   const double* src64 = f64 ? static_cast<const double*>(io->src) : nullptr;
-  if (!f64 && (f64_grid || L.lap64)) {
+  // strict / mixed smoothing of an fp32 source: pass 1 reads the fp32 boxes itself
+  const bool from32 = !f64 && f64_grid && lap &&
+                      laplacian64_from32_ok(static_cast<const float*>(io->src), N, rs,
+                                            p->laplacian_kernel_size);
+  if (!f64 && (f64_grid || L.lap64) && !from32) {
     if ((rc = unstage(static_cast<const float*>(io->src), (int)rs, F, M, N, g64_in, true, nullptr,
                       st)))
       return rc;
@@ -366,7 +370,12 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   double* points64 = f64_grid ? static_cast<double*>(io->points) : nullptr;
   if (f64_grid) {
     mark(ev, 1, st);
-    if (lap) {
+    if (from32) {
+      if ((rc = laplacian64_from32(static_cast<const float*>(io->src), rs, fs, points64, g64_tmp,
+                                   F, M, N, p->laplacian_lambda, p->laplacian_kernel_size,
+                                   p->laplacian_iterations, L.mixed, st)))
+        return rc;
+    } else if (lap) {
       if ((rc = (L.mixed ? laplacian_mixed : laplacian_f64)(
                src64, points64, g64_tmp, F, M, N, p->laplacian_lambda, p->laplacian_kernel_size,
                p->laplacian_iterations, st)))

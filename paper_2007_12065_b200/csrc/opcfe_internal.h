@@ -48,6 +48,13 @@ int narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int 
 // strict (fp64, reference operation order) kernels: strict.cu
 int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
                   int ksize, int iters, cudaStream_t st);
+// the strict / mixed Laplacian of an fp32 source (row stride rs, frame stride fs floats):
+// pass 1 reads the fp32 boxes directly (exact widening), no conversion pass; k = 3, even N,
+// 16-B source rows (laplacian64_from32_ok)
+bool laplacian64_from32_ok(const float* in, int N, long long rs, int ksize);
+int laplacian64_from32(const float* in, long long rs, long long fs, double* out, double* tmp,
+                       int F, int M, int N, double lam, int ksize, int iters, bool mixed,
+                       cudaStream_t st);
 // precision "mixed": rsqrt pair weights, FMA sums, f64 points (k = 3, even N;
 // otherwise laplacian_f64)
 int laplacian_mixed(const double* in, double* out, double* tmp, int F, int M, int N, double lam,

@@ -203,18 +203,33 @@ __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_kernel(const double* __
 // MIXED (precision "mixed"): the pair weight 1/dist is rsqrt(|d|^2) (MUFU.RSQ64H + Newton,
 // ~1 ulp) instead of an IEEE sqrt and an IEEE division, and the sums are FMA-contracted:
 // float64 vertices within a few ulp per pass of the reference's, not bit-exact.
-template <int RPT, bool MIXED>
+// SRC = float: the first pass of a float32 source reads its fp32 box directly (the
+// widening to f64 is exact, so the results are those of an f64 copy of the source) --
+// no separate conversion pass; the box then starts 4 points left (16-B rule for 12-B
+// points) and the output tile gets its own room.
+template <typename SRC>
+__host__ __device__ constexpr int lap_box_lpad() { return sizeof(SRC) == 8 ? 2 : 4; }
+template <int RPT, typename SRC>
+__host__ __device__ constexpr int lap_raw_doubles() {
+  constexpr int BXW = kSTW + 2 * lap_box_lpad<SRC>(), BXH = kSTH * RPT + 2;
+  constexpr int raw = (BXW * 3 * BXH * (int)sizeof(SRC) + 127) / 128 * 128 / 8;
+  constexpr int out = (kSTW * 3 * kSTH * RPT * 8 + 127) / 128 * 128 / 8;
+  return raw > out ? raw : out;
+}
+template <int RPT, bool MIXED, typename SRC = double>
 __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_tma_kernel(
     const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, int M,
     int N, double lam) {
   constexpr int TH = kSTH * RPT;
-  constexpr int BXW = kSTW + 4, BXH = TH + 2;  // TMA box (points)
-  constexpr int RAWF = (BXW * 3 * BXH * 8 + 127) / 128 * 128 / 8;
+  constexpr int LPAD = lap_box_lpad<SRC>();
+  constexpr int BXW = kSTW + 2 * LPAD, BXH = TH + 2;  // TMA box (points)
+  constexpr int RAWF = lap_raw_doubles<RPT, SRC>();
   constexpr int BW = kSTW + 2, PL = BW * BXH;
   static_assert(kSTW * 3 * TH <= RAWF, "the output tile reuses the raw box");
   extern __shared__ __align__(16) char smem_raw[];
   uint64_t* barp;
   double* raw = reinterpret_cast<double*>(smem_aligned_base(smem_raw, &barp));
+  const SRC* raw_s = reinterpret_cast<const SRC*>(raw);
   double* sm = raw + RAWF;
   uint64_t& bar = *barp;
   const int f = blockIdx.z;
@@ -223,17 +238,17 @@ __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_tma_kernel(
   if (tid == 0) {
     mbar_init(&bar, 1);
     fence_mbar_init();
-    mbar_expect_tx(&bar, BXW * 3 * BXH * 8);
-    tma_load_3d(raw, &tin, &bar, (v0 - 2) * 3, u0 - 1, f);
+    mbar_expect_tx(&bar, BXW * 3 * BXH * (int)sizeof(SRC));
+    tma_load_3d(raw, &tin, &bar, (v0 - LPAD) * 3, u0 - 1, f);
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  for (int q = tid; q < PL; q += kSNT) {  // AoS box (r, c + 1) -> planes (r, c)
+  for (int q = tid; q < PL; q += kSNT) {  // AoS box (r, c + LPAD - 1) -> planes (r, c)
     const int r = q / BW, c = q - r * BW;
-    const double* p = raw + (r * BXW + c + 1) * 3;
-    sm[q] = p[0];
-    sm[PL + q] = p[1];
-    sm[2 * PL + q] = p[2];
+    const SRC* p = raw_s + (r * BXW + c + LPAD - 1) * 3;
+    sm[q] = (double)p[0];
+    sm[PL + q] = (double)p[1];
+    sm[2 * PL + q] = (double)p[2];
   }
   __syncthreads();  // raw is dead from here: the output tile [TH][32][3]
   const int v = v0 + tx;
@@ -919,20 +934,20 @@ int lap_launch(const double* in, double* out, int F, int M, int N, int h, double
   return check_launch("laplacian_f64_kernel");
 }
 
-template <int RPT, bool MIXED>
-int lap_tma_launch_t(const double* in, double* out, int F, int M, int N, double lam,
-                     cudaStream_t st) {
+template <int RPT, bool MIXED, typename SRC = double>
+int lap_tma_launch_t(const SRC* in, long long in_rs, long long in_fs, double* out, int F, int M,
+                     int N, double lam, cudaStream_t st) {
   constexpr int TH = kSTH * RPT, BXH = TH + 2;
-  constexpr int RAWF = ((kSTW + 4) * 3 * BXH * 8 + 127) / 128 * 128 / 8;
+  constexpr int RAWF = lap_raw_doubles<RPT, SRC>();
   CUtensorMap mi, mo;
   int rc;
-  if ((rc = make_tmap_3d(&mi, in, true, 3ull * N, M, F, 3ull * N, 3ull * N * M, (kSTW + 4) * 3,
-                         BXH)) ||
+  if ((rc = make_tmap_3d(&mi, in, sizeof(SRC) == 8, 3ull * N, M, F, (uint64_t)in_rs,
+                         (uint64_t)in_fs, (kSTW + 2 * lap_box_lpad<SRC>()) * 3, BXH)) ||
       (rc = make_tmap_3d(&mo, out, true, 3ull * N, M, F, 3ull * N, 3ull * N * M, kSTW * 3, TH)))
     return rc;
   constexpr int smem = (RAWF + 3 * (kSTW + 2) * BXH) * (int)sizeof(double) + kSmemSlack;
   static std::atomic<unsigned long long> attr_mask{0};
-  auto kern = laplacian_f64_tma_kernel<RPT, MIXED>;
+  auto kern = laplacian_f64_tma_kernel<RPT, MIXED, SRC>;
   if ((rc = ensure_smem_attr(kern, smem, attr_mask))) return rc;
   dim3 grid((N + kSTW - 1) / kSTW, (M + TH - 1) / TH, F);
   kern<<<grid, dim3(kSTW, kSTH), smem, st>>>(mi, mo, M, N, lam);
@@ -944,12 +959,12 @@ int lap_tma_launch_t(const double* in, double* out, int F, int M, int N, double 
 // CTAs / SM: 5.26)
 int lap_tma_launch(const double* in, double* out, int F, int M, int N, double lam,
                    cudaStream_t st) {
-  return lap_tma_launch_t<3, false>(in, out, F, M, N, lam, st);
+  return lap_tma_launch_t<3, false>(in, 3ll * N, 3ll * N * M, out, F, M, N, lam, st);
 }
 
 int lap_mixed_launch(const double* in, double* out, int F, int M, int N, double lam,
                      cudaStream_t st) {
-  return lap_tma_launch_t<3, true>(in, out, F, M, N, lam, st);
+  return lap_tma_launch_t<3, true>(in, 3ll * N, 3ll * N * M, out, F, M, N, lam, st);
 }
 
 // OPCFE_BIL64_TMA=0 keeps the per-thread staging of the strict k = 3 bilateral (A/B)
@@ -1035,6 +1050,38 @@ int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int 
     to_out = !to_out;
   }
   return OK;
+}
+
+// OPCFE_LAP64_FROM32=0 keeps the separate fp32 -> f64 conversion pass (A/B)
+static const bool g_lap_from32 = [] {
+  const char* v = std::getenv("OPCFE_LAP64_FROM32");
+  return v == nullptr || v[0] != '0';
+}();
+
+bool laplacian64_from32_ok(const float* in, int N, long long rs, int ksize) {
+  return g_lap_from32 && g_lap_tma && ksize == 3 && N % 2 == 0 && (rs * 4) % 16 == 0 &&
+         reinterpret_cast<uintptr_t>(in) % 16 == 0;
+}
+
+int laplacian64_from32(const float* in, long long rs, long long fs, double* out, double* tmp,
+                       int F, int M, int N, double lam, int ksize, int iters, bool mixed,
+                       cudaStream_t st) {
+  if (!laplacian64_from32_ok(in, N, rs, ksize) || F < 1 || M < 1 || iters < 1 || !in || !out ||
+      (iters > 1 && !tmp))
+    return fail(ERR_INVALID, "laplacian64_from32: unsupported shape or arguments");
+  // pass 1 straight from the fp32 source; passes 2..L on the f64 grid (ping-pong as
+  // laplacian_f64: the last pass lands in `out`)
+  double* dst = (iters % 2) == 1 ? out : tmp;
+  int rc = mixed ? lap_tma_launch_t<3, true, float>(in, rs, fs, dst, F, M, N, lam, st)
+                 : lap_tma_launch_t<3, false, float>(in, rs, fs, dst, F, M, N, lam, st);
+  const long long g_rs = 3ll * N, g_fs = 3ll * N * M;
+  for (int it = 1; it < iters && rc == OK; ++it) {
+    const double* src = dst;
+    dst = dst == out ? tmp : out;
+    rc = mixed ? lap_tma_launch_t<3, true>(src, g_rs, g_fs, dst, F, M, N, lam, st)
+               : lap_tma_launch_t<3, false>(src, g_rs, g_fs, dst, F, M, N, lam, st);
+  }
+  return rc;
 }
 
 int laplacian_mixed(const double* in, double* out, double* tmp, int F, int M, int N, double lam,

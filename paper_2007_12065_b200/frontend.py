@@ -30,6 +30,16 @@ from .mesh import HalfEdgeMesh
 from .smoothing import BilateralParams, LaplacianParams
 
 
+def _lap_from32(N: int, src_kind: int, kernel_size: int) -> bool:
+    """Whether a strict / mixed front end smooths an fp32 source without the conversion
+    pass (csrc/strict.cu laplacian64_from32_ok: k = 3, even N, 16-B source rows; the
+    front end's own buffers are 16-B aligned)."""
+    on = os.environ.get("OPCFE_LAP64_FROM32", "1")[:1] != "0" and \
+        os.environ.get("OPCFE_LAP64_TMA", "1")[:1] != "0"
+    rows16 = src_kind == 0 or (3 * N) % 4 == 0                # padded grids: pitch % 4 == 0
+    return on and src_kind != 2 and kernel_size == 3 and N % 2 == 0 and rows16
+
+
 def _mixed_fc_fused(N: int, iterations: int) -> bool:
     """Whether the mixed front end computes its FC data inside the fused bilateral
     iteration 1 (csrc/bilateral.cu bilateral_fc_in_iteration1): even N, >= 2 iterations."""
@@ -178,7 +188,8 @@ class FrontEnd:
         bil64 = bil is not None and (strict or bil.kernel_size > BILATERAL_MAX_K32)
         n = 3                                                   # triangulate: count, scan, emit
         if f64 or lap64:
-            n += 1 if src_kind != 2 else 0                      # source -> f64 (unstage)
+            from32 = f64 and lap is not None and _lap_from32(N, src_kind, lap.kernel_size)
+            n += 1 if (src_kind != 2 and not from32) else 0     # source -> f64 (unstage)
             n += lap.iterations if lap else 0                   # laplacian_f64
             n += 1 if (lap or f64) else 0                       # validity bits (+ fp32 grid)
             n += 1 if (f64 and extras) else 0                   # tri_extras_f64

@@ -669,3 +669,26 @@ def test_mixed_fused_fc_data_bit_identical(tmp_path):
         res[v] = np.load(path)
     for k in ("C2", "hole", "hole7", "hole9", "tiny"):
         assert same(res["0"][k], res["1"][k]), k
+
+
+@pytest.mark.parametrize("precision", ["strict", "mixed"])
+@pytest.mark.parametrize("shape", [(72, 96), (50, 66), (33, 128)])
+def test_f64_chain_from_fp32_source_equals_f64_source(fe, precision, shape):
+    """A strict / mixed front end fed float32 frames (the first Laplacian pass reads the
+    fp32 boxes itself when N is even and the rows are 16-B multiples) equals the same
+    front end fed those values as float64: bit for bit, with and without the direct path."""
+    M, N = shape
+    rng = np.random.default_rng(M * N)
+    opc = fe.synthetic.room_scene(n=max(M, N) + 1, noise=0.002, seed=M)[:M, :N].astype(np.float32)
+    opc[rng.random((M, N)) < 0.05] = np.nan
+    out = {}
+    for dt in (torch.float32, torch.float64):
+        eng = fe.FrontEnd(M, N, 2, laplacian=fe.LaplacianParams(0.9, 3, 4),
+                          bilateral=fe.BilateralParams(0.1, 0.2, 3, 2), l_max=0.05,
+                          src_dtype=dt, precision=precision)
+        res = eng.run(torch.from_numpy(opc).to("cuda", dt).expand(2, -1, -1, -1).contiguous())
+        T = res.n_tri[0]
+        out[dt] = (res.points.cpu().numpy(), res.normals[:, :T].cpu().numpy(),
+                   res.trimap.cpu().numpy())
+    for a, b in zip(out[torch.float32], out[torch.float64]):
+        assert same(a, b)
