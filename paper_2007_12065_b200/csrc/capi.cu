@@ -370,15 +370,18 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
   double* points64 = f64_grid ? static_cast<double*>(io->points) : nullptr;
   if (f64_grid) {
     mark(ev, 1, st);
+    // the first (TMA) pass also writes the validity bits (k = 3, even N)
+    const bool mask_fused = lap && laplacian64_mask_fused(N, p->laplacian_kernel_size);
+    uint32_t* lap_mask = mask_fused ? vmask : nullptr;
     if (from32) {
       if ((rc = laplacian64_from32(static_cast<const float*>(io->src), rs, fs, points64, g64_tmp,
                                    F, M, N, p->laplacian_lambda, p->laplacian_kernel_size,
-                                   p->laplacian_iterations, L.mixed, st)))
+                                   p->laplacian_iterations, L.mixed, st, lap_mask)))
         return rc;
     } else if (lap) {
       if ((rc = (L.mixed ? laplacian_mixed : laplacian_f64)(
                src64, points64, g64_tmp, F, M, N, p->laplacian_lambda, p->laplacian_kernel_size,
-               p->laplacian_iterations, st)))
+               p->laplacian_iterations, st, lap_mask)))
         return rc;
     } else if (src64 != points64) {
       const cudaError_t e = cudaMemcpyAsync(points64, src64, (size_t)F * M * N * 3 * sizeof(double),
@@ -386,8 +389,10 @@ int front_end_impl(int F, int M, int N, const opcfe_front_end_params* p,
       if (e != cudaSuccess)
         return fail(ERR_CUDA, std::string("front_end: copy: ") + cudaGetErrorString(e));
     }
-    // validity bits of the smoothed grid (the NaN mask is iteration-invariant)
-    if ((rc = stage_in(points64, true, 3ll * N, 3ll * N * M, F, M, N, nullptr, pitch, vmask, st)))
+    // validity bits of the smoothed grid (the NaN mask is iteration-invariant), unless the
+    // first Laplacian pass wrote them
+    if (!mask_fused &&
+        (rc = stage_in(points64, true, 3ll * N, 3ll * N * M, F, M, N, nullptr, pitch, vmask, st)))
       return rc;
   } else if (L.lap64) {
     mark(ev, 1, st);

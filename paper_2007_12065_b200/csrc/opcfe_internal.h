@@ -46,19 +46,22 @@ int narrow_indices(const int64_t* src, int32_t* dst, int F, long long rows, int 
                    const int64_t* n_rows, long long src_fs, long long dst_fs, cudaStream_t st);
 
 // strict (fp64, reference operation order) kernels: strict.cu
+// vmask (nullable): the first pass also writes the grid's validity bits when
+// laplacian64_mask_fused(N, ksize) (k = 3, even N: the TMA kernels)
 int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
-                  int ksize, int iters, cudaStream_t st);
+                  int ksize, int iters, cudaStream_t st, uint32_t* vmask = nullptr);
+bool laplacian64_mask_fused(int N, int ksize);
 // the strict / mixed Laplacian of an fp32 source (row stride rs, frame stride fs floats):
 // pass 1 reads the fp32 boxes directly (exact widening), no conversion pass; k = 3, even N,
 // 16-B source rows (laplacian64_from32_ok)
 bool laplacian64_from32_ok(const float* in, int N, long long rs, int ksize);
 int laplacian64_from32(const float* in, long long rs, long long fs, double* out, double* tmp,
                        int F, int M, int N, double lam, int ksize, int iters, bool mixed,
-                       cudaStream_t st);
+                       cudaStream_t st, uint32_t* vmask = nullptr);
 // precision "mixed": rsqrt pair weights, FMA sums, f64 points (k = 3, even N;
 // otherwise laplacian_f64)
 int laplacian_mixed(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
-                    int ksize, int iters, cudaStream_t st);
+                    int ksize, int iters, cudaStream_t st, uint32_t* vmask = nullptr);
 int bilateral_f64(const double* centroids, const double* normals_in, int F, int Mq, int Nq,
                   double sigma_length, double sigma_angle, int ksize, int iters, double* buf_a,
                   double* buf_b, double* out_fc, const int64_t* trimap, void* out_mesh,

@@ -219,7 +219,7 @@ __host__ __device__ constexpr int lap_raw_doubles() {
 template <int RPT, bool MIXED, typename SRC = double>
 __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_tma_kernel(
     const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, int M,
-    int N, double lam) {
+    int N, double lam, uint32_t* __restrict__ vmask) {
   constexpr int TH = kSTH * RPT;
   constexpr int LPAD = lap_box_lpad<SRC>();
   constexpr int BXW = kSTW + 2 * LPAD, BXH = TH + 2;  // TMA box (points)
@@ -257,6 +257,11 @@ __global__ void __launch_bounds__(kSNT, 5) laplacian_f64_tma_kernel(
     const int ty_k = ty + k * kSTH, u = u0 + ty_k;
     const int c0 = (ty_k + 1) * BW + tx + 1;
     double px = sm[c0], py = sm[PL + c0], pz = sm[2 * PL + c0];
+    if (vmask != nullptr) {  // pass 1: the grid's validity bits (iteration-invariant), one
+                             // word per warp row segment (off-grid lanes read NaN: 0)
+      const unsigned bits = __ballot_sync(0xffffffffu, isfinite(px) && isfinite(py) && isfinite(pz));
+      if (tx == 0 && u < M) vmask[((long long)f * M + u) * ((N + 31) / 32) + blockIdx.x] = bits;
+    }
     if (u > 0 && u < M - 1 && v > 0 && v < N - 1 && px == px && py == py && pz == pz) {
       double wsum = 0.0, ax = 0.0, ay = 0.0, az = 0.0;
 #pragma unroll
@@ -936,7 +941,7 @@ int lap_launch(const double* in, double* out, int F, int M, int N, int h, double
 
 template <int RPT, bool MIXED, typename SRC = double>
 int lap_tma_launch_t(const SRC* in, long long in_rs, long long in_fs, double* out, int F, int M,
-                     int N, double lam, cudaStream_t st) {
+                     int N, double lam, cudaStream_t st, uint32_t* vmask = nullptr) {
   constexpr int TH = kSTH * RPT, BXH = TH + 2;
   constexpr int RAWF = lap_raw_doubles<RPT, SRC>();
   CUtensorMap mi, mo;
@@ -950,7 +955,7 @@ int lap_tma_launch_t(const SRC* in, long long in_rs, long long in_fs, double* ou
   auto kern = laplacian_f64_tma_kernel<RPT, MIXED, SRC>;
   if ((rc = ensure_smem_attr(kern, smem, attr_mask))) return rc;
   dim3 grid((N + kSTW - 1) / kSTW, (M + TH - 1) / TH, F);
-  kern<<<grid, dim3(kSTW, kSTH), smem, st>>>(mi, mo, M, N, lam);
+  kern<<<grid, dim3(kSTW, kSTH), smem, st>>>(mi, mo, M, N, lam, vmask);
   return check_launch("laplacian_f64_tma_kernel");
 }
 
@@ -958,13 +963,13 @@ int lap_tma_launch_t(const SRC* in, long long in_rs, long long in_fs, double* ou
 // against 6.79 (two rows) and 7.07 (one); mixed 4.49 against 4.56 / 4.85 (four rows, 3
 // CTAs / SM: 5.26)
 int lap_tma_launch(const double* in, double* out, int F, int M, int N, double lam,
-                   cudaStream_t st) {
-  return lap_tma_launch_t<3, false>(in, 3ll * N, 3ll * N * M, out, F, M, N, lam, st);
+                   cudaStream_t st, uint32_t* vmask) {
+  return lap_tma_launch_t<3, false>(in, 3ll * N, 3ll * N * M, out, F, M, N, lam, st, vmask);
 }
 
 int lap_mixed_launch(const double* in, double* out, int F, int M, int N, double lam,
-                     cudaStream_t st) {
-  return lap_tma_launch_t<3, true>(in, 3ll * N, 3ll * N * M, out, F, M, N, lam, st);
+                     cudaStream_t st, uint32_t* vmask) {
+  return lap_tma_launch_t<3, true>(in, 3ll * N, 3ll * N * M, out, F, M, N, lam, st, vmask);
 }
 
 // OPCFE_BIL64_TMA=0 keeps the per-thread staging of the strict k = 3 bilateral (A/B)
@@ -1026,7 +1031,7 @@ static const bool g_lap_tma = [] {
 }();
 
 int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
-                  int ksize, int iters, cudaStream_t st) {
+                  int ksize, int iters, cudaStream_t st, uint32_t* vmask) {
   if (F < 1 || M < 1 || N < 1 || iters < 1 || ksize < 3 || (ksize % 2) == 0 || !in || !out)
     return fail(ERR_INVALID, "laplacian_f64: bad shape or parameters");
   if (iters > 1 && tmp == nullptr) return fail(ERR_INVALID, "laplacian_f64: tmp buffer required");
@@ -1040,7 +1045,8 @@ int laplacian_f64(const double* in, double* out, double* tmp, int F, int M, int 
     double* dst = to_out ? out : tmp;
     int rc;
     // k = 3 with a 16-B f64 row stride (N even): TMA-staged; otherwise per-thread loads
-    if (h == 1 && N % 2 == 0 && g_lap_tma) rc = lap_tma_launch(src, dst, F, M, N, lam, st);
+    if (h == 1 && N % 2 == 0 && g_lap_tma)
+      rc = lap_tma_launch(src, dst, F, M, N, lam, st, it == 0 ? vmask : nullptr);
     else if (h == 1) rc = lap_launch<1, true>(src, dst, F, M, N, h, lam, st);
     else if (h == 2) rc = lap_launch<2, true>(src, dst, F, M, N, h, lam, st);
     else if (lap_smem(h) <= kSmemMax) rc = lap_launch<0, true>(src, dst, F, M, N, h, lam, st);
@@ -1058,6 +1064,8 @@ static const bool g_lap_from32 = [] {
   return v == nullptr || v[0] != '0';
 }();
 
+bool laplacian64_mask_fused(int N, int ksize) { return g_lap_tma && ksize == 3 && N % 2 == 0; }
+
 bool laplacian64_from32_ok(const float* in, int N, long long rs, int ksize) {
   return g_lap_from32 && g_lap_tma && ksize == 3 && N % 2 == 0 && (rs * 4) % 16 == 0 &&
          reinterpret_cast<uintptr_t>(in) % 16 == 0;
@@ -1065,15 +1073,15 @@ bool laplacian64_from32_ok(const float* in, int N, long long rs, int ksize) {
 
 int laplacian64_from32(const float* in, long long rs, long long fs, double* out, double* tmp,
                        int F, int M, int N, double lam, int ksize, int iters, bool mixed,
-                       cudaStream_t st) {
+                       cudaStream_t st, uint32_t* vmask) {
   if (!laplacian64_from32_ok(in, N, rs, ksize) || F < 1 || M < 1 || iters < 1 || !in || !out ||
       (iters > 1 && !tmp))
     return fail(ERR_INVALID, "laplacian64_from32: unsupported shape or arguments");
   // pass 1 straight from the fp32 source; passes 2..L on the f64 grid (ping-pong as
   // laplacian_f64: the last pass lands in `out`)
   double* dst = (iters % 2) == 1 ? out : tmp;
-  int rc = mixed ? lap_tma_launch_t<3, true, float>(in, rs, fs, dst, F, M, N, lam, st)
-                 : lap_tma_launch_t<3, false, float>(in, rs, fs, dst, F, M, N, lam, st);
+  int rc = mixed ? lap_tma_launch_t<3, true, float>(in, rs, fs, dst, F, M, N, lam, st, vmask)
+                 : lap_tma_launch_t<3, false, float>(in, rs, fs, dst, F, M, N, lam, st, vmask);
   const long long g_rs = 3ll * N, g_fs = 3ll * N * M;
   for (int it = 1; it < iters && rc == OK; ++it) {
     const double* src = dst;
@@ -1085,11 +1093,11 @@ int laplacian64_from32(const float* in, long long rs, long long fs, double* out,
 }
 
 int laplacian_mixed(const double* in, double* out, double* tmp, int F, int M, int N, double lam,
-                    int ksize, int iters, cudaStream_t st) {
+                    int ksize, int iters, cudaStream_t st, uint32_t* vmask) {
   // the fp32-pair kernel covers k = 3 with a 16-B f64 row stride; otherwise the strict
   // kernels (exact, so within every bound the mixed mode promises)
   if (!(ksize == 3 && N % 2 == 0 && g_lap_tma))
-    return laplacian_f64(in, out, tmp, F, M, N, lam, ksize, iters, st);
+    return laplacian_f64(in, out, tmp, F, M, N, lam, ksize, iters, st, vmask);
   if (F < 1 || M < 1 || N < 1 || iters < 1 || !in || !out)
     return fail(ERR_INVALID, "laplacian_mixed: bad shape or parameters");
   if (iters > 1 && tmp == nullptr) return fail(ERR_INVALID, "laplacian_mixed: tmp buffer required");
@@ -1100,7 +1108,7 @@ int laplacian_mixed(const double* in, double* out, double* tmp, int F, int M, in
   for (int it = 0; it < iters; ++it) {
     double* dst = to_out ? out : tmp;
     int rc;
-    if ((rc = lap_mixed_launch(src, dst, F, M, N, lam, st))) return rc;
+    if ((rc = lap_mixed_launch(src, dst, F, M, N, lam, st, it == 0 ? vmask : nullptr))) return rc;
     src = dst;
     to_out = !to_out;
   }

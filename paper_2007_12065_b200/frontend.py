@@ -40,6 +40,12 @@ def _lap_from32(N: int, src_kind: int, kernel_size: int) -> bool:
     return on and src_kind != 2 and kernel_size == 3 and N % 2 == 0 and rows16
 
 
+def _lap_mask_fused(N: int, kernel_size: int) -> bool:
+    """Whether the strict / mixed Laplacian's first pass writes the validity bits itself
+    (csrc/strict.cu laplacian64_mask_fused: the TMA kernels, k = 3, even N)."""
+    return os.environ.get("OPCFE_LAP64_TMA", "1")[:1] != "0" and kernel_size == 3 and N % 2 == 0
+
+
 def _mixed_fc_fused(N: int, iterations: int) -> bool:
     """Whether the mixed front end computes its FC data inside the fused bilateral
     iteration 1 (csrc/bilateral.cu bilateral_fc_in_iteration1): even N, >= 2 iterations."""
@@ -191,7 +197,8 @@ class FrontEnd:
             from32 = f64 and lap is not None and _lap_from32(N, src_kind, lap.kernel_size)
             n += 1 if (src_kind != 2 and not from32) else 0     # source -> f64 (unstage)
             n += lap.iterations if lap else 0                   # laplacian_f64
-            n += 1 if (lap or f64) else 0                       # validity bits (+ fp32 grid)
+            mask_fused = f64 and lap is not None and _lap_mask_fused(N, lap.kernel_size)
+            n += 1 if (lap or f64) and not mask_fused else 0    # validity bits (+ fp32 grid)
             n += 1 if (f64 and extras) else 0                   # tri_extras_f64
         else:
             n += lap.iterations if lap else 0
