@@ -12,7 +12,7 @@ from summarize import HERE, METRICS, OUT, raw_metrics  # noqa: E402
 KERNELS = (("lap", "Laplacian pass (laplacian_f64_tma_kernel<3, MIXED>)"),
            ("fc", "FC data (fc_rows_kernel)"),
            ("bil", "bilateral iteration (strict: bilateral_f64s_kernel; mixed: bilateral_kernel "
-                   "iteration 1 from the FC arrays)"))
+                   "iteration 1 -- from the f64 grid since r02o, from the FC arrays before)"))
 
 
 def launch_table(path):
